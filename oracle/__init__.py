@@ -1,0 +1,226 @@
+"""CPU oracle for the detector-tomography hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this package.  The product package
+``paper_2404_02844_b200`` never imports it, and the two share no code.
+
+This module is a ctypes shim around ``qdt_oracle.c`` (plain fp64 C, one thread,
+``-O2 -ffp-contract=off``): argument marshalling only, every number is computed in C.
+Each C function cites the PAPER.md passage it follows.
+
+Parity status: every function below is pinned by a
+``-m "not gpu"`` test in ``tests/test_oracle_pins.py``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "qdt_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+_i64p = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (plain C, no FMA contraction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(
+            ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=gnu11", "-shared",
+             "-fPIC", _SRC, "-o", tmp, "-lquadmath", "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = ctypes.CDLL(build())
+        i64, f64 = ctypes.c_int64, ctypes.c_double
+        P64 = ctypes.POINTER(ctypes.c_int64)
+        L.or_band.argtypes = [f64, i64, f64, i64, P64, P64]
+        L.or_band.restype = None
+        L.or_poisson_pmf.argtypes = [i64, f64]
+        L.or_poisson_pmf.restype = f64
+        L.or_build_probes.argtypes = [_f64p, i64, i64, f64, i64, _i64p, _i64p, _i64p,
+                                      ctypes.c_void_p]
+        L.or_build_probes.restype = ctypes.c_int
+        L.or_project_simplex.argtypes = [_f64p, i64, _f64p, _f64p]
+        L.or_project_simplex.restype = f64
+        L.or_project_rows.argtypes = [_f64p, i64, i64, _f64p]
+        L.or_project_rows.restype = None
+        L.or_forward.argtypes = [_i64p, _i64p, _i64p, _f64p, i64, _f64p, ctypes.c_void_p, i64,
+                                 _f64p]
+        L.or_forward.restype = None
+        L.or_laplacian.argtypes = [_f64p, i64, i64, _f64p]
+        L.or_laplacian.restype = None
+        L.or_backward.argtypes = [_i64p, _i64p, _i64p, _f64p, i64, i64, _f64p, _f64p, i64, f64,
+                                  _f64p]
+        L.or_backward.restype = None
+        L.or_regul.argtypes = [_f64p, i64, i64]
+        L.or_regul.restype = f64
+        L.or_objective.argtypes = [_i64p, _i64p, _i64p, _f64p, i64, i64, _f64p, _f64p, i64, f64]
+        L.or_objective.restype = f64
+        L.or_kkt.argtypes = [_f64p, _f64p, i64, i64, ctypes.POINTER(f64)]
+        L.or_kkt.restype = f64
+        L.or_sqs_weights.argtypes = [_i64p, _i64p, _i64p, _f64p, i64, i64, f64, _f64p]
+        L.or_sqs_weights.restype = None
+        L.or_power_iteration.argtypes = [_i64p, _i64p, _i64p, _f64p, i64, i64, i64]
+        L.or_power_iteration.restype = f64
+        L.or_solve.argtypes = [_i64p, _i64p, _i64p, _f64p, i64, i64, _f64p, i64, f64, f64, i64,
+                               ctypes.c_int, ctypes.c_int, i64, ctypes.c_void_p, _f64p,
+                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                               ctypes.POINTER(f64)]
+        L.or_solve.restype = i64
+        _lib = L
+    return _lib
+
+
+def _f(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+class Probes:
+    """Banded F in probe-major storage (lo, len, off, val) as built by the oracle."""
+
+    def __init__(self, alpha2, M: int, c_sigma: float = 6.0, margin: int = 16):
+        alpha2 = _f(alpha2)
+        D = alpha2.shape[0]
+        self.D, self.M = D, int(M)
+        self.alpha2 = alpha2
+        self.lo = np.zeros(D, np.int64)
+        self.len = np.zeros(D, np.int64)
+        self.off = np.zeros(D + 1, np.int64)
+        L = lib()
+        rc = L.or_build_probes(alpha2, D, self.M, c_sigma, margin, self.lo, self.len, self.off,
+                               None)
+        if rc != 0:
+            raise ValueError("or_build_probes: invalid arguments")
+        self.nnz = int(self.off[-1])
+        self.val = np.zeros(self.nnz, np.float64)
+        L.or_build_probes(alpha2, D, self.M, c_sigma, margin, self.lo, self.len, self.off,
+                          self.val.ctypes.data)
+
+    @property
+    def hi(self):
+        return self.lo + self.len - 1
+
+    def dense(self) -> np.ndarray:
+        """Dense D x M copy of F (small instances only)."""
+        F = np.zeros((self.D, self.M))
+        for d in range(self.D):
+            F[d, self.lo[d]:self.lo[d] + self.len[d]] = self.val[self.off[d]:self.off[d + 1]]
+        return F
+
+    def _args(self):
+        return self.lo, self.len, self.off, self.val, self.D
+
+
+def band(mu: float, M: int, c_sigma: float = 6.0, margin: int = 16):
+    lo, hi = ctypes.c_int64(), ctypes.c_int64()
+    lib().or_band(float(mu), int(M), float(c_sigma), int(margin), ctypes.byref(lo),
+                  ctypes.byref(hi))
+    return lo.value, hi.value
+
+
+def poisson_pmf(k: int, mu: float) -> float:
+    return lib().or_poisson_pmf(int(k), float(mu))
+
+
+def project_simplex(x):
+    x = _f(x)
+    y = np.empty_like(x)
+    w = np.empty_like(x)
+    tau = lib().or_project_simplex(x, x.shape[0], y, w)
+    return y, tau
+
+
+def project_rows(X):
+    X = _f(X)
+    Y = np.empty_like(X)
+    lib().or_project_rows(X, X.shape[0], X.shape[1], Y)
+    return Y
+
+
+def forward(F: Probes, Theta, P=None):
+    """R = F Theta - P (P omitted: R = F Theta)."""
+    Theta = _f(Theta)
+    N = Theta.shape[1] if Theta.ndim == 2 else 1
+    R = np.empty((F.D, N))
+    Pp = None if P is None else _f(P)
+    lib().or_forward(*F._args(), Theta, None if Pp is None else Pp.ctypes.data, N, R)
+    return R
+
+
+def backward(F: Probes, R, Theta, gamma: float = 0.0):
+    """G = F^T R + gamma L Theta (half gradient)."""
+    R, Theta = _f(R), _f(Theta)
+    N = Theta.shape[1]
+    G = np.empty((F.M, N))
+    lib().or_backward(*F._args(), F.M, R, Theta, N, float(gamma), G)
+    return G
+
+
+def laplacian(Theta):
+    Theta = _f(Theta)
+    LT = np.empty_like(Theta)
+    lib().or_laplacian(Theta, Theta.shape[0], Theta.shape[1], LT)
+    return LT
+
+
+def regul(Theta) -> float:
+    Theta = _f(Theta)
+    return lib().or_regul(Theta, Theta.shape[0], Theta.shape[1])
+
+
+def objective(F: Probes, P, Theta, gamma: float) -> float:
+    P, Theta = _f(P), _f(Theta)
+    return lib().or_objective(*F._args(), F.M, P, Theta, Theta.shape[1], float(gamma))
+
+
+def kkt(Theta, G):
+    Theta, G = _f(Theta), _f(G)
+    rp = ctypes.c_double()
+    r = lib().or_kkt(Theta, G, Theta.shape[0], Theta.shape[1], ctypes.byref(rp))
+    return r, rp.value
+
+
+def sqs_weights(F: Probes, gamma: float):
+    w = np.empty(F.M)
+    lib().or_sqs_weights(*F._args(), F.M, float(gamma), w)
+    return w
+
+
+def power_iteration(F: Probes, k_pow: int = 100) -> float:
+    return lib().or_power_iteration(*F._args(), F.M, int(k_pow))
+
+
+STEP_SQS, STEP_LIPSCHITZ = 0, 1
+
+
+def solve(F: Probes, P, gamma: float, tol: float, iters: int, step: int = STEP_SQS,
+          accel: int = 0, kkt_every: int = 1, theta0=None):
+    """Projected-gradient solve; returns dict(theta, trace, kkt, kkt_paper, iters_done, step)."""
+    P = _f(P)
+    N = P.shape[1]
+    Theta = np.empty((F.M, N))
+    trace = np.full(iters + 1, np.nan)
+    kt = np.full(iters + 1, np.nan)
+    kp = np.full(iters + 1, np.nan)
+    st = ctypes.c_double()
+    t0 = None if theta0 is None else _f(theta0)
+    done = lib().or_solve(*F._args(), F.M, P, N, float(gamma), float(tol), int(iters), int(step),
+                          int(accel), int(kkt_every), None if t0 is None else t0.ctypes.data,
+                          Theta, trace.ctypes.data, kt.ctypes.data, kp.ctypes.data,
+                          ctypes.byref(st))
+    return dict(theta=Theta, trace=trace[:done + 1], kkt=kt[:done + 1], kkt_paper=kp[:done + 1],
+                iters_done=int(done), step=st.value)
