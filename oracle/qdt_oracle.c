@@ -16,6 +16,11 @@
  * P (D x N) outcome probabilities, eq. Matrix PAPER.md:48-50.
  *
  * Parity status of every function is listed in DESIGN.md section "Oracle pins".
+ *
+ * Scalar reductions over whole matrices (||R||_F^2, the regulariser sum, the KKT sums,
+ * power-iteration norms) accumulate in x87 extended precision: a plain double running sum
+ * of 10^7 - 10^8 nonnegative terms carries a biased rounding error (measured 5e-10 relative
+ * on the Large config) that would exceed the objective gate of reading R5.
  */
 #include <math.h>
 #include <quadmath.h>
@@ -217,13 +222,21 @@ void or_backward(const int64_t *lo, const int64_t *len, const int64_t *off, cons
 /* sum_n sum_{i=0}^{M-2} (Theta_{i,n} - Theta_{i+1,n})^2   (eq. regul) */
 double or_regul(const double *Theta, int64_t M, int64_t N)
 {
-    double s = 0.0;
+    long double s = 0.0L; /* long scalar sums accumulate in extended precision (see header) */
     for (int64_t k = 0; k + 1 < M; k++)
         for (int64_t n = 0; n < N; n++) {
             double d = Theta[k * N + n] - Theta[(k + 1) * N + n];
-            s += d * d;
+            s += (long double)(d * d);
         }
-    return s;
+    return (double)s;
+}
+
+/* ||R||_F^2 over D x N entries, extended-precision accumulator */
+static double sumsq(const double *R, int64_t n)
+{
+    long double s = 0.0L;
+    for (int64_t i = 0; i < n; i++) s += (long double)(R[i] * R[i]);
+    return (double)s;
 }
 
 /* f(Theta) = ||P - F Theta||_2^2 + gamma * regul   (eq. min_obj2 PAPER.md:70 + eq. regul) */
@@ -233,8 +246,7 @@ double or_objective(const int64_t *lo, const int64_t *len, const int64_t *off, c
 {
     double *R = (double *)malloc((size_t)(D * N) * sizeof(double));
     or_forward(lo, len, off, val, D, Theta, P, N, R);
-    double s = 0.0;
-    for (int64_t i = 0; i < D * N; i++) s += R[i] * R[i];
+    double s = sumsq(R, D * N);
     free(R);
     return s + gamma * or_regul(Theta, M, N);
 }
@@ -245,7 +257,7 @@ double or_objective(const int64_t *lo, const int64_t *len, const int64_t *off, c
  * df = 2G (reading R0).  Returns the unclamped value; *paper_out gets the clamped one. */
 double or_kkt(const double *Theta, const double *G, int64_t M, int64_t N, double *paper_out)
 {
-    double s = 0.0, sp = 0.0;
+    long double s = 0.0L, sp = 0.0L;
     for (int64_t k = 0; k < M; k++) {
         double mn = INFINITY;
         for (int64_t n = 0; n < N; n++) {
@@ -258,12 +270,12 @@ double or_kkt(const double *Theta, const double *G, int64_t M, int64_t N, double
             double df = 2.0 * G[k * N + n];
             double a = Theta[k * N + n] * (df + lam);
             double b = Theta[k * N + n] * (df + lamp);
-            s += a * a;
-            sp += b * b;
+            s += (long double)(a * a);
+            sp += (long double)(b * b);
         }
     }
-    if (paper_out) *paper_out = sqrt(sp / ((double)N * (double)M));
-    return sqrt(s / ((double)N * (double)M));
+    if (paper_out) *paper_out = sqrt((double)sp / ((double)N * (double)M));
+    return sqrt((double)s / ((double)N * (double)M));
 }
 
 /* ------------------------------------------------------------------------------------
@@ -295,15 +307,12 @@ double or_power_iteration(const int64_t *lo, const int64_t *len, const int64_t *
     for (int64_t it = 0; it < K_pow; it++) {
         or_forward(lo, len, off, val, D, v, NULL, 1, q);
         or_backward(lo, len, off, val, D, M, q, v, 1, 0.0, u);
-        double nn = 0.0;
-        for (int64_t k = 0; k < M; k++) nn += u[k] * u[k];
-        nn = sqrt(nn);
+        double nn = sqrt(sumsq(u, M));
         if (nn == 0.0) break;
         for (int64_t k = 0; k < M; k++) v[k] = u[k] / nn;
     }
     or_forward(lo, len, off, val, D, v, NULL, 1, q);
-    double rho = 0.0;
-    for (int64_t d = 0; d < D; d++) rho += q[d] * q[d];
+    double rho = sumsq(q, D);
     free(v);
     free(u);
     free(q);
@@ -381,11 +390,7 @@ int64_t or_solve(const int64_t *lo, const int64_t *len, const int64_t *off, cons
                 Gt = NULL;
             }
         }
-        {
-            double s = 0.0;
-            for (int64_t i = 0; i < D * N; i++) s += R[i] * R[i];
-            fk = s + gamma * or_regul(Theta, M, N);
-        }
+        fk = sumsq(R, D * N) + gamma * or_regul(Theta, M, N);
         if (Gt && (k % kkt_every == 0)) rk = or_kkt(Theta, Gt, M, N, &rpk);
         if (trace) trace[k] = fk;
         if (kkt_trace) kkt_trace[k] = rk;
@@ -401,8 +406,7 @@ int64_t or_solve(const int64_t *lo, const int64_t *len, const int64_t *off, cons
     if (k == iters) {
         or_forward(lo, len, off, val, D, Theta, P, N, R);
         or_backward(lo, len, off, val, D, M, R, Theta, N, gamma, G);
-        double s = 0.0;
-        for (int64_t i = 0; i < D * N; i++) s += R[i] * R[i];
+        double s = sumsq(R, D * N);
         double rp;
         double r = or_kkt(Theta, G, M, N, &rp);
         if (trace) trace[iters] = s + gamma * or_regul(Theta, M, N);

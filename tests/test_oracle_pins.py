@@ -410,3 +410,16 @@ def test_medium_ground_truth_rows():
     T = qs.theta_medium(50, 10)
     np.testing.assert_allclose(T[1, :2], [0.1, 0.9], atol=1e-15)
     np.testing.assert_allclose(T.sum(axis=1), 1.0, atol=1e-12)
+
+
+def test_objective_sum_accuracy_many_terms():
+    # f = ||F Theta - P||^2 over 2e6 entries vs an exactly rounded sum (math.fsum) of the
+    # dense residual: the accumulation must stay within the reading-R5 gate (1e-10) by far.
+    rng = np.random.default_rng(21)
+    D, M, N = 2000, 200, 1000
+    F = oracle.Probes(np.sort(rng.uniform(0, 150, D)), M)
+    Th = np.full((M, N), 1.0 / N)
+    P = rng.dirichlet(np.ones(N) * 0.05, D)
+    R = F.dense() @ Th - P
+    ref = math.fsum((R * R).ravel())
+    assert oracle.objective(F, P, Th, 0.0) == pytest.approx(ref, rel=1e-14)
