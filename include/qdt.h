@@ -1,0 +1,181 @@
+/*
+ * qdt.h -- C ABI of the B200-native phase-insensitive detector-tomography solver
+ *          (hot path of arXiv:2404.02844, "Scalable quantum detector tomography by
+ *          high-performance computing").
+ *
+ * Problem (eq. min; regulariser eq. regul):
+ *     min_Theta  f(Theta) = ||P - F Theta||_F^2 + gamma * sum_n sum_{k=0}^{M-2} (Theta_{k,n} - Theta_{k+1,n})^2
+ *     s.t.       Theta_{k,n} >= 0,  sum_n Theta_{k,n} = 1   for every Fock row k.
+ *   Theta (= Pi of the paper) : M x N, row-major, row k = Fock level, column n = outcome.
+ *   F                          : D x M, F_{d,k} = mu_d^k e^{-mu_d} / k!,  mu_d = |alpha_d|^2
+ *                                (eq. Fmatrix), stored banded.
+ *   P                          : D x N, row-major outcome probabilities (eq. Matrix).
+ *
+ * Method (DESIGN.md "Readings" R0-R12): projected gradient.  One iteration k maps
+ *   Theta_k -> Theta_{k+1} = P_{S^M}( Y_k - t o G(Y_k) ),   G = F^T (F Y - P) + gamma L Y = grad f / 2,
+ * with the row-wise simplex projection P_{S^M} of eq. Mp1_proj, Y_k = Theta_k
+ * (plain) or the FISTA extrapolation, and t a fixed diagonal metric: SQS row weights
+ * t_k = 1/w_k, w = F^T F 1 + 4 gamma, or one Lipschitz scalar 1/(1.01 rho + 4 gamma) with rho
+ * from 100 power iterations.  Convergence measure: the KKT residual of PAPER.md:563-567.
+ *
+ * Conventions (all functions):
+ *   - Every call returns qdt_status; QDT_OK == 0.  No C++ exception crosses the ABI.  On a
+ *     non-OK status, qdt_last_error(ctx) returns a message naming the offending argument.
+ *   - Ownership: the caller owns every input and output buffer (caller-allocated, sizes as
+ *     stated).  Handles are created by qdt_init / qdt_build_probes / qdt_probes_from_banded
+ *     and released by qdt_finalize / qdt_probes_free.  No caller pointer is kept after a
+ *     call returns.
+ *   - Pointers are HOST pointers unless `mem_device` (solve/objective options) is 1; then P,
+ *     Theta and theta0 are device pointers on ctx's device, ordered on ctx's stream.
+ *   - A ctx is not thread-safe: one ctx per (process, GPU).
+ *   - Multi-GPU is SPMD over the Fock axis: with nranks > 1 every rank calls every function
+ *     with identical replicated inputs; qdt_build_probes, qdt_solve and qdt_objective are
+ *     collective (NCCL over NVLink).  Rank g owns Fock rows [k_begin, k_end) (cost balanced).
+ *   - There is no CPU fallback: without a CUDA device every call returns QDT_ERR_CUDA.
+ */
+#ifndef QDT_H
+#define QDT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    QDT_OK = 0,
+    QDT_ERR_INVALID_ARG = 1, /* a size/scalar/option out of range, or a NULL required pointer */
+    QDT_ERR_UNSORTED = 2,    /* alpha2 not nondecreasing */
+    QDT_ERR_NONFINITE = 3,   /* NaN/Inf in alpha2, P, theta0, or a non-finite objective */
+    QDT_ERR_OOM = 4,         /* device allocation failed / memory plan exceeds free HBM */
+    QDT_ERR_CUDA = 5,        /* CUDA runtime error (no device, launch failure, ...) */
+    QDT_ERR_NCCL = 6,        /* NCCL unavailable or a collective failed */
+    QDT_ERR_TRUNCATED = 7,   /* strict_mass: a probe row loses mass at the cutoff M */
+    QDT_ERR_STATE = 8        /* handle/ctx mismatch (e.g. probes built on another ctx) */
+} qdt_status;
+
+typedef enum {
+    QDT_STEP_SQS = 0,       /* row-constant diagonal majorizer, t_k = 1 / (F^T F 1 + 4 gamma)_k */
+    QDT_STEP_LIPSCHITZ = 1  /* scalar t = 1 / (1.01 rho + 4 gamma), rho: 100 power iterations   */
+} qdt_step_mode;
+
+typedef struct qdt_ctx qdt_ctx;       /* device, stream, NCCL comm, workspace, last error  */
+typedef struct qdt_probes qdt_probes; /* banded F of this rank's Fock slice + tile plans     */
+
+typedef struct {
+    int32_t device;             /* CUDA device ordinal                                       */
+    int32_t rank, nranks;       /* SPMD rank / world size (1 = single GPU)                   */
+    const void *nccl_unique_id; /* 128-byte ncclUniqueId (same on every rank); NULL if nranks==1 */
+    void *cuda_stream;          /* cudaStream_t to run on; NULL -> ctx-owned stream           */
+} qdt_init_opts;
+
+typedef struct {
+    double c_sigma;      /* band half-width in units of sqrt(mu) (reading R1), default 6     */
+    int32_t margin;      /* extra rows above the band, default 16                            */
+    int32_t strict_mass; /* 1: a band clipped at M-1 is an error (QDT_ERR_TRUNCATED)        */
+} qdt_probe_opts;
+
+typedef struct {
+    int32_t step;          /* qdt_step_mode, default QDT_STEP_SQS                              */
+    int32_t accel;         /* 0 = plain projected gradient, 1 = FISTA extrapolation            */
+    const double *theta0;  /* initial Theta (M x N, or local rows if !gather); NULL -> 1/N     */
+    int32_t check_every;   /* host polls the device stop flag every this many iterations (16)  */
+    int32_t kkt_every;     /* FISTA: evaluate r_KKT(Theta_k) every this many iterations (1)    */
+    int32_t mem_device;    /* 1: P / theta0 / theta_out are device pointers                    */
+    int32_t gather_theta;  /* nranks>1: 1 -> theta_out is the full M x N on every rank         */
+    int32_t use_graph;     /* 1 (default): replay the iteration as a CUDA graph                */
+} qdt_solve_opts;
+
+typedef struct {
+    int64_t iters_done;    /* k at which the solve stopped (== iters if the cap was hit)       */
+    int32_t converged;     /* 1 if r_KKT(Theta_k) <= tol stopped the solve                     */
+    double kkt0;           /* r_KKT(Theta_0)                                                   */
+    double kkt;            /* r_KKT(Theta_iters_done), unclamped multiplier (reading R7)       */
+    double kkt_paper;      /* same with the paper's clamped lambda = max(0, -min df)           */
+    double f_final;        /* f(Theta_iters_done)                                               */
+    double step_scalar;    /* LIPSCHITZ step t (0 for SQS)                                     */
+    int64_t k_begin, k_end;/* this rank's Fock rows                                            */
+    int64_t nnz;           /* stored entries of F on this rank                                  */
+    double min_row_mass;   /* min_d sum_k F_{d,k} over stored bands (truncation diagnostic)    */
+    int64_t uncovered_rows;/* Fock rows (this rank) touched by no probe band (reading R9)      */
+} qdt_solve_info;
+
+/* ------------------------------------------------------------------------------ context */
+/* Create a context on opts->device.  nranks > 1 initialises an NCCL communicator from
+ * opts->nccl_unique_id (collective over all ranks).  opts == NULL -> device 0, 1 rank. */
+qdt_status qdt_init(qdt_ctx **ctx, const qdt_init_opts *opts);
+qdt_status qdt_finalize(qdt_ctx *ctx);
+/* Thread-local message for the last non-OK status of ctx (never NULL). */
+const char *qdt_last_error(const qdt_ctx *ctx);
+
+/* ------------------------------------------------------------------------------ probes */
+/* S0: build the banded probe matrix F from host alpha2[D] (mu_d = |alpha_d|^2,
+ * finite, >= 0, nondecreasing) for Fock cutoff M (eq. Fmatrix; band:
+ * reading R1).  Band edges and values are computed on the device (log-space Poisson pmf,
+ * Loader's saddle-point form).  opts == NULL -> defaults.  Collective when nranks > 1: rank
+ * g stores only entries with k in its Fock slice.
+ * Errors: D < 1, M < 1 -> INVALID_ARG; non-finite or negative mu -> INVALID_ARG;
+ * decreasing mu -> UNSORTED; strict_mass and a clipped band -> TRUNCATED. */
+qdt_status qdt_build_probes(qdt_ctx *ctx, const double *alpha2, int64_t D, int64_t M,
+                            const qdt_probe_opts *opts, qdt_probes **out);
+qdt_status qdt_probes_free(qdt_probes *probes);
+/* Band tables and sizes of this rank: any output pointer may be NULL.  lo/len: host
+ * int64[D] (global first row and length of the locally stored band), val: host double[nnz]
+ * (probe-major, the band of probe d at [off_d, off_d + len_d), off_d = sum_{e<d} len_e). */
+qdt_status qdt_probes_export(qdt_ctx *ctx, const qdt_probes *probes, int64_t *nnz,
+                             int64_t *k_begin, int64_t *k_end, int64_t *lo, int64_t *len,
+                             double *val);
+
+/* ------------------------------------------------------------------------------ solve */
+/* Projected-gradient solve.  P: D x N (host, or device if
+ * opts->mem_device).  N >= 1, gamma >= 0 finite, tol >= 0, iters >= 0.
+ * theta_out: M x N (or the local (k_end-k_begin) x N rows when nranks > 1 and
+ * !gather_theta) receiving Theta_{iters_done}.  trace_out (may be NULL): host double[iters+1],
+ * trace_out[k] = f(Theta_k) for k <= iters_done (reading R3); kkt_out (may be NULL): host
+ * double[iters+1] with r_KKT(Theta_k) (NaN where not evaluated).  Early stop at the first
+ * k with r_KKT(Theta_k) <= tol returns Theta_k.  info may be NULL.  Collective. */
+qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double *P, int64_t N, double gamma,
+                     double tol, int64_t iters, const qdt_solve_opts *opts, double *theta_out,
+                     double *trace_out, double *kkt_out, qdt_solve_info *info);
+
+/* f(Theta) = ||P - F Theta||^2 + gamma * regul (eq. min_obj2 + eq. regul) and, if kkt_out
+ * != NULL, r_KKT(Theta) (unclamped, reading R7).  Theta: M x N (all ranks pass the full
+ * matrix).  mem_device as in qdt_solve_opts.  Collective. */
+qdt_status qdt_objective(qdt_ctx *ctx, const qdt_probes *F, const double *P, const double *theta,
+                         int64_t N, double gamma, int32_t mem_device, double *f_out,
+                         double *kkt_out);
+
+/* ------------------------------------------------------------------------------ kernel hooks
+ * The individual steps of one iteration, for per-kernel parity tests.  They run the same
+ * kernels as qdt_solve.  All arrays are HOST pointers, full (global) sizes, nranks == 1. */
+/* R = F Theta - P (P may be NULL: R = F Theta).  Theta M x N, R D x N. */
+qdt_status qdt_residual(qdt_ctx *ctx, const qdt_probes *F, const double *theta, const double *P,
+                        int64_t N, double *R_out);
+/* G = F^T R + gamma L Theta (half gradient, reading R0).  R D x N, Theta M x N, G M x N. */
+qdt_status qdt_gradient(qdt_ctx *ctx, const qdt_probes *F, const double *R, const double *theta,
+                        int64_t N, double gamma, double *G_out);
+/* One iteration of the given step/accel=0 map on Theta: Theta_next = P_{S^M}(Theta - t o G). */
+qdt_status qdt_step(qdt_ctx *ctx, const qdt_probes *F, const double *P, const double *theta,
+                    int64_t N, double gamma, int32_t step_mode, double *theta_next);
+/* Row-wise simplex projection Y = P_{S^M}(X) of an M x N matrix (warp Michelot). */
+qdt_status qdt_project_rows(qdt_ctx *ctx, const double *X, int64_t M, int64_t N, double *Y_out);
+/* Step setup: SQS weights w[M] = F^T F 1 + 4 gamma (w_out may be NULL) and the power-
+ * iteration estimate rho of lambda_max(F^T F) after k_pow iterations (rho_out may be NULL). */
+qdt_status qdt_step_setup(qdt_ctx *ctx, const qdt_probes *F, double gamma, int32_t k_pow,
+                          double *w_out, double *rho_out);
+
+/* ------------------------------------------------------------------------------ profiling */
+/* When enabled, qdt_solve runs without a graph and brackets every kernel launch with CUDA
+ * events on ctx's stream; qdt_profile_get returns per-kernel (count, total ms) for the kernel
+ * names "probe_edges", "probe_values", "fwd_partial", "reduce_R", "bwd_step", "scalars",
+ * "allreduce_R", "halo". */
+qdt_status qdt_profile_enable(qdt_ctx *ctx, int32_t enable);
+qdt_status qdt_profile_get(qdt_ctx *ctx, const char *kernel, int64_t *count, double *total_ms);
+/* Number of kernels this library launched on ctx since qdt_init (graph nodes counted per
+ * replay). */
+qdt_status qdt_launch_count(qdt_ctx *ctx, int64_t *count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QDT_H */

@@ -1,0 +1,296 @@
+"""B200-native phase-insensitive quantum detector tomography (arXiv:2404.02844 hot path).
+
+Thin Python binding over the C ABI in ``include/qdt.h`` (``libqdt.so``, built in-tree for
+sm_100a).  The functions below carry the C names and only marshal arguments: numpy arrays
+are passed as host pointers, CUDA torch tensors as device pointers (``mem_device = 1``).
+Every step of the solve runs in the library's CUDA kernels; there is no CPU fallback -- if
+``libqdt.so`` is missing or no GPU is present the calls raise.
+
+    ctx = qdt_init(device=0)
+    F = qdt_build_probes(ctx, alpha2, M)
+    out = qdt_solve(ctx, F, P, gamma=1e-5, tol=0.0, iters=100)   # dict(theta, trace, kkt, info)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libqdt.so")
+
+QDT_STEP_SQS, QDT_STEP_LIPSCHITZ = 0, 1
+STATUS = {0: "QDT_OK", 1: "QDT_ERR_INVALID_ARG", 2: "QDT_ERR_UNSORTED", 3: "QDT_ERR_NONFINITE",
+          4: "QDT_ERR_OOM", 5: "QDT_ERR_CUDA", 6: "QDT_ERR_NCCL", 7: "QDT_ERR_TRUNCATED",
+          8: "QDT_ERR_STATE"}
+
+# every symbol include/qdt.h declares (checked by tests/test_abi.py)
+ABI_SYMBOLS = ["qdt_init", "qdt_finalize", "qdt_last_error", "qdt_build_probes", "qdt_probes_free",
+               "qdt_probes_export", "qdt_solve", "qdt_objective", "qdt_residual", "qdt_gradient",
+               "qdt_step", "qdt_project_rows", "qdt_step_setup", "qdt_profile_enable",
+               "qdt_profile_get", "qdt_launch_count"]
+
+
+class QdtError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class InitOpts(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int32), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
+                ("nccl_unique_id", ctypes.c_void_p), ("cuda_stream", ctypes.c_void_p)]
+
+
+class ProbeOpts(ctypes.Structure):
+    _fields_ = [("c_sigma", ctypes.c_double), ("margin", ctypes.c_int32),
+                ("strict_mass", ctypes.c_int32)]
+
+
+class SolveOpts(ctypes.Structure):
+    _fields_ = [("step", ctypes.c_int32), ("accel", ctypes.c_int32), ("theta0", ctypes.c_void_p),
+                ("check_every", ctypes.c_int32), ("kkt_every", ctypes.c_int32),
+                ("mem_device", ctypes.c_int32), ("gather_theta", ctypes.c_int32),
+                ("use_graph", ctypes.c_int32)]
+
+
+class SolveInfo(ctypes.Structure):
+    _fields_ = [("iters_done", ctypes.c_int64), ("converged", ctypes.c_int32),
+                ("kkt0", ctypes.c_double), ("kkt", ctypes.c_double), ("kkt_paper", ctypes.c_double),
+                ("f_final", ctypes.c_double), ("step_scalar", ctypes.c_double),
+                ("k_begin", ctypes.c_int64), ("k_end", ctypes.c_int64), ("nnz", ctypes.c_int64),
+                ("min_row_mass", ctypes.c_double), ("uncovered_rows", ctypes.c_int64)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libqdt.so (raises if it is missing: there is no fallback path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(path)
+    vp, i32, i64, f64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+    P = ctypes.POINTER
+    L.qdt_init.argtypes = [P(vp), P(InitOpts)]
+    L.qdt_finalize.argtypes = [vp]
+    L.qdt_last_error.argtypes = [vp]
+    L.qdt_last_error.restype = ctypes.c_char_p
+    L.qdt_build_probes.argtypes = [vp, vp, i64, i64, P(ProbeOpts), P(vp)]
+    L.qdt_probes_free.argtypes = [vp]
+    L.qdt_probes_export.argtypes = [vp, vp, P(i64), P(i64), P(i64), vp, vp, vp]
+    L.qdt_solve.argtypes = [vp, vp, vp, i64, f64, f64, i64, P(SolveOpts), vp, vp, vp, P(SolveInfo)]
+    L.qdt_objective.argtypes = [vp, vp, vp, vp, i64, f64, i32, P(f64), P(f64)]
+    L.qdt_residual.argtypes = [vp, vp, vp, vp, i64, vp]
+    L.qdt_gradient.argtypes = [vp, vp, vp, vp, i64, f64, vp]
+    L.qdt_step.argtypes = [vp, vp, vp, vp, i64, f64, i32, vp]
+    L.qdt_project_rows.argtypes = [vp, vp, i64, i64, vp]
+    L.qdt_step_setup.argtypes = [vp, vp, f64, i32, vp, P(f64)]
+    L.qdt_profile_enable.argtypes = [vp, i32]
+    L.qdt_profile_get.argtypes = [vp, ctypes.c_char_p, P(i64), P(f64)]
+    L.qdt_launch_count.argtypes = [vp, P(i64)]
+    for s in ABI_SYMBOLS:
+        if s != "qdt_last_error":
+            getattr(L, s).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _check(ctx, status):
+    if status != 0:
+        msg = load_library().qdt_last_error(ctx.ptr if isinstance(ctx, Context) else ctx)
+        raise QdtError(status, (msg or b"").decode())
+
+
+class Context:
+    def __init__(self, ptr):
+        self.ptr = ptr
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and _lib is not None:
+            _lib.qdt_finalize(self.ptr)
+            self.ptr = None
+
+
+class Probes:
+    def __init__(self, ctx, ptr, D, M):
+        self.ctx, self.ptr, self.D, self.M = ctx, ptr, D, M
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and _lib is not None:
+            _lib.qdt_probes_free(self.ptr)
+            self.ptr = None
+
+
+def _host(a, dtype=np.float64):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+def _is_cuda_tensor(x):
+    return hasattr(x, "is_cuda") and x.is_cuda
+
+
+def qdt_init(device: int = 0, rank: int = 0, nranks: int = 1, nccl_unique_id: bytes | None = None,
+             cuda_stream: int | None = None) -> Context:
+    L = load_library()
+    uid = ctypes.create_string_buffer(nccl_unique_id, 128) if nccl_unique_id else None
+    o = InitOpts(device, rank, nranks, ctypes.cast(uid, ctypes.c_void_p) if uid else None,
+                 cuda_stream)
+    p = ctypes.c_void_p()
+    st = L.qdt_init(ctypes.byref(p), ctypes.byref(o))
+    if st != 0:
+        raise QdtError(st, (L.qdt_last_error(None) or b"").decode())
+    return Context(p)
+
+
+def qdt_finalize(ctx: Context):
+    if ctx.ptr:
+        _check(ctx, load_library().qdt_finalize(ctx.ptr))
+        ctx.ptr = None
+
+
+def qdt_build_probes(ctx: Context, alpha2, M: int, c_sigma: float = 6.0, margin: int = 16,
+                     strict_mass: bool = False) -> Probes:
+    a = _host(alpha2)
+    o = ProbeOpts(c_sigma, margin, int(strict_mass))
+    p = ctypes.c_void_p()
+    _check(ctx, load_library().qdt_build_probes(ctx.ptr, a.ctypes.data, a.shape[0], int(M),
+                                                ctypes.byref(o), ctypes.byref(p)))
+    return Probes(ctx, p, a.shape[0], int(M))
+
+
+def qdt_probes_export(ctx: Context, F: Probes, values: bool = True):
+    L = load_library()
+    nnz, kb, ke = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    _check(ctx, L.qdt_probes_export(ctx.ptr, F.ptr, ctypes.byref(nnz), ctypes.byref(kb),
+                                    ctypes.byref(ke), None, None, None))
+    lo = np.zeros(F.D, np.int64)
+    ln = np.zeros(F.D, np.int64)
+    val = np.zeros(max(1, nnz.value), np.float64)
+    _check(ctx, L.qdt_probes_export(ctx.ptr, F.ptr, None, None, None, lo.ctypes.data,
+                                    ln.ctypes.data, val.ctypes.data if values else None))
+    return dict(lo=lo, len=ln, val=val[:nnz.value], nnz=nnz.value, k_begin=kb.value,
+                k_end=ke.value)
+
+
+def qdt_solve(ctx: Context, F: Probes, P, gamma: float, tol: float = 0.0, iters: int = 100,
+              step: int = QDT_STEP_SQS, accel: bool = False, theta0=None, check_every: int = 16,
+              kkt_every: int = 1, gather_theta: bool = False, use_graph: bool = True,
+              theta_out=None):
+    """Projected-gradient solve.  P: numpy (host) or CUDA tensor (device, then theta0 and
+    theta_out are device tensors too).  Returns dict(theta, trace, kkt, info)."""
+    L = load_library()
+    dev = _is_cuda_tensor(P)
+    if dev:
+        import torch
+        D, N = P.shape
+        Pp = P.contiguous()
+        rows = F.M
+        if theta_out is None:
+            theta_out = torch.empty((rows, N), dtype=torch.float64, device=P.device)
+        t0 = theta0.contiguous() if theta0 is not None else None
+        p_ptr, out_ptr = Pp.data_ptr(), theta_out.data_ptr()
+        t0_ptr = t0.data_ptr() if t0 is not None else None
+    else:
+        Pp = _host(P)
+        D, N = Pp.shape
+        if theta_out is None:
+            theta_out = np.empty((F.M, N))
+        t0 = _host(theta0) if theta0 is not None else None
+        p_ptr, out_ptr = Pp.ctypes.data, theta_out.ctypes.data
+        t0_ptr = t0.ctypes.data if t0 is not None else None
+    trace = np.full(iters + 1, np.nan)
+    kkt = np.full(iters + 1, np.nan)
+    o = SolveOpts(step, int(accel), t0_ptr, check_every, kkt_every, int(dev), int(gather_theta),
+                  int(use_graph))
+    info = SolveInfo()
+    _check(ctx, L.qdt_solve(ctx.ptr, F.ptr, p_ptr, N, float(gamma), float(tol), int(iters),
+                            ctypes.byref(o), out_ptr, trace.ctypes.data, kkt.ctypes.data,
+                            ctypes.byref(info)))
+    k = info.iters_done
+    return dict(theta=theta_out, trace=trace[:k + 1], kkt=kkt[:k + 1], info=info.as_dict())
+
+
+def qdt_objective(ctx: Context, F: Probes, P, theta, gamma: float):
+    L = load_library()
+    dev = _is_cuda_tensor(P)
+    if dev:
+        Pp, Tp = P.contiguous(), theta.contiguous()
+        pp, tp, N = Pp.data_ptr(), Tp.data_ptr(), Pp.shape[1]
+    else:
+        Pp, Tp = _host(P), _host(theta)
+        pp, tp, N = Pp.ctypes.data, Tp.ctypes.data, Pp.shape[1]
+    f, r = ctypes.c_double(), ctypes.c_double()
+    _check(ctx, L.qdt_objective(ctx.ptr, F.ptr, pp, tp, N, float(gamma), int(dev), ctypes.byref(f),
+                                ctypes.byref(r)))
+    return f.value, r.value
+
+
+def qdt_residual(ctx: Context, F: Probes, theta, P=None):
+    Th = _host(theta)
+    N = Th.shape[1]
+    Pp = _host(P) if P is not None else None
+    R = np.empty((F.D, N))
+    _check(ctx, load_library().qdt_residual(ctx.ptr, F.ptr, Th.ctypes.data,
+                                            Pp.ctypes.data if Pp is not None else None, N,
+                                            R.ctypes.data))
+    return R
+
+
+def qdt_gradient(ctx: Context, F: Probes, R, theta, gamma: float):
+    Rr, Th = _host(R), _host(theta)
+    N = Th.shape[1]
+    G = np.empty((F.M, N))
+    _check(ctx, load_library().qdt_gradient(ctx.ptr, F.ptr, Rr.ctypes.data, Th.ctypes.data, N,
+                                            float(gamma), G.ctypes.data))
+    return G
+
+
+def qdt_step(ctx: Context, F: Probes, P, theta, gamma: float, step: int = QDT_STEP_SQS):
+    Pp, Th = _host(P), _host(theta)
+    out = np.empty_like(Th)
+    _check(ctx, load_library().qdt_step(ctx.ptr, F.ptr, Pp.ctypes.data, Th.ctypes.data,
+                                        Th.shape[1], float(gamma), int(step), out.ctypes.data))
+    return out
+
+
+def qdt_project_rows(ctx: Context, X):
+    Xx = _host(X)
+    Y = np.empty_like(Xx)
+    _check(ctx, load_library().qdt_project_rows(ctx.ptr, Xx.ctypes.data, Xx.shape[0],
+                                                Xx.shape[1], Y.ctypes.data))
+    return Y
+
+
+def qdt_step_setup(ctx: Context, F: Probes, gamma: float, k_pow: int = 100, weights: bool = True,
+                   power: bool = True):
+    w = np.empty(F.M) if weights else None
+    rho = ctypes.c_double()
+    _check(ctx, load_library().qdt_step_setup(ctx.ptr, F.ptr, float(gamma), int(k_pow),
+                                              w.ctypes.data if weights else None,
+                                              ctypes.byref(rho) if power else None))
+    return w, (rho.value if power else None)
+
+
+def qdt_profile_enable(ctx: Context, enable: bool = True):
+    _check(ctx, load_library().qdt_profile_enable(ctx.ptr, int(enable)))
+
+
+def qdt_profile_get(ctx: Context, kernel: str):
+    c, ms = ctypes.c_int64(), ctypes.c_double()
+    _check(ctx, load_library().qdt_profile_get(ctx.ptr, kernel.encode(), ctypes.byref(c),
+                                               ctypes.byref(ms)))
+    return c.value, ms.value
+
+
+def qdt_launch_count(ctx: Context) -> int:
+    c = ctypes.c_int64()
+    _check(ctx, load_library().qdt_launch_count(ctx.ptr, ctypes.byref(c)))
+    return c.value

@@ -1,0 +1,1284 @@
+// qdt_api.cu -- host runtime behind include/qdt.h: context, probe handle, Fock-axis shard
+// and tile planner, memory plan, CUDA-graph iteration loop, NCCL exchange (multi-GPU).
+//
+// Every numerical step runs in the kernels of qdt_kernels.cu; this file only validates,
+// plans, allocates, launches and copies.  There is no CPU compute path.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/qdt.h"
+#include "qdt_internal.h"
+
+using namespace qdt;
+
+// ------------------------------------------------------------------------------ NCCL (dlopen)
+// NCCL is loaded at run time (libnccl.so.2, the copy torch already mapped when present) so
+// that single-GPU use needs no NCCL at all.  Only the few entry points used are declared.
+namespace {
+typedef void *nccl_comm_t;
+typedef struct { char internal[128]; } nccl_uid_t;
+typedef int nccl_result_t;
+enum { NCCL_FLOAT64 = 8, NCCL_SUM = 0 };
+struct NcclApi {
+    void *h = nullptr;
+    nccl_result_t (*commInitRank)(nccl_comm_t *, int, nccl_uid_t, int) = nullptr;
+    nccl_result_t (*commDestroy)(nccl_comm_t) = nullptr;
+    nccl_result_t (*allReduce)(const void *, void *, size_t, int, int, nccl_comm_t,
+                               cudaStream_t) = nullptr;
+    nccl_result_t (*send)(const void *, size_t, int, int, nccl_comm_t, cudaStream_t) = nullptr;
+    nccl_result_t (*recv)(void *, size_t, int, int, nccl_comm_t, cudaStream_t) = nullptr;
+    nccl_result_t (*groupStart)() = nullptr;
+    nccl_result_t (*groupEnd)() = nullptr;
+    const char *(*getErrorString)(nccl_result_t) = nullptr;
+    bool load(std::string &err)
+    {
+        if (h) return true;
+        const char *names[] = {"libnccl.so.2", "libnccl.so"};
+        for (const char *n : names)
+            if ((h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+        if (!h) {
+            err = "NCCL not found (dlopen libnccl.so.2 failed)";
+            return false;
+        }
+#define QDT_SYM(f, s)                                              \
+    *(void **)(&f) = dlsym(h, s);                                  \
+    if (!f) {                                                      \
+        err = std::string("NCCL symbol missing: ") + s;            \
+        return false;                                              \
+    }
+        QDT_SYM(commInitRank, "ncclCommInitRank");
+        QDT_SYM(commDestroy, "ncclCommDestroy");
+        QDT_SYM(allReduce, "ncclAllReduce");
+        QDT_SYM(send, "ncclSend");
+        QDT_SYM(recv, "ncclRecv");
+        QDT_SYM(groupStart, "ncclGroupStart");
+        QDT_SYM(groupEnd, "ncclGroupEnd");
+        QDT_SYM(getErrorString, "ncclGetErrorString");
+#undef QDT_SYM
+        return true;
+    }
+};
+NcclApi g_nccl;
+}  // namespace
+
+// ------------------------------------------------------------------------------ structures
+struct DevBuf {
+    void *p = nullptr;
+    size_t n = 0;
+};
+
+struct qdt_ctx {
+    int device = 0, rank = 0, nranks = 1;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    nccl_comm_t comm = nullptr;
+    std::string err;
+    bool profiling = false;
+    std::map<std::string, std::pair<int64_t, double>> prof;
+    std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+    int64_t launches = 0;
+    std::map<std::string, DevBuf> ws;  // grow-only workspace
+    int nblkR = 148 * 4;
+};
+
+struct Plan {
+    int N = 0, T = 0, CG = 0, RG = 0, TC = 0, KC = 0, KR = 0, TF = 0, nthr = 0;
+    int ntiles = 0;
+    int32_t *d_tile_dA = nullptr, *d_tile_dB = nullptr;
+    int nbunits = 0;
+    BwdUnit *d_bunits = nullptr;
+    int64_t nslots = 0;
+    int nfunits = 0;
+    FwdUnit *d_funits = nullptr;
+    int64_t nrpart = 0;
+    int64_t *d_red_beg = nullptr, *d_red_rows = nullptr;
+    ~Plan()
+    {
+        cudaFree(d_tile_dA);
+        cudaFree(d_tile_dB);
+        cudaFree(d_bunits);
+        cudaFree(d_funits);
+        cudaFree(d_red_beg);
+        cudaFree(d_red_rows);
+    }
+};
+
+struct qdt_probes {
+    qdt_ctx *ctx = nullptr;
+    int64_t D = 0, M = 0, kb = 0, ke = 0, Ml = 0;
+    double c_sigma = 6.0;
+    int margin = 16;
+    double *d_alpha2 = nullptr;
+    int32_t *d_lo = nullptr, *d_len = nullptr;
+    int64_t *d_off = nullptr;
+    double *d_val = nullptr;
+    int64_t nnz = 0;
+    std::vector<int32_t> lo_g, hi_g, lo_l, len_l;
+    std::vector<int64_t> off;
+    double min_row_mass = 1.0;
+    int64_t uncovered = 0;
+    std::map<int, std::unique_ptr<Plan>> plans;
+    Band band() const { return Band{d_lo, d_len, d_off, d_val}; }
+    ~qdt_probes()
+    {
+        cudaFree(d_alpha2);
+        cudaFree(d_lo);
+        cudaFree(d_len);
+        cudaFree(d_off);
+        cudaFree(d_val);
+    }
+};
+
+// ------------------------------------------------------------------------------ errors
+static thread_local std::string tl_err;
+
+static qdt_status fail(qdt_ctx *ctx, qdt_status st, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    tl_err = buf;
+    if (ctx) ctx->err = buf;
+    return st;
+}
+
+#define CK(call)                                                                                \
+    do {                                                                                        \
+        cudaError_t e_ = (call);                                                                \
+        if (e_ != cudaSuccess)                                                                  \
+            return fail(ctx, e_ == cudaErrorMemoryAllocation ? QDT_ERR_OOM : QDT_ERR_CUDA,      \
+                        "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__);   \
+    } while (0)
+
+#define CKN(call)                                                                               \
+    do {                                                                                        \
+        nccl_result_t r_ = (call);                                                              \
+        if (r_ != 0)                                                                            \
+            return fail(ctx, QDT_ERR_NCCL, "%s: %s", #call, g_nccl.getErrorString(r_));         \
+    } while (0)
+
+#define CKS(call)                            \
+    do {                                     \
+        qdt_status s_ = (call);              \
+        if (s_ != QDT_OK) return s_;         \
+    } while (0)
+
+template <class T>
+static qdt_status ws_get(qdt_ctx *ctx, const char *name, size_t count, T **out)
+{
+    DevBuf &b = ctx->ws[name];
+    size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+    if (b.n < bytes) {
+        if (b.p) cudaFree(b.p);
+        b.p = nullptr;
+        b.n = 0;
+        cudaError_t e = cudaMalloc(&b.p, bytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(ctx, QDT_ERR_OOM, "workspace '%s': cudaMalloc(%zu) failed: %s", name, bytes,
+                        cudaGetErrorString(e));
+        }
+        b.n = bytes;
+    }
+    *out = (T *)b.p;
+    return QDT_OK;
+}
+
+// kernel launch bookkeeping: counts launches; in profiling mode brackets with events
+template <class F>
+static cudaError_t run_k(qdt_ctx *ctx, const char *name, int nlaunch, F &&f)
+{
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (ctx->profiling) {
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, ctx->stream);
+    }
+    cudaError_t e = f();
+    ctx->launches += nlaunch;
+    if (ctx->profiling) {
+        cudaEventRecord(b, ctx->stream);
+        ctx->pending.push_back({name, {a, b}});
+    }
+    return e;
+}
+
+static void flush_profile(qdt_ctx *ctx)
+{
+    if (ctx->pending.empty()) return;
+    cudaStreamSynchronize(ctx->stream);
+    for (auto &p : ctx->pending) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, p.second.first, p.second.second);
+        auto &slot = ctx->prof[p.first];
+        slot.first += 1;
+        slot.second += ms;
+        cudaEventDestroy(p.second.first);
+        cudaEventDestroy(p.second.second);
+    }
+    ctx->pending.clear();
+}
+
+// ------------------------------------------------------------------------------ context
+extern "C" qdt_status qdt_init(qdt_ctx **out, const qdt_init_opts *o)
+{
+    qdt_ctx *ctx = nullptr;
+    if (!out) return fail(nullptr, QDT_ERR_INVALID_ARG, "qdt_init: ctx out-pointer is NULL");
+    *out = nullptr;
+    int dev = o ? o->device : 0;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(nullptr, QDT_ERR_CUDA, "qdt_init: no CUDA device (%s)", cudaGetErrorString(e));
+    }
+    if (dev < 0 || dev >= ndev)
+        return fail(nullptr, QDT_ERR_INVALID_ARG, "qdt_init: device %d out of range [0,%d)", dev,
+                    ndev);
+    std::unique_ptr<qdt_ctx> c(new qdt_ctx());
+    ctx = c.get();
+    c->device = dev;
+    c->rank = o ? o->rank : 0;
+    c->nranks = o ? std::max(1, o->nranks) : 1;
+    if (c->rank < 0 || c->rank >= c->nranks)
+        return fail(nullptr, QDT_ERR_INVALID_ARG, "qdt_init: rank %d not in [0,%d)", c->rank,
+                    c->nranks);
+    CK(cudaSetDevice(dev));
+    if (o && o->cuda_stream) {
+        c->stream = (cudaStream_t)o->cuda_stream;
+    } else {
+        CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+    }
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    c->nblkR = nsm * 4;
+    CK(prepare_kernels());
+    if (c->nranks > 1) {
+        if (!o->nccl_unique_id)
+            return fail(nullptr, QDT_ERR_INVALID_ARG, "qdt_init: nranks > 1 needs nccl_unique_id");
+        std::string err;
+        if (!g_nccl.load(err)) return fail(nullptr, QDT_ERR_NCCL, "qdt_init: %s", err.c_str());
+        nccl_uid_t uid;
+        memcpy(&uid, o->nccl_unique_id, sizeof uid);
+        nccl_result_t r = g_nccl.commInitRank(&c->comm, c->nranks, uid, c->rank);
+        if (r != 0)
+            return fail(nullptr, QDT_ERR_NCCL, "ncclCommInitRank: %s", g_nccl.getErrorString(r));
+    }
+    *out = c.release();
+    return QDT_OK;
+}
+
+extern "C" qdt_status qdt_finalize(qdt_ctx *ctx)
+{
+    if (!ctx) return QDT_OK;
+    cudaSetDevice(ctx->device);
+    flush_profile(ctx);
+    for (auto &kv : ctx->ws) cudaFree(kv.second.p);
+    if (ctx->comm) g_nccl.commDestroy(ctx->comm);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return QDT_OK;
+}
+
+extern "C" const char *qdt_last_error(const qdt_ctx *ctx)
+{
+    if (ctx && !ctx->err.empty()) return ctx->err.c_str();
+    return tl_err.c_str();
+}
+
+extern "C" qdt_status qdt_profile_enable(qdt_ctx *ctx, int32_t enable)
+{
+    if (!ctx) return fail(nullptr, QDT_ERR_INVALID_ARG, "ctx is NULL");
+    flush_profile(ctx);
+    ctx->profiling = enable != 0;
+    if (enable) ctx->prof.clear();
+    return QDT_OK;
+}
+
+extern "C" qdt_status qdt_profile_get(qdt_ctx *ctx, const char *kernel, int64_t *count,
+                                      double *total_ms)
+{
+    if (!ctx || !kernel) return fail(ctx, QDT_ERR_INVALID_ARG, "ctx/kernel is NULL");
+    flush_profile(ctx);
+    auto it = ctx->prof.find(kernel);
+    if (count) *count = it == ctx->prof.end() ? 0 : it->second.first;
+    if (total_ms) *total_ms = it == ctx->prof.end() ? 0.0 : it->second.second;
+    return QDT_OK;
+}
+
+extern "C" qdt_status qdt_launch_count(qdt_ctx *ctx, int64_t *count)
+{
+    if (!ctx || !count) return fail(ctx, QDT_ERR_INVALID_ARG, "ctx/count is NULL");
+    *count = ctx->launches;
+    return QDT_OK;
+}
+
+// ------------------------------------------------------------------------------ collectives
+static qdt_status allreduce(qdt_ctx *ctx, double *buf, size_t n, const char *name)
+{
+    if (ctx->nranks == 1 || n == 0) return QDT_OK;
+    nccl_result_t r = 0;
+    cudaError_t e = run_k(ctx, name, 1, [&]() {
+        r = g_nccl.allReduce(buf, buf, n, NCCL_FLOAT64, NCCL_SUM, ctx->comm, ctx->stream);
+        return cudaSuccess;
+    });
+    (void)e;
+    if (r != 0) return fail(ctx, QDT_ERR_NCCL, "ncclAllReduce(%s): %s", name, g_nccl.getErrorString(r));
+    return QDT_OK;
+}
+
+// ------------------------------------------------------------------------------ planner
+// Fock-axis shard cut (multi-GPU): contiguous [k_g, k_{g+1}) at equal prefix sums of the
+// per-row cost c(k) = 16 + 0.7 cov(k) (bytes-equivalent per column).
+static void shard_bounds(const std::vector<int32_t> &lo, const std::vector<int32_t> &hi, int64_t M,
+                         int nranks, std::vector<int64_t> &cuts)
+{
+    std::vector<int64_t> diff(M + 1, 0);
+    for (size_t d = 0; d < lo.size(); d++) {
+        diff[lo[d]] += 1;
+        diff[(int64_t)hi[d] + 1] -= 1;
+    }
+    std::vector<double> pre(M + 1, 0.0);
+    int64_t cov = 0;
+    for (int64_t k = 0; k < M; k++) {
+        cov += diff[k];
+        pre[k + 1] = pre[k] + 16.0 + 0.7 * (double)cov;
+    }
+    cuts.assign(nranks + 1, 0);
+    cuts[nranks] = M;
+    for (int g = 1; g < nranks; g++) {
+        double target = pre[M] * g / nranks;
+        int64_t k = std::lower_bound(pre.begin(), pre.end(), target) - pre.begin();
+        cuts[g] = std::min<int64_t>(std::max<int64_t>(k, cuts[g - 1] + 1), M);
+    }
+    for (int g = 1; g <= nranks; g++) cuts[g] = std::max(cuts[g], cuts[g - 1]);
+}
+
+static qdt_status build_plan(qdt_ctx *ctx, qdt_probes *p, int N, Plan **out)
+{
+    auto it = p->plans.find(N);
+    if (it != p->plans.end()) {
+        *out = it->second.get();
+        return QDT_OK;
+    }
+    std::unique_ptr<Plan> pl(new Plan());
+    pl->N = N;
+    pl->nthr = bwd_threads(N, &pl->CG, &pl->RG, &pl->TC);
+    if (pl->CG * pl->RG > 1024)
+        return fail(ctx, QDT_ERR_INVALID_ARG, "N = %d too large for this build (max 8192)", N);
+    pl->T = pl->RG * TR;
+    pl->KC = std::min(32, std::max(2, 800 / N));
+    pl->KR = std::min(32, std::max(4, 2048 / N));
+    pl->TF = 256;
+    const int64_t Ml = p->Ml, kb = p->kb, D = p->D;
+    const int T = pl->T, TF = pl->TF, KP = pl->RG * TR;
+
+    // ---- bwd tiles and windows
+    const int ntiles = (int)((Ml + T - 1) / T);
+    pl->ntiles = ntiles;
+    std::vector<int32_t> dA(ntiles, INT32_MAX), dB(ntiles, 0);
+    for (int64_t d = 0; d < D; d++) {
+        if (p->len_l[d] == 0) continue;
+        int64_t a = (p->lo_l[d] - kb) / T, b = (p->lo_l[d] + p->len_l[d] - 1 - kb) / T;
+        for (int64_t t = a; t <= b; t++) {
+            dA[t] = std::min<int32_t>(dA[t], (int32_t)d);
+            dB[t] = std::max<int32_t>(dB[t], (int32_t)d + 1);
+        }
+    }
+    for (int t = 0; t < ntiles; t++)
+        if (dA[t] == INT32_MAX) dA[t] = dB[t] = 0;
+    // split cap: windows wider than Wcap probes are split along the probe axis
+    const int Wcap = std::max(64, 4 * pl->KC);
+    std::vector<BwdUnit> bu;
+    bu.reserve(ntiles + 64);
+    int64_t slot = 0;
+    for (int t = 0; t < ntiles; t++) {
+        int W = dB[t] - dA[t];
+        int ns = std::max(1, (W + Wcap - 1) / Wcap);
+        int chunk = ns > 1 ? (W + ns - 1) / ns : W;
+        for (int s = 0; s < ns; s++) {
+            BwdUnit u;
+            u.k0 = t * T;
+            u.k1 = (int32_t)std::min<int64_t>(Ml, (int64_t)(t + 1) * T);
+            u.p0 = dA[t] + s * chunk;
+            u.p1 = std::min(dB[t], u.p0 + chunk);
+            if (u.p1 < u.p0) u.p1 = u.p0;
+            u.tile = t;
+            u.slot = s;
+            u.nsplit = ns;
+            u.pad = 0;
+            u.slot_base = ns > 1 ? slot : 0;
+            bu.push_back(u);
+        }
+        if (ns > 1) slot += ns;
+    }
+    pl->nslots = slot;
+    // heavy (widest probe range) units first
+    std::stable_sort(bu.begin(), bu.end(),
+                     [](const BwdUnit &x, const BwdUnit &y) { return (x.p1 - x.p0) > (y.p1 - y.p0); });
+    pl->nbunits = (int)bu.size();
+
+    // ---- fwd tiles, probe groups, per-probe partial-row lists
+    const int nft = (int)((Ml + TF - 1) / TF);
+    std::vector<int32_t> fA(nft, INT32_MAX), fB(nft, 0);
+    for (int64_t d = 0; d < D; d++) {
+        if (p->len_l[d] == 0) continue;
+        int64_t a = (p->lo_l[d] - kb) / TF, b = (p->lo_l[d] + p->len_l[d] - 1 - kb) / TF;
+        for (int64_t t = a; t <= b; t++) {
+            fA[t] = std::min<int32_t>(fA[t], (int32_t)d);
+            fB[t] = std::max<int32_t>(fB[t], (int32_t)d + 1);
+        }
+    }
+    std::vector<FwdUnit> fu;
+    std::vector<std::vector<int64_t>> lists(D);
+    int64_t poff = 0;
+    for (int t = 0; t < nft; t++) {
+        if (fA[t] == INT32_MAX) continue;
+        const int64_t r0 = (int64_t)t * TF, r1 = std::min<int64_t>(Ml, r0 + TF);
+        for (int g0 = fA[t]; g0 < fB[t]; g0 += KP) {
+            const int g1 = std::min(fB[t], g0 + KP);
+            int64_t k0 = INT64_MAX, k1 = -1;
+            for (int d = g0; d < g1; d++) {
+                if (p->len_l[d] == 0) continue;
+                int64_t a = std::max<int64_t>(r0, p->lo_l[d] - kb);
+                int64_t b = std::min<int64_t>(r1, p->lo_l[d] + p->len_l[d] - kb);
+                if (a >= b) continue;
+                k0 = std::min(k0, a);
+                k1 = std::max(k1, b);
+                lists[d].push_back(poff + (d - g0));
+            }
+            if (k1 < 0) continue;
+            FwdUnit u;
+            u.k0 = (int32_t)k0;
+            u.k1 = (int32_t)k1;
+            u.p0 = g0;
+            u.p1 = g1;
+            u.poff = poff;
+            fu.push_back(u);
+            poff += g1 - g0;
+        }
+    }
+    pl->nrpart = poff;
+    std::stable_sort(fu.begin(), fu.end(), [](const FwdUnit &x, const FwdUnit &y) {
+        return (int64_t)(x.p1 - x.p0) * (x.k1 - x.k0) > (int64_t)(y.p1 - y.p0) * (y.k1 - y.k0);
+    });
+    pl->nfunits = (int)fu.size();
+    std::vector<int64_t> red_beg(D + 1, 0), red_rows;
+    for (int64_t d = 0; d < D; d++) red_beg[d + 1] = red_beg[d] + (int64_t)lists[d].size();
+    red_rows.reserve(red_beg[D]);
+    for (int64_t d = 0; d < D; d++) red_rows.insert(red_rows.end(), lists[d].begin(), lists[d].end());
+
+    // ---- upload
+    CK(cudaMalloc(&pl->d_tile_dA, sizeof(int32_t) * std::max(1, ntiles)));
+    CK(cudaMalloc(&pl->d_tile_dB, sizeof(int32_t) * std::max(1, ntiles)));
+    CK(cudaMalloc(&pl->d_bunits, sizeof(BwdUnit) * std::max<size_t>(1, bu.size())));
+    CK(cudaMalloc(&pl->d_funits, sizeof(FwdUnit) * std::max<size_t>(1, fu.size())));
+    CK(cudaMalloc(&pl->d_red_beg, sizeof(int64_t) * (D + 1)));
+    CK(cudaMalloc(&pl->d_red_rows, sizeof(int64_t) * std::max<size_t>(1, red_rows.size())));
+    cudaStream_t s = ctx->stream;
+    CK(cudaMemcpyAsync(pl->d_tile_dA, dA.data(), sizeof(int32_t) * ntiles, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(pl->d_tile_dB, dB.data(), sizeof(int32_t) * ntiles, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(pl->d_bunits, bu.data(), sizeof(BwdUnit) * bu.size(), cudaMemcpyHostToDevice, s));
+    if (!fu.empty())
+        CK(cudaMemcpyAsync(pl->d_funits, fu.data(), sizeof(FwdUnit) * fu.size(), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(pl->d_red_beg, red_beg.data(), sizeof(int64_t) * (D + 1), cudaMemcpyHostToDevice, s));
+    if (!red_rows.empty())
+        CK(cudaMemcpyAsync(pl->d_red_rows, red_rows.data(), sizeof(int64_t) * red_rows.size(),
+                           cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    *out = pl.get();
+    p->plans[N] = std::move(pl);
+    return QDT_OK;
+}
+
+// ------------------------------------------------------------------------------ probes
+extern "C" qdt_status qdt_build_probes(qdt_ctx *ctx, const double *alpha2, int64_t D, int64_t M,
+                                       const qdt_probe_opts *o, qdt_probes **out)
+{
+    if (!ctx) return fail(nullptr, QDT_ERR_INVALID_ARG, "qdt_build_probes: ctx is NULL");
+    if (!out || !alpha2) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_build_probes: NULL pointer");
+    *out = nullptr;
+    if (D < 1) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_build_probes: D = %lld < 1", (long long)D);
+    if (M < 1 || M > INT32_MAX - 64)
+        return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_build_probes: M = %lld out of range", (long long)M);
+    if (D > INT32_MAX) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_build_probes: D too large");
+    for (int64_t d = 0; d < D; d++) {
+        if (!isfinite(alpha2[d]) || alpha2[d] < 0.0)
+            return fail(ctx, QDT_ERR_INVALID_ARG, "alpha2[%lld] = %g is not finite and >= 0",
+                        (long long)d, alpha2[d]);
+        if (d > 0 && alpha2[d] < alpha2[d - 1])
+            return fail(ctx, QDT_ERR_UNSORTED, "alpha2 not nondecreasing at d = %lld", (long long)d);
+    }
+    double c_sigma = o ? o->c_sigma : 6.0;
+    int margin = o ? o->margin : 16;
+    if (!(c_sigma > 0.0) || !isfinite(c_sigma) || margin < 0)
+        return fail(ctx, QDT_ERR_INVALID_ARG, "probe opts: c_sigma must be > 0, margin >= 0");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    std::unique_ptr<qdt_probes> p(new qdt_probes());
+    p->ctx = ctx;
+    p->D = D;
+    p->M = M;
+    p->c_sigma = c_sigma;
+    p->margin = margin;
+    // S0 (a): band edges on the device
+    CK(cudaMalloc(&p->d_alpha2, sizeof(double) * D));
+    CK(cudaMemcpyAsync(p->d_alpha2, alpha2, sizeof(double) * D, cudaMemcpyHostToDevice, s));
+    int32_t *d_hi = nullptr;
+    CK(cudaMalloc(&p->d_lo, sizeof(int32_t) * D));
+    CK(cudaMalloc(&d_hi, sizeof(int32_t) * D));
+    CK(run_k(ctx, "probe_edges", 1,
+             [&]() { return launch_probe_edges(p->d_alpha2, D, M, c_sigma, margin, p->d_lo, d_hi, s); }));
+    p->lo_g.resize(D);
+    p->hi_g.resize(D);
+    CK(cudaMemcpyAsync(p->lo_g.data(), p->d_lo, sizeof(int32_t) * D, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(p->hi_g.data(), d_hi, sizeof(int32_t) * D, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    cudaFree(d_hi);
+    if (o && o->strict_mass) {
+        for (int64_t d = 0; d < D; d++) {
+            double mu = alpha2[d];
+            if (mu > 0.0 && p->hi_g[d] == M - 1 && mu + c_sigma * sqrt(mu) > (double)(M - 1))
+                return fail(ctx, QDT_ERR_TRUNCATED,
+                            "probe %lld (|alpha|^2 = %g) is clipped by the cutoff M = %lld",
+                            (long long)d, mu, (long long)M);
+        }
+    }
+    // shard the Fock axis
+    std::vector<int64_t> cuts;
+    shard_bounds(p->lo_g, p->hi_g, M, ctx->nranks, cuts);
+    p->kb = cuts[ctx->rank];
+    p->ke = cuts[ctx->rank + 1];
+    p->Ml = p->ke - p->kb;
+    if (p->Ml < 1) return fail(ctx, QDT_ERR_INVALID_ARG, "rank %d owns no Fock rows (M too small)", ctx->rank);
+    p->lo_l.resize(D);
+    p->len_l.resize(D);
+    p->off.resize(D + 1);
+    p->off[0] = 0;
+    for (int64_t d = 0; d < D; d++) {
+        int64_t a = std::max<int64_t>(p->lo_g[d], p->kb), b = std::min<int64_t>(p->hi_g[d], p->ke - 1);
+        p->lo_l[d] = (int32_t)a;
+        p->len_l[d] = b >= a ? (int32_t)(b - a + 1) : 0;
+        p->off[d + 1] = p->off[d] + p->len_l[d];
+    }
+    p->nnz = p->off[D];
+    {   // uncovered rows of this slice (reading R9)
+        std::vector<int32_t> diff(p->Ml + 1, 0);
+        for (int64_t d = 0; d < D; d++)
+            if (p->len_l[d]) {
+                diff[p->lo_l[d] - p->kb] += 1;
+                diff[p->lo_l[d] - p->kb + p->len_l[d]] -= 1;
+            }
+        int64_t c = 0, unc = 0;
+        for (int64_t k = 0; k < p->Ml; k++) {
+            c += diff[k];
+            unc += (c == 0);
+        }
+        p->uncovered = unc;
+    }
+    CK(cudaMemcpyAsync(p->d_lo, p->lo_l.data(), sizeof(int32_t) * D, cudaMemcpyHostToDevice, s));
+    CK(cudaMalloc(&p->d_len, sizeof(int32_t) * D));
+    CK(cudaMemcpyAsync(p->d_len, p->len_l.data(), sizeof(int32_t) * D, cudaMemcpyHostToDevice, s));
+    CK(cudaMalloc(&p->d_off, sizeof(int64_t) * (D + 1)));
+    CK(cudaMemcpyAsync(p->d_off, p->off.data(), sizeof(int64_t) * (D + 1), cudaMemcpyHostToDevice, s));
+    CK(cudaMalloc(&p->d_val, sizeof(double) * std::max<int64_t>(1, p->nnz)));
+    // S0 (b): values on the device
+    CK(run_k(ctx, "probe_values", 1, [&]() { return launch_probe_values(p->d_alpha2, D, p->band(), s); }));
+    // stored mass per probe (diagnostic; summed over ranks)
+    double *d_s = nullptr;
+    CKS(ws_get(ctx, "probe_s", D, &d_s));
+    CK(run_k(ctx, "probe_rowsum", 1, [&]() { return launch_probe_rowsum(D, p->band(), d_s, s); }));
+    CKS(allreduce(ctx, d_s, D, "allreduce_s"));
+    std::vector<double> hs(D);
+    CK(cudaMemcpyAsync(hs.data(), d_s, sizeof(double) * D, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    p->min_row_mass = *std::min_element(hs.begin(), hs.end());
+    *out = p.release();
+    return QDT_OK;
+}
+
+extern "C" qdt_status qdt_probes_free(qdt_probes *p)
+{
+    if (!p) return QDT_OK;
+    cudaSetDevice(p->ctx->device);
+    delete p;
+    return QDT_OK;
+}
+
+extern "C" qdt_status qdt_probes_export(qdt_ctx *ctx, const qdt_probes *p, int64_t *nnz,
+                                        int64_t *k_begin, int64_t *k_end, int64_t *lo,
+                                        int64_t *len, double *val)
+{
+    if (!ctx || !p) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_probes_export: NULL handle");
+    if (p->ctx != ctx) return fail(ctx, QDT_ERR_STATE, "probes were built on another ctx");
+    if (nnz) *nnz = p->nnz;
+    if (k_begin) *k_begin = p->kb;
+    if (k_end) *k_end = p->ke;
+    for (int64_t d = 0; d < p->D; d++) {
+        if (lo) lo[d] = p->lo_l[d];
+        if (len) len[d] = p->len_l[d];
+    }
+    if (val && p->nnz) {
+        CK(cudaMemcpyAsync(val, p->d_val, sizeof(double) * p->nnz, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+    return QDT_OK;
+}
+
+// ------------------------------------------------------------------------------ step setup
+// SQS weights (t_k = 1/w_k) or the power-iteration Lipschitz scalar (reading R2).
+static qdt_status step_setup(qdt_ctx *ctx, qdt_probes *p, Plan *pl, int mode, double gamma,
+                             int k_pow, double *d_tstep, double *d_w, double *rho_out,
+                             double *tscalar_out)
+{
+    cudaStream_t s = ctx->stream;
+    const int64_t D = p->D, Ml = p->Ml;
+    if (mode == QDT_STEP_SQS || d_w) {
+        double *d_s;
+        CKS(ws_get(ctx, "setup_s", D, &d_s));
+        CK(run_k(ctx, "probe_rowsum", 1, [&]() { return launch_probe_rowsum(D, p->band(), d_s, s); }));
+        CKS(allreduce(ctx, d_s, D, "allreduce_s"));
+        CK(run_k(ctx, "sqs_weights", 1, [&]() {
+            return launch_sqs_weights(pl->ntiles, pl->T, pl->d_tile_dA, pl->d_tile_dB, (int)Ml, p->kb,
+                                      p->band(), d_s, gamma, d_w,
+                                      mode == QDT_STEP_SQS ? d_tstep : nullptr, s);
+        }));
+    }
+    if (mode == QDT_STEP_LIPSCHITZ || rho_out) {
+        // v0 = 1/sqrt(M); K_pow iterations of v <- F^T F v / ||F^T F v||; rho = ||F v||^2
+        double *v, *u, *q, *part, *nrm;
+        const int nb = ctx->nblkR;
+        CKS(ws_get(ctx, "pow_v", Ml, &v));
+        CKS(ws_get(ctx, "pow_u", Ml, &u));
+        CKS(ws_get(ctx, "pow_q", D, &q));
+        CKS(ws_get(ctx, "pow_part", nb, &part));
+        CKS(ws_get(ctx, "pow_nrm", 2, &nrm));
+        CK(launch_fill(v, Ml, 1.0 / sqrt((double)p->M), s));
+        ctx->launches++;
+        for (int i = 0; i < k_pow; i++) {
+            CK(run_k(ctx, "pow_fwd", 1, [&]() { return launch_pow_fwd(D, p->band(), v, p->kb, q, s); }));
+            CKS(allreduce(ctx, q, D, "allreduce_pow"));
+            CK(run_k(ctx, "pow_bwd", 1, [&]() {
+                return launch_pow_bwd(pl->ntiles, pl->T, pl->d_tile_dA, pl->d_tile_dB, (int)Ml, p->kb,
+                                      p->band(), q, u, s);
+            }));
+            CK(run_k(ctx, "pow_norm", 3, [&]() {
+                cudaError_t e = launch_sumsq(u, Ml, part, nb, s);
+                if (e == cudaSuccess) e = launch_reduce_vec(part, nb, 1, 1, nrm, s);
+                return e;
+            }));
+            CKS(allreduce(ctx, nrm, 1, "allreduce_pow"));
+            CK(run_k(ctx, "pow_scale", 1, [&]() { return launch_scale(v, u, nrm, Ml, s); }));
+        }
+        CK(run_k(ctx, "pow_fwd", 1, [&]() { return launch_pow_fwd(D, p->band(), v, p->kb, q, s); }));
+        CKS(allreduce(ctx, q, D, "allreduce_pow"));
+        CK(run_k(ctx, "pow_norm", 2, [&]() {
+            cudaError_t e = launch_sumsq(q, D, part, nb, s);
+            if (e == cudaSuccess) e = launch_reduce_vec(part, nb, 1, 1, nrm, s);
+            return e;
+        }));
+        double rho = 0.0;
+        CK(cudaMemcpyAsync(&rho, nrm, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (rho_out) *rho_out = rho;
+        if (mode == QDT_STEP_LIPSCHITZ) {
+            const double t = 1.0 / (1.01 * rho + 4.0 * gamma);
+            if (tscalar_out) *tscalar_out = t;
+            CK(launch_fill(d_tstep, Ml, t, s));
+            ctx->launches++;
+        }
+    }
+    return QDT_OK;
+}
+
+extern "C" qdt_status qdt_step_setup(qdt_ctx *ctx, const qdt_probes *F, double gamma, int32_t k_pow,
+                                     double *w_out, double *rho_out)
+{
+    if (!ctx || !F) return fail(ctx, QDT_ERR_INVALID_ARG, "NULL handle");
+    if (!(gamma >= 0.0) || !isfinite(gamma) || k_pow < 0)
+        return fail(ctx, QDT_ERR_INVALID_ARG, "gamma must be finite >= 0, k_pow >= 0");
+    qdt_probes *p = const_cast<qdt_probes *>(F);
+    Plan *pl;
+    CKS(build_plan(ctx, p, 1, &pl));
+    double *d_w = nullptr, *d_t;
+    CKS(ws_get(ctx, "setup_t", p->Ml, &d_t));
+    if (w_out) CKS(ws_get(ctx, "setup_w", p->Ml, &d_w));
+    double rho = 0.0;
+    CKS(step_setup(ctx, p, pl, w_out ? QDT_STEP_SQS : QDT_STEP_LIPSCHITZ, gamma, k_pow, d_t, d_w,
+                   rho_out ? &rho : nullptr, nullptr));
+    if (w_out) {
+        CK(cudaMemcpyAsync(w_out, d_w, sizeof(double) * p->Ml, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+    if (rho_out) *rho_out = rho;
+    return QDT_OK;
+}
+
+// ------------------------------------------------------------------------------ iteration
+struct SolveBufs {
+    double *theta[3] = {nullptr, nullptr, nullptr};  // (Ml + 2) x N, pointer to local row 0
+    double *R[2] = {nullptr, nullptr};
+    double *RY = nullptr;
+    double *rpart = nullptr, *partR = nullptr, *partT = nullptr, *vec = nullptr;
+    double *tstep = nullptr, *scratch = nullptr, *P = nullptr;
+    double *trace = nullptr, *kkt = nullptr, *kktp = nullptr, *beta = nullptr;
+    int *counters = nullptr;
+    DevState *state = nullptr;
+};
+
+struct IterCfg {
+    qdt_probes *p;
+    Plan *pl;
+    int N;
+    double gamma, tol;
+    int fista;
+    int kkt_every;
+    int64_t trace_len;
+};
+
+static qdt_status fwd_reduce(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, const double *theta,
+                             double *R, bool withP)
+{
+    cudaStream_t s = ctx->stream;
+    Plan *pl = c.pl;
+    qdt_probes *p = c.p;
+    FwdArgs fa;
+    fa.N = c.N;
+    fa.CG = pl->CG;
+    fa.RG = pl->RG;
+    fa.KR = pl->KR;
+    fa.units = pl->d_funits;
+    fa.band = p->band();
+    fa.theta = theta;
+    fa.kb = p->kb;
+    fa.rpart = b.rpart;
+    fa.state = b.state;
+    CK(run_k(ctx, "fwd_partial", 1, [&]() { return launch_fwd(fa, pl->nfunits, pl->TC, s, nullptr); }));
+    const bool multi = ctx->nranks > 1;
+    CK(run_k(ctx, "reduce_R", 1, [&]() {
+        return launch_reduce_R(b.rpart, pl->d_red_beg, pl->d_red_rows, (withP && !multi) ? b.P : nullptr,
+                               R, p->D, c.N, b.partR, ctx->nblkR, b.state, s);
+    }));
+    if (multi) {
+        CKS(allreduce(ctx, R, (size_t)p->D * c.N, "allreduce_R"));
+        if (withP)
+            CK(run_k(ctx, "reduce_R", 1, [&]() {
+                return launch_sub_p_sumsq(R, b.P, p->D * (int64_t)c.N, b.partR, ctx->nblkR, b.state, s);
+            }));
+    }
+    return QDT_OK;
+}
+
+static BwdArgs bwd_args(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, const double *R,
+                        const double *theta, const double *theta_prev, double *out, bool fista)
+{
+    (void)ctx;
+    BwdArgs a;
+    Plan *pl = c.pl;
+    a.N = c.N;
+    a.CG = pl->CG;
+    a.RG = pl->RG;
+    a.KC = pl->KC;
+    a.units = pl->d_bunits;
+    a.band = c.p->band();
+    a.R = R;
+    a.theta = theta;
+    a.theta_prev = fista ? theta_prev : nullptr;
+    a.beta = fista ? b.beta : nullptr;
+    a.kkt_every = c.kkt_every;
+    a.kb = c.p->kb;
+    a.M = c.p->M;
+    a.Ml = (int)c.p->Ml;
+    a.tstep = b.tstep;
+    a.gamma = c.gamma;
+    a.out = out;
+    a.scratch = b.scratch;
+    a.counters = b.counters;
+    a.part = b.partT;
+    a.state = b.state;
+    return a;
+}
+
+static qdt_status halo_exchange(qdt_ctx *ctx, const IterCfg &c, double *theta)
+{
+    if (ctx->nranks == 1) return QDT_OK;
+    const int N = c.N, r = ctx->rank;
+    const int64_t Ml = c.p->Ml;
+    nccl_result_t e = 0;
+    run_k(ctx, "halo", 1, [&]() {
+        g_nccl.groupStart();
+        if (r > 0) {
+            e |= g_nccl.send(theta, N, NCCL_FLOAT64, r - 1, ctx->comm, ctx->stream);
+            e |= g_nccl.recv(theta - N, N, NCCL_FLOAT64, r - 1, ctx->comm, ctx->stream);
+        }
+        if (r + 1 < ctx->nranks) {
+            e |= g_nccl.send(theta + (Ml - 1) * N, N, NCCL_FLOAT64, r + 1, ctx->comm, ctx->stream);
+            e |= g_nccl.recv(theta + Ml * N, N, NCCL_FLOAT64, r + 1, ctx->comm, ctx->stream);
+        }
+        e |= g_nccl.groupEnd();
+        return cudaSuccess;
+    });
+    if (e != 0) return fail(ctx, QDT_ERR_NCCL, "halo exchange failed");
+    return QDT_OK;
+}
+
+static qdt_status scalars(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, int final_eval)
+{
+    cudaStream_t s = ctx->stream;
+    CK(run_k(ctx, "scalars", 1, [&]() {
+        return launch_scalars_local(b.partR, ctx->nblkR, b.partT, c.pl->ntiles, ctx->rank == 0, b.vec,
+                                    b.state, s);
+    }));
+    CKS(allreduce(ctx, b.vec, NV, "allreduce_scalars"));
+    CK(run_k(ctx, "scalars", 1, [&]() {
+        return launch_finalize(b.vec, c.N, c.p->M, c.gamma, c.tol, final_eval, final_eval ? 1 : c.kkt_every,
+                               b.trace, b.kkt, b.kktp, c.trace_len, b.state, s);
+    }));
+    return QDT_OK;
+}
+
+// one iteration with phase index j (buffer rotation)
+static qdt_status iteration(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, int64_t j)
+{
+    cudaStream_t s = ctx->stream;
+    Plan *pl = c.pl;
+    if (!c.fista) {
+        double *cur = b.theta[j % 2], *nxt = b.theta[(j + 1) % 2];
+        CKS(fwd_reduce(ctx, c, b, cur, b.R[0], true));
+        BwdArgs a = bwd_args(ctx, c, b, b.R[0], cur, nullptr, nxt, false);
+        CK(run_k(ctx, "bwd_step", 1, [&]() { return launch_bwd(a, pl->nbunits, pl->TC, BWD_STEP, s); }));
+        CKS(halo_exchange(ctx, c, nxt));
+    } else {
+        double *cur = b.theta[j % 3], *prev = b.theta[(j + 2) % 3], *nxt = b.theta[(j + 1) % 3];
+        double *Rk = b.R[j % 2], *Rkm1 = b.R[(j + 1) % 2];
+        CKS(fwd_reduce(ctx, c, b, cur, Rk, true));
+        CK(run_k(ctx, "fista_rcomb", 1, [&]() {
+            return launch_fista_rcomb(b.RY, Rk, Rkm1, b.beta, c.p->D * (int64_t)c.N, b.state, s);
+        }));
+        BwdArgs ev = bwd_args(ctx, c, b, Rk, cur, prev, nxt, true);
+        CK(run_k(ctx, "bwd_eval", 1, [&]() { return launch_bwd(ev, pl->nbunits, pl->TC, BWD_EVAL, s); }));
+        BwdArgs a = bwd_args(ctx, c, b, b.RY, cur, prev, nxt, true);
+        CK(run_k(ctx, "bwd_step", 1, [&]() { return launch_bwd(a, pl->nbunits, pl->TC, BWD_STEP, s); }));
+        CKS(halo_exchange(ctx, c, nxt));
+    }
+    CKS(scalars(ctx, c, b, 0));
+    return QDT_OK;
+}
+
+static qdt_status upload_rows(qdt_ctx *ctx, double *dst, const double *src, int64_t rows, int N,
+                              bool device_src)
+{
+    CK(cudaMemcpyAsync(dst, src, sizeof(double) * rows * N,
+                       device_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, ctx->stream));
+    return QDT_OK;
+}
+
+static qdt_status check_finite_host(qdt_ctx *ctx, const double *x, int64_t n, const char *what)
+{
+    for (int64_t i = 0; i < n; i++)
+        if (!isfinite(x[i]))
+            return fail(ctx, QDT_ERR_NONFINITE, "%s[%lld] is not finite", what, (long long)i);
+    return QDT_OK;
+}
+
+extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double *P, int64_t N,
+                                double gamma, double tol, int64_t iters, const qdt_solve_opts *o,
+                                double *theta_out, double *trace_out, double *kkt_out,
+                                qdt_solve_info *info)
+{
+    if (!ctx) return fail(nullptr, QDT_ERR_INVALID_ARG, "qdt_solve: ctx is NULL");
+    if (!F || !P || !theta_out) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: NULL pointer");
+    if (F->ctx != ctx) return fail(ctx, QDT_ERR_STATE, "qdt_solve: probes built on another ctx");
+    if (N < 1 || N > 8192) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: N = %lld not in [1, 8192]", (long long)N);
+    if (!(gamma >= 0.0) || !isfinite(gamma)) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: gamma must be finite and >= 0");
+    if (!(tol >= 0.0)) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: tol must be >= 0");
+    if (iters < 0) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: iters < 0");
+    qdt_solve_opts opt = {QDT_STEP_SQS, 0, nullptr, 16, 1, 0, 0, 1};
+    if (o) opt = *o;
+    if (opt.step != QDT_STEP_SQS && opt.step != QDT_STEP_LIPSCHITZ)
+        return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: unknown step mode %d", opt.step);
+    if (opt.check_every < 1) opt.check_every = 16;
+    if (opt.kkt_every < 1) opt.kkt_every = 1;
+    const bool dev = opt.mem_device != 0;
+    qdt_probes *p = const_cast<qdt_probes *>(F);
+    const int64_t D = p->D, Ml = p->Ml, M = p->M;
+    if (!dev) {
+        CKS(check_finite_host(ctx, P, D * N, "P"));
+        if (opt.theta0)
+            CKS(check_finite_host(ctx, opt.theta0, (ctx->nranks > 1 && !opt.gather_theta ? Ml : M) * N,
+                                  "theta0"));
+    }
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    Plan *pl;
+    CKS(build_plan(ctx, p, (int)N, &pl));
+    // memory plan (fails before allocating the big buffers)
+    {
+        const int nb = opt.accel ? 3 : 2;
+        double need = 8.0 * ((double)nb * (Ml + 2) * N + (opt.accel ? 3.0 : 1.0) * D * N + D * N +
+                             (double)pl->nrpart * N + (double)pl->nslots * pl->T * N + 2.0 * Ml);
+        size_t fr = 0, tot = 0;
+        CK(cudaMemGetInfo(&fr, &tot));
+        size_t have = fr;
+        for (auto &kv : ctx->ws) have += kv.second.n;
+        if (need > 0.97 * (double)have)
+            return fail(ctx, QDT_ERR_OOM, "memory plan: need %.2f GB, %.2f GB available", need / 1e9,
+                        have / 1e9);
+    }
+    const int fista = opt.accel ? 1 : 0;
+    const int nbuf = fista ? 3 : 2;
+    SolveBufs b;
+    const size_t rowsz = (size_t)(Ml + 2) * N;
+    const char *tn[3] = {"theta0", "theta1", "theta2"};
+    for (int i = 0; i < nbuf; i++) {
+        double *t;
+        CKS(ws_get(ctx, tn[i], rowsz, &t));
+        b.theta[i] = t + N;
+        CK(cudaMemsetAsync(t, 0, sizeof(double) * rowsz, s));
+    }
+    CKS(ws_get(ctx, "R0", D * N, &b.R[0]));
+    if (fista) {
+        CKS(ws_get(ctx, "R1", D * N, &b.R[1]));
+        CKS(ws_get(ctx, "RY", D * N, &b.RY));
+        CK(cudaMemsetAsync(b.R[1], 0, sizeof(double) * D * N, s));
+    }
+    CKS(ws_get(ctx, "rpart", std::max<int64_t>(1, pl->nrpart) * N, &b.rpart));
+    CKS(ws_get(ctx, "partR", ctx->nblkR, &b.partR));
+    CKS(ws_get(ctx, "partT", (size_t)pl->ntiles * NSC_TILE, &b.partT));
+    CK(cudaMemsetAsync(b.partT, 0, sizeof(double) * pl->ntiles * NSC_TILE, s));
+    CKS(ws_get(ctx, "vec", NV, &b.vec));
+    CKS(ws_get(ctx, "tstep", Ml, &b.tstep));
+    CKS(ws_get(ctx, "scratch", std::max<int64_t>(1, pl->nslots) * pl->T * N, &b.scratch));
+    CKS(ws_get(ctx, "counters", std::max(1, pl->ntiles), &b.counters));
+    CK(cudaMemsetAsync(b.counters, 0, sizeof(int) * std::max(1, pl->ntiles), s));
+    CKS(ws_get(ctx, "state", 1, &b.state));
+    const int64_t tl = iters + 1;
+    CKS(ws_get(ctx, "trace", tl, &b.trace));
+    CKS(ws_get(ctx, "kkt", tl, &b.kkt));
+    CKS(ws_get(ctx, "kktp", tl, &b.kktp));
+    CK(launch_fill(b.trace, tl, NAN, s));
+    CK(launch_fill(b.kkt, tl, NAN, s));
+    CK(launch_fill(b.kktp, tl, NAN, s));
+    ctx->launches += 3;
+    if (dev) {
+        b.P = const_cast<double *>(P);
+    } else {
+        CKS(ws_get(ctx, "P", D * N, &b.P));
+        CK(cudaMemcpyAsync(b.P, P, sizeof(double) * D * N, cudaMemcpyHostToDevice, s));
+    }
+    std::vector<double> betas;
+    if (fista) {
+        CKS(ws_get(ctx, "beta", tl, &b.beta));
+        betas.resize(tl);
+        double tau = 1.0;
+        for (int64_t k = 0; k < tl; k++) {
+            double tn_ = (1.0 + sqrt(1.0 + 4.0 * tau * tau)) / 2.0;
+            betas[k] = (tau - 1.0) / tn_;
+            tau = tn_;
+        }
+        CK(cudaMemcpyAsync(b.beta, betas.data(), sizeof(double) * tl, cudaMemcpyHostToDevice, s));
+    }
+    // Theta_0 = 1/N or theta0 (full M x N; local rows when nranks > 1 and
+    // !gather_theta)
+    if (opt.theta0) {
+        const double *src = opt.theta0;
+        if (ctx->nranks == 1 || opt.gather_theta) src += p->kb * N;
+        CKS(upload_rows(ctx, b.theta[0], src, Ml, (int)N, dev));
+    } else {
+        CK(launch_fill(b.theta[0], Ml * N, 1.0 / (double)N, s));
+        ctx->launches++;
+    }
+    IterCfg c{p, pl, (int)N, gamma, tol, fista, fista ? opt.kkt_every : 1, tl};
+    CKS(halo_exchange(ctx, c, b.theta[0]));
+    if (fista) CK(cudaMemcpyAsync(b.theta[2] - N, b.theta[0] - N, sizeof(double) * rowsz, cudaMemcpyDeviceToDevice, s));
+    double tscalar = 0.0;
+    CKS(step_setup(ctx, p, pl, opt.step, gamma, 100, b.tstep, nullptr, nullptr, &tscalar));
+    DevState st0;
+    memset(&st0, 0, sizeof st0);
+    st0.iters_done = -1;
+    CK(cudaMemcpyAsync(b.state, &st0, sizeof st0, cudaMemcpyHostToDevice, s));
+
+    // ---- the hot loop: graph of `period` iterations replayed
+    const int period = fista ? 6 : 2;
+    const bool use_graph = opt.use_graph && !ctx->profiling && iters >= period;
+    DevState hst;
+    int64_t done = 0;
+    bool stopped = false;
+    cudaGraphExec_t gexec = nullptr;
+    int64_t graph_launches = 0;
+    if (use_graph) {
+        cudaGraph_t g;
+        int64_t l0 = ctx->launches;
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        qdt_status cs = QDT_OK;
+        for (int j = 0; j < period && cs == QDT_OK; j++) cs = iteration(ctx, c, b, j);
+        cudaError_t ee = cudaStreamEndCapture(s, &g);
+        if (cs != QDT_OK) return cs;
+        CK(ee);
+        graph_launches = ctx->launches - l0;
+        ctx->launches = l0;
+        CK(cudaGraphInstantiate(&gexec, g, 0));
+        cudaGraphDestroy(g);
+    }
+    const int64_t check = tol > 0.0 ? std::max<int64_t>(period, (opt.check_every / period) * period) : INT64_MAX;
+    int64_t since = 0;
+    while (done < iters) {
+        if (use_graph && iters - done >= period) {
+            CK(cudaGraphLaunch(gexec, s));
+            ctx->launches += graph_launches;
+            done += period;
+            since += period;
+        } else {
+            CKS(iteration(ctx, c, b, done));
+            done += 1;
+            since += 1;
+        }
+        if (since >= check) {
+            since = 0;
+            CK(cudaMemcpyAsync(&hst, b.state, sizeof hst, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            if (hst.stop) {
+                stopped = true;
+                break;
+            }
+        }
+    }
+    if (gexec) cudaGraphExecDestroy(gexec);
+    // ---- final evaluation at Theta_iters (if no early stop)
+    CK(cudaMemcpyAsync(&hst, b.state, sizeof hst, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    stopped = hst.stop != 0;
+    if (!stopped) {
+        IterCfg cf = c;
+        cf.fista = 0;
+        double *cur = b.theta[iters % nbuf];
+        CKS(fwd_reduce(ctx, cf, b, cur, b.R[0], true));
+        BwdArgs a = bwd_args(ctx, cf, b, b.R[0], cur, nullptr, nullptr, false);
+        CK(run_k(ctx, "bwd_eval", 1, [&]() { return launch_bwd(a, pl->nbunits, pl->TC, BWD_EVAL, s); }));
+        CKS(scalars(ctx, cf, b, 1));
+        CK(cudaMemcpyAsync(&hst, b.state, sizeof hst, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    if (hst.nonfinite)
+        return fail(ctx, QDT_ERR_NONFINITE, "non-finite objective at iteration %lld", (long long)hst.iters_done);
+    const int64_t kd = hst.iters_done;
+    const double *res = b.theta[kd % nbuf];
+    // ---- outputs
+    const bool gather = ctx->nranks > 1 && opt.gather_theta;
+    if (gather) {
+        // assemble the full M x N on every rank (allreduce of zero-padded slices)
+        double *full;
+        CKS(ws_get(ctx, "gather", M * N, &full));
+        CK(cudaMemsetAsync(full, 0, sizeof(double) * M * N, s));
+        CK(cudaMemcpyAsync(full + p->kb * N, res, sizeof(double) * Ml * N, cudaMemcpyDeviceToDevice, s));
+        CKS(allreduce(ctx, full, (size_t)M * N, "gather"));
+        CK(cudaMemcpyAsync(theta_out, full, sizeof(double) * M * N,
+                           dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+    } else {
+        CK(cudaMemcpyAsync(theta_out, res, sizeof(double) * Ml * N,
+                           dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+    }
+    std::vector<double> hk(tl);
+    if (trace_out) CK(cudaMemcpyAsync(trace_out, b.trace, sizeof(double) * tl, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hk.data(), b.kkt, sizeof(double) * tl, cudaMemcpyDeviceToHost, s));
+    double kp_last = NAN;
+    CK(cudaMemcpyAsync(&kp_last, b.kktp + kd, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (kkt_out) memcpy(kkt_out, hk.data(), sizeof(double) * tl);
+    flush_profile(ctx);
+    if (info) {
+        info->iters_done = kd;
+        info->converged = hst.converged;
+        info->kkt0 = hk[0];
+        info->kkt = hk[kd];
+        info->kkt_paper = kp_last;
+        double fl = NAN;
+        CK(cudaMemcpyAsync(&fl, b.trace + kd, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        info->f_final = fl;
+        info->step_scalar = tscalar;
+        info->k_begin = p->kb;
+        info->k_end = p->ke;
+        info->nnz = p->nnz;
+        info->min_row_mass = p->min_row_mass;
+        info->uncovered_rows = p->uncovered;
+    }
+    (void)stopped;
+    return QDT_OK;
+}
+
+// ------------------------------------------------------------------------------ objective
+extern "C" qdt_status qdt_objective(qdt_ctx *ctx, const qdt_probes *F, const double *P,
+                                    const double *theta, int64_t N, double gamma,
+                                    int32_t mem_device, double *f_out, double *kkt_out)
+{
+    if (!ctx) return fail(nullptr, QDT_ERR_INVALID_ARG, "qdt_objective: ctx is NULL");
+    if (!F || !P || !theta || !f_out) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_objective: NULL pointer");
+    if (F->ctx != ctx) return fail(ctx, QDT_ERR_STATE, "probes built on another ctx");
+    if (N < 1 || N > 8192) return fail(ctx, QDT_ERR_INVALID_ARG, "N out of range");
+    if (!(gamma >= 0.0) || !isfinite(gamma)) return fail(ctx, QDT_ERR_INVALID_ARG, "gamma must be finite >= 0");
+    qdt_probes *p = const_cast<qdt_probes *>(F);
+    const int64_t D = p->D, Ml = p->Ml;
+    const bool dev = mem_device != 0;
+    if (!dev) {
+        CKS(check_finite_host(ctx, P, D * N, "P"));
+        CKS(check_finite_host(ctx, theta, p->M * N, "theta"));
+    }
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    Plan *pl;
+    CKS(build_plan(ctx, p, (int)N, &pl));
+    SolveBufs b;
+    double *t;
+    const size_t rowsz = (size_t)(Ml + 2) * N;
+    CKS(ws_get(ctx, "theta0", rowsz, &t));
+    b.theta[0] = t + N;
+    CK(cudaMemsetAsync(t, 0, sizeof(double) * rowsz, s));
+    CK(cudaMemcpyAsync(b.theta[0] - (p->kb > 0 ? N : 0), theta + (p->kb > 0 ? (p->kb - 1) * N : 0),
+                       sizeof(double) * (Ml + (p->kb > 0) + (p->ke < p->M)) * N,
+                       dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    CKS(ws_get(ctx, "R0", D * N, &b.R[0]));
+    CKS(ws_get(ctx, "rpart", std::max<int64_t>(1, pl->nrpart) * N, &b.rpart));
+    CKS(ws_get(ctx, "partR", ctx->nblkR, &b.partR));
+    CKS(ws_get(ctx, "partT", (size_t)pl->ntiles * NSC_TILE, &b.partT));
+    CKS(ws_get(ctx, "vec", NV, &b.vec));
+    CKS(ws_get(ctx, "tstep", Ml, &b.tstep));
+    CKS(ws_get(ctx, "scratch", std::max<int64_t>(1, pl->nslots) * pl->T * N, &b.scratch));
+    CKS(ws_get(ctx, "counters", std::max(1, pl->ntiles), &b.counters));
+    CK(cudaMemsetAsync(b.counters, 0, sizeof(int) * std::max(1, pl->ntiles), s));
+    CKS(ws_get(ctx, "state", 1, &b.state));
+    CKS(ws_get(ctx, "trace", 1, &b.trace));
+    CKS(ws_get(ctx, "kkt", 1, &b.kkt));
+    CKS(ws_get(ctx, "kktp", 1, &b.kktp));
+    if (dev) {
+        b.P = const_cast<double *>(P);
+    } else {
+        CKS(ws_get(ctx, "P", D * N, &b.P));
+        CK(cudaMemcpyAsync(b.P, P, sizeof(double) * D * N, cudaMemcpyHostToDevice, s));
+    }
+    DevState st0;
+    memset(&st0, 0, sizeof st0);
+    CK(cudaMemcpyAsync(b.state, &st0, sizeof st0, cudaMemcpyHostToDevice, s));
+    IterCfg c{p, pl, (int)N, gamma, 0.0, 0, 1, 1};
+    CKS(fwd_reduce(ctx, c, b, b.theta[0], b.R[0], true));
+    BwdArgs a = bwd_args(ctx, c, b, b.R[0], b.theta[0], nullptr, nullptr, false);
+    CK(run_k(ctx, "bwd_eval", 1, [&]() { return launch_bwd(a, pl->nbunits, pl->TC, BWD_EVAL, s); }));
+    CKS(scalars(ctx, c, b, 1));
+    double f = 0, r = 0;
+    CK(cudaMemcpyAsync(&f, b.trace, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&r, b.kkt, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *f_out = f;
+    if (kkt_out) *kkt_out = r;
+    return QDT_OK;
+}
+
+// ------------------------------------------------------------------------------ kernel hooks
+static qdt_status hook_common(qdt_ctx *ctx, const qdt_probes *F, int64_t N, Plan **pl)
+{
+    if (!ctx) return fail(nullptr, QDT_ERR_INVALID_ARG, "ctx is NULL");
+    if (!F) return fail(ctx, QDT_ERR_INVALID_ARG, "probes is NULL");
+    if (F->ctx != ctx) return fail(ctx, QDT_ERR_STATE, "probes built on another ctx");
+    if (ctx->nranks != 1) return fail(ctx, QDT_ERR_INVALID_ARG, "kernel hooks are single-rank only");
+    if (N < 1 || N > 8192) return fail(ctx, QDT_ERR_INVALID_ARG, "N out of range");
+    CK(cudaSetDevice(ctx->device));
+    return build_plan(ctx, const_cast<qdt_probes *>(F), (int)N, pl);
+}
+
+extern "C" qdt_status qdt_residual(qdt_ctx *ctx, const qdt_probes *F, const double *theta,
+                                   const double *P, int64_t N, double *R_out)
+{
+    Plan *pl;
+    CKS(hook_common(ctx, F, N, &pl));
+    if (!theta || !R_out) return fail(ctx, QDT_ERR_INVALID_ARG, "NULL pointer");
+    qdt_probes *p = const_cast<qdt_probes *>(F);
+    cudaStream_t s = ctx->stream;
+    SolveBufs b;
+    double *t;
+    CKS(ws_get(ctx, "theta0", (size_t)(p->Ml + 2) * N, &t));
+    b.theta[0] = t + N;
+    CK(cudaMemcpyAsync(b.theta[0], theta, sizeof(double) * p->Ml * N, cudaMemcpyHostToDevice, s));
+    CKS(ws_get(ctx, "R0", p->D * N, &b.R[0]));
+    CKS(ws_get(ctx, "rpart", std::max<int64_t>(1, pl->nrpart) * N, &b.rpart));
+    CKS(ws_get(ctx, "partR", ctx->nblkR, &b.partR));
+    if (P) {
+        CKS(ws_get(ctx, "P", p->D * N, &b.P));
+        CK(cudaMemcpyAsync(b.P, P, sizeof(double) * p->D * N, cudaMemcpyHostToDevice, s));
+    }
+    IterCfg c{p, pl, (int)N, 0.0, 0.0, 0, 1, 1};
+    CKS(fwd_reduce(ctx, c, b, b.theta[0], b.R[0], P != nullptr));
+    CK(cudaMemcpyAsync(R_out, b.R[0], sizeof(double) * p->D * N, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return QDT_OK;
+}
+
+extern "C" qdt_status qdt_gradient(qdt_ctx *ctx, const qdt_probes *F, const double *R,
+                                   const double *theta, int64_t N, double gamma, double *G_out)
+{
+    Plan *pl;
+    CKS(hook_common(ctx, F, N, &pl));
+    if (!theta || !R || !G_out) return fail(ctx, QDT_ERR_INVALID_ARG, "NULL pointer");
+    if (!(gamma >= 0.0) || !isfinite(gamma)) return fail(ctx, QDT_ERR_INVALID_ARG, "gamma must be finite >= 0");
+    qdt_probes *p = const_cast<qdt_probes *>(F);
+    cudaStream_t s = ctx->stream;
+    SolveBufs b;
+    double *t, *G;
+    CKS(ws_get(ctx, "theta0", (size_t)(p->Ml + 2) * N, &t));
+    b.theta[0] = t + N;
+    CK(cudaMemcpyAsync(b.theta[0], theta, sizeof(double) * p->Ml * N, cudaMemcpyHostToDevice, s));
+    CKS(ws_get(ctx, "R0", p->D * N, &b.R[0]));
+    CK(cudaMemcpyAsync(b.R[0], R, sizeof(double) * p->D * N, cudaMemcpyHostToDevice, s));
+    CKS(ws_get(ctx, "theta1", (size_t)(p->Ml + 2) * N, &G));
+    CKS(ws_get(ctx, "scratch", std::max<int64_t>(1, pl->nslots) * pl->T * N, &b.scratch));
+    CKS(ws_get(ctx, "counters", std::max(1, pl->ntiles), &b.counters));
+    CK(cudaMemsetAsync(b.counters, 0, sizeof(int) * std::max(1, pl->ntiles), s));
+    IterCfg c{p, pl, (int)N, gamma, 0.0, 0, 1, 1};
+    BwdArgs a = bwd_args(ctx, c, b, b.R[0], b.theta[0], nullptr, G, false);
+    a.state = nullptr;
+    CK(run_k(ctx, "bwd_grad", 1, [&]() { return launch_bwd(a, pl->nbunits, pl->TC, BWD_GRAD, s); }));
+    CK(cudaMemcpyAsync(G_out, G, sizeof(double) * p->Ml * N, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return QDT_OK;
+}
+
+extern "C" qdt_status qdt_step(qdt_ctx *ctx, const qdt_probes *F, const double *P,
+                               const double *theta, int64_t N, double gamma, int32_t step_mode,
+                               double *theta_next)
+{
+    if (!theta_next) return fail(ctx, QDT_ERR_INVALID_ARG, "NULL pointer");
+    qdt_solve_opts o = {step_mode, 0, theta, 16, 1, 0, 0, 0};
+    return qdt_solve(ctx, F, P, N, gamma, 0.0, 1, &o, theta_next, nullptr, nullptr, nullptr);
+}
+
+extern "C" qdt_status qdt_project_rows(qdt_ctx *ctx, const double *X, int64_t M, int64_t N,
+                                       double *Y_out)
+{
+    if (!ctx) return fail(nullptr, QDT_ERR_INVALID_ARG, "ctx is NULL");
+    if (!X || !Y_out) return fail(ctx, QDT_ERR_INVALID_ARG, "NULL pointer");
+    if (M < 1 || N < 1 || N > INT32_MAX) return fail(ctx, QDT_ERR_INVALID_ARG, "bad shape");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    double *dx, *dy;
+    CKS(ws_get(ctx, "projX", M * N, &dx));
+    CKS(ws_get(ctx, "projY", M * N, &dy));
+    CK(cudaMemcpyAsync(dx, X, sizeof(double) * M * N, cudaMemcpyHostToDevice, s));
+    CK(run_k(ctx, "project_rows", 1, [&]() { return launch_project_rows(dx, M, (int)N, dy, s); }));
+    CK(cudaMemcpyAsync(Y_out, dy, sizeof(double) * M * N, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return QDT_OK;
+}

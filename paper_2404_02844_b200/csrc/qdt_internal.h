@@ -1,0 +1,132 @@
+// qdt_internal.h -- declarations shared by the host runtime (qdt_api.cu) and the sm_100a
+// kernels (qdt_kernels.cu).  Not part of the public ABI (include/qdt.h is).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace qdt {
+
+// Bwd work unit: rows [k0, k1) (local) of bwd tile `tile`, probe range [p0, p1) of its window.
+// A tile whose window is wider than the split cap is cut into nsplit units along the probe
+// axis (split-K); each writes a partial G into scratch slot slot_base + slot and the last one
+// to finish sums the slots in slot order (deterministic) and runs the epilogue.
+struct BwdUnit {
+    int32_t k0, k1;
+    int32_t p0, p1;
+    int32_t tile;
+    int32_t slot;
+    int32_t nsplit;
+    int32_t pad;
+    int64_t slot_base;
+};
+
+// Fwd work unit: Rpart rows [poff, poff + p1 - p0) receive sum_{k in [k0,k1)} F[d,k] Theta[k,:]
+// for d in [p0, p1).  [k0, k1) is already tightened to the union of the group's bands.
+struct FwdUnit {
+    int32_t k0, k1;
+    int32_t p0, p1;
+    int64_t poff;
+};
+
+// Band tables of the local Fock slice: probe d stores rows [lo[d], lo[d] + len[d]) (GLOBAL row
+// indices) at val[off[d] ...]; len[d] == 0 when the band misses the slice.
+struct Band {
+    const int32_t *lo;
+    const int32_t *len;
+    const int64_t *off;
+    const double *val;
+};
+
+enum BwdMode { BWD_STEP = 0, BWD_GRAD = 1, BWD_EVAL = 2 };
+
+// per-tile scalar partials written by the bwd kernel
+enum { SC_KKT = 0, SC_KKTP = 1, SC_REG = 2, SC_DTH = 3, NSC_TILE = 4 };
+// reduced scalar vector (after the cross-rank allreduce)
+enum { V_R2 = 0, V_KKT = 1, V_KKTP = 2, V_REG = 3, V_DTH = 4, NV = 5 };
+
+// device-side solve state (stop flag and iteration counter; graph-replay safe)
+struct DevState {
+    int32_t stop;
+    int32_t converged;
+    int64_t it;
+    int64_t iters_done;
+    int32_t nonfinite;
+    int32_t pad;
+};
+
+struct BwdArgs {
+    int N, CG, RG, KC;
+    const BwdUnit *units;
+    Band band;
+    const double *R;
+    const double *theta;       // local row 0; rows -1 and Ml readable (halo)
+    const double *theta_prev;  // FISTA: Theta_{k-1} (same layout) or nullptr
+    const double *beta;        // FISTA: beta_k indexed by state->it (nullptr -> plain)
+    int kkt_every;             // MODE_EVAL runs only when state->it % kkt_every == 0
+    int64_t kb, M;
+    int Ml;
+    const double *tstep;       // per local row
+    double gamma;
+    double *out;               // Theta_next (local row 0) or G
+    double *scratch;
+    int *counters;
+    double *part;              // [ntiles x NSC_TILE]
+    const DevState *state;
+};
+
+struct FwdArgs {
+    int N, CG, RG, KR;
+    const FwdUnit *units;
+    Band band;
+    const double *theta;       // local row 0
+    int64_t kb;
+    double *rpart;
+    const DevState *state;
+};
+
+// launchers (qdt_kernels.cu); return cudaGetLastError()
+cudaError_t launch_probe_edges(const double *alpha2, int64_t D, int64_t M, double c_sigma,
+                               int margin, int32_t *lo, int32_t *hi, cudaStream_t s);
+cudaError_t launch_probe_values(const double *alpha2, int64_t D, Band b, cudaStream_t s);
+cudaError_t launch_probe_rowsum(int64_t D, Band b, double *s_out, cudaStream_t s);
+cudaError_t launch_sqs_weights(int ntiles, int T, const int32_t *tile_dA, const int32_t *tile_dB,
+                               int Ml, int64_t kb, Band b, const double *s, double gamma,
+                               double *w, double *tstep, cudaStream_t st);
+cudaError_t launch_pow_fwd(int64_t D, Band b, const double *v, int64_t kb, double *q,
+                           cudaStream_t s);
+cudaError_t launch_pow_bwd(int ntiles, int T, const int32_t *tile_dA, const int32_t *tile_dB,
+                           int Ml, int64_t kb, Band b, const double *q, double *u,
+                           cudaStream_t s);
+cudaError_t launch_sumsq(const double *x, int64_t n, double *part, int nblk, cudaStream_t s);
+cudaError_t launch_reduce_vec(const double *part, int nblk, int stride, int nvals, double *out,
+                              cudaStream_t s);
+cudaError_t launch_scale(double *v, const double *u, const double *nrm2, int64_t n,
+                         cudaStream_t s);
+cudaError_t launch_fill(double *x, int64_t n, double v, cudaStream_t s);
+
+cudaError_t prepare_kernels();
+int fwd_threads(int N, int *CG, int *RG, int *TC);
+int bwd_threads(int N, int *CG, int *RG, int *TC);
+constexpr int TR = 4;  // rows (bwd) / probes (fwd) per thread
+
+cudaError_t launch_fwd(const FwdArgs &a, int nunits, int TC, cudaStream_t s, size_t *smem_out);
+cudaError_t launch_bwd(const BwdArgs &a, int nunits, int TC, int mode, cudaStream_t s);
+size_t bwd_smem_bytes(int N, int RG, int KC, bool fista);
+size_t fwd_smem_bytes(int N, int RG, int KR);
+cudaError_t launch_reduce_R(const double *rpart, const int64_t *red_beg, const int64_t *red_rows,
+                            const double *P, double *R, int64_t D, int N, double *partR,
+                            int nblk, const DevState *st, cudaStream_t s);
+cudaError_t launch_sub_p_sumsq(double *R, const double *P, int64_t n, double *partR, int nblk,
+                               const DevState *st, cudaStream_t s);
+cudaError_t launch_scalars_local(const double *partR, int nblkR, const double *partT,
+                                 int ntiles, int include_r2, double *vec, const DevState *st,
+                                 cudaStream_t s);
+cudaError_t launch_finalize(const double *vec, int64_t N, int64_t M, double gamma, double tol,
+                            int final_eval, int kkt_every, double *trace, double *kkt,
+                            double *kktp, int64_t trace_len, DevState *st, cudaStream_t s);
+cudaError_t launch_project_rows(const double *X, int64_t M, int N, double *Y, cudaStream_t s);
+cudaError_t launch_fista_rcomb(double *RY, const double *Rk, const double *Rkm1,
+                               const double *beta, int64_t n, const DevState *st,
+                               cudaStream_t s);
+
+}  // namespace qdt

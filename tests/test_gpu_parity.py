@@ -1,0 +1,277 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element
+on the same seeded inputs (-m gpu).  Tolerances:
+  band edges, counts, indices            exact
+  F values                               4 eps (8 + |ln F|) relative (exp conditioning)
+  R, G, projections (single op)          1e-13 x scale (fp64 sums in a different order)
+  Theta after identical iteration counts 1e-9 max-abs      (north_star)
+  objective trace                        1e-10 relative + cancellation floor (reading R5)
+"""
+import numpy as np
+import pytest
+
+import oracle
+import qdt_synth as qs
+
+pytestmark = pytest.mark.gpu
+
+EPS = 2.220446049250313e-16
+
+
+@pytest.fixture(scope="module")
+def q():
+    import paper_2404_02844_b200 as q
+    from paper_2404_02844_b200 import build
+    build.build()
+    return q
+
+
+@pytest.fixture(scope="module")
+def ctx(q):
+    return q.qdt_init(0)
+
+
+def _trace_ok(tg, to, P):
+    tg, to = np.asarray(tg), np.asarray(to)
+    floor = 4 * EPS * np.sqrt(np.sum(P ** 2)) * np.sqrt(np.abs(to))
+    return np.all(np.abs(tg - to) <= 1e-10 * np.abs(to) + floor + 1e-300)
+
+
+# ----------------------------------------------------------------------------- S0 probes
+@pytest.mark.parametrize("name", ["tiny", "medium", "edge"])
+def test_probe_parity(q, ctx, name):
+    if name == "edge":
+        a2 = np.array([0.0, 0.0, 1e-3, 0.1, 1.0, 15.9, 16.0, 16.1, 39.9, 40.0, 77.0, 120.0, 500.0])
+        M = 100
+    else:
+        I = getattr(qs, name)()
+        a2, M = I.alpha2, I.M
+    Fo = oracle.Probes(a2, M)
+    Fg = q.qdt_build_probes(ctx, a2, M)
+    ex = q.qdt_probes_export(ctx, Fg)
+    np.testing.assert_array_equal(ex["lo"], Fo.lo)
+    np.testing.assert_array_equal(ex["len"], Fo.len)
+    assert ex["nnz"] == Fo.nnz
+    # F = exp(l): a relative error of F is an absolute error of l = ln F, so the bound scales
+    # with |ln F| (a few ulps of the log's magnitude)
+    tol = 4 * EPS * (8 + np.abs(np.log(np.maximum(Fo.val, 1e-300))))
+    assert np.all(np.abs(ex["val"] - Fo.val) <= tol * Fo.val)
+
+
+def test_probe_parity_megascale_edges_and_sample(q, ctx):
+    a2 = np.geomspace(1.0, 9e5, 10 ** 4)
+    M = 10 ** 6
+    Fg = q.qdt_build_probes(ctx, a2, M)
+    ex = q.qdt_probes_export(ctx, Fg)
+    lo_hi = np.array([oracle.band(m, M) for m in a2])
+    np.testing.assert_array_equal(ex["lo"], lo_hi[:, 0])
+    np.testing.assert_array_equal(ex["len"], lo_hi[:, 1] - lo_hi[:, 0] + 1)
+    off = np.concatenate([[0], np.cumsum(ex["len"])])
+    rng = np.random.default_rng(0)
+    for d in rng.choice(10 ** 4, 60, replace=False):
+        for j in rng.choice(ex["len"][d], 5):
+            ref = oracle.poisson_pmf(ex["lo"][d] + j, a2[d])
+            assert abs(ex["val"][off[d] + j] - ref) <= 4 * EPS * (8 + abs(np.log(ref))) * ref
+
+
+# ----------------------------------------------------------------------------- S5 projection
+@pytest.mark.parametrize("N", [1, 2, 10, 31, 32, 33, 100, 257, 1000])
+def test_projection_parity(q, ctx, N):
+    rng = np.random.default_rng(N)
+    X = rng.normal(0, 1, (300, N)) * rng.choice([0.01, 1, 30], (300, 1))
+    X[0] = 0.0
+    X[1] = 1.0 / N
+    Yg = q.qdt_project_rows(ctx, X)
+    Yo = oracle.project_rows(X)
+    scale = np.maximum(1.0, np.abs(X).max(axis=1, keepdims=True))
+    assert np.all(np.abs(Yg - Yo) <= 1e-14 * N * scale)
+    assert Yg.min() >= 0
+
+
+# ----------------------------------------------------------------------------- S2, S3, S4
+def _cases():
+    out = []
+    for name in ["tiny", "medium"]:
+        I = getattr(qs, name)()
+        out.append((name, I.alpha2, I.M, I.P, I.gamma))
+    for seed, (D, M, N) in enumerate([(1, 1, 1), (3, 7, 5), (50, 333, 17), (400, 97, 100),
+                                      (3000, 64, 10), (20, 2000, 3)]):
+        I = qs.random_instance(seed, D, M, N)
+        out.append((f"rand{D}x{M}x{N}", I.alpha2, I.M, I.P, I.gamma))
+    # many low-mu probes: every tile window is wider than the split cap (split-K path)
+    rng = np.random.default_rng(9)
+    a2 = np.sort(rng.uniform(0, 6, 2500))
+    out.append(("splitK", a2, 40, rng.dirichlet(np.ones(100), 2500), 1e-3))
+    return out
+
+
+CASES = _cases()
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_residual_gradient_parity(q, ctx, case):
+    _, a2, M, P, gamma = case
+    N = P.shape[1]
+    rng = np.random.default_rng(1)
+    Th = oracle.project_rows(rng.normal(0.5, 0.5, (M, N)))
+    Fo = oracle.Probes(a2, M)
+    Fg = q.qdt_build_probes(ctx, a2, M)
+    Ro = oracle.forward(Fo, Th, P)
+    Rg = q.qdt_residual(ctx, Fg, Th, P)
+    sR = max(1.0, np.abs(P).max())
+    assert np.abs(Rg - Ro).max() <= 1e-13 * sR
+    Go = oracle.backward(Fo, Ro, Th, gamma)
+    Gg = q.qdt_gradient(ctx, Fg, Ro, Th, gamma)
+    sG = max(1.0, np.abs(Go).max())
+    assert np.abs(Gg - Go).max() <= 1e-13 * sG
+
+
+@pytest.mark.parametrize("case", CASES[:4], ids=[c[0] for c in CASES[:4]])
+def test_step_setup_parity(q, ctx, case):
+    _, a2, M, P, gamma = case
+    Fo = oracle.Probes(a2, M)
+    Fg = q.qdt_build_probes(ctx, a2, M)
+    w, rho = q.qdt_step_setup(ctx, Fg, gamma, 100)
+    np.testing.assert_allclose(w, oracle.sqs_weights(Fo, gamma), rtol=1e-13)
+    assert rho == pytest.approx(oracle.power_iteration(Fo, 100), rel=1e-12)
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+@pytest.mark.parametrize("step", [0, 1])
+def test_one_step_parity(q, ctx, case, step):
+    _, a2, M, P, gamma = case
+    N = P.shape[1]
+    Fo = oracle.Probes(a2, M)
+    Fg = q.qdt_build_probes(ctx, a2, M)
+    Th = np.full((M, N), 1.0 / N)
+    ro = oracle.solve(Fo, P, gamma, 0.0, 1, step=step)
+    rg = q.qdt_solve(ctx, Fg, P, gamma, 0.0, 1, step=step, use_graph=False)
+    assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-12
+    assert _trace_ok(rg["trace"], ro["trace"], P)
+    del Th
+
+
+# ----------------------------------------------------------------------------- full solves
+@pytest.mark.parametrize("step,accel,iters", [(0, 0, 2000), (1, 0, 2000), (0, 1, 2000)])
+def test_tiny_solve_parity(q, ctx, step, accel, iters):
+    I = qs.tiny()
+    Fo = oracle.Probes(I.alpha2, I.M)
+    Fg = q.qdt_build_probes(ctx, I.alpha2, I.M)
+    ke = 50 if accel else 1
+    ro = oracle.solve(Fo, I.P, I.gamma, 0.0, iters, step=step, accel=accel, kkt_every=ke)
+    rg = q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, iters, step=step, accel=bool(accel),
+                     kkt_every=ke)
+    assert rg["info"]["iters_done"] == ro["iters_done"] == iters
+    assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9
+    assert _trace_ok(rg["trace"], ro["trace"], I.P)
+    m = ~np.isnan(ro["kkt"])
+    np.testing.assert_array_equal(m, ~np.isnan(rg["kkt"]))
+    np.testing.assert_allclose(rg["kkt"][m], ro["kkt"][m], rtol=1e-8, atol=1e-15)
+    # P9 invariants on the GPU iterate
+    Th = rg["theta"]
+    assert Th.min() >= 0 and np.abs(Th.sum(1) - 1).max() <= 4 * Th.shape[1] * EPS
+    if not accel:
+        tr = rg["trace"]
+        assert np.all(tr[1:] <= tr[:-1] * (1 + 1e-12))
+
+
+@pytest.mark.parametrize("accel", [0, 1])
+def test_medium_solve_parity(q, ctx, accel):
+    I = qs.medium()
+    Fo = oracle.Probes(I.alpha2, I.M)
+    Fg = q.qdt_build_probes(ctx, I.alpha2, I.M)
+    iters = 200
+    ro = oracle.solve(Fo, I.P, I.gamma, 0.0, iters, accel=accel, kkt_every=10 if accel else 1)
+    rg = q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, iters, accel=bool(accel),
+                     kkt_every=10 if accel else 1)
+    assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9
+    assert _trace_ok(rg["trace"], ro["trace"], I.P)
+
+
+def test_early_stop_parity(q, ctx):
+    I = qs.tiny()
+    Fo = oracle.Probes(I.alpha2, I.M)
+    Fg = q.qdt_build_probes(ctx, I.alpha2, I.M)
+    full = oracle.solve(Fo, I.P, I.gamma, 0.0, 300)
+    tol = full["kkt"][137] * (1 + 1e-7)
+    ro = oracle.solve(Fo, I.P, I.gamma, tol, 300)
+    rg = q.qdt_solve(ctx, Fg, I.P, I.gamma, tol, 300, check_every=16)
+    assert rg["info"]["iters_done"] == ro["iters_done"]
+    assert rg["info"]["converged"] == 1
+    assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-12
+
+
+def test_splitk_and_uncovered_rows(q, ctx):
+    # low-mu probes only: rows above the bands are uncovered (reading R9); gamma = 0 freezes
+    # them at 1/N, gamma > 0 diffuses them.  Windows exceed the split cap (split-K fix-up).
+    rng = np.random.default_rng(4)
+    a2 = np.sort(rng.uniform(0, 8, 1500))
+    M, N = 120, 33
+    P = rng.dirichlet(np.ones(N), 1500)
+    Fo = oracle.Probes(a2, M)
+    Fg = q.qdt_build_probes(ctx, a2, M)
+    for gamma in [0.0, 1e-2]:
+        ro = oracle.solve(Fo, P, gamma, 0.0, 150)
+        rg = q.qdt_solve(ctx, Fg, P, gamma, 0.0, 150)
+        assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9
+        assert rg["info"]["uncovered_rows"] == M - 1 - Fo.hi.max()
+        if gamma == 0.0:
+            assert np.all(rg["theta"][Fo.hi.max() + 1:] == 1.0 / N)
+
+
+def test_deterministic_and_device_pointers(q, ctx):
+    torch = pytest.importorskip("torch")
+    I = qs.medium()
+    Fg = q.qdt_build_probes(ctx, I.alpha2, I.M)
+    a = q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, 50)
+    b = q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, 50)
+    np.testing.assert_array_equal(a["theta"], b["theta"])
+    np.testing.assert_array_equal(a["trace"], b["trace"])
+    Pd = torch.tensor(I.P, device="cuda")
+    c = q.qdt_solve(ctx, Fg, Pd, I.gamma, 0.0, 50)
+    np.testing.assert_array_equal(c["theta"].cpu().numpy(), a["theta"])
+    f, r = q.qdt_objective(ctx, Fg, I.P, a["theta"], I.gamma)
+    Fo = oracle.Probes(I.alpha2, I.M)
+    assert f == pytest.approx(oracle.objective(Fo, I.P, a["theta"], I.gamma), rel=1e-12)
+
+
+def test_error_paths(q, ctx):
+    with pytest.raises(q.QdtError, match="UNSORTED"):
+        q.qdt_build_probes(ctx, np.array([1.0, 0.5]), 10)
+    with pytest.raises(q.QdtError, match="INVALID_ARG"):
+        q.qdt_build_probes(ctx, np.array([-1.0]), 10)
+    with pytest.raises(q.QdtError, match="INVALID_ARG"):
+        q.qdt_build_probes(ctx, np.array([1.0]), 0)
+    with pytest.raises(q.QdtError, match="TRUNCATED"):
+        q.qdt_build_probes(ctx, np.array([40.0]), 50, strict_mass=True)
+    F = q.qdt_build_probes(ctx, np.array([1.0, 2.0]), 10)
+    P = np.full((2, 3), 1 / 3)
+    P[1, 1] = np.nan
+    with pytest.raises(q.QdtError, match="NONFINITE"):
+        q.qdt_solve(ctx, F, P, 0.0, 0.0, 5)
+    with pytest.raises(q.QdtError, match="INVALID_ARG"):
+        q.qdt_solve(ctx, F, np.full((2, 3), 1 / 3), -1.0, 0.0, 5)
+
+
+@pytest.mark.slow
+def test_large_solve_parity(q, ctx):
+    I = qs.large()
+    Fo = oracle.Probes(I.alpha2, I.M)
+    Fg = q.qdt_build_probes(ctx, I.alpha2, I.M)
+    ro = oracle.solve(Fo, I.P, I.gamma, 0.0, 3)
+    rg = q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, 3)
+    assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9
+    assert _trace_ok(rg["trace"], ro["trace"], I.P)
+
+
+@pytest.mark.slow
+def test_megascale_solve_parity(q, ctx):
+    """Full-size bench workload, same launch configuration as bench.py (graph replay)."""
+    I = qs.megascale()
+    Fo = oracle.Probes(I.alpha2, I.M)
+    Fg = q.qdt_build_probes(ctx, I.alpha2, I.M)
+    ro = oracle.solve(Fo, I.P, I.gamma, 0.0, 2)
+    rg = q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, 2, use_graph=True)
+    assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9
+    assert _trace_ok(rg["trace"], ro["trace"], I.P)
+    Th = rg["theta"]
+    assert Th.min() >= 0 and np.abs(Th.sum(1) - 1).max() <= 4 * Th.shape[1] * EPS
