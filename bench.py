@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""Benchmark of the detector-tomography hot path (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {qdt,reference}] [--config megascale]
+
+A "step" is one projected-gradient iteration (residual, gradient, stencil,
+SQS step, row-wise simplex projection, scalars) over the whole Theta of the workload.  The
+default workload is BASELINE.json's Megascale configuration (M = 10^6 Fock levels, N = 100
+outcomes, D = 10^4 log-spaced probes, gamma = 1e-5), the 10^8-element reconstruction the
+north_star quotes its HBM-roofline target on; it fits one B200.
+Synthetic, seeded inputs (qdt_synth).  Theta (800 MB) is larger than the 126 MB L2, so no L2
+flush is needed between iterations.
+
+Metric: POVM-element gradient+projection updates/s = M * N * K / T_K (reading R10), T_K the
+CUDA-event time of K iterations bracketed by barrier + synchronize, max over ranks.  With N
+GPUs the Fock axis is sharded (NCCL allreduce of the D x N residual, halo rows): strong
+scaling of one reconstruction.
+
+--impl reference runs the CPU oracle (oracle/, plain fp64 C, one thread) on the same
+workload; each step is one oracle iteration on a bounded sample of the Fock rows (S evenly
+spaced row slabs), sized so that the run ends within a few minutes.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "POVM-element gradient+projection updates/s"
+UNIT = "updates/s"
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons DURING the timed region (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        time.sleep(0.2)
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 5 + i and r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def algorithmic_bytes(M, N, D, nnz):
+    """Per-kernel algorithmic bytes per launch."""
+    return {
+        # bwd_step: read Theta_k (+ its halo rows, counted once), write Theta_{k+1}, read F, read R
+        "bwd_step": 16.0 * M * N + 8.0 * nnz + 8.0 * D * N,
+        # fwd_partial: read Theta_k and F (partials written are implementation traffic)
+        "fwd_partial": 8.0 * M * N + 8.0 * nnz,
+        # reduce_R: read P, write R
+        "reduce_R": 16.0 * D * N,
+        # whole fused-iteration target (SURVEY 8d B_alg)
+        "iteration": 16.0 * M * N + 8.0 * nnz + 24.0 * D * N,
+    }
+
+
+def run_qdt(args):
+    import numpy as np
+    import torch
+
+    import paper_2404_02844_b200 as q
+    import qdt_synth as qs
+
+    rank, local, world = env_rank()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    uid = None
+    if world > 1:
+        t = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            t.copy_(torch.frombuffer(bytearray(q.qdt_nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(t, 0)
+        uid = bytes(t.cpu().numpy().tobytes())
+    ctx = q.qdt_init(local, rank, world, uid, stream.cuda_stream)
+
+    I = qs.CONFIGS[args.config]()
+    M, N, D = I.M, I.N, I.D
+    F = q.qdt_build_probes(ctx, I.alpha2, M)
+    ex = q.qdt_probes_export(ctx, F, values=False)
+    nnz_local = ex["nnz"]
+    Pd = torch.tensor(I.P, device="cuda")
+    rows_local = ex["k_end"] - ex["k_begin"]
+    th_out = torch.empty((rows_local, N), dtype=torch.float64, device="cuda")
+
+    def solve(iters, **kw):
+        return q.qdt_solve(ctx, F, Pd, I.gamma, 0.0, iters, theta_out=th_out, **kw)
+
+    # warm-up (untimed): plans, graphs, workspace
+    solve(max(3, args.warmup))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- timed: exactly K iterations, inputs resident in HBM
+    l0 = q.qdt_launch_count(ctx)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(stream)
+        out = solve(args.steps)
+        e1.record(stream)
+        barrier()
+    launches = q.qdt_launch_count(ctx) - l0
+    ms = e0.elapsed_time(e1)
+    loop_ms = out["info"]["loop_ms"]
+    if dist:
+        tt = torch.tensor([ms, loop_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms, loop_ms = float(tt[0]), float(tt[1])
+    value = M * N * args.steps / (ms / 1e3)
+
+    # ---- per-kernel timing (CUDA events on the library's stream, same workload, no graph)
+    prof_iters = min(args.steps, 20)
+    q.qdt_profile_enable(ctx, True)
+    solve(prof_iters)
+    kern = {}
+    for name in ["fwd_partial", "reduce_R", "bwd_step", "scalars", "allreduce_R", "halo"]:
+        c, t = q.qdt_profile_get(ctx, name)
+        if c:
+            kern[name] = {"count": c, "avg_ms": t / c}
+    q.qdt_profile_enable(ctx, False)
+    # dominant kernel roofline (HBM bound; achieved = algorithmic bytes / avg launch time)
+    hbm, src = peaks()
+    ab = algorithmic_bytes(rows_local, N, D, nnz_local)
+    dom = max(("bwd_step", "fwd_partial"), key=lambda k: kern.get(k, {}).get("avg_ms", 0))
+    dom_ms = kern[dom]["avg_ms"] if dom in kern else float("nan")
+    achieved = ab[dom] / (dom_ms / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f)
+        traffic = tr.get(args.config, {}).get(dom)
+    except Exception:
+        pass
+    for k in kern:
+        if k in ab:
+            kern[k]["achieved_gbs"] = ab[k] / (kern[k]["avg_ms"] / 1e3) / 1e9
+
+    # ---- end to end through the public API with HOST buffers (pinned), per solve call
+    e2e = None
+    if not args.no_e2e:
+        P_host = torch.tensor(I.P).pin_memory()
+        a_host = torch.tensor(I.alpha2).pin_memory()
+        th_host = torch.empty((rows_local, N), dtype=torch.float64).pin_memory()
+        barrier()
+        t0 = time.perf_counter()
+        e0.record(stream)
+        F2 = q.qdt_build_probes(ctx, a_host.numpy(), M)
+        q.qdt_solve(ctx, F2, P_host.numpy(), I.gamma, 0.0, args.steps, theta_out=th_host.numpy())
+        e1.record(stream)
+        barrier()
+        e2e_ms = max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3)
+        if dist:
+            tt = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_ms = float(tt[0])
+        del F2
+        e2e = {"value": M * N * args.steps / (e2e_ms / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(8 * D * N + 8 * D),
+               "d2h_bytes_per_step": int(8 * rows_local * N + 8 * (args.steps + 1) * 2),
+               "ms": e2e_ms,
+               "step": "one qdt_build_probes + qdt_solve(K iterations) call with host alpha2/P/"
+                       "theta (pinned); bytes are per call"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (qdt_synth, seed 0)",
+        "config": {"workload": args.config, "M": M, "N": N, "D": D, "gamma": I.gamma,
+                   "nnz": int(nnz_local) if world == 1 else None, "step_mode": "SQS",
+                   "parallelism": f"fock-shard{world}" if world > 1 else "single",
+                   "l2": "Theta (8*M*N bytes) > 126 MB L2; no flush needed"},
+        "loop_ms_per_step": loop_ms / args.steps,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
+                     "peak_source": src, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": traffic, "alg_bytes_per_launch": ab[dom]},
+        "kernels": kern,
+        "iteration_roofline": {"alg_bytes": ab["iteration"],
+                               "achieved_gbs": ab["iteration"] / (ms / args.steps / 1e3) / 1e9,
+                               "frac": ab["iteration"] / (ms / args.steps / 1e3) / 1e9 / hbm},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "final_objective": float(out["trace"][-1]),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(I, args)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------------------ oracle legs
+def _slab_sample(I, Fo, n_slabs, rows_per_slab):
+    """Sub-problems on S evenly spaced Fock-row slabs: the probes whose bands meet a slab, their
+    bands clipped to it.  Same per-element arithmetic as a full oracle iteration."""
+    import numpy as np
+    slabs = []
+    M = I.M
+    for j in range(n_slabs):
+        a = int((j + 0.5) * M / n_slabs - rows_per_slab / 2)
+        a = max(0, min(M - rows_per_slab, a))
+        b = a + rows_per_slab
+        lo, hi = Fo.lo, Fo.lo + Fo.len - 1
+        ds = np.nonzero((hi >= a) & (lo < b))[0]
+        l2 = np.maximum(lo[ds], a)
+        h2 = np.minimum(hi[ds], b - 1)
+        ln = h2 - l2 + 1
+        off = np.concatenate([[0], np.cumsum(ln)]).astype(np.int64)
+        val = np.concatenate([Fo.val[Fo.off[d] + (l2[i] - lo[d]): Fo.off[d] + (h2[i] - lo[d]) + 1]
+                              for i, d in enumerate(ds)]) if len(ds) else np.zeros(0)
+        slabs.append(dict(lo=(l2 - a).astype(np.int64), len=ln.astype(np.int64), off=off,
+                          val=np.ascontiguousarray(val), D=len(ds), M=rows_per_slab,
+                          P=np.ascontiguousarray(I.P[ds])))
+    return slabs
+
+
+def _oracle_slab_step(o, s, theta, t, gamma):
+    """One oracle iteration on a slab sub-problem: R = F Theta - P; G = F^T R + gamma L Theta;
+    Theta <- P_S(Theta - t G) (oracle functions, in or_solve's order)."""
+    import numpy as np
+    L = o.lib()
+    N = theta.shape[1]
+    R = np.empty((s["D"], N))
+    L.or_forward(s["lo"], s["len"], s["off"], s["val"], s["D"], theta, s["P"].ctypes.data, N, R)
+    G = np.empty_like(theta)
+    L.or_backward(s["lo"], s["len"], s["off"], s["val"], s["D"], s["M"], R, theta, N, gamma, G)
+    X = theta - t[:, None] * G
+    L.or_project_rows(np.ascontiguousarray(X), s["M"], N, theta)
+
+
+def _oracle_sample_run(I, steps, warmup, rows_total, n_slabs=20):
+    import numpy as np
+
+    import oracle as o
+    Fo = o.Probes(I.alpha2, I.M)
+    rows = max(64, rows_total // n_slabs)
+    slabs = _slab_sample(I, Fo, n_slabs, rows)
+    thetas, ts = [], []
+    for s in slabs:
+        w = np.empty(s["M"])
+        o.lib().or_sqs_weights(s["lo"], s["len"], s["off"], s["val"], s["D"], s["M"], I.gamma, w)
+        ts.append(np.where(w > 0, 1.0 / np.where(w > 0, w, 1.0), 0.0))
+        thetas.append(np.full((s["M"], I.N), 1.0 / I.N))
+    for _ in range(warmup):
+        for s, th, t in zip(slabs, thetas, ts):
+            _oracle_slab_step(o, s, th, t, I.gamma)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        for s, th, t in zip(slabs, thetas, ts):
+            _oracle_slab_step(o, s, th, t, I.gamma)
+    dt = time.perf_counter() - t0
+    upd = steps * n_slabs * rows * I.N
+    return upd / dt, dt, n_slabs * rows
+
+
+def cpu_baseline(I, args):
+    """Oracle timed on this host (one thread), bounded sample (~10-30 s of CPU work)."""
+    try:
+        rows = min(I.M, 60000)
+        v, dt, r = _oracle_sample_run(I, 3, 1, rows)
+        return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                "sample": f"3 oracle iterations (SQS) on {r} Fock rows = 20 evenly spaced slabs of "
+                          f"the {args.config} instance ({dt:.1f} s)",
+                "host_cpu": _cpu_model(), "nproc": os.cpu_count()}
+    except Exception as e:  # pragma: no cover
+        return {"value": None, "unit": UNIT, "cores": 1, "kind": "oracle", "error": repr(e)}
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_reference(args):
+    rank, _, world = env_rank()
+    if rank != 0:
+        return
+    import qdt_synth as qs
+    I = qs.CONFIGS[args.config]()
+    # size the per-step sample so that (steps + warmup) steps take ~150 s single-threaded
+    # (measured oracle cost ~8.5 us per row-iteration at N = 100)
+    per_row = 8.5e-6 * I.N / 100
+    rows = int(150.0 / max(1, args.steps + args.warmup) / per_row)
+    rows = max(20 * 64, min(I.M, rows))
+    v, dt, r = _oracle_sample_run(I, args.steps, args.warmup, rows)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (qdt_synth, seed 0)",
+            "config": {"workload": args.config, "M": I.M, "N": I.N, "D": I.D, "gamma": I.gamma,
+                       "step_mode": "SQS", "parallelism": "single-thread oracle"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"each step = one oracle iteration on {r} Fock rows "
+                                       f"(20 evenly spaced slabs)", "host_cpu": _cpu_model()},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="qdt", choices=["qdt", "reference"])
+    ap.add_argument("--config", default="megascale", choices=["tiny", "medium", "large",
+                                                              "megascale"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_qdt(args)
+
+
+if __name__ == "__main__":
+    main()

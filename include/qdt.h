@@ -98,9 +98,18 @@ typedef struct {
     int64_t nnz;           /* stored entries of F on this rank                                  */
     double min_row_mass;   /* min_d sum_k F_{d,k} over stored bands (truncation diagnostic)    */
     int64_t uncovered_rows;/* Fock rows (this rank) touched by no probe band (reading R9)      */
+    double loop_ms;        /* CUDA-event time of the iteration loop on ctx's stream            */
 } qdt_solve_info;
 
 /* ------------------------------------------------------------------------------ context */
+/* Write a fresh 128-byte NCCL unique id (rank 0 of a multi-GPU job calls this and
+ * broadcasts it).  Errors: NCCL unavailable -> QDT_ERR_NCCL. */
+qdt_status qdt_nccl_unique_id(void *out128);
+/* Host-only Fock-axis shard planner (used by qdt_build_probes; exported for tests): given
+ * band edges lo[D], hi[D] (inclusive, global rows), cut [0, M) into nranks contiguous
+ * slices at equal prefix sums of the per-row cost 16 + 0.7 cov(k).  cuts: int64[nranks+1]. */
+qdt_status qdt_shard_cuts(const int64_t *lo, const int64_t *hi, int64_t D, int64_t M,
+                          int32_t nranks, int64_t *cuts);
 /* Create a context on opts->device.  nranks > 1 initialises an NCCL communicator from
  * opts->nccl_unique_id (collective over all ranks).  opts == NULL -> device 0, 1 rank. */
 qdt_status qdt_init(qdt_ctx **ctx, const qdt_init_opts *opts);

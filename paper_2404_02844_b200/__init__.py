@@ -29,7 +29,7 @@ STATUS = {0: "QDT_OK", 1: "QDT_ERR_INVALID_ARG", 2: "QDT_ERR_UNSORTED", 3: "QDT_
 ABI_SYMBOLS = ["qdt_init", "qdt_finalize", "qdt_last_error", "qdt_build_probes", "qdt_probes_free",
                "qdt_probes_export", "qdt_solve", "qdt_objective", "qdt_residual", "qdt_gradient",
                "qdt_step", "qdt_project_rows", "qdt_step_setup", "qdt_profile_enable",
-               "qdt_profile_get", "qdt_launch_count"]
+               "qdt_profile_get", "qdt_launch_count", "qdt_nccl_unique_id", "qdt_shard_cuts"]
 
 
 class QdtError(RuntimeError):
@@ -60,7 +60,8 @@ class SolveInfo(ctypes.Structure):
                 ("kkt0", ctypes.c_double), ("kkt", ctypes.c_double), ("kkt_paper", ctypes.c_double),
                 ("f_final", ctypes.c_double), ("step_scalar", ctypes.c_double),
                 ("k_begin", ctypes.c_int64), ("k_end", ctypes.c_int64), ("nnz", ctypes.c_int64),
-                ("min_row_mass", ctypes.c_double), ("uncovered_rows", ctypes.c_int64)]
+                ("min_row_mass", ctypes.c_double), ("uncovered_rows", ctypes.c_int64),
+                ("loop_ms", ctypes.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -96,6 +97,8 @@ def load_library(path: str = LIB_PATH):
     L.qdt_profile_enable.argtypes = [vp, i32]
     L.qdt_profile_get.argtypes = [vp, ctypes.c_char_p, P(i64), P(f64)]
     L.qdt_launch_count.argtypes = [vp, P(i64)]
+    L.qdt_nccl_unique_id.argtypes = [vp]
+    L.qdt_shard_cuts.argtypes = [vp, vp, i64, i64, i32, vp]
     for s in ABI_SYMBOLS:
         if s != "qdt_last_error":
             getattr(L, s).restype = ctypes.c_int
@@ -294,3 +297,21 @@ def qdt_launch_count(ctx: Context) -> int:
     c = ctypes.c_int64()
     _check(ctx, load_library().qdt_launch_count(ctx.ptr, ctypes.byref(c)))
     return c.value
+
+
+def qdt_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    st = load_library().qdt_nccl_unique_id(buf)
+    if st != 0:
+        raise QdtError(st, (load_library().qdt_last_error(None) or b"").decode())
+    return buf.raw
+
+
+def qdt_shard_cuts(lo, hi, M: int, nranks: int):
+    lo_, hi_ = _host(lo, np.int64), _host(hi, np.int64)
+    cuts = np.zeros(nranks + 1, np.int64)
+    st = load_library().qdt_shard_cuts(lo_.ctypes.data, hi_.ctypes.data, lo_.shape[0], int(M),
+                                       int(nranks), cuts.ctypes.data)
+    if st != 0:
+        raise QdtError(st, (load_library().qdt_last_error(None) or b"").decode())
+    return cuts

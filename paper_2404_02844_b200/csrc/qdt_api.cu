@@ -40,6 +40,7 @@ struct NcclApi {
     nccl_result_t (*send)(const void *, size_t, int, int, nccl_comm_t, cudaStream_t) = nullptr;
     nccl_result_t (*recv)(void *, size_t, int, int, nccl_comm_t, cudaStream_t) = nullptr;
     nccl_result_t (*groupStart)() = nullptr;
+    nccl_result_t (*getUniqueId)(nccl_uid_t *) = nullptr;
     nccl_result_t (*groupEnd)() = nullptr;
     const char *(*getErrorString)(nccl_result_t) = nullptr;
     bool load(std::string &err)
@@ -66,6 +67,7 @@ struct NcclApi {
         QDT_SYM(groupStart, "ncclGroupStart");
         QDT_SYM(groupEnd, "ncclGroupEnd");
         QDT_SYM(getErrorString, "ncclGetErrorString");
+        QDT_SYM(getUniqueId, "ncclGetUniqueId");
 #undef QDT_SYM
         return true;
     }
@@ -94,7 +96,7 @@ struct qdt_ctx {
 };
 
 struct Plan {
-    int N = 0, T = 0, CG = 0, RG = 0, TC = 0, KC = 0, KR = 0, TF = 0, nthr = 0;
+    int N = 0, T = 0, CG = 0, RG = 0, TC = 0, KC = 0, KR = 0, TF = 0, nthr = 0, SEG = 32;
     int ntiles = 0;
     int32_t *d_tile_dA = nullptr, *d_tile_dB = nullptr;
     int nbunits = 0;
@@ -234,6 +236,18 @@ static void flush_profile(qdt_ctx *ctx)
 }
 
 // ------------------------------------------------------------------------------ context
+extern "C" qdt_status qdt_nccl_unique_id(void *out128)
+{
+    if (!out128) return fail(nullptr, QDT_ERR_INVALID_ARG, "qdt_nccl_unique_id: NULL");
+    std::string err;
+    if (!g_nccl.load(err)) return fail(nullptr, QDT_ERR_NCCL, "%s", err.c_str());
+    nccl_uid_t uid;
+    nccl_result_t r = g_nccl.getUniqueId(&uid);
+    if (r != 0) return fail(nullptr, QDT_ERR_NCCL, "ncclGetUniqueId: %s", g_nccl.getErrorString(r));
+    memcpy(out128, &uid, sizeof uid);
+    return QDT_OK;
+}
+
 extern "C" qdt_status qdt_init(qdt_ctx **out, const qdt_init_opts *o)
 {
     qdt_ctx *ctx = nullptr;
@@ -369,6 +383,24 @@ static void shard_bounds(const std::vector<int32_t> &lo, const std::vector<int32
     for (int g = 1; g <= nranks; g++) cuts[g] = std::max(cuts[g], cuts[g - 1]);
 }
 
+extern "C" qdt_status qdt_shard_cuts(const int64_t *lo, const int64_t *hi, int64_t D, int64_t M,
+                                     int32_t nranks, int64_t *cuts)
+{
+    if (!lo || !hi || !cuts || D < 1 || M < 1 || nranks < 1)
+        return fail(nullptr, QDT_ERR_INVALID_ARG, "qdt_shard_cuts: bad arguments");
+    std::vector<int32_t> l(D), h(D);
+    for (int64_t d = 0; d < D; d++) {
+        if (lo[d] < 0 || hi[d] < lo[d] || hi[d] >= M)
+            return fail(nullptr, QDT_ERR_INVALID_ARG, "qdt_shard_cuts: band %lld invalid", (long long)d);
+        l[d] = (int32_t)lo[d];
+        h[d] = (int32_t)hi[d];
+    }
+    std::vector<int64_t> c;
+    shard_bounds(l, h, M, nranks, c);
+    for (int g = 0; g <= nranks; g++) cuts[g] = c[g];
+    return QDT_OK;
+}
+
 static qdt_status build_plan(qdt_ctx *ctx, qdt_probes *p, int N, Plan **out)
 {
     auto it = p->plans.find(N);
@@ -382,6 +414,9 @@ static qdt_status build_plan(qdt_ctx *ctx, qdt_probes *p, int N, Plan **out)
     if (pl->CG * pl->RG > 1024)
         return fail(ctx, QDT_ERR_INVALID_ARG, "N = %d too large for this build (max 8192)", N);
     pl->T = pl->RG * TR;
+    // row-epilogue segment: smallest power of two with ceil(N/SEG) <= 16 values per lane
+    pl->SEG = 1;
+    while (pl->SEG < 32 && (N + pl->SEG - 1) / pl->SEG > 16) pl->SEG <<= 1;
     pl->KC = std::min(32, std::max(2, 800 / N));
     pl->KR = std::min(32, std::max(4, 2048 / N));
     pl->TF = 256;
@@ -403,7 +438,7 @@ static qdt_status build_plan(qdt_ctx *ctx, qdt_probes *p, int N, Plan **out)
     for (int t = 0; t < ntiles; t++)
         if (dA[t] == INT32_MAX) dA[t] = dB[t] = 0;
     // split cap: windows wider than Wcap probes are split along the probe axis
-    const int Wcap = std::max(64, 4 * pl->KC);
+    const int Wcap = std::min(WCAP_MAX, std::max(64, 4 * pl->KC));
     std::vector<BwdUnit> bu;
     bu.reserve(ntiles + 64);
     int64_t slot = 0;
@@ -794,6 +829,7 @@ static BwdArgs bwd_args(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, const doub
     a.CG = pl->CG;
     a.RG = pl->RG;
     a.KC = pl->KC;
+    a.SEG = pl->SEG;
     a.units = pl->d_bunits;
     a.band = c.p->band();
     a.R = R;
@@ -1003,7 +1039,7 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
         CK(launch_fill(b.theta[0], Ml * N, 1.0 / (double)N, s));
         ctx->launches++;
     }
-    IterCfg c{p, pl, (int)N, gamma, tol, fista, fista ? opt.kkt_every : 1, tl};
+    IterCfg c{p, pl, (int)N, gamma, tol, fista, opt.kkt_every, tl};
     CKS(halo_exchange(ctx, c, b.theta[0]));
     if (fista) CK(cudaMemcpyAsync(b.theta[2] - N, b.theta[0] - N, sizeof(double) * rowsz, cudaMemcpyDeviceToDevice, s));
     double tscalar = 0.0;
@@ -1035,6 +1071,10 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
         CK(cudaGraphInstantiate(&gexec, g, 0));
         cudaGraphDestroy(g);
     }
+    cudaEvent_t ev0, ev1;
+    CK(cudaEventCreate(&ev0));
+    CK(cudaEventCreate(&ev1));
+    CK(cudaEventRecord(ev0, s));
     const int64_t check = tol > 0.0 ? std::max<int64_t>(period, (opt.check_every / period) * period) : INT64_MAX;
     int64_t since = 0;
     while (done < iters) {
@@ -1058,6 +1098,7 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
             }
         }
     }
+    CK(cudaEventRecord(ev1, s));
     if (gexec) cudaGraphExecDestroy(gexec);
     // ---- final evaluation at Theta_iters (if no early stop)
     CK(cudaMemcpyAsync(&hst, b.state, sizeof hst, cudaMemcpyDeviceToHost, s));
@@ -1066,6 +1107,7 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     if (!stopped) {
         IterCfg cf = c;
         cf.fista = 0;
+        cf.kkt_every = 1;
         double *cur = b.theta[iters % nbuf];
         CKS(fwd_reduce(ctx, cf, b, cur, b.R[0], true));
         BwdArgs a = bwd_args(ctx, cf, b, b.R[0], cur, nullptr, nullptr, false);
@@ -1117,7 +1159,12 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
         info->nnz = p->nnz;
         info->min_row_mass = p->min_row_mass;
         info->uncovered_rows = p->uncovered;
+        float lm = 0.f;
+        cudaEventElapsedTime(&lm, ev0, ev1);
+        info->loop_ms = lm;
     }
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
     (void)stopped;
     return QDT_OK;
 }

@@ -56,6 +56,7 @@ struct DevState {
 
 struct BwdArgs {
     int N, CG, RG, KC;
+    int SEG;                   // lanes per Fock row in the row epilogue (power of two <= 32)
     const BwdUnit *units;
     Band band;
     const double *R;
@@ -108,6 +109,7 @@ cudaError_t prepare_kernels();
 int fwd_threads(int N, int *CG, int *RG, int *TC);
 int bwd_threads(int N, int *CG, int *RG, int *TC);
 constexpr int TR = 4;  // rows (bwd) / probes (fwd) per thread
+constexpr int WCAP_MAX = 128;  // max probes per work unit (split cap / fwd group)
 
 cudaError_t launch_fwd(const FwdArgs &a, int nunits, int TC, cudaStream_t s, size_t *smem_out);
 cudaError_t launch_bwd(const BwdArgs &a, int nunits, int TC, int mode, cudaStream_t s);

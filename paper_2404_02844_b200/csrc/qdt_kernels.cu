@@ -76,6 +76,53 @@ __device__ __forceinline__ void block_sum(double (&v)[NV_], double *red /* smem 
     }
 }
 
+// Segment (SEG lanes, power of two, aligned inside a warp) reductions: one Fock row per segment.
+__device__ __forceinline__ double seg_sum(double v, int SEG)
+{
+    for (int o = SEG >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ int seg_sum_i(int v, int SEG)
+{
+    for (int o = SEG >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double seg_max(double v, int SEG)
+{
+    for (int o = SEG >> 1; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ double seg_min(double v, int SEG)
+{
+    for (int o = SEG >> 1; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool pred)
+{
+    unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    int sz = pred ? 16 : 0;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz)
+                 : "memory");
+}
+// Stage n contiguous doubles src[0..n) into smem dst; elements outside [v0, v1) are zero-filled.
+// vec: 16-byte copies (n, v0, v1 even; src, dst 16-byte aligned).
+__device__ __forceinline__ void stage_run(double *dst, const double *src, int n, int v0, int v1,
+                                         const double *dummy, bool vec)
+{
+    if (vec) {
+        for (int c = threadIdx.x; c < (n >> 1); c += blockDim.x) {
+            const int i = c << 1;
+            const bool ok = i >= v0 && i < v1;
+            cp_async16(dst + i, ok ? src + i : dummy, ok);
+        }
+    } else {
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+            const bool ok = i >= v0 && i < v1;
+            cp_async8(dst + i, ok ? src + i : dummy, ok);
+        }
+    }
+}
+
 // Euclidean projection threshold of one row onto the simplex by
 // Michelot's method, one warp per row: tau_0 = (sum x - 1)/N; repeatedly keep A = {x > tau},
 // tau = (sum_A x - 1)/|A| until |A| stops shrinking (<= N rounds; A only shrinks).
@@ -145,10 +192,12 @@ __device__ __forceinline__ double stirlerr(double k)
     return (S0 - (S1 - (S2 - (S3 - S4 * k2) * k2) * k2) * k2) / k;
 }
 
-// Deviance term bd0(x, mu) = x ln(x/mu) + mu - x, by its series near x = mu.
+// Deviance term bd0(x, mu) = x ln(x/mu) + mu - x.  For |x - mu| < (x + mu)/2 it is summed as
+// the series (x-mu) v + 2x sum_j v^(2j+1)/(2j+1), v = (x-mu)/(x+mu) (no cancellation; v^2 <= 1/4
+// so ~27 terms at most); outside, the direct form cancels by at most a factor ~2.5.
 __device__ __forceinline__ double bd0(double x, double mu)
 {
-    if (fabs(x - mu) < 0.1 * (x + mu)) {
+    if (fabs(x - mu) < 0.5 * (x + mu)) {
         double v = (x - mu) / (x + mu);
         double s = (x - mu) * v;
         double ej = 2.0 * x * v;
@@ -292,6 +341,8 @@ template <int TC>
 __global__ void __launch_bounds__(256) k_fwd(FwdArgs a)
 {
     extern __shared__ __align__(16) double smem[];
+    __shared__ int32_t s_lo[WCAP_MAX], s_len[WCAP_MAX];
+    __shared__ int64_t s_off[WCAP_MAX];
     if (a.state && a.state->stop) return;
     const int N = a.N, CG = a.CG, RG = a.RG, KR = a.KR;
     const int KP = RG * TR, KPP = KP + 2;
@@ -306,30 +357,34 @@ __global__ void __launch_bounds__(256) k_fwd(FwdArgs a)
     const int nrows = u.k1 - u.k0;
     const int nch = (nrows + KR - 1) / KR;
 
+    const int lane = tid & 31, warp = tid >> 5, nw = nthr >> 5;
+    const bool vec = (N & 1) == 0;
+    for (int j = tid; j < np; j += nthr) {
+        s_lo[j] = a.band.lo[u.p0 + j];
+        s_len[j] = a.band.len[u.p0 + j];
+        s_off[j] = a.band.off[u.p0 + j];
+    }
+    __syncthreads();
     auto stage = [&](int buf, int c) {
         const int kbeg = u.k0 + c * KR;
         const int kr = min(KR, u.k1 - kbeg);
-        double *T = Tc + buf * tsz;
-        const double *src = a.theta + (int64_t)kbeg * N;
-        for (int i = tid; i < KR * N; i += nthr) {
-            bool ok = i < kr * N;
-            cp_async8(&T[i], ok ? src + i : a.theta, ok);
-        }
+        stage_run(Tc + buf * tsz, a.theta + (int64_t)kbeg * N, KR * N, 0, kr * N, a.theta, vec);
         double *F = Fc + buf * KR * KPP;
-        for (int i = tid; i < KP * KR; i += nthr) {
-            int p = i / KR, r = i - (i / KR) * KR;
-            int d = u.p0 + p;
-            bool ok = false;
-            const double *s = a.band.val;
-            if (p < np && r < kr) {
-                int64_t kg = a.kb + kbeg + r;
-                int lo = a.band.lo[d], len = a.band.len[d];
-                if (kg >= lo && kg < lo + len) {
-                    ok = true;
-                    s = a.band.val + a.band.off[d] + (kg - lo);
-                }
+        const int64_t kg0 = a.kb + kbeg;
+        for (int p = warp; p < KP; p += nw) {      // one warp per probe of the unit
+            const int d = u.p0 + p;
+            int ra = 0, rb = 0;
+            const double *src = a.band.val;
+            if (p < np) {
+                const int64_t lo = s_lo[p], len = s_len[p];
+                ra = (int)max((int64_t)0, lo - kg0);
+                rb = (int)min((int64_t)kr, lo + len - kg0);
+                src = a.band.val + s_off[p] + (kg0 - lo);
             }
-            cp_async8(&F[r * KPP + p], s, ok);
+            for (int r = lane; r < KR; r += 32) {
+                const bool ok = r >= ra && r < rb;
+                cp_async8(&F[r * KPP + p], ok ? src + r : a.band.val, ok);
+            }
         }
     };
 
@@ -346,7 +401,7 @@ __global__ void __launch_bounds__(256) k_fwd(FwdArgs a)
         cp_async_commit();
         cp_async_wait<1>();
         __syncthreads();
-        if (gth) {
+        if (gth && rg * TR < np) {
             const double *T = Tc + (c & 1) * tsz + cg;
             const double *F = Fc + (c & 1) * KR * KPP + rg * TR;
             const int kr = min(KR, nrows - c * KR);
@@ -434,12 +489,20 @@ __global__ void k_fista_rcomb(double *RY, const double *Rk, const double *Rkm1, 
 }
 
 // ------------------------------------------------------------------------------ S3-S6 bwd
-template <int TC, int MODE, bool FISTA>
+// One CTA per work unit (a Fock tile, or one probe-range split of a heavy tile):
+//   GEMM   G[T x N] = F_tile^T[T x W] R_win[W x N]  (thread (rg,cg): TR rows x TC columns)
+//   epi 1  G += gamma L Y   (stencil, eq. regul; free ends at k = 0, M-1, reading R8)
+//   epi 2  one SEG-lane segment per Fock row, the row held in registers:
+//          KKT partial (df = 2G), regulariser pair (k, k+1),
+//          X = Y - t_k G, Michelot threshold, Theta_next = max(X - tau, 0).
+template <int TC, int MODE, bool FISTA, int VMAX>
 __global__ void __launch_bounds__(256) k_bwd(BwdArgs a)
 {
     extern __shared__ __align__(16) double smem[];
     __shared__ double red[32 * NSC_TILE];
     __shared__ int s_last;
+    __shared__ int32_t s_lo[WCAP_MAX], s_len[WCAP_MAX];
+    __shared__ int64_t s_off[WCAP_MAX];
     const DevState *st = a.state;
     if (st && st->stop) return;
     const int64_t it = st ? st->it : 0;
@@ -449,13 +512,15 @@ __global__ void __launch_bounds__(256) k_bwd(BwdArgs a)
     const int N = a.N, CG = a.CG, RG = a.RG, KC = a.KC;
     const int T = RG * TR;
     const int tid = threadIdx.x, nthr = blockDim.x;
+    const int lane = tid & 31, warp = tid >> 5, nw = nthr >> 5;
     const int rg = tid / CG, cg = tid - (tid / CG) * CG;
     const bool gth = tid < RG * CG;
+    const bool vec = (N & 1) == 0;
     const BwdUnit u = a.units[blockIdx.x];
     const int k0 = u.k0, Tt = u.k1 - u.k0;
     const int thsz = (T + 2) * N;
-    const int rsz = KC * N + CG * TC;
-    double *Th = smem;                                 // (T+2) x N : Theta_k rows k0-1 .. k1
+    const int rsz = (KC * N + CG * TC + 1) & ~1;
+    double *Th = smem;                                 // (T+2) x N : rows k0-1 .. k1 of Theta_k
     double *Tp = Th + thsz;                            // FISTA: Theta_{k-1}
     double *Gs = FISTA ? Tp + thsz : Tp;               // T x N
     double *Fc = Gs + T * N;                           // 2 x KC x T
@@ -464,43 +529,43 @@ __global__ void __launch_bounds__(256) k_bwd(BwdArgs a)
 
     auto load_theta = [&]() {
         const int tot = (Tt + 2) * N;
+        const int64_t kg0 = a.kb + k0 - 1;               // global row of smem row 0
+        const int v0 = kg0 < 0 ? N : 0;
+        const int v1 = (kg0 + Tt + 1 >= a.M) ? (int)(a.M - kg0) * N : tot;
         const int64_t base = (int64_t)(k0 - 1) * N;
-        for (int i = tid; i < tot; i += nthr) {
-            int r = i / N;
-            int64_t kg = a.kb + k0 - 1 + r;
-            bool ok = kg >= 0 && kg < a.M;
-            cp_async8(&Th[i], ok ? a.theta + base + i : a.theta, ok);
-            if (FISTA) cp_async8(&Tp[i], ok ? a.theta_prev + base + i : a.theta, ok);
-        }
+        stage_run(Th, a.theta + base, tot, v0, v1, a.theta, vec);
+        if (FISTA) stage_run(Tp, a.theta_prev + base, tot, v0, v1, a.theta, vec);
     };
     if (u.nsplit == 1 && need_theta) load_theta();
     cp_async_commit();
+    for (int j = tid; j < u.p1 - u.p0; j += nthr) {   // band tables of the unit's probes
+        s_lo[j] = a.band.lo[u.p0 + j];
+        s_len[j] = a.band.len[u.p0 + j];
+        s_off[j] = a.band.off[u.p0 + j];
+    }
+    __syncthreads();
 
     auto stage = [&](int buf, int c) {
         const int pbeg = u.p0 + c * KC;
         double *F = Fc + buf * KC * T;
-        for (int i = tid; i < KC * T; i += nthr) {
-            int j = i / T, r = i - (i / T) * T;
-            int d = pbeg + j;
-            bool ok = false;
-            const double *s = a.band.val;
-            if (d < u.p1 && r < Tt) {
-                int64_t kg = a.kb + k0 + r;
-                int lo = a.band.lo[d], len = a.band.len[d];
-                if (kg >= lo && kg < lo + len) {
-                    ok = true;
-                    s = a.band.val + a.band.off[d] + (kg - lo);
-                }
+        const int64_t kg0 = a.kb + k0;
+        for (int j = warp; j < KC; j += nw) {      // one warp per probe of the chunk
+            const int d = pbeg + j;
+            int ra = 0, rb = 0;
+            const double *src = a.band.val;
+            if (d < u.p1) {
+                const int64_t lo = s_lo[d - u.p0], len = s_len[d - u.p0];
+                ra = (int)max((int64_t)0, lo - kg0);
+                rb = (int)min((int64_t)Tt, lo + len - kg0);
+                src = a.band.val + s_off[d - u.p0] + (kg0 - lo);
             }
-            cp_async8(&F[i], s, ok);
+            for (int r = lane; r < T; r += 32) {
+                const bool ok = r >= ra && r < rb;
+                cp_async8(&F[j * T + r], ok ? src + r : a.band.val, ok);
+            }
         }
-        double *Rr = Rc + buf * rsz;
         const int kc = min(KC, u.p1 - pbeg);
-        const double *src = a.R + (int64_t)pbeg * N;
-        for (int i = tid; i < KC * N; i += nthr) {
-            bool ok = i < kc * N;
-            cp_async8(&Rr[i], ok ? src + i : a.R, ok);
-        }
+        stage_run(Rc + buf * rsz, a.R + (int64_t)pbeg * N, KC * N, 0, kc * N, a.R, vec);
     };
 
     double acc[TR][TC];
@@ -579,89 +644,210 @@ __global__ void __launch_bounds__(256) k_bwd(BwdArgs a)
     cp_async_wait<0>();
     __syncthreads();
 
-    // ---- epilogue 1: G = acc + gamma L Y   (eq. regul; free ends, reading R8)
-    auto Yv = [&](int r, int n) -> double {
-        double t = Th[r * N + n];
-        if (FISTA) t = t + beta * (t - Tp[r * N + n]);
-        return t;
-    };
+    // ---- epilogue 1: park the GEMM result in shared memory (row pass below adds the stencil)
     if (gth) {
 #pragma unroll
         for (int i = 0; i < TR; i++) {
             const int row = rg * TR + i;
-            if (row >= Tt) continue;
-            const int64_t kg = a.kb + k0 + row;
 #pragma unroll
             for (int cc = 0; cc < TC; cc++) {
                 const int n = cg + cc * CG;
-                if (n >= N) continue;
-                double g = acc[i][cc];
-                if (a.gamma != 0.0) {
-                    double yc = Yv(row + 1, n), lap = 0.0;
-                    if (kg > 0) lap += yc - Yv(row, n);
-                    if (kg < a.M - 1) lap += yc - Yv(row + 2, n);
-                    g = fma(a.gamma, lap, g);
-                }
-                if (MODE == BWD_GRAD)
-                    a.out[(int64_t)(k0 + row) * N + n] = g;
-                else
-                    Gs[row * N + n] = g;
+                if (row < Tt && n < N) Gs[row * N + n] = acc[i][cc];
             }
+        }
+    }
+    __syncthreads();
+
+    // ---- epilogue 2: one SEG-lane segment per Fock row, row values in registers:
+    //      G = acc + gamma L Y (eq. regul, free ends at global k = 0, M-1: reading R8),
+    //      regulariser pair (k, k+1), KKT partial (df = 2G, reading R7),
+    //      X = Y - t_k G, Michelot threshold (reading R4), Theta_next = max(X - tau, 0).
+    double sc[NSC_TILE] = {0.0, 0.0, 0.0, 0.0};
+    const bool do_kkt = ((MODE == BWD_EVAL) || !FISTA) && (it % a.kkt_every) == 0;
+    const double gamma = a.gamma;
+    if constexpr (VMAX > 0) {
+        const int SEG = a.SEG;
+        // rows per pass: as many segments as fill the tile in the fewest passes; warps beyond
+        // them skip the row pass (idle warps cost no issue slots)
+        const int maxseg = nthr / SEG;
+        const int passes = (Tt + maxseg - 1) / maxseg;
+        const int nseg = passes ? (Tt + passes - 1) / passes : 1;
+        const int seg = tid / SEG, sl = tid & (SEG - 1);
+        bool colok[VMAX];
+#pragma unroll
+        for (int v = 0; v < VMAX; v++) colok[v] = sl + SEG * v < N;
+        if ((warp * 32) / SEG >= nseg) goto rowpass_done;   // warp-uniform
+        for (int rb = 0; rb < Tt; rb += nseg) {
+            const int row = rb + seg;
+            const bool act = row < Tt && seg < nseg && row < rb + nseg;
+            const int kl = k0 + row;
+            const int64_t kg = a.kb + kl;
+            const bool has_prev = kg > 0, has_next = kg + 1 < a.M;
+            const double *thr = Th + (row + 1) * N + sl;
+            double th[VMAX], g[VMAX];
+#pragma unroll
+            for (int v = 0; v < VMAX; v++) {
+                const bool ok = act && colok[v];
+                const double t0 = ok ? thr[SEG * v] : 0.0;
+                const double tn = (ok && has_next) ? thr[SEG * v + N] : t0;
+                double gg = ok ? Gs[row * N + sl + SEG * v] : 0.0;
+                if (has_next) {
+                    const double dd = t0 - tn;
+                    sc[SC_REG] += dd * dd;
+                }
+                if (gamma != 0.0) {
+                    const double tp = (ok && has_prev) ? thr[SEG * v - N] : t0;
+                    double lap;
+                    if (FISTA) {
+                        const double *tq = Tp + (row + 1) * N + sl + SEG * v;
+                        const double y0 = t0 + beta * (t0 - (ok ? tq[0] : 0.0));
+                        const double yp = has_prev ? tp + beta * (tp - (ok ? tq[-N] : 0.0)) : y0;
+                        const double yn = has_next ? tn + beta * (tn - (ok ? tq[N] : 0.0)) : y0;
+                        lap = (y0 - yp) + (y0 - yn);
+                    } else {
+                        lap = (t0 - tp) + (t0 - tn);
+                    }
+                    gg = fma(gamma, lap, gg);
+                }
+                th[v] = t0;
+                g[v] = gg;
+            }
+            if (MODE == BWD_GRAD) {
+                if (act) {
+                    double *o = a.out + (int64_t)kl * N + sl;
+#pragma unroll
+                    for (int v = 0; v < VMAX; v++)
+                        if (colok[v]) o[SEG * v] = g[v];
+                }
+                continue;
+            }
+            if (do_kkt) {
+                double mn = INFINITY;
+#pragma unroll
+                for (int v = 0; v < VMAX; v++)
+                    if (colok[v]) mn = fmin(mn, g[v]);
+                mn = 2.0 * seg_min(mn, SEG);
+                const double lam = act ? -mn : 0.0, lamp = fmax(lam, 0.0);
+#pragma unroll
+                for (int v = 0; v < VMAX; v++) {
+                    const double df = 2.0 * g[v];
+                    const double x1 = th[v] * (df + lam), x2 = th[v] * (df + lamp);
+                    sc[SC_KKT] += x1 * x1;
+                    sc[SC_KKTP] += x2 * x2;
+                }
+            }
+            if (MODE == BWD_STEP) {
+                const double t = act ? a.tstep[kl] : 0.0;
+                double s = 0.0, xm = -INFINITY;
+#pragma unroll
+                for (int v = 0; v < VMAX; v++) {
+                    const bool ok = act && colok[v] && (seg < nseg);
+                    double y = th[v];
+                    if (FISTA && ok) y = y + beta * (y - Tp[(row + 1) * N + sl + SEG * v]);
+                    const double xv = y - t * g[v];
+                    g[v] = ok ? xv : -INFINITY;
+                    s += ok ? xv : 0.0;
+                    xm = fmax(xm, g[v]);
+                }
+                s = seg_sum(s, SEG);
+                xm = seg_max(xm, SEG);
+                // start from the larger of two lower bounds of the threshold: the mean bound
+                // (sum x - 1)/N and max x - 1 (the largest coordinate projects to <= 1); from a
+                // lower bound the Michelot/Newton updates increase monotonically to tau*.
+                int cnt = N + 1;
+                double tau = fmax((s - 1.0) / (double)N, xm - 1.0);
+                bool done = !act || seg >= nseg;
+                for (int round = 0; round <= N; round++) {
+                    if (__all_sync(0xffffffffu, done)) break;
+                    double ps = 0.0;
+                    int pc = 0;
+#pragma unroll
+                    for (int v = 0; v < VMAX; v++) {
+                        const bool in = g[v] > tau;
+                        ps += in ? g[v] : 0.0;
+                        pc += in;
+                    }
+                    ps = seg_sum(ps, SEG);
+                    pc = seg_sum_i(pc, SEG);
+                    if (!done) {
+                        if (pc >= cnt) {
+                            done = true;
+                        } else {
+                            cnt = pc;
+                            tau = (ps - 1.0) / (double)pc;
+                        }
+                    }
+                }
+                if (act && seg < nseg) {
+                    double *o = a.out + (int64_t)kl * N + sl;
+#pragma unroll
+                    for (int v = 0; v < VMAX; v++)
+                        if (colok[v]) o[SEG * v] = fmax(g[v] - tau, 0.0);
+                }
+            }
+        }
+    rowpass_done:;
+    } else {
+        // wide rows (N > 512): one warp per row, values streamed from shared memory
+        for (int row = warp; row < Tt; row += nw) {
+            const int kl = k0 + row;
+            const int64_t kg = a.kb + kl;
+            double *g = Gs + row * N;
+            const double *th = Th + (row + 1) * N;
+            if (gamma != 0.0)
+                for (int n = lane; n < N; n += 32) {
+                    auto Y = [&](int r) {
+                        double t = Th[r * N + n];
+                        if (FISTA) t = t + beta * (t - Tp[r * N + n]);
+                        return t;
+                    };
+                    const double yc = Y(row + 1);
+                    double lap = 0.0;
+                    if (kg > 0) lap += yc - Y(row);
+                    if (kg < a.M - 1) lap += yc - Y(row + 2);
+                    g[n] = fma(gamma, lap, g[n]);
+                }
+            if (MODE == BWD_GRAD) {
+                for (int n = lane; n < N; n += 32) a.out[(int64_t)kl * N + n] = g[n];
+                continue;
+            }
+            if (kg + 1 < a.M)
+                for (int n = lane; n < N; n += 32) {
+                    const double dd = th[n] - th[n + N];
+                    sc[SC_REG] += dd * dd;
+                }
+            if (do_kkt) {
+                double mn = INFINITY;
+                for (int n = lane; n < N; n += 32) mn = fmin(mn, 2.0 * g[n]);
+                mn = warp_min(mn);
+                const double lam = -mn, lamp = fmax(lam, 0.0);
+                for (int n = lane; n < N; n += 32) {
+                    const double df = 2.0 * g[n];
+                    const double x1 = th[n] * (df + lam), x2 = th[n] * (df + lamp);
+                    sc[SC_KKT] += x1 * x1;
+                    sc[SC_KKTP] += x2 * x2;
+                }
+            }
+            if (MODE == BWD_STEP) {
+                const double t = a.tstep[kl];
+                double s = 0.0;
+                for (int n = lane; n < N; n += 32) {
+                    double y = th[n];
+                    if (FISTA) y = y + beta * (y - Tp[(row + 1) * N + n]);
+                    const double x = y - t * g[n];
+                    g[n] = x;
+                    s += x;
+                }
+                __syncwarp();
+                s = warp_sum(s);
+                const double tau = michelot_tau(g, N, s);
+                double *o = a.out + (int64_t)kl * N;
+                for (int n = lane; n < N; n += 32) o[n] = fmax(g[n] - tau, 0.0);
+            }
+            __syncwarp();
         }
     }
     if (MODE == BWD_GRAD) return;
-    __syncthreads();
-
-    // ---- epilogue 2: one warp per Fock row: KKT, regul, step, projection, write
-    const int lane = tid & 31, warp = tid >> 5, nw = nthr >> 5;
-    double sc[NSC_TILE] = {0.0, 0.0, 0.0, 0.0};
-    const bool do_kkt = (MODE == BWD_EVAL) || !FISTA;
-    for (int row = warp; row < Tt; row += nw) {
-        const int kl = k0 + row;
-        const int64_t kg = a.kb + kl;
-        double *g = Gs + row * N;
-        const double *th = Th + (row + 1) * N;
-        if (kg + 1 < a.M) {  // pair (kg, kg+1) of eq. regul, at Theta_k
-            const double *th1 = th + N;
-            for (int n = lane; n < N; n += 32) {
-                double dd = th[n] - th1[n];
-                sc[SC_REG] += dd * dd;
-            }
-        }
-        if (do_kkt) {  // PAPER.md:565-567 with df = 2G
-            double mn = INFINITY;
-            for (int n = lane; n < N; n += 32) mn = fmin(mn, 2.0 * g[n]);
-            mn = warp_min(mn);
-            const double lam = -mn, lamp = fmax(lam, 0.0);
-            for (int n = lane; n < N; n += 32) {
-                double df = 2.0 * g[n];
-                double x1 = th[n] * (df + lam), x2 = th[n] * (df + lamp);
-                sc[SC_KKT] += x1 * x1;
-                sc[SC_KKTP] += x2 * x2;
-            }
-        }
-        if (MODE == BWD_STEP) {
-            const double t = a.tstep[kl];
-            double s = 0.0;
-            for (int n = lane; n < N; n += 32) {
-                double y = FISTA ? th[n] + beta * (th[n] - Tp[(row + 1) * N + n]) : th[n];
-                double x = y - t * g[n];
-                g[n] = x;
-                s += x;
-            }
-            __syncwarp();
-            s = warp_sum(s);
-            const double tau = michelot_tau(g, N, s);
-            double *o = a.out + (int64_t)kl * N;
-            for (int n = lane; n < N; n += 32) {
-                double y = fmax(g[n] - tau, 0.0);
-                o[n] = y;
-                double dd = y - th[n];
-                sc[SC_DTH] += dd * dd;
-            }
-        }
-        __syncwarp();
-    }
     block_sum<NSC_TILE>(sc, red);
     if (tid == 0) {
         double *p = a.part + (int64_t)u.tile * NSC_TILE;
@@ -833,7 +1019,7 @@ size_t bwd_smem_bytes(int N, int RG, int KC, bool fista)
     pick_shape(N, &CG, &RGx, &TC);
     const size_t T = (size_t)RG * TR;
     size_t el = (T + 2) * N * (fista ? 2 : 1) + T * N + 2 * (size_t)KC * T +
-                2 * ((size_t)KC * N + (size_t)CG * TC);
+                2 * (((size_t)KC * N + (size_t)CG * TC + 1) & ~(size_t)1);
     return el * sizeof(double);
 }
 size_t fwd_smem_bytes(int N, int RG, int KR)
@@ -853,16 +1039,27 @@ static cudaError_t fwd_tc(const FwdArgs &a, int nunits, int nthr, size_t smem, c
 }
 
 // opt every kernel with dynamic smem into the large carve-out (once, before any graph capture)
+template <int TC, int VM>
+static cudaError_t prep_bwd()
+{
+    const int big = 200 * 1024;
+    cudaError_t e = cudaFuncSetAttribute(k_bwd<TC, BWD_STEP, false, VM>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_bwd<TC, BWD_STEP, true, VM>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_bwd<TC, BWD_GRAD, false, VM>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_bwd<TC, BWD_EVAL, false, VM>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_bwd<TC, BWD_EVAL, true, VM>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    return e;
+}
 template <int TC>
 static cudaError_t prep_tc()
 {
     const int big = 200 * 1024;
     cudaError_t e = cudaFuncSetAttribute(k_fwd<TC>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_bwd<TC, BWD_STEP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_bwd<TC, BWD_STEP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_bwd<TC, BWD_GRAD, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_bwd<TC, BWD_EVAL, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_bwd<TC, BWD_EVAL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    if (e == cudaSuccess) e = prep_bwd<TC, 4>();
+    if (e == cudaSuccess) e = prep_bwd<TC, 8>();
+    if (e == cudaSuccess) e = prep_bwd<TC, 13>();
+    if (e == cudaSuccess) e = prep_bwd<TC, 16>();
+    if (e == cudaSuccess) e = prep_bwd<TC, 0>();
     return e;
 }
 cudaError_t prepare_kernels()
@@ -897,7 +1094,17 @@ cudaError_t launch_fwd(const FwdArgs &a, int nunits, int TC, cudaStream_t s, siz
 template <int TC, int MODE, bool FISTA>
 static cudaError_t bwd_tcm(const BwdArgs &a, int nunits, int nthr, size_t smem, cudaStream_t s)
 {
-    k_bwd<TC, MODE, FISTA><<<nunits, nthr, smem, s>>>(a);
+    const int vpl = (a.N + a.SEG - 1) / a.SEG;
+    if (vpl <= 4)
+        k_bwd<TC, MODE, FISTA, 4><<<nunits, nthr, smem, s>>>(a);
+    else if (vpl <= 8)
+        k_bwd<TC, MODE, FISTA, 8><<<nunits, nthr, smem, s>>>(a);
+    else if (vpl <= 13)
+        k_bwd<TC, MODE, FISTA, 13><<<nunits, nthr, smem, s>>>(a);
+    else if (vpl <= 16)
+        k_bwd<TC, MODE, FISTA, 16><<<nunits, nthr, smem, s>>>(a);
+    else
+        k_bwd<TC, MODE, FISTA, 0><<<nunits, nthr, smem, s>>>(a);
     return cudaGetLastError();
 }
 
