@@ -106,8 +106,22 @@ struct Plan {
     FwdUnit *d_funits = nullptr;
     int64_t nrpart = 0;
     int64_t *d_red_beg = nullptr, *d_red_rows = nullptr;
+    // sweep path (DMMA kernels, N <= 128): NB n-blocks; bwd/fwd units; reduce lists
+    int NB = 0;
+    int nR = 0;                       // partR entries written by the residual reduction
+    int sw_nbunits = 0;
+    SwUnit *d_swunits = nullptr;
+    int64_t sw_nslots = 0;
+    int sw_nfunits = 0;
+    FwUnit *d_fwunits = nullptr;
+    int64_t sw_nrpart = 0;
+    int64_t *d_sw_red_beg = nullptr, *d_sw_red_rows = nullptr;
     ~Plan()
     {
+        cudaFree(d_swunits);
+        cudaFree(d_fwunits);
+        cudaFree(d_sw_red_beg);
+        cudaFree(d_sw_red_rows);
         cudaFree(d_tile_dA);
         cudaFree(d_tile_dB);
         cudaFree(d_bunits);
@@ -132,9 +146,20 @@ struct qdt_probes {
     double min_row_mass = 1.0;
     int64_t uncovered = 0;
     std::map<int, std::unique_ptr<Plan>> plans;
+    // sweep tiling (independent of N): ST-row tiles, probe windows, tiled F blocks
+    int sw_ntiles = 0;
+    std::vector<int32_t> sw_dA, sw_dB;
+    std::vector<int64_t> sw_fboff;
+    int32_t *d_sw_dA = nullptr, *d_sw_dB = nullptr;
+    int64_t *d_fb_off = nullptr;
+    double *d_Fb = nullptr;
     Band band() const { return Band{d_lo, d_len, d_off, d_val}; }
     ~qdt_probes()
     {
+        cudaFree(d_sw_dA);
+        cudaFree(d_sw_dB);
+        cudaFree(d_fb_off);
+        cudaFree(d_Fb);
         cudaFree(d_alpha2);
         cudaFree(d_lo);
         cudaFree(d_len);
@@ -282,6 +307,7 @@ extern "C" qdt_status qdt_init(qdt_ctx **out, const qdt_init_opts *o)
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     c->nblkR = nsm * 4;
     CK(prepare_kernels());
+    CK(prepare_sweep_kernels());
     if (c->nranks > 1) {
         if (!o->nccl_unique_id)
             return fail(nullptr, QDT_ERR_INVALID_ARG, "qdt_init: nranks > 1 needs nccl_unique_id");
@@ -398,6 +424,141 @@ extern "C" qdt_status qdt_shard_cuts(const int64_t *lo, const int64_t *hi, int64
     std::vector<int64_t> c;
     shard_bounds(l, h, M, nranks, c);
     for (int g = 0; g <= nranks; g++) cuts[g] = c[g];
+    return QDT_OK;
+}
+
+// Sweep tiling of the local slice (once per probe handle): ST-row tiles, their contiguous probe
+// windows [dA, dB) and the tiled F blocks (W_t x STP doubles, zero outside each band).
+static qdt_status build_sweep_tiling(qdt_ctx *ctx, qdt_probes *p)
+{
+    if (p->d_Fb) return QDT_OK;
+    const int64_t Ml = p->Ml, kb = p->kb, D = p->D;
+    const int nt = (int)((Ml + ST - 1) / ST);
+    p->sw_ntiles = nt;
+    p->sw_dA.assign(nt, INT32_MAX);
+    p->sw_dB.assign(nt, 0);
+    for (int64_t d = 0; d < D; d++) {
+        if (p->len_l[d] == 0) continue;
+        const int64_t a = (p->lo_l[d] - kb) / ST, b = (p->lo_l[d] + p->len_l[d] - 1 - kb) / ST;
+        for (int64_t t = a; t <= b; t++) {
+            p->sw_dA[t] = std::min<int32_t>(p->sw_dA[t], (int32_t)d);
+            p->sw_dB[t] = std::max<int32_t>(p->sw_dB[t], (int32_t)d + 1);
+        }
+    }
+    for (int t = 0; t < nt; t++)
+        if (p->sw_dA[t] == INT32_MAX) p->sw_dA[t] = p->sw_dB[t] = (t > 0 ? p->sw_dB[t - 1] : 0);
+    p->sw_fboff.assign(nt + 1, 0);
+    for (int t = 0; t < nt; t++) p->sw_fboff[t + 1] = p->sw_fboff[t] + (int64_t)(p->sw_dB[t] - p->sw_dA[t]) * STP;
+    cudaStream_t s = ctx->stream;
+    CK(cudaMalloc(&p->d_sw_dA, sizeof(int32_t) * nt));
+    CK(cudaMalloc(&p->d_sw_dB, sizeof(int32_t) * nt));
+    CK(cudaMalloc(&p->d_fb_off, sizeof(int64_t) * (nt + 1)));
+    CK(cudaMalloc(&p->d_Fb, sizeof(double) * std::max<int64_t>(2, p->sw_fboff[nt] + 2)));
+    CK(cudaMemcpyAsync(p->d_sw_dA, p->sw_dA.data(), sizeof(int32_t) * nt, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(p->d_sw_dB, p->sw_dB.data(), sizeof(int32_t) * nt, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(p->d_fb_off, p->sw_fboff.data(), sizeof(int64_t) * (nt + 1), cudaMemcpyHostToDevice, s));
+    CK(run_k(ctx, "tile_F", 1, [&]() {
+        return launch_tile_F(p->band(), kb, (int)Ml, nt, p->d_sw_dA, p->d_sw_dB, p->d_fb_off, p->d_Fb, s);
+    }));
+    CK(cudaStreamSynchronize(s));
+    return QDT_OK;
+}
+
+static bool sweep_enabled()
+{
+    const char *e = getenv("QDT_SWEEP");
+    return !(e && e[0] == '0');
+}
+
+// Sweep units for N: bwd units (tile, probe sub-range <= SWCAP, split-K slots), fwd units (runs
+// of <= FW_MAXT tiles whose union window is <= FWCAP probes; wider windows split by FWCAP), and
+// per-probe lists of partial rows in ascending Fock order.
+static qdt_status build_sweep_plan(qdt_ctx *ctx, qdt_probes *p, Plan *pl)
+{
+    CKS(build_sweep_tiling(ctx, p));
+    const int nt = p->sw_ntiles;
+    const int64_t D = p->D;
+    std::vector<SwUnit> bu;
+    int64_t slot = 0;
+    for (int t = 0; t < nt; t++) {
+        const int dA = p->sw_dA[t], W = p->sw_dB[t] - dA;
+        const int ns = std::max(1, (W + SWCAP - 1) / SWCAP);
+        int chunk = ns > 1 ? (W + ns - 1) / ns : W;
+        if (ns > 1) chunk = ((chunk + SKC - 1) / SKC) * SKC;
+        for (int s = 0; s < ns; s++) {
+            SwUnit u;
+            u.tile = t;
+            u.p0 = std::min(dA + s * chunk, dA + W);
+            u.p1 = std::min(dA + W, u.p0 + chunk);
+            u.slot = s;
+            u.nsplit = ns;
+            u.pad = 0;
+            u.slot_base = ns > 1 ? slot : 0;
+            bu.push_back(u);
+        }
+        if (ns > 1) slot += ns;
+    }
+    pl->sw_nslots = slot;
+    std::stable_sort(bu.begin(), bu.end(),
+                     [](const SwUnit &x, const SwUnit &y) { return (x.p1 - x.p0) > (y.p1 - y.p0); });
+    pl->sw_nbunits = (int)bu.size();
+
+    std::vector<FwUnit> fu;
+    std::vector<std::vector<int64_t>> lists(D);
+    int64_t poff = 0;
+    auto emit = [&](int t0, int t1, int u0, int u1) {
+        if (u1 <= u0) return;
+        FwUnit u;
+        u.t0 = t0;
+        u.t1 = t1;
+        u.u0 = u0;
+        u.u1 = u1;
+        u.poff = poff;
+        fu.push_back(u);
+        for (int d = u0; d < u1; d++) lists[d].push_back(poff + (d - u0));
+        poff += u1 - u0;
+    };
+    int g0 = -1, gu0 = 0, gu1 = 0;
+    for (int t = 0; t < nt; t++) {
+        const int dA = p->sw_dA[t], dB = p->sw_dB[t];
+        const bool empty = dB <= dA;
+        if (g0 >= 0 && !empty && std::max(gu1, dB) - gu0 <= FWCAP && t - g0 < FW_MAXT) {
+            gu1 = std::max(gu1, dB);
+            continue;
+        }
+        if (g0 >= 0) emit(g0, t, gu0, gu1);
+        g0 = -1;
+        if (empty) continue;
+        if (dB - dA > FWCAP) {
+            for (int a0 = dA; a0 < dB; a0 += FWCAP) emit(t, t + 1, a0, std::min(dB, a0 + FWCAP));
+            continue;
+        }
+        g0 = t;
+        gu0 = dA;
+        gu1 = dB;
+    }
+    if (g0 >= 0) emit(g0, nt, gu0, gu1);
+    pl->sw_nrpart = poff;
+    std::vector<int64_t> red_beg(D + 1, 0), red_rows;
+    for (int64_t d = 0; d < D; d++) red_beg[d + 1] = red_beg[d] + (int64_t)lists[d].size();
+    red_rows.reserve(red_beg[D]);
+    for (int64_t d = 0; d < D; d++) red_rows.insert(red_rows.end(), lists[d].begin(), lists[d].end());
+    std::stable_sort(fu.begin(), fu.end(), [](const FwUnit &x, const FwUnit &y) {
+        return (int64_t)(x.u1 - x.u0) * (x.t1 - x.t0) > (int64_t)(y.u1 - y.u0) * (y.t1 - y.t0);
+    });
+    pl->sw_nfunits = (int)fu.size();
+    cudaStream_t s = ctx->stream;
+    CK(cudaMalloc(&pl->d_swunits, sizeof(SwUnit) * std::max<size_t>(1, bu.size())));
+    CK(cudaMalloc(&pl->d_fwunits, sizeof(FwUnit) * std::max<size_t>(1, fu.size())));
+    CK(cudaMalloc(&pl->d_sw_red_beg, sizeof(int64_t) * (D + 1)));
+    CK(cudaMalloc(&pl->d_sw_red_rows, sizeof(int64_t) * std::max<size_t>(1, red_rows.size())));
+    if (!bu.empty()) CK(cudaMemcpyAsync(pl->d_swunits, bu.data(), sizeof(SwUnit) * bu.size(), cudaMemcpyHostToDevice, s));
+    if (!fu.empty()) CK(cudaMemcpyAsync(pl->d_fwunits, fu.data(), sizeof(FwUnit) * fu.size(), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(pl->d_sw_red_beg, red_beg.data(), sizeof(int64_t) * (D + 1), cudaMemcpyHostToDevice, s));
+    if (!red_rows.empty())
+        CK(cudaMemcpyAsync(pl->d_sw_red_rows, red_rows.data(), sizeof(int64_t) * red_rows.size(),
+                           cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
     return QDT_OK;
 }
 
@@ -536,6 +697,9 @@ static qdt_status build_plan(qdt_ctx *ctx, qdt_probes *p, int N, Plan **out)
         CK(cudaMemcpyAsync(pl->d_red_rows, red_rows.data(), sizeof(int64_t) * red_rows.size(),
                            cudaMemcpyHostToDevice, s));
     CK(cudaStreamSynchronize(s));
+    pl->NB = sweep_enabled() ? sweep_nb(N) : 0;
+    if (pl->NB) CKS(build_sweep_plan(ctx, p, pl.get()));
+    pl->nR = pl->NB && ctx->nranks == 1 ? (int)((D + 7) / 8) : ctx->nblkR;
     *out = pl.get();
     p->plans[N] = std::move(pl);
     return QDT_OK;
@@ -774,6 +938,8 @@ struct SolveBufs {
     double *trace = nullptr, *kkt = nullptr, *kktp = nullptr, *beta = nullptr;
     int *counters = nullptr;
     DevState *state = nullptr;
+    double *sc2_stage = nullptr;
+    int *sc2_arrive = nullptr;
 };
 
 struct IterCfg {
@@ -792,6 +958,38 @@ static qdt_status fwd_reduce(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, const
     cudaStream_t s = ctx->stream;
     Plan *pl = c.pl;
     qdt_probes *p = c.p;
+    const bool multi = ctx->nranks > 1;
+    if (pl->NB) {
+        SweepFwdArgs fa;
+        fa.N = c.N;
+        fa.Ml = (int)p->Ml;
+        fa.units = pl->d_fwunits;
+        fa.fb_off = p->d_fb_off;
+        fa.tile_dA = p->d_sw_dA;
+        fa.tile_dB = p->d_sw_dB;
+        fa.Fb = p->d_Fb;
+        fa.theta = theta;
+        fa.rpart = b.rpart;
+        fa.state = b.state;
+        CK(run_k(ctx, "fwd_partial", 1, [&]() { return launch_fwd_mma(fa, pl->sw_nfunits, pl->NB, s); }));
+        if (!multi) {
+            CK(run_k(ctx, "reduce_R", 1, [&]() {
+                return launch_reduce_R2(b.rpart, pl->d_sw_red_beg, pl->d_sw_red_rows, withP ? b.P : nullptr,
+                                        R, (int)p->D, c.N, b.partR, b.state, s);
+            }));
+            return QDT_OK;
+        }
+        CK(run_k(ctx, "reduce_R", 1, [&]() {
+            return launch_reduce_R2(b.rpart, pl->d_sw_red_beg, pl->d_sw_red_rows, nullptr, R, (int)p->D,
+                                    c.N, nullptr, b.state, s);
+        }));
+        CKS(allreduce(ctx, R, (size_t)p->D * c.N, "allreduce_R"));
+        if (withP)
+            CK(run_k(ctx, "reduce_R", 1, [&]() {
+                return launch_sub_p_sumsq(R, b.P, p->D * (int64_t)c.N, b.partR, pl->nR, b.state, s);
+            }));
+        return QDT_OK;
+    }
     FwdArgs fa;
     fa.N = c.N;
     fa.CG = pl->CG;
@@ -804,16 +1002,15 @@ static qdt_status fwd_reduce(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, const
     fa.rpart = b.rpart;
     fa.state = b.state;
     CK(run_k(ctx, "fwd_partial", 1, [&]() { return launch_fwd(fa, pl->nfunits, pl->TC, s, nullptr); }));
-    const bool multi = ctx->nranks > 1;
     CK(run_k(ctx, "reduce_R", 1, [&]() {
         return launch_reduce_R(b.rpart, pl->d_red_beg, pl->d_red_rows, (withP && !multi) ? b.P : nullptr,
-                               R, p->D, c.N, b.partR, ctx->nblkR, b.state, s);
+                               R, p->D, c.N, b.partR, pl->nR, b.state, s);
     }));
     if (multi) {
         CKS(allreduce(ctx, R, (size_t)p->D * c.N, "allreduce_R"));
         if (withP)
             CK(run_k(ctx, "reduce_R", 1, [&]() {
-                return launch_sub_p_sumsq(R, b.P, p->D * (int64_t)c.N, b.partR, ctx->nblkR, b.state, s);
+                return launch_sub_p_sumsq(R, b.P, p->D * (int64_t)c.N, b.partR, pl->nR, b.state, s);
             }));
     }
     return QDT_OK;
@@ -873,19 +1070,51 @@ static qdt_status halo_exchange(qdt_ctx *ctx, const IterCfg &c, double *theta)
     return QDT_OK;
 }
 
-static qdt_status scalars(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, int final_eval)
+// S6: tile partials (ntiles of them, from whichever bwd kernel ran) + ||R||^2 partials -> trace,
+// KKT, stop flag.  Single GPU: one k_scalars2 launch; multi-GPU: k_scalars2 (local sums),
+// allreduce of the 5-vector, k_finalize.
+static qdt_status scalars(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, int final_eval, int ntiles)
 {
     cudaStream_t s = ctx->stream;
+    const bool multi = ctx->nranks > 1;
+    const int ke = final_eval ? 1 : c.kkt_every;
     CK(run_k(ctx, "scalars", 1, [&]() {
-        return launch_scalars_local(b.partR, ctx->nblkR, b.partT, c.pl->ntiles, ctx->rank == 0, b.vec,
-                                    b.state, s);
+        return launch_scalars2(b.partR, c.pl->nR, b.partT, ntiles, ctx->rank == 0, b.sc2_stage, b.sc2_arrive,
+                               b.vec, c.N, c.p->M, c.gamma, c.tol, final_eval, ke, b.trace, b.kkt, b.kktp,
+                               c.trace_len, b.state, multi ? 0 : 1, s);
     }));
+    if (!multi) return QDT_OK;
     CKS(allreduce(ctx, b.vec, NV, "allreduce_scalars"));
     CK(run_k(ctx, "scalars", 1, [&]() {
-        return launch_finalize(b.vec, c.N, c.p->M, c.gamma, c.tol, final_eval, final_eval ? 1 : c.kkt_every,
-                               b.trace, b.kkt, b.kktp, c.trace_len, b.state, s);
+        return launch_finalize(b.vec, c.N, c.p->M, c.gamma, c.tol, final_eval, ke, b.trace, b.kkt, b.kktp,
+                               c.trace_len, b.state, s);
     }));
     return QDT_OK;
+}
+
+static SweepArgs sweep_args(const IterCfg &c, SolveBufs &b, const double *R, const double *theta,
+                            double *out)
+{
+    SweepArgs a;
+    a.N = c.N;
+    a.Ml = (int)c.p->Ml;
+    a.kb = c.p->kb;
+    a.M = c.p->M;
+    a.units = c.pl->d_swunits;
+    a.fb_off = c.p->d_fb_off;
+    a.tile_dA = c.p->d_sw_dA;
+    a.Fb = c.p->d_Fb;
+    a.R = R;
+    a.theta = theta;
+    a.out = out;
+    a.tstep = b.tstep;
+    a.gamma = c.gamma;
+    a.scratch = b.scratch;
+    a.counters = b.counters;
+    a.part = b.partT;
+    a.kkt_every = c.kkt_every;
+    a.state = b.state;
+    return a;
 }
 
 // one iteration with phase index j (buffer rotation)
@@ -893,7 +1122,15 @@ static qdt_status iteration(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, int64_
 {
     cudaStream_t s = ctx->stream;
     Plan *pl = c.pl;
-    if (!c.fista) {
+    int ntiles = pl->ntiles;
+    if (!c.fista && pl->NB) {
+        double *cur = b.theta[j % 2], *nxt = b.theta[(j + 1) % 2];
+        CKS(fwd_reduce(ctx, c, b, cur, b.R[0], true));
+        SweepArgs a = sweep_args(c, b, b.R[0], cur, nxt);
+        CK(run_k(ctx, "bwd_step", 1, [&]() { return launch_bwd_mma(a, pl->sw_nbunits, pl->NB, s); }));
+        CKS(halo_exchange(ctx, c, nxt));
+        ntiles = c.p->sw_ntiles;
+    } else if (!c.fista) {
         double *cur = b.theta[j % 2], *nxt = b.theta[(j + 1) % 2];
         CKS(fwd_reduce(ctx, c, b, cur, b.R[0], true));
         BwdArgs a = bwd_args(ctx, c, b, b.R[0], cur, nullptr, nxt, false);
@@ -912,7 +1149,33 @@ static qdt_status iteration(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, int64_
         CK(run_k(ctx, "bwd_step", 1, [&]() { return launch_bwd(a, pl->nbunits, pl->TC, BWD_STEP, s); }));
         CKS(halo_exchange(ctx, c, nxt));
     }
-    CKS(scalars(ctx, c, b, 0));
+    CKS(scalars(ctx, c, b, 0, ntiles));
+    return QDT_OK;
+}
+
+// Workspace shared by solve / objective / hooks, sized for both the general and the sweep plan.
+// Buffers read by bulk copies carry 2+ doubles of slack past their last element.
+static qdt_status common_bufs(qdt_ctx *ctx, qdt_probes *p, Plan *pl, int64_t N, SolveBufs &b)
+{
+    cudaStream_t s = ctx->stream;
+    const int64_t D = p->D;
+    CKS(ws_get(ctx, "R0", D * N + 4, &b.R[0]));
+    CKS(ws_get(ctx, "rpart", std::max<int64_t>(1, std::max(pl->nrpart, pl->sw_nrpart)) * N + 4, &b.rpart));
+    CKS(ws_get(ctx, "partR", std::max(ctx->nblkR, pl->nR), &b.partR));
+    const int nt = std::max(1, std::max(pl->ntiles, p->sw_ntiles));
+    CKS(ws_get(ctx, "partT", (size_t)nt * NSC_TILE, &b.partT));
+    CK(cudaMemsetAsync(b.partT, 0, sizeof(double) * nt * NSC_TILE, s));
+    CKS(ws_get(ctx, "vec", NV, &b.vec));
+    CKS(ws_get(ctx, "tstep", p->Ml, &b.tstep));
+    const int64_t scr = std::max<int64_t>(1, std::max<int64_t>(pl->nslots * pl->T * N, pl->sw_nslots * 512 * pl->NB));
+    CKS(ws_get(ctx, "scratch", scr, &b.scratch));
+    CKS(ws_get(ctx, "counters", nt, &b.counters));
+    CK(cudaMemsetAsync(b.counters, 0, sizeof(int) * nt, s));
+    CKS(ws_get(ctx, "state", 1, &b.state));
+    CK(cudaMemsetAsync(b.state, 0, sizeof(DevState), s));  // it = 0, stop = 0 (hooks); solve re-inits
+    CKS(ws_get(ctx, "sc2_stage", SC2_BLOCKS * NV, &b.sc2_stage));
+    CKS(ws_get(ctx, "sc2_arrive", 1, &b.sc2_arrive));
+    CK(cudaMemsetAsync(b.sc2_arrive, 0, sizeof(int), s));
     return QDT_OK;
 }
 
@@ -967,7 +1230,9 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     {
         const int nb = opt.accel ? 3 : 2;
         double need = 8.0 * ((double)nb * (Ml + 2) * N + (opt.accel ? 3.0 : 1.0) * D * N + D * N +
-                             (double)pl->nrpart * N + (double)pl->nslots * pl->T * N + 2.0 * Ml);
+                             (double)std::max(pl->nrpart, pl->sw_nrpart) * N +
+                             (double)std::max<int64_t>(pl->nslots * pl->T * N, pl->sw_nslots * 512 * pl->NB) +
+                             2.0 * Ml);
         size_t fr = 0, tot = 0;
         CK(cudaMemGetInfo(&fr, &tot));
         size_t have = fr;
@@ -983,26 +1248,16 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     const char *tn[3] = {"theta0", "theta1", "theta2"};
     for (int i = 0; i < nbuf; i++) {
         double *t;
-        CKS(ws_get(ctx, tn[i], rowsz, &t));
+        CKS(ws_get(ctx, tn[i], rowsz + 2, &t));
         b.theta[i] = t + N;
         CK(cudaMemsetAsync(t, 0, sizeof(double) * rowsz, s));
     }
-    CKS(ws_get(ctx, "R0", D * N, &b.R[0]));
+    CKS(common_bufs(ctx, p, pl, N, b));
     if (fista) {
         CKS(ws_get(ctx, "R1", D * N, &b.R[1]));
         CKS(ws_get(ctx, "RY", D * N, &b.RY));
         CK(cudaMemsetAsync(b.R[1], 0, sizeof(double) * D * N, s));
     }
-    CKS(ws_get(ctx, "rpart", std::max<int64_t>(1, pl->nrpart) * N, &b.rpart));
-    CKS(ws_get(ctx, "partR", ctx->nblkR, &b.partR));
-    CKS(ws_get(ctx, "partT", (size_t)pl->ntiles * NSC_TILE, &b.partT));
-    CK(cudaMemsetAsync(b.partT, 0, sizeof(double) * pl->ntiles * NSC_TILE, s));
-    CKS(ws_get(ctx, "vec", NV, &b.vec));
-    CKS(ws_get(ctx, "tstep", Ml, &b.tstep));
-    CKS(ws_get(ctx, "scratch", std::max<int64_t>(1, pl->nslots) * pl->T * N, &b.scratch));
-    CKS(ws_get(ctx, "counters", std::max(1, pl->ntiles), &b.counters));
-    CK(cudaMemsetAsync(b.counters, 0, sizeof(int) * std::max(1, pl->ntiles), s));
-    CKS(ws_get(ctx, "state", 1, &b.state));
     const int64_t tl = iters + 1;
     CKS(ws_get(ctx, "trace", tl, &b.trace));
     CKS(ws_get(ctx, "kkt", tl, &b.kkt));
@@ -1112,7 +1367,7 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
         CKS(fwd_reduce(ctx, cf, b, cur, b.R[0], true));
         BwdArgs a = bwd_args(ctx, cf, b, b.R[0], cur, nullptr, nullptr, false);
         CK(run_k(ctx, "bwd_eval", 1, [&]() { return launch_bwd(a, pl->nbunits, pl->TC, BWD_EVAL, s); }));
-        CKS(scalars(ctx, cf, b, 1));
+        CKS(scalars(ctx, cf, b, 1, pl->ntiles));
         CK(cudaMemcpyAsync(&hst, b.state, sizeof hst, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
     }
@@ -1193,22 +1448,13 @@ extern "C" qdt_status qdt_objective(qdt_ctx *ctx, const qdt_probes *F, const dou
     SolveBufs b;
     double *t;
     const size_t rowsz = (size_t)(Ml + 2) * N;
-    CKS(ws_get(ctx, "theta0", rowsz, &t));
+    CKS(ws_get(ctx, "theta0", rowsz + 2, &t));
     b.theta[0] = t + N;
     CK(cudaMemsetAsync(t, 0, sizeof(double) * rowsz, s));
     CK(cudaMemcpyAsync(b.theta[0] - (p->kb > 0 ? N : 0), theta + (p->kb > 0 ? (p->kb - 1) * N : 0),
                        sizeof(double) * (Ml + (p->kb > 0) + (p->ke < p->M)) * N,
                        dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
-    CKS(ws_get(ctx, "R0", D * N, &b.R[0]));
-    CKS(ws_get(ctx, "rpart", std::max<int64_t>(1, pl->nrpart) * N, &b.rpart));
-    CKS(ws_get(ctx, "partR", ctx->nblkR, &b.partR));
-    CKS(ws_get(ctx, "partT", (size_t)pl->ntiles * NSC_TILE, &b.partT));
-    CKS(ws_get(ctx, "vec", NV, &b.vec));
-    CKS(ws_get(ctx, "tstep", Ml, &b.tstep));
-    CKS(ws_get(ctx, "scratch", std::max<int64_t>(1, pl->nslots) * pl->T * N, &b.scratch));
-    CKS(ws_get(ctx, "counters", std::max(1, pl->ntiles), &b.counters));
-    CK(cudaMemsetAsync(b.counters, 0, sizeof(int) * std::max(1, pl->ntiles), s));
-    CKS(ws_get(ctx, "state", 1, &b.state));
+    CKS(common_bufs(ctx, p, pl, N, b));
     CKS(ws_get(ctx, "trace", 1, &b.trace));
     CKS(ws_get(ctx, "kkt", 1, &b.kkt));
     CKS(ws_get(ctx, "kktp", 1, &b.kktp));
@@ -1225,7 +1471,7 @@ extern "C" qdt_status qdt_objective(qdt_ctx *ctx, const qdt_probes *F, const dou
     CKS(fwd_reduce(ctx, c, b, b.theta[0], b.R[0], true));
     BwdArgs a = bwd_args(ctx, c, b, b.R[0], b.theta[0], nullptr, nullptr, false);
     CK(run_k(ctx, "bwd_eval", 1, [&]() { return launch_bwd(a, pl->nbunits, pl->TC, BWD_EVAL, s); }));
-    CKS(scalars(ctx, c, b, 1));
+    CKS(scalars(ctx, c, b, 1, pl->ntiles));
     double f = 0, r = 0;
     CK(cudaMemcpyAsync(&f, b.trace, sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&r, b.kkt, sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -1257,12 +1503,10 @@ extern "C" qdt_status qdt_residual(qdt_ctx *ctx, const qdt_probes *F, const doub
     cudaStream_t s = ctx->stream;
     SolveBufs b;
     double *t;
-    CKS(ws_get(ctx, "theta0", (size_t)(p->Ml + 2) * N, &t));
+    CKS(ws_get(ctx, "theta0", (size_t)(p->Ml + 2) * N + 2, &t));
     b.theta[0] = t + N;
     CK(cudaMemcpyAsync(b.theta[0], theta, sizeof(double) * p->Ml * N, cudaMemcpyHostToDevice, s));
-    CKS(ws_get(ctx, "R0", p->D * N, &b.R[0]));
-    CKS(ws_get(ctx, "rpart", std::max<int64_t>(1, pl->nrpart) * N, &b.rpart));
-    CKS(ws_get(ctx, "partR", ctx->nblkR, &b.partR));
+    CKS(common_bufs(ctx, p, pl, N, b));
     if (P) {
         CKS(ws_get(ctx, "P", p->D * N, &b.P));
         CK(cudaMemcpyAsync(b.P, P, sizeof(double) * p->D * N, cudaMemcpyHostToDevice, s));
@@ -1285,15 +1529,12 @@ extern "C" qdt_status qdt_gradient(qdt_ctx *ctx, const qdt_probes *F, const doub
     cudaStream_t s = ctx->stream;
     SolveBufs b;
     double *t, *G;
-    CKS(ws_get(ctx, "theta0", (size_t)(p->Ml + 2) * N, &t));
+    CKS(ws_get(ctx, "theta0", (size_t)(p->Ml + 2) * N + 2, &t));
     b.theta[0] = t + N;
     CK(cudaMemcpyAsync(b.theta[0], theta, sizeof(double) * p->Ml * N, cudaMemcpyHostToDevice, s));
-    CKS(ws_get(ctx, "R0", p->D * N, &b.R[0]));
+    CKS(common_bufs(ctx, p, pl, N, b));
     CK(cudaMemcpyAsync(b.R[0], R, sizeof(double) * p->D * N, cudaMemcpyHostToDevice, s));
-    CKS(ws_get(ctx, "theta1", (size_t)(p->Ml + 2) * N, &G));
-    CKS(ws_get(ctx, "scratch", std::max<int64_t>(1, pl->nslots) * pl->T * N, &b.scratch));
-    CKS(ws_get(ctx, "counters", std::max(1, pl->ntiles), &b.counters));
-    CK(cudaMemsetAsync(b.counters, 0, sizeof(int) * std::max(1, pl->ntiles), s));
+    CKS(ws_get(ctx, "theta1", (size_t)(p->Ml + 2) * N + 2, &G));
     IterCfg c{p, pl, (int)N, gamma, 0.0, 0, 1, 1};
     BwdArgs a = bwd_args(ctx, c, b, b.R[0], b.theta[0], nullptr, G, false);
     a.state = nullptr;

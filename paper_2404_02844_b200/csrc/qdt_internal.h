@@ -85,6 +85,69 @@ struct FwdArgs {
     const DevState *state;
 };
 
+// ---- sweep path (qdt_sweep.cu): fp64 tensor-core (DMMA) kernels for N <= 128
+constexpr int ST = 64;          // Fock rows per sweep tile (8 DMMA m-blocks)
+constexpr int STP = ST + 4;     // pitch of a tiled-F row: conflict-free A fragments
+constexpr int SKC = 16;         // probes per staged bwd chunk (4 DMMA k-steps)
+constexpr int SWCAP = 128;      // bwd split cap (probes per unit)
+constexpr int FWCAP = 64;       // fwd unit union-window cap (probes)
+constexpr int FW_MAXT = 16;     // fwd unit length cap (tiles)
+constexpr int SC2_BLOCKS = 64;  // first-level blocks of the scalar reduction
+
+struct SwUnit {                 // bwd unit: tile, probe range [p0, p1) of its window, split-K info
+    int32_t tile, p0, p1, slot, nsplit, pad;
+    int64_t slot_base;
+};
+struct FwUnit {                 // fwd unit: tiles [t0, t1), union window [u0, u1), partial rows
+    int32_t t0, t1, u0, u1;
+    int64_t poff;
+};
+struct SweepArgs {
+    int N, Ml;
+    int64_t kb, M;
+    const SwUnit *units;
+    const int64_t *fb_off;
+    const int32_t *tile_dA;
+    const double *Fb;
+    const double *R;
+    const double *theta;        // local row 0; rows -1 and Ml readable
+    double *out;
+    const double *tstep;
+    double gamma;
+    double *scratch;
+    int *counters;
+    double *part;
+    int kkt_every;
+    const DevState *state;
+};
+struct SweepFwdArgs {
+    int N, Ml;
+    const FwUnit *units;
+    const int64_t *fb_off;
+    const int32_t *tile_dA, *tile_dB;
+    const double *Fb;
+    const double *theta;
+    double *rpart;
+    const DevState *state;
+};
+cudaError_t prepare_sweep_kernels();
+int sweep_nb(int N);            // DMMA n-blocks instantiated for N (0: N too wide, general path)
+size_t sweep_bwd_smem(int N, int NB);
+size_t sweep_fwd_smem(int N, int NB);
+cudaError_t launch_tile_F(Band b, int64_t kb, int Ml, int ntiles, const int32_t *tile_dA,
+                          const int32_t *tile_dB, const int64_t *fb_off, double *Fb,
+                          cudaStream_t s);
+cudaError_t launch_bwd_mma(const SweepArgs &a, int nunits, int NB, cudaStream_t s);
+cudaError_t launch_fwd_mma(const SweepFwdArgs &a, int nunits, int NB, cudaStream_t s);
+cudaError_t launch_reduce_R2(const double *rpart, const int64_t *red_beg, const int64_t *red_rows,
+                             const double *P, double *R, int D, int N, double *partR,
+                             const DevState *st, cudaStream_t s);
+cudaError_t launch_scalars2(const double *partR, int nR, const double *partT, int ntiles,
+                            int include_r2, double *stage, int *arrive, double *vec, int64_t N,
+                            int64_t M, double gamma, double tol, int final_eval, int kkt_every,
+                            double *trace, double *kkt, double *kktp, int64_t trace_len,
+                            DevState *st, int finalize, cudaStream_t s);
+
 // launchers (qdt_kernels.cu); return cudaGetLastError()
 cudaError_t launch_probe_edges(const double *alpha2, int64_t D, int64_t M, double c_sigma,
                                int margin, int32_t *lo, int32_t *hi, cudaStream_t s);
