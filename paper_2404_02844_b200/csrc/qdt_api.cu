@@ -1359,6 +1359,22 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     CK(cudaMemcpyAsync(&hst, b.state, sizeof hst, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     stopped = hst.stop != 0;
+    if (stopped && hst.converged && !hst.nonfinite && pl->NB && !fista) {
+        // the sweep loop evaluates the unclamped KKT only; re-evaluate Theta_kd once with the
+        // general kernels so that trace/kkt/kkt_paper at kd come from one consistent pass
+        DevState sr = hst;
+        sr.stop = 0;
+        sr.it = hst.iters_done;
+        CK(cudaMemcpyAsync(b.state, &sr, sizeof sr, cudaMemcpyHostToDevice, s));
+        IterCfg cf = c;
+        cf.kkt_every = 1;
+        double *cur = b.theta[hst.iters_done % nbuf];
+        CKS(fwd_reduce(ctx, cf, b, cur, b.R[0], true));
+        BwdArgs a = bwd_args(ctx, cf, b, b.R[0], cur, nullptr, nullptr, false);
+        CK(run_k(ctx, "bwd_eval", 1, [&]() { return launch_bwd(a, pl->nbunits, pl->TC, BWD_EVAL, s); }));
+        CKS(scalars(ctx, cf, b, 1, pl->ntiles));
+        CK(cudaMemcpyAsync(b.state, &hst, sizeof hst, cudaMemcpyHostToDevice, s));
+    }
     if (!stopped) {
         IterCfg cf = c;
         cf.fista = 0;

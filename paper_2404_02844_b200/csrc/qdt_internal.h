@@ -93,6 +93,7 @@ constexpr int SWCAP = 128;      // bwd split cap (probes per unit)
 constexpr int FWCAP = 64;       // fwd unit union-window cap (probes)
 constexpr int FW_MAXT = 16;     // fwd unit length cap (tiles)
 constexpr int SC2_BLOCKS = 64;  // first-level blocks of the scalar reduction
+constexpr int SW_NBMAX = 16;    // sweep path: N <= 8 * SW_NBMAX outcomes
 
 struct SwUnit {                 // bwd unit: tile, probe range [p0, p1) of its window, split-K info
     int32_t tile, p0, p1, slot, nsplit, pad;

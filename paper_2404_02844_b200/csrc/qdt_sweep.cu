@@ -137,6 +137,140 @@ __global__ void k_tile_F(Band b, int64_t kb, int Ml, const int32_t *tile_dA, con
     }
 }
 
+// ------------------------------------------------------------------------------ row epilogue
+// One Fock row k held by a quad (4 lanes, t4 = lane & 3) in the DMMA accumulator layout: columns
+// c = 8 nb + 2 t4 + i.  On entry acc = (F^T R)[k, c]; thr points at Theta_k[k, 0] in shared
+// memory with rows k-1 and k+1 at -N and +N.  Steps:
+//   G = acc + gamma (L Theta)_k                        eq. regul, ends: reading R8
+//   sreg += (Theta_k - Theta_{k+1})^2                  regulariser value of the pair (k, k+1)
+//   KKT:  lam = -min_n 2G;  skkt += (Theta (2G + lam))^2      PAPER.md:563-567, reading R7
+//   X = Theta - t_k G;  tau by Michelot rounds;  out = max(X - tau, 0)   eq. Mp1_proj, reading R4
+// NB = ceil(N/8): only the last n-block can hold columns >= N; they are neutralised (+inf for the
+// row min, -inf for X) and never stored.  FULL: an interior row of a full tile (row active,
+// neighbours k-1 and k+1 exist): no per-row predicates.  EVEN: N even, pairs move as double2.
+template <int NB, bool FULL, bool EVEN>
+__device__ __forceinline__ void row_step(double (&acc)[NB][2], const double *thr, int N, int t4,
+                                         bool act, bool has_prev, bool has_next, double gamma,
+                                         double tk, bool do_kkt, bool want_kktp, double &sreg,
+                                         double &skkt, double &skktp, double *orow)
+{
+    const int cl = 8 * (NB - 1) + 2 * t4;
+    const bool v0 = cl < N, v1 = cl + 1 < N;
+    const bool hp = FULL || has_prev, hn = FULL || has_next;
+    double mn = INFINITY;
+#pragma unroll
+    for (int nb = 0; nb < NB; nb++) {
+        const int c = 8 * nb + 2 * t4;
+        double t0[2], tp[2], tn[2];
+        if (EVEN) {
+            const double2 a = *reinterpret_cast<const double2 *>(thr + c);
+            const double2 b = *reinterpret_cast<const double2 *>(thr + c - N);
+            const double2 d = *reinterpret_cast<const double2 *>(thr + c + N);
+            t0[0] = a.x, t0[1] = a.y, tp[0] = b.x, tp[1] = b.y, tn[0] = d.x, tn[1] = d.y;
+        } else {
+#pragma unroll
+            for (int i = 0; i < 2; i++) t0[i] = thr[c + i], tp[i] = thr[c + i - N], tn[i] = thr[c + i + N];
+        }
+#pragma unroll
+        for (int i = 0; i < 2; i++) {
+            const bool valid = (nb < NB - 1) || (i ? v1 : v0);
+            const bool ok = FULL ? valid : (act && valid);
+            const double a0 = t0[i];
+            const double an = hn ? tn[i] : a0;
+            const double ap = hp ? tp[i] : a0;
+            const double dd = a0 - an;
+            double g = acc[nb][i];
+            if (gamma != 0.0) g = fma(gamma, (a0 - ap) + (a0 - an), g);
+            if (ok) {
+                sreg = fma(dd, dd, sreg);
+                mn = fmin(mn, g);
+            }
+            acc[nb][i] = ok ? g : INFINITY;
+        }
+    }
+    double lam = 0.0, lamp = 0.0;
+    if (do_kkt) {
+        mn = 2.0 * quad_min(mn);
+        lam = -mn;
+        lamp = fmax(lam, 0.0);
+    }
+    double s = 0.0, xm = -INFINITY;
+#pragma unroll
+    for (int nb = 0; nb < NB; nb++) {
+        const int c = 8 * nb + 2 * t4;
+        double t0[2];
+        if (EVEN) {
+            const double2 a = *reinterpret_cast<const double2 *>(thr + c);
+            t0[0] = a.x, t0[1] = a.y;
+        } else {
+            t0[0] = thr[c], t0[1] = thr[c + 1];
+        }
+#pragma unroll
+        for (int i = 0; i < 2; i++) {
+            const bool valid = (nb < NB - 1) || (i ? v1 : v0);
+            const bool ok = FULL ? valid : (act && valid);
+            const double g = acc[nb][i];
+            if (do_kkt && ok) {
+                const double x1 = t0[i] * fma(2.0, g, lam);
+                skkt = fma(x1, x1, skkt);
+                if (want_kktp) {
+                    const double x2 = t0[i] * fma(2.0, g, lamp);
+                    skktp = fma(x2, x2, skktp);
+                }
+            }
+            const double x = fma(-tk, g, t0[i]);
+            acc[nb][i] = ok ? x : -INFINITY;
+            if (ok) {
+                s += x;
+                xm = fmax(xm, x);
+            }
+        }
+    }
+    s = quad_sum(s);
+    xm = quad_max(xm);
+    // Michelot from the larger of two lower bounds of tau* (the mean bound and max - 1): the
+    // active-set updates then increase monotonically to tau* (reading R4)
+    int cnt = N + 1;
+    double tau = fmax((s - 1.0) / (double)N, xm - 1.0);
+    bool done = !(FULL || act);
+    for (int round = 0; round <= N; round++) {
+        if (__all_sync(0xffffffffu, done)) break;
+        double ps = 0.0;
+        int pc = 0;
+#pragma unroll
+        for (int nb = 0; nb < NB; nb++)
+#pragma unroll
+            for (int i = 0; i < 2; i++)
+                if (acc[nb][i] > tau) {
+                    ps += acc[nb][i];
+                    pc++;
+                }
+        ps = quad_sum(ps);
+        pc = quad_sum_i(pc);
+        if (!done) {
+            if (pc >= cnt) {
+                done = true;
+            } else {
+                cnt = pc;
+                tau = (ps - 1.0) / (double)pc;
+            }
+        }
+    }
+    if (FULL || act) {
+#pragma unroll
+        for (int nb = 0; nb < NB; nb++) {
+            const int c = 8 * nb + 2 * t4;
+            const double o0 = fmax(acc[nb][0] - tau, 0.0), o1 = fmax(acc[nb][1] - tau, 0.0);
+            if (EVEN) {
+                if (nb < NB - 1 || v0) *reinterpret_cast<double2 *>(orow + c) = make_double2(o0, o1);
+            } else {
+                if (nb < NB - 1 || v0) orow[c] = o0;
+                if (nb < NB - 1 || v1) orow[c + 1] = o1;
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------------------------ bwd sweep
 // Smem: Theta tile (ST+2 rows incl. halo) | F chunks 2 x SKC x STP | R chunks 2 x (SKC*N + pad)
 template <int NB>
@@ -281,111 +415,29 @@ __global__ void __launch_bounds__(256, 2) k_bwd_mma(SweepArgs a)
     }
     mbar_wait(&bars[0], 0);
 
-    // ---- epilogue: the quad (4 lanes) g4 of warp w owns local row r = 8w + g4, columns
-    //      c = 8 nb + 2 t4 + i.  G = acc + gamma L Theta; regulariser pair (k, k+1); KKT;
-    //      X = Theta - t_k G; Michelot threshold; Theta_next = max(X - tau, 0).
+    // ---- epilogue: the quad (4 lanes) g4 of warp w owns local row r = 8w + g4 (row_step)
     const int r = 8 * warp + g4;
     const bool act = r < Tt;
     const int kl = k0 + r;
     const int64_t kg = a.kb + kl;
     const bool has_prev = kg > 0, has_next = kg + 1 < a.M;
     const double *thr = Th + th_sh + (r + 1) * N;
-    const double gamma = a.gamma;
     double sreg = 0.0, skkt = 0.0, skktp = 0.0;
-    // G = acc + gamma L Theta (in place); invalid entries -> +inf (neutral for the row min)
-#pragma unroll
-    for (int nb = 0; nb < NB; nb++)
-#pragma unroll
-        for (int i = 0; i < 2; i++) {
-            const int c = 8 * nb + 2 * t4 + i;
-            const bool ok = act && c < N;
-            const double t0 = ok ? thr[c] : 0.0;
-            const double tn = (ok && has_next) ? thr[c + N] : t0;
-            const double tp = (ok && has_prev) ? thr[c - N] : t0;
-            const double dd = t0 - tn;
-            sreg = fma(dd, dd, sreg);
-            double gg = acc[nb][i];
-            if (gamma != 0.0) gg = fma(gamma, (t0 - tp) + (t0 - tn), gg);
-            acc[nb][i] = ok ? gg : INFINITY;
-        }
     const bool do_kkt = (it % a.kkt_every) == 0;
-    if (do_kkt) {
-        double mn = INFINITY;
-#pragma unroll
-        for (int nb = 0; nb < NB; nb++) mn = fmin(mn, fmin(acc[nb][0], acc[nb][1]));
-        mn = 2.0 * quad_min(mn);
-        const double lam = act ? -mn : 0.0, lamp = fmax(lam, 0.0);
-#pragma unroll
-        for (int nb = 0; nb < NB; nb++)
-#pragma unroll
-            for (int i = 0; i < 2; i++) {
-                const int c = 8 * nb + 2 * t4 + i;
-                if (act && c < N) {
-                    const double t0 = thr[c];
-                    const double df = 2.0 * acc[nb][i];
-                    const double x1 = t0 * (df + lam), x2 = t0 * (df + lamp);
-                    skkt = fma(x1, x1, skkt);
-                    skktp = fma(x2, x2, skktp);
-                }
-            }
-    }
-    {
-        const double tk = act ? a.tstep[kl] : 0.0;
-        double s = 0.0, xm = -INFINITY;
-#pragma unroll
-        for (int nb = 0; nb < NB; nb++)
-#pragma unroll
-            for (int i = 0; i < 2; i++) {
-                const int c = 8 * nb + 2 * t4 + i;
-                const bool ok = act && c < N;
-                const double xv = ok ? thr[c] - tk * acc[nb][i] : -INFINITY;
-                acc[nb][i] = xv;
-                s += ok ? xv : 0.0;
-                xm = fmax(xm, xv);
-            }
-        s = quad_sum(s);
-        xm = quad_max(xm);
-        // Michelot from the larger of two lower bounds of tau* (mean bound and max - 1): the
-        // active-set updates then increase monotonically to tau* (reading R4)
-        int cnt = N + 1;
-        double tau = fmax((s - 1.0) / (double)N, xm - 1.0);
-        bool done = !act;
-        for (int round = 0; round <= N; round++) {
-            if (__all_sync(0xffffffffu, done)) break;
-            double ps = 0.0;
-            int pc = 0;
-#pragma unroll
-            for (int nb = 0; nb < NB; nb++)
-#pragma unroll
-                for (int i = 0; i < 2; i++) {
-                    const bool in = acc[nb][i] > tau;
-                    ps += in ? acc[nb][i] : 0.0;
-                    pc += in;
-                }
-            ps = quad_sum(ps);
-            pc = quad_sum_i(pc);
-            if (!done) {
-                if (pc >= cnt) {
-                    done = true;
-                } else {
-                    cnt = pc;
-                    tau = (ps - 1.0) / (double)pc;
-                }
-            }
-        }
-        if (act) {
-            double *o = a.out + (int64_t)kl * N;
-#pragma unroll
-            for (int nb = 0; nb < NB; nb++)
-#pragma unroll
-                for (int i = 0; i < 2; i++) {
-                    const int c = 8 * nb + 2 * t4 + i;
-                    if (c < N) o[c] = fmax(acc[nb][i] - tau, 0.0);
-                }
-        }
-    }
+    const double tk = act ? a.tstep[kl] : 0.0;
+    double *orow = a.out + (int64_t)kl * N;
+    const bool full = Tt == ST && a.kb + k0 > 0 && a.kb + k0 + ST < a.M;   // block-uniform
+    const bool even = (N & 1) == 0;
+    if (full && even)
+        row_step<NB, true, true>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk, do_kkt, false,
+                                 sreg, skkt, skktp, orow);
+    else if (full)
+        row_step<NB, true, false>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk, do_kkt, false,
+                                  sreg, skkt, skktp, orow);
+    else
+        row_step<NB, false, false>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk, do_kkt, false,
+                                   sreg, skkt, skktp, orow);
     // ---- per-tile scalar partials (fixed order: lanes, then warps)
-    if (!act || !has_next) sreg = 0.0;
     sreg = wsum(sreg);
     skkt = wsum(skkt);
     skktp = wsum(skktp);
@@ -672,40 +724,32 @@ static cudaError_t prep_nb()
     return e;
 }
 
+#define QDT_FOR_NB(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16)
+
 cudaError_t prepare_sweep_kernels()
 {
     static bool done = false;
     if (done) return cudaSuccess;
-    cudaError_t e = prep_nb<2>();
-    if (e == cudaSuccess) e = prep_nb<4>();
-    if (e == cudaSuccess) e = prep_nb<8>();
-    if (e == cudaSuccess) e = prep_nb<13>();
-    if (e == cudaSuccess) e = prep_nb<16>();
+    cudaError_t e = cudaSuccess;
+#define QDT_PREP(nb) if (e == cudaSuccess) e = prep_nb<nb>();
+    QDT_FOR_NB(QDT_PREP)
+#undef QDT_PREP
     done = e == cudaSuccess;
     return e;
 }
 
-int sweep_nb(int N)
-{
-    const int nb = (N + 7) / 8;
-    if (nb <= 2) return 2;
-    if (nb <= 4) return 4;
-    if (nb <= 8) return 8;
-    if (nb <= 13) return 13;
-    if (nb <= 16) return 16;
-    return 0;
-}
+// exact n-block count: only the last n-block of a row can hold padding columns
+int sweep_nb(int N) { return (N >= 1 && N <= 8 * SW_NBMAX) ? (N + 7) / 8 : 0; }
 
 cudaError_t launch_bwd_mma(const SweepArgs &a, int nunits, int NB, cudaStream_t s)
 {
     if (nunits <= 0) return cudaSuccess;
     const size_t smem = sweep_bwd_smem(a.N, NB);
     switch (NB) {
-        case 2: k_bwd_mma<2><<<nunits, 256, smem, s>>>(a); break;
-        case 4: k_bwd_mma<4><<<nunits, 256, smem, s>>>(a); break;
-        case 8: k_bwd_mma<8><<<nunits, 256, smem, s>>>(a); break;
-        case 13: k_bwd_mma<13><<<nunits, 256, smem, s>>>(a); break;
-        case 16: k_bwd_mma<16><<<nunits, 256, smem, s>>>(a); break;
+#define QDT_CASE(nb) \
+    case nb: k_bwd_mma<nb><<<nunits, 256, smem, s>>>(a); break;
+        QDT_FOR_NB(QDT_CASE)
+#undef QDT_CASE
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
@@ -716,11 +760,10 @@ cudaError_t launch_fwd_mma(const SweepFwdArgs &a, int nunits, int NB, cudaStream
     if (nunits <= 0) return cudaSuccess;
     const size_t smem = sweep_fwd_smem(a.N, NB);
     switch (NB) {
-        case 2: k_fwd_mma<2><<<nunits, 256, smem, s>>>(a); break;
-        case 4: k_fwd_mma<4><<<nunits, 256, smem, s>>>(a); break;
-        case 8: k_fwd_mma<8><<<nunits, 256, smem, s>>>(a); break;
-        case 13: k_fwd_mma<13><<<nunits, 256, smem, s>>>(a); break;
-        case 16: k_fwd_mma<16><<<nunits, 256, smem, s>>>(a); break;
+#define QDT_CASE(nb) \
+    case nb: k_fwd_mma<nb><<<nunits, 256, smem, s>>>(a); break;
+        QDT_FOR_NB(QDT_CASE)
+#undef QDT_CASE
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
