@@ -179,7 +179,8 @@ def run_qdt(args):
     q.qdt_profile_enable(ctx, True)
     solve(prof_iters)
     kern = {}
-    for name in ["fwd_partial", "reduce_R", "bwd_step", "scalars", "allreduce_R", "halo"]:
+    for name in ["fwd_partial", "reduce_R", "bwd_step", "bwd_heavy", "sweep_fused", "fwd_heavy", "scalars",
+                 "allreduce_R", "halo"]:
         c, t = q.qdt_profile_get(ctx, name)
         if c:
             kern[name] = {"count": c, "avg_ms": t / c}

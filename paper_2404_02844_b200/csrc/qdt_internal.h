@@ -90,7 +90,7 @@ constexpr int ST = 64;          // Fock rows per sweep tile (8 DMMA m-blocks)
 constexpr int STP = ST + 4;     // pitch of a tiled-F row: conflict-free A fragments
 constexpr int SKC = 16;         // probes per staged bwd chunk (4 DMMA k-steps)
 constexpr int SWCAP = 128;      // bwd split cap (probes per unit)
-constexpr int FWCAP = 64;       // fwd unit union-window cap (probes)
+constexpr int FWCAP = 32;       // fwd unit union-window cap (probes): <= 4 DMMA n-blocks
 constexpr int FW_MAXT = 16;     // fwd unit length cap (tiles)
 constexpr int SC2_BLOCKS = 64;  // first-level blocks of the scalar reduction
 constexpr int SW_NBMAX = 16;    // sweep path: N <= 8 * SW_NBMAX outcomes
@@ -131,6 +131,28 @@ struct SweepFwdArgs {
     double *rpart;
     const DevState *state;
 };
+struct SweepFusedArgs {
+    int N, Ml, cap;             // cap: max window of a light tile (ring slots), multiple of 8
+    int64_t kb, M;
+    const int32_t *range;       // per CTA: [ta, tb) light tiles
+    const int64_t *poff;        // per CTA: first partial row (probe tile_dA[ta])
+    const int64_t *fb_off;
+    const int32_t *tile_dA, *tile_dB;
+    const double *Fb;
+    const double *R;
+    const double *theta;
+    double *out;
+    const double *tstep;
+    double gamma;
+    double *rpart;
+    double *part;               // scalar partials: CTA c writes slot part_base + c
+    int part_base;
+    int kkt_every;
+    const DevState *state;
+};
+constexpr int SW_FUSED_SMEM_MAX = 220 * 1024;
+size_t sweep_fused_smem(int N, int NB, int cap);
+cudaError_t launch_sweep_fused(const SweepFusedArgs &a, int nctas, int NB, cudaStream_t s);
 cudaError_t prepare_sweep_kernels();
 int sweep_nb(int N);            // DMMA n-blocks instantiated for N (0: N too wide, general path)
 size_t sweep_bwd_smem(int N, int NB);

@@ -148,8 +148,8 @@ __global__ void k_tile_F(Band b, int64_t kb, int Ml, const int32_t *tile_dA, con
 // NB = ceil(N/8): only the last n-block can hold columns >= N; they are neutralised (+inf for the
 // row min, -inf for X) and never stored.  FULL: an interior row of a full tile (row active,
 // neighbours k-1 and k+1 exist): no per-row predicates.  EVEN: N even, pairs move as double2.
-template <int NB, bool FULL, bool EVEN>
-__device__ __forceinline__ void row_step(double (&acc)[NB][2], const double *thr, int N, int t4,
+template <int NB, bool FULL, bool EVEN, bool SMEM_OUT = false>
+__device__ __forceinline__ void row_step(double (&acc)[NB][2], double *thr, int N, int t4,
                                          bool act, bool has_prev, bool has_next, double gamma,
                                          double tk, bool do_kkt, bool want_kktp, double &sreg,
                                          double &skkt, double &skktp, double *orow)
@@ -157,59 +157,58 @@ __device__ __forceinline__ void row_step(double (&acc)[NB][2], const double *thr
     const int cl = 8 * (NB - 1) + 2 * t4;
     const bool v0 = cl < N, v1 = cl + 1 < N;
     const bool hp = FULL || has_prev, hn = FULL || has_next;
+    const bool ract = FULL || act;
+#define QDT_VALID(nb, i) ((nb) < NB - 1 ? ract : (ract && ((i) ? v1 : v0)))
+    // ---- pass 1: G = acc + gamma L Theta, regulariser pair, row min of G (for the KKT)
     double mn = INFINITY;
 #pragma unroll
     for (int nb = 0; nb < NB; nb++) {
         const int c = 8 * nb + 2 * t4;
         double t0[2], tp[2], tn[2];
         if (EVEN) {
-            const double2 a = *reinterpret_cast<const double2 *>(thr + c);
-            const double2 b = *reinterpret_cast<const double2 *>(thr + c - N);
-            const double2 d = *reinterpret_cast<const double2 *>(thr + c + N);
-            t0[0] = a.x, t0[1] = a.y, tp[0] = b.x, tp[1] = b.y, tn[0] = d.x, tn[1] = d.y;
+            const double2 x = *reinterpret_cast<const double2 *>(thr + c);
+            const double2 y = *reinterpret_cast<const double2 *>(thr + c - N);
+            const double2 z = *reinterpret_cast<const double2 *>(thr + c + N);
+            t0[0] = x.x, t0[1] = x.y, tp[0] = y.x, tp[1] = y.y, tn[0] = z.x, tn[1] = z.y;
         } else {
 #pragma unroll
             for (int i = 0; i < 2; i++) t0[i] = thr[c + i], tp[i] = thr[c + i - N], tn[i] = thr[c + i + N];
         }
 #pragma unroll
         for (int i = 0; i < 2; i++) {
-            const bool valid = (nb < NB - 1) || (i ? v1 : v0);
-            const bool ok = FULL ? valid : (act && valid);
             const double a0 = t0[i];
-            const double an = hn ? tn[i] : a0;
-            const double ap = hp ? tp[i] : a0;
-            const double dd = a0 - an;
-            double g = acc[nb][i];
-            if (gamma != 0.0) g = fma(gamma, (a0 - ap) + (a0 - an), g);
-            if (ok) {
-                sreg = fma(dd, dd, sreg);
-                mn = fmin(mn, g);
+            const double d1 = a0 - (hp ? tp[i] : a0);
+            const double d2 = a0 - (hn ? tn[i] : a0);
+            const double g = fma(gamma, d1 + d2, acc[nb][i]);
+            if (QDT_VALID(nb, i)) {
+                sreg = fma(d2, d2, sreg);
+                mn = g < mn ? g : mn;
             }
-            acc[nb][i] = ok ? g : INFINITY;
+            acc[nb][i] = g;
         }
     }
+    if (SMEM_OUT) __syncthreads();  // neighbour rows read: each row may now be overwritten by its owner
     double lam = 0.0, lamp = 0.0;
     if (do_kkt) {
-        mn = 2.0 * quad_min(mn);
-        lam = -mn;
-        lamp = fmax(lam, 0.0);
+        lam = -2.0 * quad_min(mn);
+        lamp = lam > 0.0 ? lam : 0.0;
     }
-    double s = 0.0, xm = -INFINITY;
+    // ---- pass 2: KKT terms, X = Theta - t_k G, row sum / max / min of X
+    double s = 0.0, xm = -INFINITY, xn = INFINITY;
 #pragma unroll
     for (int nb = 0; nb < NB; nb++) {
         const int c = 8 * nb + 2 * t4;
         double t0[2];
         if (EVEN) {
-            const double2 a = *reinterpret_cast<const double2 *>(thr + c);
-            t0[0] = a.x, t0[1] = a.y;
+            const double2 x = *reinterpret_cast<const double2 *>(thr + c);
+            t0[0] = x.x, t0[1] = x.y;
         } else {
             t0[0] = thr[c], t0[1] = thr[c + 1];
         }
 #pragma unroll
         for (int i = 0; i < 2; i++) {
-            const bool valid = (nb < NB - 1) || (i ? v1 : v0);
-            const bool ok = FULL ? valid : (act && valid);
             const double g = acc[nb][i];
+            const bool ok = QDT_VALID(nb, i);
             if (do_kkt && ok) {
                 const double x1 = t0[i] * fma(2.0, g, lam);
                 skkt = fma(x1, x1, skkt);
@@ -219,55 +218,102 @@ __device__ __forceinline__ void row_step(double (&acc)[NB][2], const double *thr
                 }
             }
             const double x = fma(-tk, g, t0[i]);
-            acc[nb][i] = ok ? x : -INFINITY;
             if (ok) {
                 s += x;
-                xm = fmax(xm, x);
+                xm = x > xm ? x : xm;
+                xn = x < xn ? x : xn;
             }
+            acc[nb][i] = ok ? x : -INFINITY;
         }
     }
     s = quad_sum(s);
     xm = quad_max(xm);
-    // Michelot from the larger of two lower bounds of tau* (the mean bound and max - 1): the
-    // active-set updates then increase monotonically to tau* (reading R4)
+    xn = quad_min(xn);
+    // ---- threshold (reading R4).  tau0 = (sum X - 1)/N is exact when every entry stays active
+    // (min X > tau0); otherwise Michelot rounds from the lower bound max(tau0, max X - 1): each
+    // round takes A = {X > tau}, tau <- (sum_A X - 1)/|A|, and stops as soon as min_A X > tau
+    // (then {X > tau} = A: the fixed point) or |A| stops shrinking.
+    double tau = (s - 1.0) / (double)N;
+    bool done = !ract || xn > tau;
+    if (!done) tau = fmax(tau, xm - 1.0);
     int cnt = N + 1;
-    double tau = fmax((s - 1.0) / (double)N, xm - 1.0);
-    bool done = !(FULL || act);
     for (int round = 0; round <= N; round++) {
         if (__all_sync(0xffffffffu, done)) break;
-        double ps = 0.0;
+        double ps = 0.0, mA = INFINITY;
         int pc = 0;
 #pragma unroll
         for (int nb = 0; nb < NB; nb++)
 #pragma unroll
-            for (int i = 0; i < 2; i++)
-                if (acc[nb][i] > tau) {
-                    ps += acc[nb][i];
+            for (int i = 0; i < 2; i++) {
+                const double x = acc[nb][i];
+                if (x > tau) {
+                    ps += x;
                     pc++;
+                    mA = x < mA ? x : mA;
                 }
+            }
         ps = quad_sum(ps);
         pc = quad_sum_i(pc);
+        mA = quad_min(mA);
         if (!done) {
             if (pc >= cnt) {
                 done = true;
             } else {
                 cnt = pc;
                 tau = (ps - 1.0) / (double)pc;
+                done = mA > tau;
             }
         }
     }
-    if (FULL || act) {
+    if (ract) {
 #pragma unroll
         for (int nb = 0; nb < NB; nb++) {
             const int c = 8 * nb + 2 * t4;
-            const double o0 = fmax(acc[nb][0] - tau, 0.0), o1 = fmax(acc[nb][1] - tau, 0.0);
+            double o0 = acc[nb][0] - tau, o1 = acc[nb][1] - tau;
+            o0 = o0 > 0.0 ? o0 : 0.0;
+            o1 = o1 > 0.0 ? o1 : 0.0;
             if (EVEN) {
-                if (nb < NB - 1 || v0) *reinterpret_cast<double2 *>(orow + c) = make_double2(o0, o1);
+                if (nb < NB - 1 || v0) {
+                    *reinterpret_cast<double2 *>(orow + c) = make_double2(o0, o1);
+                    if (SMEM_OUT) *reinterpret_cast<double2 *>(thr + c) = make_double2(o0, o1);
+                }
             } else {
-                if (nb < NB - 1 || v0) orow[c] = o0;
-                if (nb < NB - 1 || v1) orow[c + 1] = o1;
+                if (nb < NB - 1 || v0) {
+                    orow[c] = o0;
+                    if (SMEM_OUT) thr[c] = o0;
+                }
+                if (nb < NB - 1 || v1) {
+                    orow[c + 1] = o1;
+                    if (SMEM_OUT) thr[c + 1] = o1;
+                }
             }
         }
+    }
+#undef QDT_VALID
+}
+
+// bwd GEMM of one staged chunk: acc += F_chunk^T R_chunk over kc probes (k-steps of 4; only
+// the tail step is masked).  F: chunk rows (probe-major, pitch STP), lane's row 8w + g4 folded
+// in; R: chunk rows (pitch N), lane's column g4 folded in.
+template <int NB>
+__device__ __forceinline__ void gemm_bwd(double (&acc)[NB][2], const double *F, const double *R,
+                                         int kc, int N, int t4)
+{
+    const int nfull = kc >> 2;
+    for (int ks = 0; ks < nfull; ks++) {
+        const int jj = 4 * ks + t4;
+        const double av = F[jj * STP];
+        const double *rb = R + jj * N;
+#pragma unroll
+        for (int nb = 0; nb < NB; nb++) dmma(acc[nb][0], acc[nb][1], av, rb[8 * nb]);
+    }
+    if (kc & 3) {
+        const int jj = 4 * nfull + t4;
+        const bool okj = jj < kc;
+        const double av = okj ? F[jj * STP] : 0.0;
+        const double *rb = R + jj * N;
+#pragma unroll
+        for (int nb = 0; nb < NB; nb++) dmma(acc[nb][0], acc[nb][1], av, okj ? rb[8 * nb] : 0.0);
     }
 }
 
@@ -295,7 +341,7 @@ size_t sweep_bwd_smem(int N, int NB)
 }
 
 template <int NB>
-__global__ void __launch_bounds__(256, 2) k_bwd_mma(SweepArgs a)
+__global__ void __launch_bounds__(256, (NB <= 13 ? 2 : 1)) k_bwd_mma(SweepArgs a)
 {
     extern __shared__ __align__(128) double sm[];
     __shared__ __align__(8) uint64_t bars[3];
@@ -364,18 +410,7 @@ __global__ void __launch_bounds__(256, 2) k_bwd_mma(SweepArgs a)
         const int rsh = (int)(((uintptr_t)(a.R + (int64_t)(u.p0 + pb) * N) & 15) >> 3);
         const double *F = Fs + (c & 1) * SKC * STP + 8 * warp + g4;
         const double *Rr = Rs + (c & 1) * L.rsz + rsh + g4;
-        const int nks = (kc + 3) >> 2;
-        for (int ks = 0; ks < nks; ks++) {
-            const int j = 4 * ks + t4;
-            const bool okj = j < kc;
-            const double av = okj ? F[j * STP] : 0.0;
-            const double *rb = Rr + j * N;
-#pragma unroll
-            for (int nb = 0; nb < NB; nb++) {
-                const double bv = okj ? rb[8 * nb] : 0.0;
-                dmma(acc[nb][0], acc[nb][1], av, bv);
-            }
-        }
+        gemm_bwd<NB>(acc, F, Rr, kc, N, t4);
         __syncthreads();
     }
 
@@ -421,7 +456,7 @@ __global__ void __launch_bounds__(256, 2) k_bwd_mma(SweepArgs a)
     const int kl = k0 + r;
     const int64_t kg = a.kb + kl;
     const bool has_prev = kg > 0, has_next = kg + 1 < a.M;
-    const double *thr = Th + th_sh + (r + 1) * N;
+    double *thr = Th + th_sh + (r + 1) * N;
     double sreg = 0.0, skkt = 0.0, skktp = 0.0;
     const bool do_kkt = (it % a.kkt_every) == 0;
     const double tk = act ? a.tstep[kl] : 0.0;
@@ -464,6 +499,41 @@ __global__ void __launch_bounds__(256, 2) k_bwd_mma(SweepArgs a)
     }
 }
 
+// fwd GEMM, transposed so that outcomes are the M dimension and probes the N dimension:
+// C[n][d] += sum_k Theta[k][n] F[d][k] for one outcome m-block (lane row n = 8 mb + g4) and NM
+// probe n-blocks (lane columns d = 8 nb + 2 t4 + {0,1}).  A fragment a = Theta[4 ks + t4][n],
+// B fragment b = F[8 nb + g4][4 ks + t4].  Tcol: Theta + t4 N + 8 mb + g4; Frow: F + g4 STP + t4.
+// Rows k >= Tt are masked (stale shared memory); probe masks are applied by the caller via fok.
+template <int NM, bool MASKK>
+__device__ __forceinline__ void gemm_fwd_t(double (&cf)[4][2], const double *Tcol, const double *Frow,
+                                           int N, int Tt, int t4, const bool (&fok)[4])
+{
+    const int nks = (Tt + 3) >> 2;
+    for (int ks = 0; ks < nks; ks++) {
+        double av = Tcol[4 * ks * N];
+        if (MASKK) av = (4 * ks + t4 < Tt) ? av : 0.0;
+#pragma unroll
+        for (int nb = 0; nb < NM; nb++) {
+            const double bv = Frow[8 * nb * STP + 4 * ks];
+            dmma(cf[nb][0], cf[nb][1], av, fok[nb] ? bv : 0.0);
+        }
+    }
+}
+
+template <bool MASKK>
+__device__ __forceinline__ void gemm_fwd_t_nm(int nm, double (&cf)[4][2], const double *Tcol,
+                                              const double *Frow, int N, int Tt, int t4,
+                                              const bool (&fok)[4])
+{
+    switch (nm) {
+        case 1: gemm_fwd_t<1, MASKK>(cf, Tcol, Frow, N, Tt, t4, fok); break;
+        case 2: gemm_fwd_t<2, MASKK>(cf, Tcol, Frow, N, Tt, t4, fok); break;
+        case 3: gemm_fwd_t<3, MASKK>(cf, Tcol, Frow, N, Tt, t4, fok); break;
+        case 4: gemm_fwd_t<4, MASKK>(cf, Tcol, Frow, N, Tt, t4, fok); break;
+        default: break;
+    }
+}
+
 // ------------------------------------------------------------------------------ fwd sweep
 // Unit: Fock tiles [t0, t1) and the union of their probe windows [u0, u1) (<= FWCAP probes).
 // Warp w owns (m-block, n-block) pairs [w PP, (w+1) PP) of the (u1-u0)/8 x NB pair grid.
@@ -488,19 +558,8 @@ __global__ void __launch_bounds__(256, 1) k_fwd_mma(SweepFwdArgs a)
     double *Ts = sm;                    // 2 x tsz
     double *Fs = sm + 2 * tsz;          // 2 x FWCAP x STP
     const int Wu = u.u1 - u.u0;
-    const int nm = (Wu + 7) >> 3;
-    const int npair = nm * NB;
-    const int PP = (npair + 7) >> 3;
-    const int pbeg = warp * PP;
-    int mbA = 0;
-    int mbs[NB], nbs[NB];
-#pragma unroll
-    for (int i = 0; i < NB; i++) {
-        const int p = min(pbeg + i, npair - 1);
-        mbs[i] = p / NB;
-        nbs[i] = p - (p / NB) * NB;
-    }
-    if (pbeg < npair) mbA = pbeg / NB;
+    const int nm = (Wu + 7) >> 3;       // <= FWCAP / 8 = 4 probe n-blocks
+    const bool second = warp + 8 < NB;  // warp-uniform: outcome m-block warp + 8 exists
 
     if (tid == 0) {
         mbar_init(&bars[0], 1);
@@ -529,9 +588,9 @@ __global__ void __launch_bounds__(256, 1) k_fwd_mma(SweepFwdArgs a)
     };
     if (tid == 0) issue(0);
 
-    double acc[NB][2];
+    double cA[4][2], cB[4][2];
 #pragma unroll
-    for (int i = 0; i < NB; i++) acc[i][0] = acc[i][1] = 0.0;
+    for (int i = 0; i < 4; i++) cA[i][0] = cA[i][1] = cB[i][0] = cB[i][1] = 0.0;
 
     for (int j = 0; j < ntile; j++) {
         if (tid == 0 && j + 1 < ntile) issue(j + 1);
@@ -540,45 +599,224 @@ __global__ void __launch_bounds__(256, 1) k_fwd_mma(SweepFwdArgs a)
         const int k0 = t * ST;
         const int Tt = min(ST, a.Ml - k0);
         const int sh = (int)(((uintptr_t)(a.theta + (int64_t)k0 * N) & 15) >> 3);
+        // union probes outside this tile's window hold stale F rows: their B fragments -> 0
         const int ra = max(a.tile_dA[t], u.u0) - u.u0, rb = min(a.tile_dB[t], u.u1) - u.u0;
-        const double *T = Ts + (j & 1) * tsz + sh + g4;
-        const double *F = Fs + (j & 1) * FWCAP * STP + t4;
-        // A rows (probes) of the two m-blocks this warp may touch, masked to the tile's window
-        const int dA0 = 8 * mbA + g4, dA1 = dA0 + 8;
-        const bool okA0 = dA0 >= ra && dA0 < rb, okA1 = dA1 >= ra && dA1 < rb;
-        if (pbeg < npair) {
-            const int nks = (Tt + 3) >> 2;
-            for (int ks = 0; ks < nks; ks++) {
-                const int kr = 4 * ks + t4;  // row of this lane's B fragment / A column
-                const double a0 = okA0 ? F[dA0 * STP + 4 * ks] : 0.0;
-                const double a1 = okA1 ? F[dA1 * STP + 4 * ks] : 0.0;
-                const bool okr = kr < Tt;
+        bool fok[4];
 #pragma unroll
-                for (int i = 0; i < NB; i++) {
-                    if (i < PP && pbeg + i < npair) {
-                        const double av = (mbs[i] == mbA) ? a0 : a1;
-                        const double bv = okr ? T[kr * N + 8 * nbs[i]] : 0.0;
-                        dmma(acc[i][0], acc[i][1], av, bv);
-                    }
+        for (int nb = 0; nb < 4; nb++) fok[nb] = 8 * nb + g4 >= ra && 8 * nb + g4 < rb;
+        const double *T = Ts + (j & 1) * tsz + sh + t4 * N + g4;
+        const double *Frow = Fs + (j & 1) * FWCAP * STP + g4 * STP + t4;
+        if (Tt == ST) {
+            gemm_fwd_t_nm<false>(nm, cA, T + 8 * warp, Frow, N, Tt, t4, fok);
+            if (second) gemm_fwd_t_nm<false>(nm, cB, T + 8 * (warp + 8), Frow, N, Tt, t4, fok);
+        } else {
+            gemm_fwd_t_nm<true>(nm, cA, T + 8 * warp, Frow, N, Tt, t4, fok);
+            if (second) gemm_fwd_t_nm<true>(nm, cB, T + 8 * (warp + 8), Frow, N, Tt, t4, fok);
+        }
+        __syncthreads();
+    }
+    // partial rows rpart[(poff + d) * N + n]: lane holds n = 8 mb + g4, d = 8 nb + 2 t4 + {0,1}
+#pragma unroll
+    for (int pass = 0; pass < 2; pass++) {
+        const int n = 8 * (warp + 8 * pass) + g4;
+        if (n >= N || (pass && !second)) continue;
+#pragma unroll
+        for (int nb = 0; nb < 4; nb++)
+#pragma unroll
+            for (int i = 0; i < 2; i++) {
+                const int d = 8 * nb + 2 * t4 + i;
+                if (nb < nm && d < Wu) a.rpart[(u.poff + d) * (int64_t)N + n] = pass ? cB[nb][i] : cA[nb][i];
+            }
+    }
+}
+
+// ------------------------------------------------------------------------------ fused sweep
+// Persistent kernel over the "light" tiles (window <= cap probes): CTA c sweeps a contiguous tile
+// range [ta, tb) in Fock order with a 2-stage bulk-copy pipeline (Theta_k tile + halo, F block,
+// R rows of the window).  Per tile:
+//   1. G = F_blk^T R_win (DMMA), row epilogue (row_step) -> Theta_{k+1} to HBM and in place into
+//      the stage's Theta rows;
+//   2. forward partials of the NEXT iteration: ring[d] += F_blk[d, :] Theta_{k+1,tile} (DMMA) for
+//      the window's probes; the ring keeps one accumulator row per open probe (slot d mod cap);
+//   3. probes whose band ends before the next tile (d < dA_{t+1}) are flushed to their partial row
+//      rpart[poff_c + d - dfirst_c] and their slot zeroed.
+// Scalar partials (regulariser, KKT) accumulate per CTA in registers in a fixed order.
+size_t sweep_fused_smem(int N, int NB, int cap)
+{
+    const int thsz = (((ST + 2) * N + 8 * NB + 4) + 1) & ~1;
+    const int rsz = ((cap * N + 8 * NB + 4) + 1) & ~1;
+    const int stage = thsz + cap * STP + rsz;
+    return (size_t)(2 * stage + cap * 8 * NB) * sizeof(double);
+}
+
+template <int NB>
+__global__ void __launch_bounds__(256, 1) k_sweep_fused(SweepFusedArgs a)
+{
+    extern __shared__ __align__(128) double sm[];
+    __shared__ __align__(8) uint64_t bars[2];
+    __shared__ double red[8 * 3];
+    const DevState *st = a.state;
+    if (st && st->stop) return;
+    const int64_t it = st ? st->it : 0;
+    const int N = a.N, cap = a.cap;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g4 = lane >> 2, t4 = lane & 3;
+    const int thsz = (((ST + 2) * N + 8 * NB + 4) + 1) & ~1;
+    const int rsz = ((cap * N + 8 * NB + 4) + 1) & ~1;
+    const int stage = thsz + cap * STP + rsz;
+    const int RP = 8 * NB;                       // ring pitch
+    double *ring = sm + 2 * stage;
+    const int ta = a.range[2 * blockIdx.x], tb = a.range[2 * blockIdx.x + 1];
+    const int dfirst = a.tile_dA[ta];
+    const int64_t poff = a.poff[blockIdx.x];
+    const double gamma = a.gamma;
+    const bool do_kkt = (it % a.kkt_every) == 0;
+    const bool even = (N & 1) == 0;
+
+    for (int e = tid; e < cap * RP; e += 256) ring[e] = 0.0;
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    auto issue = [&](int j) {
+        const int t = ta + j;
+        const int k0 = t * ST;
+        const int Tt = min(ST, a.Ml - k0);
+        const int dA = a.tile_dA[t], W = a.tile_dB[t] - dA;
+        double *S = sm + (j & 1) * stage;
+        const double *src;
+        int sh;
+        uint32_t by;
+        aligned_span(a.theta + (int64_t)(k0 - 1) * N, (int64_t)(Tt + 2) * N, &src, &sh, &by);
+        const double *rsrc;
+        int rsh;
+        uint32_t rby;
+        aligned_span(a.R + (int64_t)dA * N, (int64_t)W * N, &rsrc, &rsh, &rby);
+        const uint32_t fby = (uint32_t)W * STP * 8;
+        uint64_t *bar = &bars[j & 1];
+        mbar_expect_tx(bar, by + (W ? fby + rby : 0));
+        bulk_g2s(S, src, by, bar);
+        if (W) {
+            bulk_g2s(S + thsz, a.Fb + a.fb_off[t], fby, bar);
+            bulk_g2s(S + thsz + cap * STP, rsrc, rby, bar);
+        }
+    };
+    const int nt = tb - ta;
+    if (tid == 0) {
+        if (nt > 0) issue(0);
+        if (nt > 1) issue(1);
+    }
+    double sreg = 0.0, skkt = 0.0, skktp = 0.0;
+    for (int j = 0; j < nt; j++) {
+        const int t = ta + j;
+        const int k0 = t * ST;
+        const int Tt = min(ST, a.Ml - k0);
+        const int dA = a.tile_dA[t], W = a.tile_dB[t] - dA;
+        double *S = sm + (j & 1) * stage;
+        const int th_sh = (int)(((uintptr_t)(a.theta + (int64_t)(k0 - 1) * N) & 15) >> 3);
+        const int r_sh = (int)(((uintptr_t)(a.R + (int64_t)dA * N) & 15) >> 3);
+        double *Th = S + th_sh;
+        const double *Fs = S + thsz;
+        const double *Rs = S + thsz + cap * STP + r_sh;
+        mbar_wait(&bars[j & 1], (j >> 1) & 1);
+
+        // ---- 1. G = F^T R (warp = m-block of 8 rows, all NB n-blocks), then the row epilogue
+        double acc[NB][2];
+#pragma unroll
+        for (int nb = 0; nb < NB; nb++) acc[nb][0] = acc[nb][1] = 0.0;
+        gemm_bwd<NB>(acc, Fs + 8 * warp + g4, Rs + g4, W, N, t4);
+        {
+            const int r = 8 * warp + g4;
+            const bool act = r < Tt;
+            const int kl = k0 + r;
+            const int64_t kg = a.kb + kl;
+            const bool has_prev = kg > 0, has_next = kg + 1 < a.M;
+            double *thr = Th + (r + 1) * N;
+            const double tk = act ? a.tstep[kl] : 0.0;
+            double *orow = a.out + (int64_t)kl * N;
+            const bool full = Tt == ST && a.kb + k0 > 0 && a.kb + k0 + ST < a.M;
+            if (full && even)
+                row_step<NB, true, true, true>(acc, thr, N, t4, act, has_prev, has_next, gamma, tk, do_kkt,
+                                               false, sreg, skkt, skktp, orow);
+            else if (full)
+                row_step<NB, true, false, true>(acc, thr, N, t4, act, has_prev, has_next, gamma, tk, do_kkt,
+                                                false, sreg, skkt, skktp, orow);
+            else
+                row_step<NB, false, false, true>(acc, thr, N, t4, act, has_prev, has_next, gamma, tk,
+                                                 do_kkt, false, sreg, skkt, skktp, orow);
+        }
+        __syncthreads();  // Theta_{k+1} tile complete in smem
+
+        // ---- 2. ring[d][n] += sum_k F_blk[d][k] Theta_{k+1}[k][n] for the window's probes
+        //      (transposed GEMM: warp w takes outcome m-blocks w and w + 8, all nm <= 4 probe
+        //      n-blocks; every (probe, outcome) pair is owned by one lane: no cross-warp sums)
+        {
+            const int nm = (W + 7) >> 3;
+            int slot[4][2];
+#pragma unroll
+            for (int nb = 0; nb < 4; nb++)
+#pragma unroll
+                for (int i = 0; i < 2; i++) slot[nb][i] = ((dA + 8 * nb + 2 * t4 + i) % cap) * RP;
+            const bool fok[4] = {true, true, true, true};
+            const double *Frow = Fs + g4 * STP + t4;
+            for (int mbo = warp; mbo < NB; mbo += 8) {
+                double cf[4][2];
+#pragma unroll
+                for (int nb = 0; nb < 4; nb++) cf[nb][0] = cf[nb][1] = 0.0;
+                const double *Tcol = Th + N + t4 * N + 8 * mbo + g4;   // Theta_{k+1}, tile row 0
+                if (Tt == ST)
+                    gemm_fwd_t_nm<false>(nm, cf, Tcol, Frow, N, Tt, t4, fok);
+                else
+                    gemm_fwd_t_nm<true>(nm, cf, Tcol, Frow, N, Tt, t4, fok);
+                const int n = 8 * mbo + g4;
+                if (n < N) {
+#pragma unroll
+                    for (int nb = 0; nb < 4; nb++)
+#pragma unroll
+                        for (int i = 0; i < 2; i++)
+                            if (nb < nm && 8 * nb + 2 * t4 + i < W) ring[slot[nb][i] + n] += cf[nb][i];
                 }
             }
         }
         __syncthreads();
-    }
-    // partial rows: rpart[(poff + d_rel) * N + c], d_rel = 8 mb + g4, c = 8 nb + 2 t4 + {0,1}
-#pragma unroll
-    for (int i = 0; i < NB; i++) {
-        if (i < PP && pbeg + i < npair) {
-            const int drel = 8 * mbs[i] + g4;
-            if (drel < Wu) {
-                double *dst = a.rpart + (u.poff + drel) * (int64_t)N;
-#pragma unroll
-                for (int e = 0; e < 2; e++) {
-                    const int c = 8 * nbs[i] + 2 * t4 + e;
-                    if (c < N) dst[c] = acc[i][e];
-                }
+        // ---- 3. flush the probes that leave the window: [dA, next dA) (all at the range end)
+        {
+            const int dnext = (j + 1 < nt) ? a.tile_dA[t + 1] : dA + W;
+            const int nl = dnext - dA;
+            for (int e = tid; e < nl * RP; e += 256) {
+                const int q = e / RP, c = e - q * RP;
+                const int d = dA + q;
+                double *rr = ring + (d % cap) * RP + c;
+                if (c < N) a.rpart[(poff + (d - dfirst)) * (int64_t)N + c] = *rr;
+                *rr = 0.0;
             }
         }
+        __syncthreads();
+        if (tid == 0 && j + 2 < nt) issue(j + 2);
+    }
+    // ---- per-CTA scalar partials (fixed order)
+    sreg = wsum(sreg);
+    skkt = wsum(skkt);
+    if (lane == 0) {
+        red[warp * 3 + 0] = skkt;
+        red[warp * 3 + 2] = sreg;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double v0 = 0.0, v2 = 0.0;
+        for (int w = 0; w < 8; w++) {
+            v0 += red[w * 3 + 0];
+            v2 += red[w * 3 + 2];
+        }
+        double *p = a.part + (int64_t)a.part_base * NSC_TILE + (int64_t)blockIdx.x * NSC_TILE;
+        if (do_kkt) {
+            p[SC_KKT] = v0;
+            p[SC_KKTP] = 0.0;
+        }
+        p[SC_REG] = v2;
+        p[SC_DTH] = 0.0;
     }
 }
 
@@ -721,6 +959,9 @@ static cudaError_t prep_nb()
     cudaError_t e = cudaFuncSetAttribute(k_bwd_mma<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_fwd_mma<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_sweep_fused<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 SW_FUSED_SMEM_MAX);
     return e;
 }
 
@@ -762,6 +1003,20 @@ cudaError_t launch_fwd_mma(const SweepFwdArgs &a, int nunits, int NB, cudaStream
     switch (NB) {
 #define QDT_CASE(nb) \
     case nb: k_fwd_mma<nb><<<nunits, 256, smem, s>>>(a); break;
+        QDT_FOR_NB(QDT_CASE)
+#undef QDT_CASE
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sweep_fused(const SweepFusedArgs &a, int nctas, int NB, cudaStream_t s)
+{
+    if (nctas <= 0) return cudaSuccess;
+    const size_t smem = sweep_fused_smem(a.N, NB, a.cap);
+    switch (NB) {
+#define QDT_CASE(nb) \
+    case nb: k_sweep_fused<nb><<<nctas, 256, smem, s>>>(a); break;
         QDT_FOR_NB(QDT_CASE)
 #undef QDT_CASE
         default: return cudaErrorInvalidValue;

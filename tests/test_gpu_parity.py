@@ -281,3 +281,25 @@ def test_megascale_solve_parity(q, ctx):
     assert _trace_ok(rg["trace"], ro["trace"], I.P)
     Th = rg["theta"]
     assert Th.min() >= 0 and np.abs(Th.sum(1) - 1).max() <= 4 * Th.shape[1] * EPS
+
+
+@pytest.mark.parametrize("N,gamma", [(20, 1e-3), (37, 0.0), (100, 1e-5), (8, 1e-2)])
+@pytest.mark.parametrize("fused", ["0", "1"])
+def test_fused_sweep_parity(q, ctx, N, gamma, fused, monkeypatch):
+    """Log-spaced probes over a long Fock axis: most tiles have narrow windows, so the solve runs
+    (QDT_FUSED=1) the fused persistent sweep on the light tiles beside the split heavy tiles, or
+    (QDT_FUSED=0) the unfused sweep; 30 iterations against the oracle, P9 invariants, trace."""
+    monkeypatch.setenv("QDT_FUSED", fused)
+    rng = np.random.default_rng(N)
+    D, M = 400, 30000
+    a2 = np.geomspace(1.0, 0.9 * M, D)
+    P = rng.dirichlet(np.ones(N) * 0.3, D)
+    Fo = oracle.Probes(a2, M)
+    Fg = q.qdt_build_probes(ctx, a2, M)
+    ro = oracle.solve(Fo, P, gamma, 0.0, 30)
+    rg = q.qdt_solve(ctx, Fg, P, gamma, 0.0, 30)
+    assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9
+    assert _trace_ok(rg["trace"], ro["trace"], P)
+    np.testing.assert_allclose(rg["kkt"], ro["kkt"], rtol=1e-8, atol=1e-15)
+    Th = rg["theta"]
+    assert Th.min() >= 0 and np.abs(Th.sum(1) - 1).max() <= 4 * N * EPS
