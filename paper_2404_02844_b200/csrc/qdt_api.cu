@@ -1249,6 +1249,7 @@ static SweepArgs sweep_args(const IterCfg &c, SolveBufs &b, const double *R, con
     a.counters = b.counters;
     a.part = b.partT;
     a.kkt_every = c.kkt_every;
+    a.nunits = 0;
     a.state = b.state;
     return a;
 }

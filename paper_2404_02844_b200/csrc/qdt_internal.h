@@ -119,6 +119,7 @@ struct SweepArgs {
     int *counters;
     double *part;
     int kkt_every;
+    int nunits;                 // set by launch_bwd_mma (persistent grid)
     const DevState *state;
 };
 struct SweepFwdArgs {

@@ -17,6 +17,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "qdt_internal.h"
 
 namespace qdt {
@@ -58,6 +60,11 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
             smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
+}
+// bulk prefetch of a global range into L2 (no shared memory, no completion tracking)
+__device__ __forceinline__ void bulk_prefetch_l2(const void *src, uint32_t bytes)
+{
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 // D(8x8) += A(8x4) B(4x8), fp64 tensor core.  Fragments (lane = 4 g + t):
 //   a = A[g][t], b = B[t][g], (c0, c1) = C[g][2t], C[g][2t+1].
@@ -148,11 +155,12 @@ __global__ void k_tile_F(Band b, int64_t kb, int Ml, const int32_t *tile_dA, con
 // NB = ceil(N/8): only the last n-block can hold columns >= N; they are neutralised (+inf for the
 // row min, -inf for X) and never stored.  FULL: an interior row of a full tile (row active,
 // neighbours k-1 and k+1 exist): no per-row predicates.  EVEN: N even, pairs move as double2.
-template <int NB, bool FULL, bool EVEN, bool SMEM_OUT = false>
-__device__ __forceinline__ void row_step(double (&acc)[NB][2], double *thr, int N, int t4,
+template <int NB, bool FULL, bool EVEN, bool SMEM_OUT>
+__device__ __forceinline__ void row_pass(double (&acc)[NB][2], const double *thr, int N, int t4,
                                          bool act, bool has_prev, bool has_next, double gamma,
                                          double tk, bool do_kkt, bool want_kktp, double &sreg,
-                                         double &skkt, double &skktp, double *orow)
+                                         double &skkt, double &skktp, double &s, double &xm,
+                                         double &xn)
 {
     const int cl = 8 * (NB - 1) + 2 * t4;
     const bool v0 = cl < N, v1 = cl + 1 < N;
@@ -194,7 +202,7 @@ __device__ __forceinline__ void row_step(double (&acc)[NB][2], double *thr, int 
         lamp = lam > 0.0 ? lam : 0.0;
     }
     // ---- pass 2: KKT terms, X = Theta - t_k G, row sum / max / min of X
-    double s = 0.0, xm = -INFINITY, xn = INFINITY;
+    s = 0.0, xm = -INFINITY, xn = INFINITY;
 #pragma unroll
     for (int nb = 0; nb < NB; nb++) {
         const int c = 8 * nb + 2 * t4;
@@ -229,6 +237,18 @@ __device__ __forceinline__ void row_step(double (&acc)[NB][2], double *thr, int 
     s = quad_sum(s);
     xm = quad_max(xm);
     xn = quad_min(xn);
+#undef QDT_VALID
+}
+
+// Threshold and output of the row (after row_pass): X in acc (-inf for invalid columns), s, xm,
+// xn its quad-reduced sum / max / min.  SMEM_OUT also writes Theta_{k+1} over the row in smem.
+template <int NB, bool FULL, bool EVEN, bool SMEM_OUT>
+__device__ __forceinline__ void row_project(double (&acc)[NB][2], double *thr, int N, int t4,
+                                            bool act, double s, double xm, double xn, double *orow)
+{
+    const int cl = 8 * (NB - 1) + 2 * t4;
+    const bool v0 = cl < N, v1 = cl + 1 < N;
+    const bool ract = FULL || act;
     // ---- threshold (reading R4).  tau0 = (sum X - 1)/N is exact when every entry stays active
     // (min X > tau0); otherwise Michelot rounds from the lower bound max(tau0, max X - 1): each
     // round takes A = {X > tau}, tau <- (sum_A X - 1)/|A|, and stops as soon as min_A X > tau
@@ -289,7 +309,18 @@ __device__ __forceinline__ void row_step(double (&acc)[NB][2], double *thr, int 
             }
         }
     }
-#undef QDT_VALID
+}
+
+template <int NB, bool FULL, bool EVEN, bool SMEM_OUT = false>
+__device__ __forceinline__ void row_step(double (&acc)[NB][2], double *thr, int N, int t4,
+                                         bool act, bool has_prev, bool has_next, double gamma,
+                                         double tk, bool do_kkt, bool want_kktp, double &sreg,
+                                         double &skkt, double &skktp, double *orow)
+{
+    double s, xm, xn;
+    row_pass<NB, FULL, EVEN, SMEM_OUT>(acc, thr, N, t4, act, has_prev, has_next, gamma, tk, do_kkt,
+                                       want_kktp, sreg, skkt, skktp, s, xm, xn);
+    row_project<NB, FULL, EVEN, SMEM_OUT>(acc, thr, N, t4, act, s, xm, xn, orow);
 }
 
 // bwd GEMM of one staged chunk: acc += F_chunk^T R_chunk over kc probes (k-steps of 4; only
@@ -340,6 +371,10 @@ size_t sweep_bwd_smem(int N, int NB)
     return (size_t)(thsz + 2 * SKC * STP + 2 * rsz) * sizeof(double);
 }
 
+// Persistent: CTA b processes units b, b + G, b + 2G, ... (heavy first).  The chunk buffers of
+// the next unit are refilled as soon as this unit's GEMM is done, the Theta tile as soon as the
+// epilogue has read it (before the Michelot rounds and stores), so the next unit's loads overlap
+// the current unit's epilogue.
 template <int NB>
 __global__ void __launch_bounds__(256, (NB <= 13 ? 2 : 1)) k_bwd_mma(SweepArgs a)
 {
@@ -353,17 +388,15 @@ __global__ void __launch_bounds__(256, (NB <= 13 ? 2 : 1)) k_bwd_mma(SweepArgs a
     const int N = a.N;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g4 = lane >> 2, t4 = lane & 3;
-    const SwUnit u = a.units[blockIdx.x];
-    const int k0 = u.tile * ST;
-    const int Tt = min(ST, a.Ml - k0);
+    const int G = gridDim.x;
+    int unit = blockIdx.x;
+    if (unit >= a.nunits) return;
     const SwLayout<NB> L(N);
     double *Th = sm;
     double *Fs = sm + L.thsz;
     double *Rs = Fs + 2 * SKC * STP;
-
-    const int W = u.p1 - u.p0;
-    const int nch = (W + SKC - 1) / SKC;
-    const double *Fg = a.Fb + a.fb_off[u.tile] + (int64_t)(u.p0 - a.tile_dA[u.tile]) * STP;
+    const bool do_kkt = (it % a.kkt_every) == 0;
+    const bool even = (N & 1) == 0;
 
     if (tid == 0) {
         mbar_init(&bars[0], 1);
@@ -372,130 +405,155 @@ __global__ void __launch_bounds__(256, (NB <= 13 ? 2 : 1)) k_bwd_mma(SweepArgs a
         fence_barrier_init();
     }
     __syncthreads();
-
-    const double *th_src;
-    int th_sh;
-    uint32_t th_bytes;
-    aligned_span(a.theta + (int64_t)(k0 - 1) * N, (int64_t)(Tt + 2) * N, &th_src, &th_sh, &th_bytes);
-    auto issue_chunk = [&](int c) {
-        const int pb = c * SKC;
-        const int kc = min(SKC, W - pb);
+    // issue helpers (thread 0 only); chunk stage / parity follow a running chunk counter
+    uint32_t c_issue = 0, c_use = 0, th_use = 0;
+    auto issue_theta = [&](const SwUnit &v) {
+        const int k0 = v.tile * ST, Tt = min(ST, a.Ml - k0);
+        const double *src;
+        int sh;
+        uint32_t by;
+        aligned_span(a.theta + (int64_t)(k0 - 1) * N, (int64_t)(Tt + 2) * N, &src, &sh, &by);
+        mbar_expect_tx(&bars[0], by);
+        bulk_g2s(Th, src, by, &bars[0]);
+    };
+    auto issue_chunk = [&](const SwUnit &v, int c) {
+        const int W = v.p1 - v.p0, pb = c * SKC, kc = min(SKC, W - pb);
         const double *rsrc;
         int rsh;
         uint32_t rbytes;
-        aligned_span(a.R + (int64_t)(u.p0 + pb) * N, (int64_t)kc * N, &rsrc, &rsh, &rbytes);
-        uint64_t *bar = &bars[1 + (c & 1)];
+        aligned_span(a.R + (int64_t)(v.p0 + pb) * N, (int64_t)kc * N, &rsrc, &rsh, &rbytes);
+        const int stg = c_issue & 1;
+        uint64_t *bar = &bars[1 + stg];
         const uint32_t fbytes = (uint32_t)kc * STP * 8;
+        const double *Fg = a.Fb + a.fb_off[v.tile] + (int64_t)(v.p0 - a.tile_dA[v.tile] + pb) * STP;
         mbar_expect_tx(bar, fbytes + rbytes);
-        bulk_g2s(Fs + (c & 1) * SKC * STP, Fg + (int64_t)pb * STP, fbytes, bar);
-        bulk_g2s(Rs + (c & 1) * L.rsz, rsrc, rbytes, bar);
+        bulk_g2s(Fs + stg * SKC * STP, Fg, fbytes, bar);
+        bulk_g2s(Rs + stg * L.rsz, rsrc, rbytes, bar);
+        c_issue++;
     };
+    SwUnit u = a.units[unit];
     if (tid == 0) {
-        if (u.nsplit == 1) {
-            mbar_expect_tx(&bars[0], th_bytes);
-            bulk_g2s(Th, th_src, th_bytes, &bars[0]);
-        }
-        if (nch > 0) issue_chunk(0);
+        if (u.nsplit == 1) issue_theta(u);
+        if (u.p1 > u.p0) issue_chunk(u, 0);
     }
-
-    double acc[NB][2];
-#pragma unroll
-    for (int nb = 0; nb < NB; nb++) acc[nb][0] = acc[nb][1] = 0.0;
-
-    for (int c = 0; c < nch; c++) {
-        if (tid == 0 && c + 1 < nch) issue_chunk(c + 1);
-        mbar_wait(&bars[1 + (c & 1)], (c >> 1) & 1);
-        const int pb = c * SKC;
-        const int kc = min(SKC, W - pb);
-        const int rsh = (int)(((uintptr_t)(a.R + (int64_t)(u.p0 + pb) * N) & 15) >> 3);
-        const double *F = Fs + (c & 1) * SKC * STP + 8 * warp + g4;
-        const double *Rr = Rs + (c & 1) * L.rsz + rsh + g4;
-        gemm_bwd<NB>(acc, F, Rr, kc, N, t4);
-        __syncthreads();
-    }
-
-    if (u.nsplit > 1) {
-        // split-K: publish the fragment-ordered partial; the last unit of the tile sums the
-        // slots in slot order (deterministic whichever unit finishes last).
-        const int64_t fsz = (int64_t)8 * NB * 64;  // doubles per slot (8 warps x NB x 32 x 2)
-        double *slot = a.scratch + (u.slot_base + u.slot) * fsz;
-#pragma unroll
-        for (int nb = 0; nb < NB; nb++) {
-            double2 v = make_double2(acc[nb][0], acc[nb][1]);
-            __stcg(reinterpret_cast<double2 *>(slot + ((warp * NB + nb) * 32 + lane) * 2), v);
-        }
-        __threadfence();
-        __syncthreads();
-        if (tid == 0) s_last = (atomicAdd(&a.counters[u.tile], 1) == u.nsplit - 1);
-        __syncthreads();
-        if (!s_last) return;
-        __threadfence();
-        if (tid == 0) {
-            mbar_expect_tx(&bars[0], th_bytes);
-            bulk_g2s(Th, th_src, th_bytes, &bars[0]);
-        }
+    while (true) {
+        const int k0 = u.tile * ST;
+        const int Tt = min(ST, a.Ml - k0);
+        const int W = u.p1 - u.p0;
+        const int nch = (W + SKC - 1) / SKC;
+        const int next = unit + G;
+        SwUnit un;
+        if (next < a.nunits) un = a.units[next];
+        double acc[NB][2];
 #pragma unroll
         for (int nb = 0; nb < NB; nb++) acc[nb][0] = acc[nb][1] = 0.0;
-        for (int s = 0; s < u.nsplit; s++) {
-            const double *sl = a.scratch + (u.slot_base + s) * fsz;
+        for (int c = 0; c < nch; c++) {
+            if (tid == 0 && c + 1 < nch) issue_chunk(u, c + 1);
+            const int stg = c_use & 1;
+            mbar_wait(&bars[1 + stg], (c_use >> 1) & 1);
+            c_use++;
+            const int pb = c * SKC;
+            const int kc = min(SKC, W - pb);
+            const int rsh = (int)(((uintptr_t)(a.R + (int64_t)(u.p0 + pb) * N) & 15) >> 3);
+            gemm_bwd<NB>(acc, Fs + stg * SKC * STP + 8 * warp + g4, Rs + stg * L.rsz + rsh + g4, kc, N, t4);
+            __syncthreads();
+        }
+        if (tid == 0 && c_issue != c_use) __trap();  // pipeline invariant
+        // chunk buffers are free: start the next unit's first chunk
+        if (tid == 0 && next < a.nunits && un.p1 > un.p0) issue_chunk(un, 0);
+
+        bool epi = true;
+        if (u.nsplit > 1) {
+            // split-K: publish the fragment-ordered partial; the last unit of the tile sums the
+            // slots in slot order (deterministic whichever unit finishes last).
+            const int64_t fsz = (int64_t)8 * NB * 64;
+            double *slot = a.scratch + (u.slot_base + u.slot) * fsz;
 #pragma unroll
-            for (int nb = 0; nb < NB; nb++) {
-                const double2 v =
-                    __ldcg(reinterpret_cast<const double2 *>(sl + ((warp * NB + nb) * 32 + lane) * 2));
-                acc[nb][0] += v.x;
-                acc[nb][1] += v.y;
+            for (int nb = 0; nb < NB; nb++)
+                __stcg(reinterpret_cast<double2 *>(slot + ((warp * NB + nb) * 32 + lane) * 2),
+                       make_double2(acc[nb][0], acc[nb][1]));
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) s_last = (atomicAdd(&a.counters[u.tile], 1) == u.nsplit - 1);
+            __syncthreads();
+            epi = s_last;
+            if (epi) {
+                __threadfence();
+                if (tid == 0) issue_theta(u);
+#pragma unroll
+                for (int nb = 0; nb < NB; nb++) acc[nb][0] = acc[nb][1] = 0.0;
+                for (int sl = 0; sl < u.nsplit; sl++) {
+                    const double *sp = a.scratch + (u.slot_base + sl) * fsz;
+#pragma unroll
+                    for (int nb = 0; nb < NB; nb++) {
+                        const double2 v =
+                            __ldcg(reinterpret_cast<const double2 *>(sp + ((warp * NB + nb) * 32 + lane) * 2));
+                        acc[nb][0] += v.x;
+                        acc[nb][1] += v.y;
+                    }
+                }
+                if (tid == 0) a.counters[u.tile] = 0;
             }
         }
-        if (tid == 0) a.counters[u.tile] = 0;
-    }
-    mbar_wait(&bars[0], 0);
-
-    // ---- epilogue: the quad (4 lanes) g4 of warp w owns local row r = 8w + g4 (row_step)
-    const int r = 8 * warp + g4;
-    const bool act = r < Tt;
-    const int kl = k0 + r;
-    const int64_t kg = a.kb + kl;
-    const bool has_prev = kg > 0, has_next = kg + 1 < a.M;
-    double *thr = Th + th_sh + (r + 1) * N;
-    double sreg = 0.0, skkt = 0.0, skktp = 0.0;
-    const bool do_kkt = (it % a.kkt_every) == 0;
-    const double tk = act ? a.tstep[kl] : 0.0;
-    double *orow = a.out + (int64_t)kl * N;
-    const bool full = Tt == ST && a.kb + k0 > 0 && a.kb + k0 + ST < a.M;   // block-uniform
-    const bool even = (N & 1) == 0;
-    if (full && even)
-        row_step<NB, true, true>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk, do_kkt, false,
-                                 sreg, skkt, skktp, orow);
-    else if (full)
-        row_step<NB, true, false>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk, do_kkt, false,
-                                  sreg, skkt, skktp, orow);
-    else
-        row_step<NB, false, false>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk, do_kkt, false,
-                                   sreg, skkt, skktp, orow);
-    // ---- per-tile scalar partials (fixed order: lanes, then warps)
-    sreg = wsum(sreg);
-    skkt = wsum(skkt);
-    skktp = wsum(skktp);
-    if (lane == 0) {
-        red[warp * 3 + 0] = skkt;
-        red[warp * 3 + 1] = skktp;
-        red[warp * 3 + 2] = sreg;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        double v0 = 0.0, v1 = 0.0, v2 = 0.0;
-        for (int w = 0; w < 8; w++) {
-            v0 += red[w * 3 + 0];
-            v1 += red[w * 3 + 1];
-            v2 += red[w * 3 + 2];
+        if (epi) {
+            mbar_wait(&bars[0], th_use & 1);
+            th_use++;
+            const int th_sh = (int)(((uintptr_t)(a.theta + (int64_t)(k0 - 1) * N) & 15) >> 3);
+            const int r = 8 * warp + g4;
+            const bool act = r < Tt;
+            const int kl = k0 + r;
+            const int64_t kg = a.kb + kl;
+            const bool has_prev = kg > 0, has_next = kg + 1 < a.M;
+            double *thr = Th + th_sh + (r + 1) * N;
+            double sreg = 0.0, skkt = 0.0, skktp = 0.0, s, xm, xn;
+            const double tk = act ? a.tstep[kl] : 0.0;
+            double *orow = a.out + (int64_t)kl * N;
+            const bool full = Tt == ST && a.kb + k0 > 0 && a.kb + k0 + ST < a.M;
+            if (full && even)
+                row_pass<NB, true, true, false>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk, do_kkt,
+                                                false, sreg, skkt, skktp, s, xm, xn);
+            else if (full)
+                row_pass<NB, true, false, false>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk, do_kkt,
+                                                 false, sreg, skkt, skktp, s, xm, xn);
+            else
+                row_pass<NB, false, false, false>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk,
+                                                  do_kkt, false, sreg, skkt, skktp, s, xm, xn);
+            __syncthreads();  // Theta tile consumed: start the next unit's tile load
+            if (tid == 0 && next < a.nunits && un.nsplit == 1) issue_theta(un);
+            if (full && even)
+                row_project<NB, true, true, false>(acc, thr, N, t4, act, s, xm, xn, orow);
+            else if (full)
+                row_project<NB, true, false, false>(acc, thr, N, t4, act, s, xm, xn, orow);
+            else
+                row_project<NB, false, false, false>(acc, thr, N, t4, act, s, xm, xn, orow);
+            // per-tile scalar partials (fixed order: lanes, then warps)
+            sreg = wsum(sreg);
+            skkt = wsum(skkt);
+            if (lane == 0) {
+                red[warp * 3 + 0] = skkt;
+                red[warp * 3 + 2] = sreg;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                double v0 = 0.0, v2 = 0.0;
+                for (int w = 0; w < 8; w++) {
+                    v0 += red[w * 3 + 0];
+                    v2 += red[w * 3 + 2];
+                }
+                double *p = a.part + (int64_t)u.tile * NSC_TILE;
+                if (do_kkt) {
+                    p[SC_KKT] = v0;
+                    p[SC_KKTP] = 0.0;
+                }
+                p[SC_REG] = v2;
+                p[SC_DTH] = 0.0;
+            }
+        } else if (tid == 0 && next < a.nunits && un.nsplit == 1) {
+            issue_theta(un);
         }
-        double *p = a.part + (int64_t)u.tile * NSC_TILE;
-        if (do_kkt) {
-            p[SC_KKT] = v0;
-            p[SC_KKTP] = v1;
-        }
-        p[SC_REG] = v2;
-        p[SC_DTH] = 0.0;
+        if (next >= a.nunits) break;
+        unit = next;
+        u = un;
     }
 }
 
@@ -537,14 +595,17 @@ __device__ __forceinline__ void gemm_fwd_t_nm(int nm, double (&cf)[4][2], const 
 // ------------------------------------------------------------------------------ fwd sweep
 // Unit: Fock tiles [t0, t1) and the union of their probe windows [u0, u1) (<= FWCAP probes).
 // Warp w owns (m-block, n-block) pairs [w PP, (w+1) PP) of the (u1-u0)/8 x NB pair grid.
+// Theta moves in half tiles of FH = 32 rows (two stages) and the F block of each tile in its own
+// two stages, so that two CTAs (16 warps) share an SM.
+constexpr int FH = ST / 2;
 size_t sweep_fwd_smem(int N, int NB)
 {
-    const int tsz = ((ST * N + 8 * NB + 4) + 1) & ~1;
+    const int tsz = ((FH * N + 8 * NB + 4) + 1) & ~1;
     return (size_t)(2 * tsz + 2 * FWCAP * STP) * sizeof(double);
 }
 
 template <int NB>
-__global__ void __launch_bounds__(256, 1) k_fwd_mma(SweepFwdArgs a)
+__global__ void __launch_bounds__(256, 2) k_fwd_mma(SweepFwdArgs a)
 {
     extern __shared__ __align__(128) double sm[];
     __shared__ __align__(8) uint64_t bars[2];
@@ -554,9 +615,9 @@ __global__ void __launch_bounds__(256, 1) k_fwd_mma(SweepFwdArgs a)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g4 = lane >> 2, t4 = lane & 3;
     const FwUnit u = a.units[blockIdx.x];
-    const int tsz = ((ST * N + 8 * NB + 4) + 1) & ~1;
-    double *Ts = sm;                    // 2 x tsz
-    double *Fs = sm + 2 * tsz;          // 2 x FWCAP x STP
+    const int tsz = ((FH * N + 8 * NB + 4) + 1) & ~1;
+    double *Ts = sm;                    // 2 x tsz (half tiles)
+    double *Fs = sm + 2 * tsz;          // 2 x FWCAP x STP (per tile)
     const int Wu = u.u1 - u.u0;
     const int nm = (Wu + 7) >> 3;       // <= FWCAP / 8 = 4 probe n-blocks
     const bool second = warp + 8 < NB;  // warp-uniform: outcome m-block warp + 8 exists
@@ -567,23 +628,32 @@ __global__ void __launch_bounds__(256, 1) k_fwd_mma(SweepFwdArgs a)
         fence_barrier_init();
     }
     __syncthreads();
-    const int ntile = u.t1 - u.t0;
-    auto issue = [&](int j) {
-        const int t = u.t0 + j;
-        const int k0 = t * ST;
-        const int Tt = min(ST, a.Ml - k0);
-        const double *src;
-        int sh;
-        uint32_t by;
-        aligned_span(a.theta + (int64_t)k0 * N, (int64_t)Tt * N, &src, &sh, &by);
-        const int dA = a.tile_dA[t], dB = a.tile_dB[t];
-        const int ra = max(dA, u.u0), rb = min(dB, u.u1);
-        uint64_t *bar = &bars[j & 1];
-        const uint32_t fby = rb > ra ? (uint32_t)(rb - ra) * STP * 8 : 0;
-        mbar_expect_tx(bar, by + fby);
-        bulk_g2s(Ts + (j & 1) * tsz, src, by, bar);
+    const int nh = 2 * (u.t1 - u.t0);   // half-tile steps
+    auto issue = [&](int h) {
+        const int t = u.t0 + (h >> 1), half = h & 1;
+        const int k0 = t * ST + half * FH;
+        const int rows = min(FH, a.Ml - k0);
+        uint64_t *bar = &bars[h & 1];
+        uint32_t fby = 0;
+        int ra = 0, dA = 0;
+        if (!half) {
+            dA = a.tile_dA[t];
+            ra = max(dA, u.u0);
+            const int rb = min(a.tile_dB[t], u.u1);
+            fby = rb > ra ? (uint32_t)(rb - ra) * STP * 8 : 0;
+        }
+        if (rows > 0) {
+            const double *src;
+            int sh;
+            uint32_t by;
+            aligned_span(a.theta + (int64_t)k0 * N, (int64_t)rows * N, &src, &sh, &by);
+            mbar_expect_tx(bar, by + fby);
+            bulk_g2s(Ts + (h & 1) * tsz, src, by, bar);
+        } else {
+            mbar_expect_tx(bar, fby);  // arrives; with fby == 0 the phase completes at once
+        }
         if (fby)
-            bulk_g2s(Fs + (j & 1) * FWCAP * STP + (ra - u.u0) * STP,
+            bulk_g2s(Fs + ((h >> 1) & 1) * FWCAP * STP + (ra - u.u0) * STP,
                      a.Fb + a.fb_off[t] + (int64_t)(ra - dA) * STP, fby, bar);
     };
     if (tid == 0) issue(0);
@@ -592,26 +662,28 @@ __global__ void __launch_bounds__(256, 1) k_fwd_mma(SweepFwdArgs a)
 #pragma unroll
     for (int i = 0; i < 4; i++) cA[i][0] = cA[i][1] = cB[i][0] = cB[i][1] = 0.0;
 
-    for (int j = 0; j < ntile; j++) {
-        if (tid == 0 && j + 1 < ntile) issue(j + 1);
-        mbar_wait(&bars[j & 1], (j >> 1) & 1);
-        const int t = u.t0 + j;
-        const int k0 = t * ST;
-        const int Tt = min(ST, a.Ml - k0);
-        const int sh = (int)(((uintptr_t)(a.theta + (int64_t)k0 * N) & 15) >> 3);
-        // union probes outside this tile's window hold stale F rows: their B fragments -> 0
-        const int ra = max(a.tile_dA[t], u.u0) - u.u0, rb = min(a.tile_dB[t], u.u1) - u.u0;
-        bool fok[4];
+    for (int h = 0; h < nh; h++) {
+        if (tid == 0 && h + 1 < nh) issue(h + 1);
+        mbar_wait(&bars[h & 1], (h >> 1) & 1);
+        const int t = u.t0 + (h >> 1), half = h & 1;
+        const int k0 = t * ST + half * FH;
+        const int rows = min(FH, a.Ml - k0);
+        if (rows > 0) {
+            const int sh = (int)(((uintptr_t)(a.theta + (int64_t)k0 * N) & 15) >> 3);
+            // union probes outside this tile's window hold stale F rows: their B fragments -> 0
+            const int ra = max(a.tile_dA[t], u.u0) - u.u0, rb = min(a.tile_dB[t], u.u1) - u.u0;
+            bool fok[4];
 #pragma unroll
-        for (int nb = 0; nb < 4; nb++) fok[nb] = 8 * nb + g4 >= ra && 8 * nb + g4 < rb;
-        const double *T = Ts + (j & 1) * tsz + sh + t4 * N + g4;
-        const double *Frow = Fs + (j & 1) * FWCAP * STP + g4 * STP + t4;
-        if (Tt == ST) {
-            gemm_fwd_t_nm<false>(nm, cA, T + 8 * warp, Frow, N, Tt, t4, fok);
-            if (second) gemm_fwd_t_nm<false>(nm, cB, T + 8 * (warp + 8), Frow, N, Tt, t4, fok);
-        } else {
-            gemm_fwd_t_nm<true>(nm, cA, T + 8 * warp, Frow, N, Tt, t4, fok);
-            if (second) gemm_fwd_t_nm<true>(nm, cB, T + 8 * (warp + 8), Frow, N, Tt, t4, fok);
+            for (int nb = 0; nb < 4; nb++) fok[nb] = 8 * nb + g4 >= ra && 8 * nb + g4 < rb;
+            const double *T = Ts + (h & 1) * tsz + sh + t4 * N + g4;
+            const double *Frow = Fs + ((h >> 1) & 1) * FWCAP * STP + g4 * STP + t4 + half * FH;
+            if (rows == FH) {
+                gemm_fwd_t_nm<false>(nm, cA, T + 8 * warp, Frow, N, FH, t4, fok);
+                if (second) gemm_fwd_t_nm<false>(nm, cB, T + 8 * (warp + 8), Frow, N, FH, t4, fok);
+            } else {
+                gemm_fwd_t_nm<true>(nm, cA, T + 8 * warp, Frow, N, rows, t4, fok);
+                if (second) gemm_fwd_t_nm<true>(nm, cB, T + 8 * (warp + 8), Frow, N, rows, t4, fok);
+            }
         }
         __syncthreads();
     }
@@ -835,12 +907,24 @@ __global__ void __launch_bounds__(256) k_reduce_R2(const double *rpart, const in
     double ss = 0.0;
     if (d < D) {
         const int64_t j0 = red_beg[d], j1 = red_beg[d + 1];
-        for (int n = lane; n < N; n += 32) {
-            double s = 0.0;
-            for (int64_t j = j0; j < j1; j++) s += rpart[red_rows[j] * N + n];
-            if (P) s -= P[(int64_t)d * N + n];
-            R[(int64_t)d * N + n] = s;
-            ss = fma(s, s, ss);
+        for (int n0 = 0; n0 < N; n0 += 128) {          // four independent columns per lane
+            double s[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int64_t j = j0; j < j1; j++) {
+                const double *src = rpart + red_rows[j] * N + n0 + lane;
+#pragma unroll
+                for (int c = 0; c < 4; c++)
+                    if (n0 + lane + 32 * c < N) s[c] += src[32 * c];
+            }
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                const int n = n0 + lane + 32 * c;
+                if (n < N) {
+                    double v = s[c];
+                    if (P) v -= P[(int64_t)d * N + n];
+                    R[(int64_t)d * N + n] = v;
+                    ss = fma(v, v, ss);
+                }
+            }
         }
     }
     ss = wsum(ss);
@@ -982,13 +1066,18 @@ cudaError_t prepare_sweep_kernels()
 // exact n-block count: only the last n-block of a row can hold padding columns
 int sweep_nb(int N) { return (N >= 1 && N <= 8 * SW_NBMAX) ? (N + 7) / 8 : 0; }
 
-cudaError_t launch_bwd_mma(const SweepArgs &a, int nunits, int NB, cudaStream_t s)
+cudaError_t launch_bwd_mma(const SweepArgs &a_in, int nunits, int NB, cudaStream_t s)
 {
     if (nunits <= 0) return cudaSuccess;
+    SweepArgs a = a_in;
+    a.nunits = nunits;
     const size_t smem = sweep_bwd_smem(a.N, NB);
+    static int nsm = 0;
+    if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    const int grid = std::min(nunits, (NB <= 13 ? 2 : 1) * nsm);
     switch (NB) {
 #define QDT_CASE(nb) \
-    case nb: k_bwd_mma<nb><<<nunits, 256, smem, s>>>(a); break;
+    case nb: k_bwd_mma<nb><<<grid, 256, smem, s>>>(a); break;
         QDT_FOR_NB(QDT_CASE)
 #undef QDT_CASE
         default: return cudaErrorInvalidValue;

@@ -2,4 +2,3 @@
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -q -x --durations=8 -p no:warnings > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 600 python bench.py --no-cpu > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
-QDT_SWEEP=0 timeout 600 python bench.py --no-cpu --no-e2e --steps 50 > gpurun_out/bench_nosweep.json 2>> gpurun_out/bench.err
