@@ -326,10 +326,11 @@ def _oracle_sample_run(I, steps, warmup, rows_total, n_slabs=20):
 def cpu_baseline(I, args):
     """Oracle timed on this host (one thread), bounded sample (~10-30 s of CPU work)."""
     try:
-        rows = min(I.M, 60000)
-        v, dt, r = _oracle_sample_run(I, 3, 1, rows)
+        # ~10-15 s of single-thread oracle work (measured ~10 us per row-iteration at N = 100)
+        rows = min(I.M, int(300000 * 100 / max(1, I.N)))
+        v, dt, r = _oracle_sample_run(I, 4, 1, rows)
         return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                "sample": f"3 oracle iterations (SQS) on {r} Fock rows = 20 evenly spaced slabs of "
+                "sample": f"4 oracle iterations (SQS) on {r} Fock rows = 20 evenly spaced slabs of "
                           f"the {args.config} instance ({dt:.1f} s)",
                 "host_cpu": _cpu_model(), "nproc": os.cpu_count()}
     except Exception as e:  # pragma: no cover

@@ -986,6 +986,10 @@ static qdt_status step_setup(qdt_ctx *ctx, qdt_probes *p, Plan *pl, int mode, do
         CK(run_k(ctx, "probe_rowsum", 1, [&]() { return launch_probe_rowsum(D, p->band(), d_s, s); }));
         CKS(allreduce(ctx, d_s, D, "allreduce_s"));
         CK(run_k(ctx, "sqs_weights", 1, [&]() {
+            if (p->d_Fb)   // tiled F of the sweep path: coalesced, one block per Fock tile
+                return launch_sqs_weights_tiled(p->sw_ntiles, (int)Ml, p->d_sw_dA, p->d_sw_dB, p->d_fb_off,
+                                                p->d_Fb, d_s, gamma, d_w,
+                                                mode == QDT_STEP_SQS ? d_tstep : nullptr, s);
             return launch_sqs_weights(pl->ntiles, pl->T, pl->d_tile_dA, pl->d_tile_dB, (int)Ml, p->kb,
                                       p->band(), d_s, gamma, d_w,
                                       mode == QDT_STEP_SQS ? d_tstep : nullptr, s);
@@ -1250,6 +1254,7 @@ static SweepArgs sweep_args(const IterCfg &c, SolveBufs &b, const double *R, con
     a.part = b.partT;
     a.kkt_every = c.kkt_every;
     a.nunits = 0;
+    a.eval = 0;
     a.state = b.state;
     return a;
 }
@@ -1371,6 +1376,29 @@ static qdt_status common_bufs(qdt_ctx *ctx, qdt_probes *p, Plan *pl, int64_t N, 
     CKS(ws_get(ctx, "sc2_stage", SC2_BLOCKS * NV, &b.sc2_stage));
     CKS(ws_get(ctx, "sc2_arrive", 1, &b.sc2_arrive));
     CK(cudaMemsetAsync(b.sc2_arrive, 0, sizeof(int), s));
+    return QDT_OK;
+}
+
+// Evaluation of f, r_KKT (both multipliers) at theta: residual, then a G pass without a step
+// (sweep kernels when the plan has them), then the final-eval scalars.
+static qdt_status eval_pass(qdt_ctx *ctx, const IterCfg &c0, SolveBufs &b, double *theta)
+{
+    cudaStream_t s = ctx->stream;
+    IterCfg c = c0;
+    c.fista = 0;
+    c.kkt_every = 1;
+    Plan *pl = c.pl;
+    CKS(fwd_reduce(ctx, c, b, theta, b.R[0], true));
+    if (pl->NB) {
+        SweepArgs a = sweep_args(c, b, b.R[0], theta, nullptr);
+        a.eval = 1;
+        CK(run_k(ctx, "bwd_eval", 1, [&]() { return launch_bwd_mma(a, pl->sw_nbunits, pl->NB, s); }));
+        CKS(scalars(ctx, c, b, 1, c.p->sw_ntiles));
+    } else {
+        BwdArgs a = bwd_args(ctx, c, b, b.R[0], theta, nullptr, nullptr, false);
+        CK(run_k(ctx, "bwd_eval", 1, [&]() { return launch_bwd(a, pl->nbunits, pl->TC, BWD_EVAL, s); }));
+        CKS(scalars(ctx, c, b, 1, pl->ntiles));
+    }
     return QDT_OK;
 }
 
@@ -1562,24 +1590,11 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
         sr.stop = 0;
         sr.it = hst.iters_done;
         CK(cudaMemcpyAsync(b.state, &sr, sizeof sr, cudaMemcpyHostToDevice, s));
-        IterCfg cf = c;
-        cf.kkt_every = 1;
-        double *cur = b.theta[hst.iters_done % nbuf];
-        CKS(fwd_reduce(ctx, cf, b, cur, b.R[0], true));
-        BwdArgs a = bwd_args(ctx, cf, b, b.R[0], cur, nullptr, nullptr, false);
-        CK(run_k(ctx, "bwd_eval", 1, [&]() { return launch_bwd(a, pl->nbunits, pl->TC, BWD_EVAL, s); }));
-        CKS(scalars(ctx, cf, b, 1, pl->ntiles));
+        CKS(eval_pass(ctx, c, b, b.theta[hst.iters_done % nbuf]));
         CK(cudaMemcpyAsync(b.state, &hst, sizeof hst, cudaMemcpyHostToDevice, s));
     }
     if (!stopped) {
-        IterCfg cf = c;
-        cf.fista = 0;
-        cf.kkt_every = 1;
-        double *cur = b.theta[iters % nbuf];
-        CKS(fwd_reduce(ctx, cf, b, cur, b.R[0], true));
-        BwdArgs a = bwd_args(ctx, cf, b, b.R[0], cur, nullptr, nullptr, false);
-        CK(run_k(ctx, "bwd_eval", 1, [&]() { return launch_bwd(a, pl->nbunits, pl->TC, BWD_EVAL, s); }));
-        CKS(scalars(ctx, cf, b, 1, pl->ntiles));
+        CKS(eval_pass(ctx, c, b, b.theta[iters % nbuf]));
         CK(cudaMemcpyAsync(&hst, b.state, sizeof hst, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
     }
@@ -1680,10 +1695,7 @@ extern "C" qdt_status qdt_objective(qdt_ctx *ctx, const qdt_probes *F, const dou
     memset(&st0, 0, sizeof st0);
     CK(cudaMemcpyAsync(b.state, &st0, sizeof st0, cudaMemcpyHostToDevice, s));
     IterCfg c{p, pl, (int)N, gamma, 0.0, 0, 1, 1};
-    CKS(fwd_reduce(ctx, c, b, b.theta[0], b.R[0], true));
-    BwdArgs a = bwd_args(ctx, c, b, b.R[0], b.theta[0], nullptr, nullptr, false);
-    CK(run_k(ctx, "bwd_eval", 1, [&]() { return launch_bwd(a, pl->nbunits, pl->TC, BWD_EVAL, s); }));
-    CKS(scalars(ctx, c, b, 1, pl->ntiles));
+    CKS(eval_pass(ctx, c, b, b.theta[0]));
     double f = 0, r = 0;
     CK(cudaMemcpyAsync(&f, b.trace, sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&r, b.kkt, sizeof(double), cudaMemcpyDeviceToHost, s));

@@ -120,6 +120,7 @@ struct SweepArgs {
     double *part;
     int kkt_every;
     int nunits;                 // set by launch_bwd_mma (persistent grid)
+    int eval;                   // 1: evaluation pass (G, KKT both multipliers, regulariser; no step)
     const DevState *state;
 };
 struct SweepFwdArgs {
@@ -155,6 +156,10 @@ constexpr int SW_FUSED_SMEM_MAX = 220 * 1024;
 size_t sweep_fused_smem(int N, int NB, int cap);
 cudaError_t launch_sweep_fused(const SweepFusedArgs &a, int nctas, int NB, cudaStream_t s);
 cudaError_t prepare_sweep_kernels();
+cudaError_t launch_sqs_weights_tiled(int ntiles, int Ml, const int32_t *tile_dA,
+                                     const int32_t *tile_dB, const int64_t *fb_off, const double *Fb,
+                                     const double *s, double gamma, double *w, double *tstep,
+                                     cudaStream_t st);
 int sweep_nb(int N);            // DMMA n-blocks instantiated for N (0: N too wide, general path)
 size_t sweep_bwd_smem(int N, int NB);
 size_t sweep_fwd_smem(int N, int NB);

@@ -348,6 +348,35 @@ __device__ __forceinline__ void gemm_bwd(double (&acc)[NB][2], const double *F, 
     }
 }
 
+// SQS row weights from the tiled F (reading R2): w_k = sum_d F_{d,k} s_d + 4 gamma with d over the
+// tile's window in increasing order, t_k = 1/w_k (0 for a frozen row).  Block per tile, thread
+// per row: the window's F rows are read coalesced across the tile's rows.
+__global__ void k_sqs_weights_tiled(int Ml, const int32_t *tile_dA, const int32_t *tile_dB,
+                                    const int64_t *fb_off, const double *Fb, const double *s,
+                                    double gamma, double *w, double *tstep)
+{
+    const int t = blockIdx.x, r = threadIdx.x;
+    const int k = t * ST + r;
+    if (k >= Ml) return;
+    const int dA = tile_dA[t], W = tile_dB[t] - dA;
+    const double *f = Fb + fb_off[t] + r;
+    double acc = 0.0;
+    for (int j = 0; j < W; j++) acc += f[(int64_t)j * STP] * s[dA + j];
+    acc += 4.0 * gamma;
+    if (w) w[k] = acc;
+    if (tstep) tstep[k] = (acc > 0.0) ? 1.0 / acc : 0.0;
+}
+
+cudaError_t launch_sqs_weights_tiled(int ntiles, int Ml, const int32_t *tile_dA,
+                                     const int32_t *tile_dB, const int64_t *fb_off, const double *Fb,
+                                     const double *s, double gamma, double *w, double *tstep,
+                                     cudaStream_t st)
+{
+    if (ntiles <= 0) return cudaSuccess;
+    k_sqs_weights_tiled<<<ntiles, ST, 0, st>>>(Ml, tile_dA, tile_dB, fb_off, Fb, s, gamma, w, tstep);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------------------ bwd sweep
 // Smem: Theta tile (ST+2 rows incl. halo) | F chunks 2 x SKC x STP | R chunks 2 x (SKC*N + pad)
 template <int NB>
@@ -509,18 +538,20 @@ __global__ void __launch_bounds__(256, (NB <= 13 ? 2 : 1)) k_bwd_mma(SweepArgs a
             const double tk = act ? a.tstep[kl] : 0.0;
             double *orow = a.out + (int64_t)kl * N;
             const bool full = Tt == ST && a.kb + k0 > 0 && a.kb + k0 + ST < a.M;
+            const bool ev = a.eval != 0;   // evaluation pass: KKT (both multipliers) + regulariser only
             if (full && even)
                 row_pass<NB, true, true, false>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk, do_kkt,
-                                                false, sreg, skkt, skktp, s, xm, xn);
+                                                ev, sreg, skkt, skktp, s, xm, xn);
             else if (full)
                 row_pass<NB, true, false, false>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk, do_kkt,
-                                                 false, sreg, skkt, skktp, s, xm, xn);
+                                                 ev, sreg, skkt, skktp, s, xm, xn);
             else
                 row_pass<NB, false, false, false>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk,
-                                                  do_kkt, false, sreg, skkt, skktp, s, xm, xn);
+                                                  do_kkt, ev, sreg, skkt, skktp, s, xm, xn);
             __syncthreads();  // Theta tile consumed: start the next unit's tile load
             if (tid == 0 && next < a.nunits && un.nsplit == 1) issue_theta(un);
-            if (full && even)
+            if (ev) {
+            } else if (full && even)
                 row_project<NB, true, true, false>(acc, thr, N, t4, act, s, xm, xn, orow);
             else if (full)
                 row_project<NB, true, false, false>(acc, thr, N, t4, act, s, xm, xn, orow);
@@ -529,21 +560,24 @@ __global__ void __launch_bounds__(256, (NB <= 13 ? 2 : 1)) k_bwd_mma(SweepArgs a
             // per-tile scalar partials (fixed order: lanes, then warps)
             sreg = wsum(sreg);
             skkt = wsum(skkt);
+            skktp = wsum(skktp);
             if (lane == 0) {
                 red[warp * 3 + 0] = skkt;
+                red[warp * 3 + 1] = skktp;
                 red[warp * 3 + 2] = sreg;
             }
             __syncthreads();
             if (tid == 0) {
-                double v0 = 0.0, v2 = 0.0;
+                double v0 = 0.0, v1 = 0.0, v2 = 0.0;
                 for (int w = 0; w < 8; w++) {
                     v0 += red[w * 3 + 0];
+                    v1 += red[w * 3 + 1];
                     v2 += red[w * 3 + 2];
                 }
                 double *p = a.part + (int64_t)u.tile * NSC_TILE;
                 if (do_kkt) {
                     p[SC_KKT] = v0;
-                    p[SC_KKTP] = 0.0;
+                    p[SC_KKTP] = v1;
                 }
                 p[SC_REG] = v2;
                 p[SC_DTH] = 0.0;
