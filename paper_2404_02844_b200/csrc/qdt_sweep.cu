@@ -473,6 +473,8 @@ __global__ void __launch_bounds__(256, (NB <= 13 ? 2 : 1)) k_bwd_mma(SweepArgs a
         const int next = unit + G;
         SwUnit un;
         if (next < a.nunits) un = a.units[next];
+        // the row's step weight, loaded before the GEMM so that its latency is hidden
+        const double tk = (8 * warp + g4 < Tt) ? __ldg(a.tstep + k0 + 8 * warp + g4) : 0.0;
         double acc[NB][2];
 #pragma unroll
         for (int nb = 0; nb < NB; nb++) acc[nb][0] = acc[nb][1] = 0.0;
@@ -535,11 +537,11 @@ __global__ void __launch_bounds__(256, (NB <= 13 ? 2 : 1)) k_bwd_mma(SweepArgs a
             const bool has_prev = kg > 0, has_next = kg + 1 < a.M;
             double *thr = Th + th_sh + (r + 1) * N;
             double sreg = 0.0, skkt = 0.0, skktp = 0.0, s, xm, xn;
-            const double tk = act ? a.tstep[kl] : 0.0;
             double *orow = a.out + (int64_t)kl * N;
             const bool full = Tt == ST && a.kb + k0 > 0 && a.kb + k0 + ST < a.M;
             const bool ev = a.eval != 0;   // evaluation pass: KKT (both multipliers) + regulariser only
-            if (full && even)
+            const bool fast = full && even;
+            if (fast)
                 row_pass<NB, true, true, false>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk, do_kkt,
                                                 ev, sreg, skkt, skktp, s, xm, xn);
             else if (full)
@@ -551,7 +553,7 @@ __global__ void __launch_bounds__(256, (NB <= 13 ? 2 : 1)) k_bwd_mma(SweepArgs a
             __syncthreads();  // Theta tile consumed: start the next unit's tile load
             if (tid == 0 && next < a.nunits && un.nsplit == 1) issue_theta(un);
             if (ev) {
-            } else if (full && even)
+            } else if (fast)
                 row_project<NB, true, true, false>(acc, thr, N, t4, act, s, xm, xn, orow);
             else if (full)
                 row_project<NB, true, false, false>(acc, thr, N, t4, act, s, xm, xn, orow);
