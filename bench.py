@@ -228,6 +228,10 @@ def run_qdt(args):
                "step": "one qdt_build_probes + qdt_solve(K iterations) call with host alpha2/P/"
                        "theta (pinned); bytes are per call"}
 
+    ttt = None
+    if not args.no_ttt and world == 1:
+        ttt = time_to_tol(q, ctx, I, stream, barrier)
+
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps,
@@ -249,6 +253,7 @@ def run_qdt(args):
         "clocks": clk.summary(),
         "e2e": e2e,
         "final_objective": float(out["trace"][-1]),
+        "time_to_tol": ttt,
     }
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(I, args)
@@ -257,6 +262,40 @@ def run_qdt(args):
     if dist:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def time_to_tol(q, ctx, I, stream, barrier, rhos=(1e-2, 1e-3, 1e-4), cap=4000):
+    """Time-to-tolerance (BASELINE.json metric): wall time of one public-API call
+    qdt_build_probes + qdt_solve(tol = rho * r_KKT(Theta_0)) with host (pinned) alpha2 / P /
+    Theta, until r_KKT(Theta_k) <= tol, for each step mode; iterations reported beside it."""
+    import numpy as np
+    import torch
+    a_host = torch.tensor(I.alpha2).pin_memory().numpy()
+    P_host = torch.tensor(I.P).pin_memory().numpy()
+    th_host = torch.empty((I.M, I.N), dtype=torch.float64).pin_memory().numpy()
+    F = q.qdt_build_probes(ctx, a_host, I.M)
+    r0 = q.qdt_solve(ctx, F, P_host, I.gamma, 0.0, 0, theta_out=th_host)["info"]["kkt0"]
+    del F
+    res = {"r_kkt0": r0, "cap_iters": cap, "modes": {}}
+    for name, accel, ke in [("SQS", False, 1), ("SQS-FISTA", True, 5)]:
+        rows = {}
+        for rho in rhos:
+            barrier()
+            t0 = time.perf_counter()
+            F = q.qdt_build_probes(ctx, a_host, I.M)
+            o = q.qdt_solve(ctx, F, P_host, I.gamma, rho * r0, cap, accel=accel, kkt_every=ke,
+                            check_every=20, theta_out=th_host)
+            barrier()
+            dt = time.perf_counter() - t0
+            del F
+            inf = o["info"]
+            rows[f"{rho:g}"] = {"converged": bool(inf["converged"]), "iters": int(inf["iters_done"]),
+                                "seconds": dt, "f": float(inf["f_final"]),
+                                "loop_ms_per_iter": inf["loop_ms"] / max(1, inf["iters_done"])}
+            if not inf["converged"]:
+                break
+        res["modes"][name] = rows
+    return res
 
 
 # ------------------------------------------------------------------------------ oracle legs
@@ -327,7 +366,7 @@ def cpu_baseline(I, args):
     """Oracle timed on this host (one thread), bounded sample (~10-30 s of CPU work)."""
     try:
         # ~10-15 s of single-thread oracle work (measured ~10 us per row-iteration at N = 100)
-        rows = min(I.M, int(300000 * 100 / max(1, I.N)))
+        rows = min(I.M, int(700000 * 100 / max(1, I.N)))
         v, dt, r = _oracle_sample_run(I, 4, 1, rows)
         return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                 "sample": f"4 oracle iterations (SQS) on {r} Fock rows = 20 evenly spaced slabs of "
@@ -382,6 +421,7 @@ def main():
                                                               "megascale"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-tol leg")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

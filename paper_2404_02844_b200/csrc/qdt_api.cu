@@ -1255,6 +1255,9 @@ static SweepArgs sweep_args(const IterCfg &c, SolveBufs &b, const double *R, con
     a.kkt_every = c.kkt_every;
     a.nunits = 0;
     a.eval = 0;
+    a.eval_gate = 0;
+    a.theta_prev = nullptr;
+    a.beta = nullptr;
     a.state = b.state;
     return a;
 }
@@ -1321,6 +1324,26 @@ static qdt_status iteration(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, int64_
         double *cur = b.theta[j % 2], *nxt = b.theta[(j + 1) % 2];
         CKS(fwd_reduce(ctx, c, b, cur, b.R[0], true));
         SweepArgs a = sweep_args(c, b, b.R[0], cur, nxt);
+        CK(run_k(ctx, "bwd_step", 1, [&]() { return launch_bwd_mma(a, pl->sw_nbunits, pl->NB, s); }));
+        CKS(halo_exchange(ctx, c, nxt));
+        ntiles = c.p->sw_ntiles;
+    } else if (c.fista && pl->NB) {
+        // FISTA on the sweep kernels: R_k, R(Y) = R_k + beta (R_k - R_{k-1}) (linear), the KKT of
+        // Theta_k on the recorded iterations (evaluation pass gated on the device), then the
+        // step from Y = Theta_k + beta (Theta_k - Theta_{k-1}) formed in the epilogue
+        double *cur = b.theta[j % 3], *prev = b.theta[(j + 2) % 3], *nxt = b.theta[(j + 1) % 3];
+        double *Rk = b.R[j % 2], *Rkm1 = b.R[(j + 1) % 2];
+        CKS(fwd_reduce(ctx, c, b, cur, Rk, true));
+        CK(run_k(ctx, "fista_rcomb", 1, [&]() {
+            return launch_fista_rcomb(b.RY, Rk, Rkm1, b.beta, c.p->D * (int64_t)c.N, b.state, s);
+        }));
+        SweepArgs ev = sweep_args(c, b, Rk, cur, nullptr);
+        ev.eval = 1;
+        ev.eval_gate = 1;
+        CK(run_k(ctx, "bwd_eval", 1, [&]() { return launch_bwd_mma(ev, pl->sw_nbunits, pl->NB, s); }));
+        SweepArgs a = sweep_args(c, b, b.RY, cur, nxt);
+        a.theta_prev = prev;
+        a.beta = b.beta;
         CK(run_k(ctx, "bwd_step", 1, [&]() { return launch_bwd_mma(a, pl->sw_nbunits, pl->NB, s); }));
         CKS(halo_exchange(ctx, c, nxt));
         ntiles = c.p->sw_ntiles;
@@ -1477,8 +1500,8 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     }
     CKS(common_bufs(ctx, p, pl, N, b));
     if (fista) {
-        CKS(ws_get(ctx, "R1", D * N, &b.R[1]));
-        CKS(ws_get(ctx, "RY", D * N, &b.RY));
+        CKS(ws_get(ctx, "R1", D * N + 4, &b.R[1]));
+        CKS(ws_get(ctx, "RY", D * N + 4, &b.RY));
         CK(cudaMemsetAsync(b.R[1], 0, sizeof(double) * D * N, s));
     }
     const int64_t tl = iters + 1;

@@ -121,6 +121,9 @@ struct SweepArgs {
     int kkt_every;
     int nunits;                 // set by launch_bwd_mma (persistent grid)
     int eval;                   // 1: evaluation pass (G, KKT both multipliers, regulariser; no step)
+    int eval_gate;              // evaluation pass runs only when state->it % kkt_every == 0
+    const double *theta_prev;   // FISTA step: Theta_{k-1} (same layout as theta)
+    const double *beta;         // FISTA step: beta_k indexed by state->it (nullptr: plain PG)
     const DevState *state;
 };
 struct SweepFwdArgs {
@@ -161,7 +164,7 @@ cudaError_t launch_sqs_weights_tiled(int ntiles, int Ml, const int32_t *tile_dA,
                                      const double *s, double gamma, double *w, double *tstep,
                                      cudaStream_t st);
 int sweep_nb(int N);            // DMMA n-blocks instantiated for N (0: N too wide, general path)
-size_t sweep_bwd_smem(int N, int NB);
+size_t sweep_bwd_smem(int N, int NB, bool fista);
 size_t sweep_fwd_smem(int N, int NB);
 cudaError_t launch_tile_F(Band b, int64_t kb, int Ml, int ntiles, const int32_t *tile_dA,
                           const int32_t *tile_dB, const int64_t *fb_off, double *Fb,

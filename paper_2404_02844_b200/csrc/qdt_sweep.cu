@@ -155,12 +155,15 @@ __global__ void k_tile_F(Band b, int64_t kb, int Ml, const int32_t *tile_dA, con
 // NB = ceil(N/8): only the last n-block can hold columns >= N; they are neutralised (+inf for the
 // row min, -inf for X) and never stored.  FULL: an interior row of a full tile (row active,
 // neighbours k-1 and k+1 exist): no per-row predicates.  EVEN: N even, pairs move as double2.
-template <int NB, bool FULL, bool EVEN, bool SMEM_OUT>
+// FIS (FISTA): tpr points at Theta_{k-1}[k, 0]; the stencil and X use the extrapolated point
+// Y = Theta_k + beta (Theta_k - Theta_{k-1}), the regulariser value uses Theta_k itself (f(Theta_k)),
+// and the KKT of Theta_k comes from a separate evaluation pass (do_kkt must be false).
+template <int NB, bool FULL, bool EVEN, bool SMEM_OUT, bool FIS = false>
 __device__ __forceinline__ void row_pass(double (&acc)[NB][2], const double *thr, int N, int t4,
                                          bool act, bool has_prev, bool has_next, double gamma,
                                          double tk, bool do_kkt, bool want_kktp, double &sreg,
                                          double &skkt, double &skktp, double &s, double &xm,
-                                         double &xn)
+                                         double &xn, const double *tpr = nullptr, double beta = 0.0)
 {
     const int cl = 8 * (NB - 1) + 2 * t4;
     const bool v0 = cl < N, v1 = cl + 1 < N;
@@ -182,12 +185,33 @@ __device__ __forceinline__ void row_pass(double (&acc)[NB][2], const double *thr
 #pragma unroll
             for (int i = 0; i < 2; i++) t0[i] = thr[c + i], tp[i] = thr[c + i - N], tn[i] = thr[c + i + N];
         }
+        double q0[2], qp[2], qn[2];   // Theta_{k-1} (FISTA only)
+        if (FIS) {
+            if (EVEN) {
+                const double2 x = *reinterpret_cast<const double2 *>(tpr + c);
+                const double2 y = *reinterpret_cast<const double2 *>(tpr + c - N);
+                const double2 z = *reinterpret_cast<const double2 *>(tpr + c + N);
+                q0[0] = x.x, q0[1] = x.y, qp[0] = y.x, qp[1] = y.y, qn[0] = z.x, qn[1] = z.y;
+            } else {
+#pragma unroll
+                for (int i = 0; i < 2; i++) q0[i] = tpr[c + i], qp[i] = tpr[c + i - N], qn[i] = tpr[c + i + N];
+            }
+        }
 #pragma unroll
         for (int i = 0; i < 2; i++) {
             const double a0 = t0[i];
-            const double d1 = a0 - (hp ? tp[i] : a0);
-            const double d2 = a0 - (hn ? tn[i] : a0);
-            const double g = fma(gamma, d1 + d2, acc[nb][i]);
+            const double an = hn ? tn[i] : a0;
+            const double d2 = a0 - an;                       // regulariser pair of Theta_k
+            double g;
+            if (FIS) {
+                const double y0 = fma(beta, a0 - q0[i], a0);
+                const double yp = hp ? fma(beta, tp[i] - qp[i], tp[i]) : y0;
+                const double yn = hn ? fma(beta, tn[i] - qn[i], tn[i]) : y0;
+                g = fma(gamma, (y0 - yp) + (y0 - yn), acc[nb][i]);
+            } else {
+                const double d1 = a0 - (hp ? tp[i] : a0);
+                g = fma(gamma, d1 + d2, acc[nb][i]);
+            }
             if (QDT_VALID(nb, i)) {
                 sreg = fma(d2, d2, sreg);
                 mn = g < mn ? g : mn;
@@ -212,6 +236,17 @@ __device__ __forceinline__ void row_pass(double (&acc)[NB][2], const double *thr
             t0[0] = x.x, t0[1] = x.y;
         } else {
             t0[0] = thr[c], t0[1] = thr[c + 1];
+        }
+        if (FIS) {   // X is taken from the extrapolated point Y
+            double q0[2];
+            if (EVEN) {
+                const double2 x = *reinterpret_cast<const double2 *>(tpr + c);
+                q0[0] = x.x, q0[1] = x.y;
+            } else {
+                q0[0] = tpr[c], q0[1] = tpr[c + 1];
+            }
+            t0[0] = fma(beta, t0[0] - q0[0], t0[0]);
+            t0[1] = fma(beta, t0[1] - q0[1], t0[1]);
         }
 #pragma unroll
         for (int i = 0; i < 2; i++) {
@@ -393,19 +428,19 @@ struct SwLayout {
     }
 };
 
-size_t sweep_bwd_smem(int N, int NB)
+size_t sweep_bwd_smem(int N, int NB, bool fista)
 {
     const int thsz = (((ST + 2) * N + 4) + 1) & ~1;
     const int rsz = ((SKC * N + 8 * NB + 4) + 1) & ~1;
-    return (size_t)(thsz + 2 * SKC * STP + 2 * rsz) * sizeof(double);
+    return (size_t)((fista ? 2 : 1) * thsz + 2 * SKC * STP + 2 * rsz) * sizeof(double);
 }
 
 // Persistent: CTA b processes units b, b + G, b + 2G, ... (heavy first).  The chunk buffers of
 // the next unit are refilled as soon as this unit's GEMM is done, the Theta tile as soon as the
 // epilogue has read it (before the Michelot rounds and stores), so the next unit's loads overlap
 // the current unit's epilogue.
-template <int NB>
-__global__ void __launch_bounds__(256, (NB <= 13 ? 2 : 1)) k_bwd_mma(SweepArgs a)
+template <int NB, bool FIS>
+__global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(SweepArgs a)
 {
     extern __shared__ __align__(128) double sm[];
     __shared__ __align__(8) uint64_t bars[3];
@@ -422,10 +457,14 @@ __global__ void __launch_bounds__(256, (NB <= 13 ? 2 : 1)) k_bwd_mma(SweepArgs a
     if (unit >= a.nunits) return;
     const SwLayout<NB> L(N);
     double *Th = sm;
-    double *Fs = sm + L.thsz;
+    double *Tq = sm + L.thsz;                       // FISTA: Theta_{k-1} tile (same rows)
+    double *Fs = sm + (FIS ? 2 : 1) * L.thsz;
     double *Rs = Fs + 2 * SKC * STP;
-    const bool do_kkt = (it % a.kkt_every) == 0;
+    // eval_gate (FISTA evaluation pass): only on iterations whose KKT is recorded
+    if (a.eval_gate && (it % a.kkt_every) != 0) return;
+    const bool do_kkt = !FIS && (it % a.kkt_every) == 0;
     const bool even = (N & 1) == 0;
+    const double beta = FIS ? a.beta[it] : 0.0;
 
     if (tid == 0) {
         mbar_init(&bars[0], 1);
@@ -442,8 +481,9 @@ __global__ void __launch_bounds__(256, (NB <= 13 ? 2 : 1)) k_bwd_mma(SweepArgs a
         int sh;
         uint32_t by;
         aligned_span(a.theta + (int64_t)(k0 - 1) * N, (int64_t)(Tt + 2) * N, &src, &sh, &by);
-        mbar_expect_tx(&bars[0], by);
+        mbar_expect_tx(&bars[0], FIS ? 2 * by : by);
         bulk_g2s(Th, src, by, &bars[0]);
+        if (FIS) bulk_g2s(Tq, a.theta_prev + (src - a.theta), by, &bars[0]);
     };
     auto issue_chunk = [&](const SwUnit &v, int c) {
         const int W = v.p1 - v.p0, pb = c * SKC, kc = min(SKC, W - pb);
@@ -541,15 +581,16 @@ __global__ void __launch_bounds__(256, (NB <= 13 ? 2 : 1)) k_bwd_mma(SweepArgs a
             const bool full = Tt == ST && a.kb + k0 > 0 && a.kb + k0 + ST < a.M;
             const bool ev = a.eval != 0;   // evaluation pass: KKT (both multipliers) + regulariser only
             const bool fast = full && even;
+            const double *tpr = Tq + th_sh + (r + 1) * N;
             if (fast)
-                row_pass<NB, true, true, false>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk, do_kkt,
-                                                ev, sreg, skkt, skktp, s, xm, xn);
+                row_pass<NB, true, true, false, FIS>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk,
+                                                     do_kkt, ev, sreg, skkt, skktp, s, xm, xn, tpr, beta);
             else if (full)
-                row_pass<NB, true, false, false>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk, do_kkt,
-                                                 ev, sreg, skkt, skktp, s, xm, xn);
+                row_pass<NB, true, false, false, FIS>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk,
+                                                      do_kkt, ev, sreg, skkt, skktp, s, xm, xn, tpr, beta);
             else
-                row_pass<NB, false, false, false>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk,
-                                                  do_kkt, ev, sreg, skkt, skktp, s, xm, xn);
+                row_pass<NB, false, false, false, FIS>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk,
+                                                       do_kkt, ev, sreg, skkt, skktp, s, xm, xn, tpr, beta);
             __syncthreads();  // Theta tile consumed: start the next unit's tile load
             if (tid == 0 && next < a.nunits && un.nsplit == 1) issue_theta(un);
             if (ev) {
@@ -1076,7 +1117,9 @@ template <int NB>
 static cudaError_t prep_nb()
 {
     const int big = 210 * 1024;  // fwd at N = 128 needs 203 KB; the opt-in cap (227 KB) includes static smem
-    cudaError_t e = cudaFuncSetAttribute(k_bwd_mma<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    cudaError_t e = cudaFuncSetAttribute(k_bwd_mma<NB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_bwd_mma<NB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_fwd_mma<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     if (e == cudaSuccess)
@@ -1107,13 +1150,19 @@ cudaError_t launch_bwd_mma(const SweepArgs &a_in, int nunits, int NB, cudaStream
     if (nunits <= 0) return cudaSuccess;
     SweepArgs a = a_in;
     a.nunits = nunits;
-    const size_t smem = sweep_bwd_smem(a.N, NB);
+    const bool fis = a.beta != nullptr && !a.eval;
+    const size_t smem = sweep_bwd_smem(a.N, NB, fis);
     static int nsm = 0;
     if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-    const int grid = std::min(nunits, (NB <= 13 ? 2 : 1) * nsm);
+    const int grid = std::min(nunits, (NB <= 13 && !fis ? 2 : 1) * nsm);
     switch (NB) {
-#define QDT_CASE(nb) \
-    case nb: k_bwd_mma<nb><<<grid, 256, smem, s>>>(a); break;
+#define QDT_CASE(nb)                                                       \
+    case nb:                                                               \
+        if (fis)                                                           \
+            k_bwd_mma<nb, true><<<grid, 256, smem, s>>>(a);                \
+        else                                                               \
+            k_bwd_mma<nb, false><<<grid, 256, smem, s>>>(a);               \
+        break;
         QDT_FOR_NB(QDT_CASE)
 #undef QDT_CASE
         default: return cudaErrorInvalidValue;

@@ -303,3 +303,23 @@ def test_fused_sweep_parity(q, ctx, N, gamma, fused, monkeypatch):
     np.testing.assert_allclose(rg["kkt"], ro["kkt"], rtol=1e-8, atol=1e-15)
     Th = rg["theta"]
     assert Th.min() >= 0 and np.abs(Th.sum(1) - 1).max() <= 4 * N * EPS
+
+
+@pytest.mark.parametrize("N,kkt_every", [(100, 1), (37, 5), (8, 3)])
+def test_fista_sweep_parity(q, ctx, N, kkt_every):
+    """SQS-FISTA on the sweep kernels (Theta_{k-1} tile staged beside Theta_k, Y formed in the
+    epilogue, device-gated KKT evaluation pass) against the oracle's FISTA, 40 iterations."""
+    rng = np.random.default_rng(100 + N)
+    D, M = 300, 20000
+    a2 = np.geomspace(1.0, 0.9 * M, D)
+    P = rng.dirichlet(np.ones(N) * 0.3, D)
+    gamma = 1e-4
+    Fo = oracle.Probes(a2, M)
+    Fg = q.qdt_build_probes(ctx, a2, M)
+    ro = oracle.solve(Fo, P, gamma, 0.0, 40, accel=1, kkt_every=kkt_every)
+    rg = q.qdt_solve(ctx, Fg, P, gamma, 0.0, 40, accel=True, kkt_every=kkt_every)
+    assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9
+    assert _trace_ok(rg["trace"], ro["trace"], P)
+    m = ~np.isnan(ro["kkt"])
+    np.testing.assert_array_equal(m, ~np.isnan(rg["kkt"]))
+    np.testing.assert_allclose(rg["kkt"][m], ro["kkt"][m], rtol=1e-8, atol=1e-15)
