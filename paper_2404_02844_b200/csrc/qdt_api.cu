@@ -1232,6 +1232,16 @@ static qdt_status scalars(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, int fina
     return QDT_OK;
 }
 
+// sweep bwd launcher: the N-split 512-thread kernel for FISTA steps (its two staged tiles leave
+// one CTA per SM: 16 warps instead of 8), the 256-thread kernel otherwise (QDT_SPLITN overrides:
+// 0 never, 1 always; measured in profiles/r01_v5)
+static cudaError_t launch_bwd_any(const SweepArgs &a, int nunits, int NB, cudaStream_t s)
+{
+    const int m = sweep_split_mode();
+    const bool fis = a.beta != nullptr && !a.eval;
+    return (m == 1 || (m == 2 && fis)) ? launch_bwd_split(a, nunits, NB, s) : launch_bwd_mma(a, nunits, NB, s);
+}
+
 static SweepArgs sweep_args(const IterCfg &c, SolveBufs &b, const double *R, const double *theta,
                             double *out)
 {
@@ -1276,7 +1286,7 @@ static qdt_status iteration(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, int64_
         SweepArgs a = sweep_args(c, b, b.R[0], cur, nxt);
         a.units = pl->d_fz_bunits;
         a.part = b.partS;
-        CK(run_k(ctx, "bwd_heavy", 1, [&]() { return launch_bwd_mma(a, pl->fz_nbh, pl->NB, s); }));
+        CK(run_k(ctx, "bwd_heavy", 1, [&]() { return launch_bwd_any(a, pl->fz_nbh, pl->NB, s); }));
         SweepFusedArgs z;
         z.N = c.N;
         z.Ml = (int)p->Ml;
@@ -1324,7 +1334,7 @@ static qdt_status iteration(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, int64_
         double *cur = b.theta[j % 2], *nxt = b.theta[(j + 1) % 2];
         CKS(fwd_reduce(ctx, c, b, cur, b.R[0], true));
         SweepArgs a = sweep_args(c, b, b.R[0], cur, nxt);
-        CK(run_k(ctx, "bwd_step", 1, [&]() { return launch_bwd_mma(a, pl->sw_nbunits, pl->NB, s); }));
+        CK(run_k(ctx, "bwd_step", 1, [&]() { return launch_bwd_any(a, pl->sw_nbunits, pl->NB, s); }));
         CKS(halo_exchange(ctx, c, nxt));
         ntiles = c.p->sw_ntiles;
     } else if (c.fista && pl->NB) {
@@ -1340,11 +1350,11 @@ static qdt_status iteration(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, int64_
         SweepArgs ev = sweep_args(c, b, Rk, cur, nullptr);
         ev.eval = 1;
         ev.eval_gate = 1;
-        CK(run_k(ctx, "bwd_eval", 1, [&]() { return launch_bwd_mma(ev, pl->sw_nbunits, pl->NB, s); }));
+        CK(run_k(ctx, "bwd_eval", 1, [&]() { return launch_bwd_any(ev, pl->sw_nbunits, pl->NB, s); }));
         SweepArgs a = sweep_args(c, b, b.RY, cur, nxt);
         a.theta_prev = prev;
         a.beta = b.beta;
-        CK(run_k(ctx, "bwd_step", 1, [&]() { return launch_bwd_mma(a, pl->sw_nbunits, pl->NB, s); }));
+        CK(run_k(ctx, "bwd_step", 1, [&]() { return launch_bwd_any(a, pl->sw_nbunits, pl->NB, s); }));
         CKS(halo_exchange(ctx, c, nxt));
         ntiles = c.p->sw_ntiles;
     } else if (!c.fista) {
@@ -1390,7 +1400,7 @@ static qdt_status common_bufs(qdt_ctx *ctx, qdt_probes *p, Plan *pl, int64_t N, 
     CK(cudaMemsetAsync(b.partT, 0, sizeof(double) * nt * NSC_TILE, s));
     CKS(ws_get(ctx, "vec", NV, &b.vec));
     CKS(ws_get(ctx, "tstep", p->Ml, &b.tstep));
-    const int64_t scr = std::max<int64_t>(1, std::max<int64_t>(pl->nslots * pl->T * N, pl->sw_nslots * 512 * pl->NB));
+    const int64_t scr = std::max<int64_t>(1, std::max<int64_t>(pl->nslots * pl->T * N, pl->sw_nslots * 1024 * ((pl->NB + 1) / 2 + 1)));
     CKS(ws_get(ctx, "scratch", scr, &b.scratch));
     CKS(ws_get(ctx, "counters", nt, &b.counters));
     CK(cudaMemsetAsync(b.counters, 0, sizeof(int) * nt, s));
@@ -1415,7 +1425,7 @@ static qdt_status eval_pass(qdt_ctx *ctx, const IterCfg &c0, SolveBufs &b, doubl
     if (pl->NB) {
         SweepArgs a = sweep_args(c, b, b.R[0], theta, nullptr);
         a.eval = 1;
-        CK(run_k(ctx, "bwd_eval", 1, [&]() { return launch_bwd_mma(a, pl->sw_nbunits, pl->NB, s); }));
+        CK(run_k(ctx, "bwd_eval", 1, [&]() { return launch_bwd_any(a, pl->sw_nbunits, pl->NB, s); }));
         CKS(scalars(ctx, c, b, 1, c.p->sw_ntiles));
     } else {
         BwdArgs a = bwd_args(ctx, c, b, b.R[0], theta, nullptr, nullptr, false);
@@ -1477,7 +1487,7 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
         const int nb = opt.accel ? 3 : 2;
         double need = 8.0 * ((double)nb * (Ml + 2) * N + (opt.accel ? 3.0 : 1.0) * D * N + D * N +
                              (double)std::max(pl->nrpart, pl->sw_nrpart) * N +
-                             (double)std::max<int64_t>(pl->nslots * pl->T * N, pl->sw_nslots * 512 * pl->NB) +
+                             (double)std::max<int64_t>(pl->nslots * pl->T * N, pl->sw_nslots * 1024 * ((pl->NB + 1) / 2 + 1)) +
                              2.0 * Ml);
         size_t fr = 0, tot = 0;
         CK(cudaMemGetInfo(&fr, &tot));
@@ -1552,7 +1562,7 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     CK(cudaMemcpyAsync(b.state, &st0, sizeof st0, cudaMemcpyHostToDevice, s));
 
     // ---- the hot loop: graph of `period` iterations replayed
-    const int period = fista ? 6 : 2;
+    const int period = fista ? 12 : 16;   // multiple of the buffer rotation (3 / 2)
     const bool use_graph = opt.use_graph && !ctx->profiling && iters >= period;
     DevState hst;
     int64_t done = 0;

@@ -170,6 +170,8 @@ cudaError_t launch_tile_F(Band b, int64_t kb, int Ml, int ntiles, const int32_t 
                           const int32_t *tile_dB, const int64_t *fb_off, double *Fb,
                           cudaStream_t s);
 cudaError_t launch_bwd_mma(const SweepArgs &a, int nunits, int NB, cudaStream_t s);
+cudaError_t launch_bwd_split(const SweepArgs &a, int nunits, int NB, cudaStream_t s);
+int sweep_split_mode();
 cudaError_t launch_fwd_mma(const SweepFwdArgs &a, int nunits, int NB, cudaStream_t s);
 cudaError_t launch_reduce_R2(const double *rpart, const int64_t *red_beg, const int64_t *red_rows,
                              const double *P, double *R, int D, int N, double *partR,

@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -155,26 +156,53 @@ __global__ void k_tile_F(Band b, int64_t kb, int Ml, const int32_t *tile_dA, con
 // NB = ceil(N/8): only the last n-block can hold columns >= N; they are neutralised (+inf for the
 // row min, -inf for X) and never stored.  FULL: an interior row of a full tile (row active,
 // neighbours k-1 and k+1 exist): no per-row predicates.  EVEN: N even, pairs move as double2.
+// Row-pair exchange of the N-split kernel: warps mb and mb + 8 hold the two column halves of the
+// same 8 rows; each reduction publishes the quad value of each row and reads the partner's after
+// a 64-thread named barrier (id 1 + mb).  Two slots alternate, so one barrier per exchange.
+struct PairX {
+    double *buf;   // [2 slots][8 m-blocks][2 halves][8 rows][4]
+    int slot, mb, h, g4, t4;
+};
+template <int K>
+__device__ __forceinline__ void pair_xchg(PairX &px, const double (&v)[K], double (&o)[K])
+{
+    double *mine = px.buf + (((px.slot * 8 + px.mb) * 2 + px.h) * 8 + px.g4) * 4;
+    const double *other = px.buf + (((px.slot * 8 + px.mb) * 2 + (1 - px.h)) * 8 + px.g4) * 4;
+    if (px.t4 == 0)
+#pragma unroll
+        for (int k = 0; k < K; k++) mine[k] = v[k];
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + px.mb) : "memory");
+#pragma unroll
+    for (int k = 0; k < K; k++) o[k] = other[k];
+    px.slot ^= 1;
+}
+
 // FIS (FISTA): tpr points at Theta_{k-1}[k, 0]; the stencil and X use the extrapolated point
 // Y = Theta_k + beta (Theta_k - Theta_{k-1}), the regulariser value uses Theta_k itself (f(Theta_k)),
 // and the KKT of Theta_k comes from a separate evaluation pass (do_kkt must be false).
-template <int NB, bool FULL, bool EVEN, bool SMEM_OUT, bool FIS = false>
-__device__ __forceinline__ void row_pass(double (&acc)[NB][2], const double *thr, int N, int t4,
+// NBA / CB (N-split kernel): the thread holds NBA column blocks starting at global block CB / 8;
+// global blocks >= NB are padding.  PAIR: the row is shared with the partner warp holding the
+// other column half; every row reduction is completed through PairX (fixed combination order).
+template <int NB, bool FULL, bool EVEN, bool SMEM_OUT, bool FIS = false, int NBA = NB, int CB = 0,
+          bool PAIR = false>
+__device__ __forceinline__ void row_pass(double (&acc)[NBA][2], const double *thr, int N, int t4,
                                          bool act, bool has_prev, bool has_next, double gamma,
                                          double tk, bool do_kkt, bool want_kktp, double &sreg,
                                          double &skkt, double &skktp, double &s, double &xm,
-                                         double &xn, const double *tpr = nullptr, double beta = 0.0)
+                                         double &xn, const double *tpr = nullptr, double beta = 0.0,
+                                         PairX *px = nullptr)
 {
     const int cl = 8 * (NB - 1) + 2 * t4;
     const bool v0 = cl < N, v1 = cl + 1 < N;
     const bool hp = FULL || has_prev, hn = FULL || has_next;
     const bool ract = FULL || act;
-#define QDT_VALID(nb, i) ((nb) < NB - 1 ? ract : (ract && ((i) ? v1 : v0)))
+#define QDT_VALID(nb, i)                                                                  \
+    (CB / 8 + (nb) < NB - 1 ? ract : (CB / 8 + (nb) == NB - 1 ? (ract && ((i) ? v1 : v0)) : false))
     // ---- pass 1: G = acc + gamma L Theta, regulariser pair, row min of G (for the KKT)
     double mn = INFINITY;
 #pragma unroll
-    for (int nb = 0; nb < NB; nb++) {
-        const int c = 8 * nb + 2 * t4;
+    for (int nb = 0; nb < NBA; nb++) {
+        const int c = CB + 8 * nb + 2 * t4;
         double t0[2], tp[2], tn[2];
         if (EVEN) {
             const double2 x = *reinterpret_cast<const double2 *>(thr + c);
@@ -222,14 +250,20 @@ __device__ __forceinline__ void row_pass(double (&acc)[NB][2], const double *thr
     if (SMEM_OUT) __syncthreads();  // neighbour rows read: each row may now be overwritten by its owner
     double lam = 0.0, lamp = 0.0;
     if (do_kkt) {
-        lam = -2.0 * quad_min(mn);
+        double m1 = quad_min(mn);
+        if (PAIR) {
+            double v[1] = {m1}, o[1];
+            pair_xchg<1>(*px, v, o);
+            m1 = fmin(m1, o[0]);
+        }
+        lam = -2.0 * m1;
         lamp = lam > 0.0 ? lam : 0.0;
     }
     // ---- pass 2: KKT terms, X = Theta - t_k G, row sum / max / min of X
     s = 0.0, xm = -INFINITY, xn = INFINITY;
 #pragma unroll
-    for (int nb = 0; nb < NB; nb++) {
-        const int c = 8 * nb + 2 * t4;
+    for (int nb = 0; nb < NBA; nb++) {
+        const int c = CB + 8 * nb + 2 * t4;
         double t0[2];
         if (EVEN) {
             const double2 x = *reinterpret_cast<const double2 *>(thr + c);
@@ -272,14 +306,22 @@ __device__ __forceinline__ void row_pass(double (&acc)[NB][2], const double *thr
     s = quad_sum(s);
     xm = quad_max(xm);
     xn = quad_min(xn);
+    if (PAIR) {
+        double v[3] = {s, xm, xn}, o[3];
+        pair_xchg<3>(*px, v, o);
+        s = px->h ? o[0] + s : s + o[0];   // half 0 + half 1 in both warps
+        xm = fmax(xm, o[1]);
+        xn = fmin(xn, o[2]);
+    }
 #undef QDT_VALID
 }
 
 // Threshold and output of the row (after row_pass): X in acc (-inf for invalid columns), s, xm,
 // xn its quad-reduced sum / max / min.  SMEM_OUT also writes Theta_{k+1} over the row in smem.
-template <int NB, bool FULL, bool EVEN, bool SMEM_OUT>
-__device__ __forceinline__ void row_project(double (&acc)[NB][2], double *thr, int N, int t4,
-                                            bool act, double s, double xm, double xn, double *orow)
+template <int NB, bool FULL, bool EVEN, bool SMEM_OUT, int NBA = NB, int CB = 0, bool PAIR = false>
+__device__ __forceinline__ void row_project(double (&acc)[NBA][2], double *thr, int N, int t4,
+                                            bool act, double s, double xm, double xn, double *orow,
+                                            PairX *px = nullptr)
 {
     const int cl = 8 * (NB - 1) + 2 * t4;
     const bool v0 = cl < N, v1 = cl + 1 < N;
@@ -297,7 +339,7 @@ __device__ __forceinline__ void row_project(double (&acc)[NB][2], double *thr, i
         double ps = 0.0, mA = INFINITY;
         int pc = 0;
 #pragma unroll
-        for (int nb = 0; nb < NB; nb++)
+        for (int nb = 0; nb < NBA; nb++)
 #pragma unroll
             for (int i = 0; i < 2; i++) {
                 const double x = acc[nb][i];
@@ -310,6 +352,13 @@ __device__ __forceinline__ void row_project(double (&acc)[NB][2], double *thr, i
         ps = quad_sum(ps);
         pc = quad_sum_i(pc);
         mA = quad_min(mA);
+        if (PAIR) {
+            double v[3] = {ps, (double)pc, mA}, o[3];
+            pair_xchg<3>(*px, v, o);
+            ps = px->h ? o[0] + ps : ps + o[0];
+            pc += (int)o[1];
+            mA = fmin(mA, o[2]);
+        }
         if (!done) {
             if (pc >= cnt) {
                 done = true;
@@ -322,22 +371,23 @@ __device__ __forceinline__ void row_project(double (&acc)[NB][2], double *thr, i
     }
     if (ract) {
 #pragma unroll
-        for (int nb = 0; nb < NB; nb++) {
-            const int c = 8 * nb + 2 * t4;
+        for (int nb = 0; nb < NBA; nb++) {
+            const int gb = CB / 8 + nb;
+            const int c = CB + 8 * nb + 2 * t4;
             double o0 = acc[nb][0] - tau, o1 = acc[nb][1] - tau;
             o0 = o0 > 0.0 ? o0 : 0.0;
             o1 = o1 > 0.0 ? o1 : 0.0;
             if (EVEN) {
-                if (nb < NB - 1 || v0) {
+                if (gb < NB - 1 || (gb == NB - 1 && v0)) {
                     *reinterpret_cast<double2 *>(orow + c) = make_double2(o0, o1);
                     if (SMEM_OUT) *reinterpret_cast<double2 *>(thr + c) = make_double2(o0, o1);
                 }
             } else {
-                if (nb < NB - 1 || v0) {
+                if (gb < NB - 1 || (gb == NB - 1 && v0)) {
                     orow[c] = o0;
                     if (SMEM_OUT) thr[c] = o0;
                 }
-                if (nb < NB - 1 || v1) {
+                if (gb < NB - 1 || (gb == NB - 1 && v1)) {
                     orow[c + 1] = o1;
                     if (SMEM_OUT) thr[c + 1] = o1;
                 }
@@ -419,8 +469,8 @@ struct SwLayout {
     int thsz, rsz;
     __device__ __host__ SwLayout(int N)
     {
-        thsz = (((ST + 2) * N + 4) + 1) & ~1;
-        rsz = ((SKC * N + 8 * NB + 4) + 1) & ~1;
+        thsz = (((ST + 2) * N + 8 * NB + 16) + 1) & ~1;
+        rsz = ((SKC * N + 8 * NB + 16) + 1) & ~1;
     }
     __device__ __host__ size_t bytes() const
     {
@@ -430,8 +480,8 @@ struct SwLayout {
 
 size_t sweep_bwd_smem(int N, int NB, bool fista)
 {
-    const int thsz = (((ST + 2) * N + 4) + 1) & ~1;
-    const int rsz = ((SKC * N + 8 * NB + 4) + 1) & ~1;
+    const int thsz = (((ST + 2) * N + 8 * NB + 16) + 1) & ~1;
+    const int rsz = ((SKC * N + 8 * NB + 16) + 1) & ~1;
     return (size_t)((fista ? 2 : 1) * thsz + 2 * SKC * STP + 2 * rsz) * sizeof(double);
 }
 
@@ -631,6 +681,217 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(Swe
         if (next >= a.nunits) break;
         unit = next;
         u = un;
+    }
+}
+
+// N-split variant of k_bwd_mma: 512 threads (16 warps) per CTA, warp w owns m-block w & 7 and
+// the column half w >> 3 (NBA = ceil(NB/2) column blocks; the last block of an odd NB is padding),
+// so that each thread holds half a row and two CTAs (32 warps) fit an SM; the two halves of a row
+// complete every row reduction through a named-barrier pair exchange (PairX).
+template <int NB, bool FIS>
+__global__ void __launch_bounds__(512, (FIS ? 1 : 2)) k_bwd_split(SweepArgs a)
+{
+    constexpr int NBA = (NB + 1) / 2;
+    extern __shared__ __align__(128) double sm[];
+    __shared__ __align__(8) uint64_t bars[3];
+    __shared__ double red[16 * 3];
+    __shared__ double xbuf[2 * 8 * 2 * 8 * 4];
+    __shared__ int s_last;
+    const DevState *st = a.state;
+    if (st && st->stop) return;
+    const int64_t it = st ? st->it : 0;
+    const int N = a.N;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g4 = lane >> 2, t4 = lane & 3;
+    const int mb = warp & 7, hh = warp >> 3;
+    const int G = gridDim.x;
+    int unit = blockIdx.x;
+    if (unit >= a.nunits) return;
+    const SwLayout<NB> L(N);
+    double *Th = sm;
+    double *Tq = sm + L.thsz;
+    double *Fs = sm + (FIS ? 2 : 1) * L.thsz;
+    double *Rs = Fs + 2 * SKC * STP;
+    if (a.eval_gate && (it % a.kkt_every) != 0) return;
+    const bool do_kkt = !FIS && (it % a.kkt_every) == 0;
+    const bool even = (N & 1) == 0;
+    const double beta = FIS ? a.beta[it] : 0.0;
+    PairX px{xbuf, 0, mb, hh, g4, t4};
+
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        mbar_init(&bars[2], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    uint32_t c_issue = 0, c_use = 0, th_use = 0;
+    auto issue_theta = [&](const SwUnit &v) {
+        const int k0 = v.tile * ST, Tt = min(ST, a.Ml - k0);
+        const double *src;
+        int sh;
+        uint32_t by;
+        aligned_span(a.theta + (int64_t)(k0 - 1) * N, (int64_t)(Tt + 2) * N, &src, &sh, &by);
+        mbar_expect_tx(&bars[0], FIS ? 2 * by : by);
+        bulk_g2s(Th, src, by, &bars[0]);
+        if (FIS) bulk_g2s(Tq, a.theta_prev + (src - a.theta), by, &bars[0]);
+    };
+    auto issue_chunk = [&](const SwUnit &v, int c) {
+        const int W = v.p1 - v.p0, pb = c * SKC, kc = min(SKC, W - pb);
+        const double *rsrc;
+        int rsh;
+        uint32_t rbytes;
+        aligned_span(a.R + (int64_t)(v.p0 + pb) * N, (int64_t)kc * N, &rsrc, &rsh, &rbytes);
+        const int stg = c_issue & 1;
+        uint64_t *bar = &bars[1 + stg];
+        const uint32_t fbytes = (uint32_t)kc * STP * 8;
+        const double *Fg = a.Fb + a.fb_off[v.tile] + (int64_t)(v.p0 - a.tile_dA[v.tile] + pb) * STP;
+        mbar_expect_tx(bar, fbytes + rbytes);
+        bulk_g2s(Fs + stg * SKC * STP, Fg, fbytes, bar);
+        bulk_g2s(Rs + stg * L.rsz, rsrc, rbytes, bar);
+        c_issue++;
+    };
+    if (tid == 0) {
+        const SwUnit u0 = a.units[unit];
+        if (u0.nsplit == 1) issue_theta(u0);
+        if (u0.p1 > u0.p0) issue_chunk(u0, 0);
+    }
+    while (true) {
+        const SwUnit u = a.units[unit];
+        const int k0 = u.tile * ST;
+        const int Tt = min(ST, a.Ml - k0);
+        const int W = u.p1 - u.p0;
+        const int nch = (W + SKC - 1) / SKC;
+        const int next = unit + G;
+        const double tk = (8 * mb + g4 < Tt) ? __ldg(a.tstep + k0 + 8 * mb + g4) : 0.0;
+        double acc[NBA][2];
+#pragma unroll
+        for (int nb = 0; nb < NBA; nb++) acc[nb][0] = acc[nb][1] = 0.0;
+        for (int c = 0; c < nch; c++) {
+            if (tid == 0 && c + 1 < nch) issue_chunk(u, c + 1);
+            const int stg = c_use & 1;
+            mbar_wait(&bars[1 + stg], (c_use >> 1) & 1);
+            c_use++;
+            const int pb = c * SKC;
+            const int kc = min(SKC, W - pb);
+            const int rsh = (int)(((uintptr_t)(a.R + (int64_t)(u.p0 + pb) * N) & 15) >> 3);
+            gemm_bwd<NBA>(acc, Fs + stg * SKC * STP + 8 * mb + g4,
+                          Rs + stg * L.rsz + rsh + g4 + 8 * NBA * hh, kc, N, t4);
+            __syncthreads();
+        }
+        if (tid == 0 && next < a.nunits) {
+            const SwUnit un = a.units[next];
+            if (un.p1 > un.p0) issue_chunk(un, 0);
+        }
+        bool epi = true;
+        if (u.nsplit > 1) {
+            const int64_t fsz = (int64_t)16 * NBA * 64;
+            double *slot = a.scratch + (u.slot_base + u.slot) * fsz;
+#pragma unroll
+            for (int nb = 0; nb < NBA; nb++)
+                __stcg(reinterpret_cast<double2 *>(slot + ((warp * NBA + nb) * 32 + lane) * 2),
+                       make_double2(acc[nb][0], acc[nb][1]));
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) s_last = (atomicAdd(&a.counters[u.tile], 1) == u.nsplit - 1);
+            __syncthreads();
+            epi = s_last;
+            if (epi) {
+                __threadfence();
+                if (tid == 0) issue_theta(u);
+#pragma unroll
+                for (int nb = 0; nb < NBA; nb++) acc[nb][0] = acc[nb][1] = 0.0;
+                for (int sl = 0; sl < u.nsplit; sl++) {
+                    const double *sp = a.scratch + (u.slot_base + sl) * fsz;
+#pragma unroll
+                    for (int nb = 0; nb < NBA; nb++) {
+                        const double2 v =
+                            __ldcg(reinterpret_cast<const double2 *>(sp + ((warp * NBA + nb) * 32 + lane) * 2));
+                        acc[nb][0] += v.x;
+                        acc[nb][1] += v.y;
+                    }
+                }
+                if (tid == 0) a.counters[u.tile] = 0;
+            }
+        }
+        if (epi) {
+            mbar_wait(&bars[0], th_use & 1);
+            th_use++;
+            const int th_sh = (int)(((uintptr_t)(a.theta + (int64_t)(k0 - 1) * N) & 15) >> 3);
+            const int r = 8 * mb + g4;
+            const bool act = r < Tt;
+            const int kl = k0 + r;
+            const int64_t kg = a.kb + kl;
+            const bool has_prev = kg > 0, has_next = kg + 1 < a.M;
+            double *thr = Th + th_sh + (r + 1) * N;
+            const double *tpr = Tq + th_sh + (r + 1) * N;
+            double sreg = 0.0, skkt = 0.0, skktp = 0.0, s, xm, xn;
+            double *orow = a.out + (int64_t)kl * N;
+            const bool full = Tt == ST && a.kb + k0 > 0 && a.kb + k0 + ST < a.M;
+            const bool fast = full && even;
+            const bool ev = a.eval != 0;
+#define QDT_SPLIT_PASS(CBV, FU, EV)                                                                    \
+    row_pass<NB, FU, EV, false, FIS, NBA, CBV, true>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk, \
+                                                     do_kkt, ev, sreg, skkt, skktp, s, xm, xn, tpr, beta, &px)
+#define QDT_SPLIT_PROJ(CBV, FU, EV) \
+    row_project<NB, FU, EV, false, NBA, CBV, true>(acc, thr, N, t4, act, s, xm, xn, orow, &px)
+            if (hh == 0) {
+                if (fast) QDT_SPLIT_PASS(0, true, true);
+                else if (full) QDT_SPLIT_PASS(0, true, false);
+                else QDT_SPLIT_PASS(0, false, false);
+            } else {
+                if (fast) QDT_SPLIT_PASS(8 * NBA, true, true);
+                else if (full) QDT_SPLIT_PASS(8 * NBA, true, false);
+                else QDT_SPLIT_PASS(8 * NBA, false, false);
+            }
+            __syncthreads();  // Theta tile consumed: start the next unit's tile load
+            if (tid == 0 && next < a.nunits) {
+                const SwUnit un = a.units[next];
+                if (un.nsplit == 1) issue_theta(un);
+            }
+            if (!ev) {
+                if (hh == 0) {
+                    if (fast) QDT_SPLIT_PROJ(0, true, true);
+                    else if (full) QDT_SPLIT_PROJ(0, true, false);
+                    else QDT_SPLIT_PROJ(0, false, false);
+                } else {
+                    if (fast) QDT_SPLIT_PROJ(8 * NBA, true, true);
+                    else if (full) QDT_SPLIT_PROJ(8 * NBA, true, false);
+                    else QDT_SPLIT_PROJ(8 * NBA, false, false);
+                }
+            }
+#undef QDT_SPLIT_PASS
+#undef QDT_SPLIT_PROJ
+            sreg = wsum(sreg);
+            skkt = wsum(skkt);
+            skktp = wsum(skktp);
+            if (lane == 0) {
+                red[warp * 3 + 0] = skkt;
+                red[warp * 3 + 1] = skktp;
+                red[warp * 3 + 2] = sreg;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+                for (int w = 0; w < 16; w++) {
+                    v0 += red[w * 3 + 0];
+                    v1 += red[w * 3 + 1];
+                    v2 += red[w * 3 + 2];
+                }
+                double *pp = a.part + (int64_t)u.tile * NSC_TILE;
+                if (do_kkt) {
+                    pp[SC_KKT] = v0;
+                    pp[SC_KKTP] = v1;
+                }
+                pp[SC_REG] = v2;
+                pp[SC_DTH] = 0.0;
+            }
+        } else if (tid == 0 && next < a.nunits) {
+            const SwUnit un = a.units[next];
+            if (un.nsplit == 1) issue_theta(un);
+        }
+        if (next >= a.nunits) break;
+        unit = next;
     }
 }
 
@@ -1121,6 +1382,10 @@ static cudaError_t prep_nb()
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_bwd_mma<NB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_bwd_split<NB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_bwd_split<NB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_fwd_mma<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_sweep_fused<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1162,6 +1427,42 @@ cudaError_t launch_bwd_mma(const SweepArgs &a_in, int nunits, int NB, cudaStream
             k_bwd_mma<nb, true><<<grid, 256, smem, s>>>(a);                \
         else                                                               \
             k_bwd_mma<nb, false><<<grid, 256, smem, s>>>(a);               \
+        break;
+        QDT_FOR_NB(QDT_CASE)
+#undef QDT_CASE
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+// N-split bwd (512 threads): used when sweep_split_on(); same arguments as launch_bwd_mma
+int sweep_split_mode()
+{
+    static int mode = -1;   // 0: never, 1: always, 2 (default): FISTA steps only
+    if (mode < 0) {
+        const char *e = getenv("QDT_SPLITN");
+        mode = e ? atoi(e) : 2;
+    }
+    return mode;
+}
+
+cudaError_t launch_bwd_split(const SweepArgs &a_in, int nunits, int NB, cudaStream_t s)
+{
+    if (nunits <= 0) return cudaSuccess;
+    SweepArgs a = a_in;
+    a.nunits = nunits;
+    const bool fis = a.beta != nullptr && !a.eval;
+    const size_t smem = sweep_bwd_smem(a.N, NB, fis);
+    static int nsm = 0;
+    if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    const int grid = std::min(nunits, (fis ? 1 : 2) * nsm);
+    switch (NB) {
+#define QDT_CASE(nb)                                                       \
+    case nb:                                                               \
+        if (fis)                                                           \
+            k_bwd_split<nb, true><<<grid, 512, smem, s>>>(a);              \
+        else                                                               \
+            k_bwd_split<nb, false><<<grid, 512, smem, s>>>(a);             \
         break;
         QDT_FOR_NB(QDT_CASE)
 #undef QDT_CASE
