@@ -419,7 +419,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="qdt", choices=["qdt", "reference"])
     ap.add_argument("--config", default="megascale", choices=["tiny", "medium", "large",
-                                                              "megascale"])
+                                                              "megascale", "stress_cut"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-tol leg")

@@ -90,7 +90,8 @@ constexpr int ST = 64;          // Fock rows per sweep tile (8 DMMA m-blocks)
 constexpr int STP = ST + 4;     // pitch of a tiled-F row: conflict-free A fragments
 constexpr int SKC = 16;         // probes per staged bwd chunk (4 DMMA k-steps)
 constexpr int SWCAP = 128;      // bwd split cap (probes per unit)
-constexpr int FWCAP = 32;       // fwd unit union-window cap (probes): <= 4 DMMA n-blocks
+constexpr int FWCAP = 48;       // fwd unit union-window cap (probes): 2 CTAs/SM of k_fwd_mma at N = 100
+constexpr int FWNB = FWCAP / 8; // fwd DMMA probe n-blocks per unit
 constexpr int FW_MAXT = 16;     // fwd unit length cap (tiles)
 constexpr int SC2_BLOCKS = 64;  // first-level blocks of the scalar reduction
 constexpr int SW_NBMAX = 16;    // sweep path: N <= 8 * SW_NBMAX outcomes

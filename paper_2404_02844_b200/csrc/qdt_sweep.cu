@@ -900,9 +900,9 @@ __global__ void __launch_bounds__(512, (FIS ? 1 : 2)) k_bwd_split(SweepArgs a)
 // probe n-blocks (lane columns d = 8 nb + 2 t4 + {0,1}).  A fragment a = Theta[4 ks + t4][n],
 // B fragment b = F[8 nb + g4][4 ks + t4].  Tcol: Theta + t4 N + 8 mb + g4; Frow: F + g4 STP + t4.
 // Rows k >= Tt are masked (stale shared memory); probe masks are applied by the caller via fok.
-template <int NM, bool MASKK>
-__device__ __forceinline__ void gemm_fwd_t(double (&cf)[4][2], const double *Tcol, const double *Frow,
-                                           int N, int Tt, int t4, const bool (&fok)[4])
+template <int NM, bool MASKK, int MX>
+__device__ __forceinline__ void gemm_fwd_t(double (&cf)[MX][2], const double *Tcol, const double *Frow,
+                                           int N, int Tt, int t4, const bool (&fok)[MX])
 {
     const int nks = (Tt + 3) >> 2;
     for (int ks = 0; ks < nks; ks++) {
@@ -916,16 +916,20 @@ __device__ __forceinline__ void gemm_fwd_t(double (&cf)[4][2], const double *Tco
     }
 }
 
-template <bool MASKK>
-__device__ __forceinline__ void gemm_fwd_t_nm(int nm, double (&cf)[4][2], const double *Tcol,
+template <bool MASKK, int MX>
+__device__ __forceinline__ void gemm_fwd_t_nm(int nm, double (&cf)[MX][2], const double *Tcol,
                                               const double *Frow, int N, int Tt, int t4,
-                                              const bool (&fok)[4])
+                                              const bool (&fok)[MX])
 {
     switch (nm) {
-        case 1: gemm_fwd_t<1, MASKK>(cf, Tcol, Frow, N, Tt, t4, fok); break;
-        case 2: gemm_fwd_t<2, MASKK>(cf, Tcol, Frow, N, Tt, t4, fok); break;
-        case 3: gemm_fwd_t<3, MASKK>(cf, Tcol, Frow, N, Tt, t4, fok); break;
-        case 4: gemm_fwd_t<4, MASKK>(cf, Tcol, Frow, N, Tt, t4, fok); break;
+        case 1: gemm_fwd_t<1, MASKK, MX>(cf, Tcol, Frow, N, Tt, t4, fok); break;
+        case 2: gemm_fwd_t<(MX >= 2 ? 2 : 1), MASKK, MX>(cf, Tcol, Frow, N, Tt, t4, fok); break;
+        case 3: gemm_fwd_t<(MX >= 3 ? 3 : 1), MASKK, MX>(cf, Tcol, Frow, N, Tt, t4, fok); break;
+        case 4: gemm_fwd_t<(MX >= 4 ? 4 : 1), MASKK, MX>(cf, Tcol, Frow, N, Tt, t4, fok); break;
+        case 5: gemm_fwd_t<(MX >= 5 ? 5 : 1), MASKK, MX>(cf, Tcol, Frow, N, Tt, t4, fok); break;
+        case 6: gemm_fwd_t<(MX >= 6 ? 6 : 1), MASKK, MX>(cf, Tcol, Frow, N, Tt, t4, fok); break;
+        case 7: gemm_fwd_t<(MX >= 7 ? 7 : 1), MASKK, MX>(cf, Tcol, Frow, N, Tt, t4, fok); break;
+        case 8: gemm_fwd_t<(MX >= 8 ? 8 : 1), MASKK, MX>(cf, Tcol, Frow, N, Tt, t4, fok); break;
         default: break;
     }
 }
@@ -957,7 +961,7 @@ __global__ void __launch_bounds__(256, 2) k_fwd_mma(SweepFwdArgs a)
     double *Ts = sm;                    // 2 x tsz (half tiles)
     double *Fs = sm + 2 * tsz;          // 2 x FWCAP x STP (per tile)
     const int Wu = u.u1 - u.u0;
-    const int nm = (Wu + 7) >> 3;       // <= FWCAP / 8 = 4 probe n-blocks
+    const int nm = (Wu + 7) >> 3;       // <= FWCAP / 8 = FWNB probe n-blocks
     const bool second = warp + 8 < NB;  // warp-uniform: outcome m-block warp + 8 exists
 
     if (tid == 0) {
@@ -996,9 +1000,9 @@ __global__ void __launch_bounds__(256, 2) k_fwd_mma(SweepFwdArgs a)
     };
     if (tid == 0) issue(0);
 
-    double cA[4][2], cB[4][2];
+    double cA[FWNB][2], cB[FWNB][2];
 #pragma unroll
-    for (int i = 0; i < 4; i++) cA[i][0] = cA[i][1] = cB[i][0] = cB[i][1] = 0.0;
+    for (int i = 0; i < FWNB; i++) cA[i][0] = cA[i][1] = cB[i][0] = cB[i][1] = 0.0;
 
     for (int h = 0; h < nh; h++) {
         if (tid == 0 && h + 1 < nh) issue(h + 1);
@@ -1010,9 +1014,9 @@ __global__ void __launch_bounds__(256, 2) k_fwd_mma(SweepFwdArgs a)
             const int sh = (int)(((uintptr_t)(a.theta + (int64_t)k0 * N) & 15) >> 3);
             // union probes outside this tile's window hold stale F rows: their B fragments -> 0
             const int ra = max(a.tile_dA[t], u.u0) - u.u0, rb = min(a.tile_dB[t], u.u1) - u.u0;
-            bool fok[4];
+            bool fok[FWNB];
 #pragma unroll
-            for (int nb = 0; nb < 4; nb++) fok[nb] = 8 * nb + g4 >= ra && 8 * nb + g4 < rb;
+            for (int nb = 0; nb < FWNB; nb++) fok[nb] = 8 * nb + g4 >= ra && 8 * nb + g4 < rb;
             const double *T = Ts + (h & 1) * tsz + sh + t4 * N + g4;
             const double *Frow = Fs + ((h >> 1) & 1) * FWCAP * STP + g4 * STP + t4 + half * FH;
             if (rows == FH) {
@@ -1031,7 +1035,7 @@ __global__ void __launch_bounds__(256, 2) k_fwd_mma(SweepFwdArgs a)
         const int n = 8 * (warp + 8 * pass) + g4;
         if (n >= N || (pass && !second)) continue;
 #pragma unroll
-        for (int nb = 0; nb < 4; nb++)
+        for (int nb = 0; nb < FWNB; nb++)
 #pragma unroll
             for (int i = 0; i < 2; i++) {
                 const int d = 8 * nb + 2 * t4 + i;
@@ -1276,38 +1280,33 @@ __global__ void __launch_bounds__(256) k_reduce_R2(const double *rpart, const in
 }
 
 // ------------------------------------------------------------------------------ scalars
-// Two-level deterministic reduction: block b sums a fixed chunk of the tile partials and of
-// partR into stage[b]; the last block to finish sums stage[0..G) in order, applies the trace /
-// KKT / stop logic (k_finalize's) and resets the arrival counter.
-__global__ void __launch_bounds__(256) k_scalars2(const double *partR, int nR, const double *partT,
-                                                  int ntiles, int include_r2, double *stage,
-                                                  int *arrive, double *vec, int64_t N, int64_t M,
-                                                  double gamma, double tol, int final_eval,
-                                                  int kkt_every, double *trace, double *kkt,
-                                                  double *kktp, int64_t trace_len, DevState *st,
-                                                  int finalize)
+// One CTA of 1024 threads: thread t sums entries t, t + 1024, ... of the tile partials and of
+// partR (fixed assignment and order), then a fixed-shape tree over warps; thread 0 applies the
+// trace / KKT / stop logic.  Deterministic, no atomics, one launch (latency ~ a few us).
+__global__ void __launch_bounds__(1024) k_scalars2(const double *partR, int nR, const double *partT,
+                                                   int ntiles, int include_r2, double *stage,
+                                                   int *arrive, double *vec, int64_t N, int64_t M,
+                                                   double gamma, double tol, int final_eval,
+                                                   int kkt_every, double *trace, double *kkt,
+                                                   double *kktp, int64_t trace_len, DevState *st,
+                                                   int finalize)
 {
-    __shared__ double red[8 * NV];
-    __shared__ int s_last;
+    __shared__ double red[32 * NV];
+    (void)stage;
+    (void)arrive;
     if (st->stop) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int G = gridDim.x;
     double v[NV];
 #pragma unroll
     for (int i = 0; i < NV; i++) v[i] = 0.0;
-    {
-        const int cr = (nR + G - 1) / G, ct = (ntiles + G - 1) / G;
-        const int r0 = blockIdx.x * cr, r1 = min(nR, r0 + cr);
-        const int t0 = blockIdx.x * ct, t1 = min(ntiles, t0 + ct);
-        if (include_r2)
-            for (int i = r0 + threadIdx.x; i < r1; i += blockDim.x) v[V_R2] += partR[i];
-        for (int t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-            const double *p = partT + (int64_t)t * NSC_TILE;
-            v[V_KKT] += p[SC_KKT];
-            v[V_KKTP] += p[SC_KKTP];
-            v[V_REG] += p[SC_REG];
-            v[V_DTH] += p[SC_DTH];
-        }
+    if (include_r2)
+        for (int i = threadIdx.x; i < nR; i += blockDim.x) v[V_R2] += partR[i];
+    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
+        const double4 q = *reinterpret_cast<const double4 *>(partT + (int64_t)t * NSC_TILE);
+        v[V_KKT] += q.x;
+        v[V_KKTP] += q.y;
+        v[V_REG] += q.z;
+        v[V_DTH] += q.w;
     }
 #pragma unroll
     for (int i = 0; i < NV; i++) v[i] = wsum(v[i]);
@@ -1315,31 +1314,22 @@ __global__ void __launch_bounds__(256) k_scalars2(const double *partR, int nR, c
 #pragma unroll
         for (int i = 0; i < NV; i++) red[warp * NV + i] = v[i];
     __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < NV; i++) {
-            double s = 0.0;
-            for (int w = 0; w < 8; w++) s += red[w * NV + i];
-            stage[blockIdx.x * NV + i] = s;
-        }
-        __threadfence();
-        s_last = atomicAdd(arrive, 1) == G - 1;
+    if (warp == 0) {
+        const int nw = blockDim.x >> 5;
+#pragma unroll
+        for (int i = 0; i < NV; i++) v[i] = lane < nw ? red[lane * NV + i] : 0.0;
+#pragma unroll
+        for (int i = 0; i < NV; i++) v[i] = wsum(v[i]);
     }
-    __syncthreads();
-    if (!s_last || threadIdx.x != 0) return;
-    __threadfence();
-    double tot[NV];
-    for (int i = 0; i < NV; i++) tot[i] = 0.0;
-    for (int b = 0; b < G; b++)
-        for (int i = 0; i < NV; i++) tot[i] += __ldcg(&stage[b * NV + i]);
-    *arrive = 0;
-    for (int i = 0; i < NV; i++) vec[i] = tot[i];
+    if (threadIdx.x != 0) return;
+    for (int i = 0; i < NV; i++) vec[i] = v[i];
     if (!finalize) return;  // multi-GPU: allreduce + k_finalize follow
     const int64_t k = st->it;
-    const double f = tot[V_R2] + gamma * tot[V_REG];
+    const double f = v[V_R2] + gamma * v[V_REG];
     const bool kv = final_eval || (k % kkt_every) == 0;
     const double nm = (double)N * (double)M;
-    const double r = kv ? sqrt(tot[V_KKT] / nm) : NAN;
-    const double rp = kv ? sqrt(tot[V_KKTP] / nm) : NAN;
+    const double r = kv ? sqrt(v[V_KKT] / nm) : NAN;
+    const double rp = kv ? sqrt(v[V_KKTP] / nm) : NAN;
     if (k < trace_len) {
         if (trace) trace[k] = f;
         if (kkt) kkt[k] = r;
@@ -1513,7 +1503,7 @@ cudaError_t launch_scalars2(const double *partR, int nR, const double *partT, in
                             double *trace, double *kkt, double *kktp, int64_t trace_len,
                             DevState *st, int finalize, cudaStream_t s)
 {
-    k_scalars2<<<SC2_BLOCKS, 256, 0, s>>>(partR, nR, partT, ntiles, include_r2, stage, arrive, vec,
+    k_scalars2<<<1, 1024, 0, s>>>(partR, nR, partT, ntiles, include_r2, stage, arrive, vec,
                                           N, M, gamma, tol, final_eval, kkt_every, trace, kkt, kktp,
                                           trace_len, st, finalize);
     return cudaGetLastError();

@@ -323,3 +323,18 @@ def test_fista_sweep_parity(q, ctx, N, kkt_every):
     m = ~np.isnan(ro["kkt"])
     np.testing.assert_array_equal(m, ~np.isnan(rg["kkt"]))
     np.testing.assert_allclose(rg["kkt"][m], ro["kkt"][m], rtol=1e-8, atol=1e-15)
+
+
+@pytest.mark.slow
+def test_stress_cut_solve_parity(q, ctx):
+    """Stress-shaped cut-down instance (M = 10^5, N = 10^3, D = 2000 log-spaced
+    probes, log bins, noiseless P): N > 128 runs the general kernels; 3 iterations."""
+    I = qs.stress_cut()
+    Fo = oracle.Probes(I.alpha2, I.M)
+    Fg = q.qdt_build_probes(ctx, I.alpha2, I.M)
+    ro = oracle.solve(Fo, I.P, I.gamma, 0.0, 3)
+    rg = q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, 3)
+    assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9
+    assert _trace_ok(rg["trace"], ro["trace"], I.P)
+    Th = rg["theta"]
+    assert Th.min() >= 0 and np.abs(Th.sum(1) - 1).max() <= 4 * Th.shape[1] * EPS
