@@ -689,11 +689,11 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(Swe
 // so that each thread holds half a row and two CTAs (32 warps) fit an SM; the two halves of a row
 // complete every row reduction through a named-barrier pair exchange (PairX).
 template <int NB, bool FIS>
-__global__ void __launch_bounds__(512, (FIS ? 1 : 2)) k_bwd_split(SweepArgs a)
+__global__ void __launch_bounds__(512, 1) k_bwd_split(SweepArgs a)
 {
     constexpr int NBA = (NB + 1) / 2;
     extern __shared__ __align__(128) double sm[];
-    __shared__ __align__(8) uint64_t bars[3];
+    __shared__ __align__(8) uint64_t bars[4];   // 0, 3: Theta buffers; 1, 2: chunk stages
     __shared__ double red[16 * 3];
     __shared__ double xbuf[2 * 8 * 2 * 8 * 4];
     __shared__ int s_last;
@@ -710,7 +710,7 @@ __global__ void __launch_bounds__(512, (FIS ? 1 : 2)) k_bwd_split(SweepArgs a)
     const SwLayout<NB> L(N);
     double *Th = sm;
     double *Tq = sm + L.thsz;
-    double *Fs = sm + (FIS ? 2 : 1) * L.thsz;
+    double *Fs = sm + 2 * L.thsz;                   // two tiles: double buffer or Theta_{k-1}
     double *Rs = Fs + 2 * SKC * STP;
     if (a.eval_gate && (it % a.kkt_every) != 0) return;
     const bool do_kkt = !FIS && (it % a.kkt_every) == 0;
@@ -722,19 +722,28 @@ __global__ void __launch_bounds__(512, (FIS ? 1 : 2)) k_bwd_split(SweepArgs a)
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
         mbar_init(&bars[2], 1);
+        mbar_init(&bars[3], 1);
         fence_barrier_init();
     }
     __syncthreads();
-    uint32_t c_issue = 0, c_use = 0, th_use = 0;
+    // Theta loads are issued and consumed in unit order (FIFO).  Plain steps double-buffer the
+    // tile (buffers Th / Tq alternate): the next non-split unit's tile is requested when the
+    // current unit starts.  FISTA uses Tq for Theta_{k-1}, single buffer.
+    uint32_t c_issue = 0, c_use = 0, th_issue = 0, th_use = 0;
+    auto th_buf = [&](uint32_t n) -> double * { return (!FIS && (n & 1)) ? Tq : Th; };
+    auto th_bar = [&](uint32_t n) -> uint64_t * { return (!FIS && (n & 1)) ? &bars[3] : &bars[0]; };
+    auto th_par = [&](uint32_t n) -> uint32_t { return FIS ? (n & 1) : ((n >> 1) & 1); };
     auto issue_theta = [&](const SwUnit &v) {
         const int k0 = v.tile * ST, Tt = min(ST, a.Ml - k0);
         const double *src;
         int sh;
         uint32_t by;
         aligned_span(a.theta + (int64_t)(k0 - 1) * N, (int64_t)(Tt + 2) * N, &src, &sh, &by);
-        mbar_expect_tx(&bars[0], FIS ? 2 * by : by);
-        bulk_g2s(Th, src, by, &bars[0]);
-        if (FIS) bulk_g2s(Tq, a.theta_prev + (src - a.theta), by, &bars[0]);
+        uint64_t *bar = th_bar(th_issue);
+        mbar_expect_tx(bar, FIS ? 2 * by : by);
+        bulk_g2s(th_buf(th_issue), src, by, bar);
+        if (FIS) bulk_g2s(Tq, a.theta_prev + (src - a.theta), by, bar);
+        th_issue++;
     };
     auto issue_chunk = [&](const SwUnit &v, int c) {
         const int W = v.p1 - v.p0, pb = c * SKC, kc = min(SKC, W - pb);
@@ -758,6 +767,10 @@ __global__ void __launch_bounds__(512, (FIS ? 1 : 2)) k_bwd_split(SweepArgs a)
     }
     while (true) {
         const SwUnit u = a.units[unit];
+        if (!FIS && tid == 0 && u.nsplit == 1 && unit + G < a.nunits) {
+            const SwUnit un = a.units[unit + G];    // prefetch: the other buffer is free
+            if (un.nsplit == 1) issue_theta(un);
+        }
         const int k0 = u.tile * ST;
         const int Tt = min(ST, a.Ml - k0);
         const int W = u.p1 - u.p0;
@@ -815,7 +828,8 @@ __global__ void __launch_bounds__(512, (FIS ? 1 : 2)) k_bwd_split(SweepArgs a)
             }
         }
         if (epi) {
-            mbar_wait(&bars[0], th_use & 1);
+            double *Thc = th_buf(th_use);
+            mbar_wait(th_bar(th_use), th_par(th_use));
             th_use++;
             const int th_sh = (int)(((uintptr_t)(a.theta + (int64_t)(k0 - 1) * N) & 15) >> 3);
             const int r = 8 * mb + g4;
@@ -823,7 +837,7 @@ __global__ void __launch_bounds__(512, (FIS ? 1 : 2)) k_bwd_split(SweepArgs a)
             const int kl = k0 + r;
             const int64_t kg = a.kb + kl;
             const bool has_prev = kg > 0, has_next = kg + 1 < a.M;
-            double *thr = Th + th_sh + (r + 1) * N;
+            double *thr = Thc + th_sh + (r + 1) * N;
             const double *tpr = Tq + th_sh + (r + 1) * N;
             double sreg = 0.0, skkt = 0.0, skktp = 0.0, s, xm, xn;
             double *orow = a.out + (int64_t)kl * N;
@@ -844,8 +858,8 @@ __global__ void __launch_bounds__(512, (FIS ? 1 : 2)) k_bwd_split(SweepArgs a)
                 else if (full) QDT_SPLIT_PASS(8 * NBA, true, false);
                 else QDT_SPLIT_PASS(8 * NBA, false, false);
             }
-            __syncthreads();  // Theta tile consumed: start the next unit's tile load
-            if (tid == 0 && next < a.nunits) {
+            __syncthreads();  // Theta tile consumed
+            if (tid == 0 && next < a.nunits && (FIS || u.nsplit > 1)) {   // not prefetched
                 const SwUnit un = a.units[next];
                 if (un.nsplit == 1) issue_theta(un);
             }
@@ -1442,10 +1456,10 @@ cudaError_t launch_bwd_split(const SweepArgs &a_in, int nunits, int NB, cudaStre
     SweepArgs a = a_in;
     a.nunits = nunits;
     const bool fis = a.beta != nullptr && !a.eval;
-    const size_t smem = sweep_bwd_smem(a.N, NB, fis);
+    const size_t smem = sweep_bwd_smem(a.N, NB, true);   // two tiles: double buffer or Theta_{k-1}
     static int nsm = 0;
     if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-    const int grid = std::min(nunits, (fis ? 1 : 2) * nsm);
+    const int grid = std::min(nunits, nsm);
     switch (NB) {
 #define QDT_CASE(nb)                                                       \
     case nb:                                                               \
