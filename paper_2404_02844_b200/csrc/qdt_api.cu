@@ -108,6 +108,7 @@ struct Plan {
     int64_t *d_red_beg = nullptr, *d_red_rows = nullptr;
     // sweep path (DMMA kernels, N <= 128): NB n-blocks; bwd/fwd units; reduce lists
     int NB = 0;
+    int NW = 0;                       // wide-N sweep (N > 128, even, <= 1024): 128-column chunks
     int nR = 0;                       // partR entries written by the residual reduction
     int sw_nbunits = 0;
     SwUnit *d_swunits = nullptr;
@@ -495,7 +496,7 @@ static bool sweep_enabled()
 static qdt_status build_fused_plan(qdt_ctx *ctx, qdt_probes *p, Plan *pl, const std::vector<SwUnit> &bu_all)
 {
     pl->fz_on = false;
-    if (ctx->nranks != 1) return QDT_OK;
+    if (ctx->nranks != 1 || pl->NB == 0) return QDT_OK;
     // the fused persistent sweep is opt-in (QDT_FUSED=1): at 8 warps per SM it is latency bound and
     // measured slower than the unfused sweep (profiles/r01_v2)
     const char *e = getenv("QDT_FUSED");
@@ -831,8 +832,9 @@ static qdt_status build_plan(qdt_ctx *ctx, qdt_probes *p, int N, Plan **out)
                            cudaMemcpyHostToDevice, s));
     CK(cudaStreamSynchronize(s));
     pl->NB = sweep_enabled() ? sweep_nb(N) : 0;
-    if (pl->NB) CKS(build_sweep_plan(ctx, p, pl.get()));
-    pl->nR = pl->NB && ctx->nranks == 1 ? (int)((D + 7) / 8) : ctx->nblkR;
+    pl->NW = (sweep_enabled() && !pl->NB && N % 2 == 0 && N <= 1024) ? 1 : 0;
+    if (pl->NB || pl->NW) CKS(build_sweep_plan(ctx, p, pl.get()));
+    pl->nR = ctx->nranks == 1 ? (int)((D + 7) / 8) : ctx->nblkR;
     *out = pl.get();
     p->plans[N] = std::move(pl);
     return QDT_OK;
@@ -1078,6 +1080,7 @@ struct SolveBufs {
     double *sc2_stage = nullptr;
     int *sc2_arrive = nullptr;
     double *partS = nullptr;   // fused sweep: heavy-tile slots [0, tsplit) + CTA slots
+    double *Gw = nullptr;      // wide-N sweep: Ml x N gradient
 };
 
 struct IterCfg {
@@ -1097,7 +1100,8 @@ static qdt_status fwd_reduce(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, const
     Plan *pl = c.pl;
     qdt_probes *p = c.p;
     const bool multi = ctx->nranks > 1;
-    if (pl->NB) {
+    if (pl->NB || pl->NW) {
+        const int fnb = pl->NB ? pl->NB : SW_NBMAX;   // wide N: 128-column chunks
         SweepFwdArgs fa;
         fa.N = c.N;
         fa.Ml = (int)p->Ml;
@@ -1109,7 +1113,7 @@ static qdt_status fwd_reduce(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, const
         fa.theta = theta;
         fa.rpart = b.rpart;
         fa.state = b.state;
-        CK(run_k(ctx, "fwd_partial", 1, [&]() { return launch_fwd_mma(fa, pl->sw_nfunits, pl->NB, s); }));
+        CK(run_k(ctx, "fwd_partial", 1, [&]() { return launch_fwd_mma(fa, pl->sw_nfunits, fnb, s); }));
         if (!multi) {
             CK(run_k(ctx, "reduce_R", 1, [&]() {
                 return launch_reduce_R2(b.rpart, pl->d_sw_red_beg, pl->d_sw_red_rows, withP ? b.P : nullptr,
@@ -1140,9 +1144,9 @@ static qdt_status fwd_reduce(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, const
     fa.rpart = b.rpart;
     fa.state = b.state;
     CK(run_k(ctx, "fwd_partial", 1, [&]() { return launch_fwd(fa, pl->nfunits, pl->TC, s, nullptr); }));
-    CK(run_k(ctx, "reduce_R", 1, [&]() {
-        return launch_reduce_R(b.rpart, pl->d_red_beg, pl->d_red_rows, (withP && !multi) ? b.P : nullptr,
-                               R, p->D, c.N, b.partR, pl->nR, b.state, s);
+    CK(run_k(ctx, "reduce_R", 1, [&]() {   // warp per probe, fixed list order (any N)
+        return launch_reduce_R2(b.rpart, pl->d_red_beg, pl->d_red_rows, (withP && !multi) ? b.P : nullptr,
+                                R, (int)p->D, c.N, multi ? nullptr : b.partR, b.state, s);
     }));
     if (multi) {
         CKS(allreduce(ctx, R, (size_t)p->D * c.N, "allreduce_R"));
@@ -1272,12 +1276,59 @@ static SweepArgs sweep_args(const IterCfg &c, SolveBufs &b, const double *R, con
     return a;
 }
 
+static WideArgs wide_args(const IterCfg &c, SolveBufs &b, const double *R, const double *theta,
+                          double *out)
+{
+    WideArgs w;
+    w.N = c.N;
+    w.Ml = (int)c.p->Ml;
+    w.ncc = (c.N + 127) / 128;
+    w.kb = c.p->kb;
+    w.M = c.p->M;
+    w.units = c.pl->d_swunits;
+    w.fb_off = c.p->d_fb_off;
+    w.tile_dA = c.p->d_sw_dA;
+    w.Fb = c.p->d_Fb;
+    w.R = R;
+    w.theta = theta;
+    w.G = b.Gw;
+    w.out = out;
+    w.tstep = b.tstep;
+    w.gamma = c.gamma;
+    w.scratch = b.scratch;
+    w.counters = b.counters;
+    w.part = b.partT;
+    w.part_b = (int64_t)c.p->sw_ntiles * w.ncc;
+    w.kkt_every = c.kkt_every;
+    w.eval = 0;
+    w.eval_gate = 0;
+    w.theta_prev = nullptr;
+    w.beta = nullptr;
+    w.state = b.state;
+    return w;
+}
+
+static int wide_nparts(const IterCfg &c)
+{
+    return c.p->sw_ntiles * ((c.N + 127) / 128) + (int)((c.p->Ml + 7) / 8);
+}
+
 // one iteration with phase index j (buffer rotation)
 static qdt_status iteration(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, int64_t j)
 {
     cudaStream_t s = ctx->stream;
     Plan *pl = c.pl;
     int ntiles = pl->ntiles;
+    if (!c.fista && pl->NW) {
+        double *cur = b.theta[j % 2], *nxt = b.theta[(j + 1) % 2];
+        CKS(fwd_reduce(ctx, c, b, cur, b.R[0], true));
+        WideArgs w = wide_args(c, b, b.R[0], cur, nxt);
+        CK(run_k(ctx, "bwd_step", 1, [&]() { return launch_grad_wide(w, pl->sw_nbunits, s); }));
+        CK(run_k(ctx, "proj_step", 1, [&]() { return launch_proj_wide(w, s); }));
+        CKS(halo_exchange(ctx, c, nxt));
+        CKS(scalars(ctx, c, b, 0, wide_nparts(c)));
+        return QDT_OK;
+    }
     if (!c.fista && pl->fz_on) {
         // R_j is resident (prologue or the previous iteration's reduce); this iteration writes
         // Theta_{j+1} and the partial rows of R_{j+1}
@@ -1337,6 +1388,26 @@ static qdt_status iteration(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, int64_
         CK(run_k(ctx, "bwd_step", 1, [&]() { return launch_bwd_any(a, pl->sw_nbunits, pl->NB, s); }));
         CKS(halo_exchange(ctx, c, nxt));
         ntiles = c.p->sw_ntiles;
+    } else if (c.fista && pl->NW) {
+        // FISTA, wide N: R_k, R(Y), gated KKT evaluation of Theta_k, then the step from Y
+        double *cur = b.theta[j % 3], *prev = b.theta[(j + 2) % 3], *nxt = b.theta[(j + 1) % 3];
+        double *Rk = b.R[j % 2], *Rkm1 = b.R[(j + 1) % 2];
+        CKS(fwd_reduce(ctx, c, b, cur, Rk, true));
+        CK(run_k(ctx, "fista_rcomb", 1, [&]() {
+            return launch_fista_rcomb(b.RY, Rk, Rkm1, b.beta, c.p->D * (int64_t)c.N, b.state, s);
+        }));
+        WideArgs ev = wide_args(c, b, Rk, cur, nullptr);
+        ev.eval = 1;
+        ev.eval_gate = 1;
+        CK(run_k(ctx, "bwd_eval", 1, [&]() { return launch_grad_wide(ev, pl->sw_nbunits, s); }));
+        CK(run_k(ctx, "proj_eval", 1, [&]() { return launch_proj_wide(ev, s); }));
+        WideArgs w = wide_args(c, b, b.RY, cur, nxt);
+        w.theta_prev = prev;
+        w.beta = b.beta;
+        CK(run_k(ctx, "bwd_step", 1, [&]() { return launch_grad_wide(w, pl->sw_nbunits, s); }));
+        CK(run_k(ctx, "proj_step", 1, [&]() { return launch_proj_wide(w, s); }));
+        CKS(halo_exchange(ctx, c, nxt));
+        ntiles = wide_nparts(c);
     } else if (c.fista && pl->NB) {
         // FISTA on the sweep kernels: R_k, R(Y) = R_k + beta (R_k - R_{k-1}) (linear), the KKT of
         // Theta_k on the recorded iterations (evaluation pass gated on the device), then the
@@ -1395,12 +1466,15 @@ static qdt_status common_bufs(qdt_ctx *ctx, qdt_probes *p, Plan *pl, int64_t N, 
         CK(cudaMemsetAsync(b.partS, 0, sizeof(double) * ns * NSC_TILE, s));
     }
     CKS(ws_get(ctx, "partR", std::max(ctx->nblkR, pl->nR), &b.partR));
-    const int nt = std::max(1, std::max(pl->ntiles, p->sw_ntiles));
+    const int ncc = (int)((N + 127) / 128);
+    const int nt = std::max(1, std::max({pl->ntiles, p->sw_ntiles * (pl->NW ? ncc : 1) + (int)((p->Ml + 7) / 8)}));
+    if (pl->NW) CKS(ws_get(ctx, "Gw", p->Ml * N + 4, &b.Gw));
     CKS(ws_get(ctx, "partT", (size_t)nt * NSC_TILE, &b.partT));
     CK(cudaMemsetAsync(b.partT, 0, sizeof(double) * nt * NSC_TILE, s));
     CKS(ws_get(ctx, "vec", NV, &b.vec));
     CKS(ws_get(ctx, "tstep", p->Ml, &b.tstep));
-    const int64_t scr = std::max<int64_t>(1, std::max<int64_t>(pl->nslots * pl->T * N, pl->sw_nslots * 1024 * ((pl->NB + 1) / 2 + 1)));
+    const int64_t scr = std::max<int64_t>(1, std::max({pl->nslots * pl->T * N, pl->sw_nslots * 1024 * ((pl->NB + 1) / 2 + 1),
+                                                       pl->NW ? pl->sw_nslots * ncc * 8192 : (int64_t)0}));
     CKS(ws_get(ctx, "scratch", scr, &b.scratch));
     CKS(ws_get(ctx, "counters", nt, &b.counters));
     CK(cudaMemsetAsync(b.counters, 0, sizeof(int) * nt, s));
@@ -1422,7 +1496,13 @@ static qdt_status eval_pass(qdt_ctx *ctx, const IterCfg &c0, SolveBufs &b, doubl
     c.kkt_every = 1;
     Plan *pl = c.pl;
     CKS(fwd_reduce(ctx, c, b, theta, b.R[0], true));
-    if (pl->NB) {
+    if (pl->NW) {
+        WideArgs w = wide_args(c, b, b.R[0], theta, nullptr);
+        w.eval = 1;
+        CK(run_k(ctx, "bwd_eval", 1, [&]() { return launch_grad_wide(w, pl->sw_nbunits, s); }));
+        CK(run_k(ctx, "proj_eval", 1, [&]() { return launch_proj_wide(w, s); }));
+        CKS(scalars(ctx, c, b, 1, wide_nparts(c)));
+    } else if (pl->NB) {
         SweepArgs a = sweep_args(c, b, b.R[0], theta, nullptr);
         a.eval = 1;
         CK(run_k(ctx, "bwd_eval", 1, [&]() { return launch_bwd_any(a, pl->sw_nbunits, pl->NB, s); }));

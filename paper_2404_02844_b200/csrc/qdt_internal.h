@@ -135,6 +135,7 @@ struct SweepFwdArgs {
     const double *Fb;
     const double *theta;
     double *rpart;
+    int ncc;                    // column chunks of 8 NB outcomes (set by launch_fwd_mma)
     const DevState *state;
 };
 struct SweepFusedArgs {
@@ -156,6 +157,32 @@ struct SweepFusedArgs {
     int kkt_every;
     const DevState *state;
 };
+struct WideArgs {               // wide-N sweep (N > 128): k_grad_wide + k_proj_wide
+    int N, Ml, ncc;             // ncc: 128-column chunks (set by launch_grad_wide)
+    int64_t kb, M;
+    const SwUnit *units;
+    const int64_t *fb_off;
+    const int32_t *tile_dA;
+    const double *Fb;
+    const double *R;
+    const double *theta;        // local row 0; rows -1 and Ml readable
+    double *G;                  // Ml x N gradient (half), written by k_grad_wide
+    double *out;                // Theta_{k+1} (k_proj_wide, not in eval)
+    const double *tstep;
+    double gamma;
+    double *scratch;
+    int *counters;              // per (tile, chunk)
+    double *part;               // grad: slot tile * ncc + cc; proj: slot part_b + block
+    int64_t part_b;
+    int kkt_every;
+    int eval;
+    int eval_gate;              // FISTA evaluation pass: only when state->it % kkt_every == 0
+    const double *theta_prev;   // FISTA step: Theta_{k-1}
+    const double *beta;         // FISTA step: beta_k by state->it (nullptr: plain)
+    const DevState *state;
+};
+cudaError_t launch_grad_wide(const WideArgs &a, int nunits, cudaStream_t s);
+cudaError_t launch_proj_wide(const WideArgs &a, cudaStream_t s);
 constexpr int SW_FUSED_SMEM_MAX = 220 * 1024;
 size_t sweep_fused_smem(int N, int NB, int cap);
 cudaError_t launch_sweep_fused(const SweepFusedArgs &a, int nctas, int NB, cudaStream_t s);

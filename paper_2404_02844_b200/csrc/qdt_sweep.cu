@@ -100,6 +100,24 @@ __device__ __forceinline__ double quad_min(double v)
     v = fmin(v, __shfl_xor_sync(0xffffffffu, v, 2));
     return v;
 }
+__device__ __forceinline__ double wmin(double v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ double wmax(double v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ int wsum_i(int v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
 __device__ __forceinline__ double wsum(double v)
 {
 #pragma unroll
@@ -413,7 +431,7 @@ __device__ __forceinline__ void row_step(double (&acc)[NB][2], double *thr, int 
 // in; R: chunk rows (pitch N), lane's column g4 folded in.
 template <int NB>
 __device__ __forceinline__ void gemm_bwd(double (&acc)[NB][2], const double *F, const double *R,
-                                         int kc, int N, int t4)
+                                         int kc, int N, int t4)   // N: pitch of the staged R rows
 {
     const int nfull = kc >> 2;
     for (int ks = 0; ks < nfull; ks++) {
@@ -956,7 +974,8 @@ __device__ __forceinline__ void gemm_fwd_t_nm(int nm, double (&cf)[MX][2], const
 constexpr int FH = ST / 2;
 size_t sweep_fwd_smem(int N, int NB)
 {
-    const int tsz = ((FH * N + 8 * NB + 4) + 1) & ~1;
+    const int TP = N > 8 * NB ? 8 * NB + 4 : N;   // wide N: column chunks of 8 NB
+    const int tsz = ((FH * TP + 8 * NB + 4) + 1) & ~1;
     return (size_t)(2 * tsz + 2 * FWCAP * STP) * sizeof(double);
 }
 
@@ -970,13 +989,20 @@ __global__ void __launch_bounds__(256, 2) k_fwd_mma(SweepFwdArgs a)
     const int N = a.N;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g4 = lane >> 2, t4 = lane & 3;
-    const FwUnit u = a.units[blockIdx.x];
-    const int tsz = ((FH * N + 8 * NB + 4) + 1) & ~1;
+    // wide N (ncc > 1): CTA (unit, column chunk cc) covers columns [cbase, cbase + ncol) with the
+    // Theta half tile staged row by row at pitch TP (conflict-free A fragments)
+    const int ncc = a.ncc;
+    const FwUnit u = a.units[blockIdx.x / ncc];
+    const int cc = blockIdx.x - (blockIdx.x / ncc) * ncc;
+    const int cbase = cc * 8 * NB;
+    const int ncol = min(8 * NB, N - cbase);
+    const int TP = ncc > 1 ? 8 * NB + 4 : N;
+    const int tsz = ((FH * TP + 8 * NB + 4) + 1) & ~1;
     double *Ts = sm;                    // 2 x tsz (half tiles)
     double *Fs = sm + 2 * tsz;          // 2 x FWCAP x STP (per tile)
     const int Wu = u.u1 - u.u0;
     const int nm = (Wu + 7) >> 3;       // <= FWCAP / 8 = FWNB probe n-blocks
-    const bool second = warp + 8 < NB;  // warp-uniform: outcome m-block warp + 8 exists
+    const bool second = warp + 8 < NB && 8 * (warp + 8) < ncol;  // warp-uniform: m-block warp + 8 used
 
     if (tid == 0) {
         mbar_init(&bars[0], 1);
@@ -998,7 +1024,12 @@ __global__ void __launch_bounds__(256, 2) k_fwd_mma(SweepFwdArgs a)
             const int rb = min(a.tile_dB[t], u.u1);
             fby = rb > ra ? (uint32_t)(rb - ra) * STP * 8 : 0;
         }
-        if (rows > 0) {
+        if (rows > 0 && ncc > 1) {
+            const uint32_t rby = (uint32_t)ncol * 8;   // N even, cbase % 8 == 0: 16-byte aligned rows
+            mbar_expect_tx(bar, rby * rows + fby);
+            for (int rr = 0; rr < rows; rr++)
+                bulk_g2s(Ts + (h & 1) * tsz + rr * TP, a.theta + (int64_t)(k0 + rr) * N + cbase, rby, bar);
+        } else if (rows > 0) {
             const double *src;
             int sh;
             uint32_t by;
@@ -1025,20 +1056,20 @@ __global__ void __launch_bounds__(256, 2) k_fwd_mma(SweepFwdArgs a)
         const int k0 = t * ST + half * FH;
         const int rows = min(FH, a.Ml - k0);
         if (rows > 0) {
-            const int sh = (int)(((uintptr_t)(a.theta + (int64_t)k0 * N) & 15) >> 3);
+            const int sh = ncc > 1 ? 0 : (int)(((uintptr_t)(a.theta + (int64_t)k0 * N) & 15) >> 3);
             // union probes outside this tile's window hold stale F rows: their B fragments -> 0
             const int ra = max(a.tile_dA[t], u.u0) - u.u0, rb = min(a.tile_dB[t], u.u1) - u.u0;
             bool fok[FWNB];
 #pragma unroll
             for (int nb = 0; nb < FWNB; nb++) fok[nb] = 8 * nb + g4 >= ra && 8 * nb + g4 < rb;
-            const double *T = Ts + (h & 1) * tsz + sh + t4 * N + g4;
+            const double *T = Ts + (h & 1) * tsz + sh + t4 * TP + g4;
             const double *Frow = Fs + ((h >> 1) & 1) * FWCAP * STP + g4 * STP + t4 + half * FH;
             if (rows == FH) {
-                gemm_fwd_t_nm<false>(nm, cA, T + 8 * warp, Frow, N, FH, t4, fok);
-                if (second) gemm_fwd_t_nm<false>(nm, cB, T + 8 * (warp + 8), Frow, N, FH, t4, fok);
+                gemm_fwd_t_nm<false>(nm, cA, T + 8 * warp, Frow, TP, FH, t4, fok);
+                if (second) gemm_fwd_t_nm<false>(nm, cB, T + 8 * (warp + 8), Frow, TP, FH, t4, fok);
             } else {
-                gemm_fwd_t_nm<true>(nm, cA, T + 8 * warp, Frow, N, rows, t4, fok);
-                if (second) gemm_fwd_t_nm<true>(nm, cB, T + 8 * (warp + 8), Frow, N, rows, t4, fok);
+                gemm_fwd_t_nm<true>(nm, cA, T + 8 * warp, Frow, TP, rows, t4, fok);
+                if (second) gemm_fwd_t_nm<true>(nm, cB, T + 8 * (warp + 8), Frow, TP, rows, t4, fok);
             }
         }
         __syncthreads();
@@ -1046,8 +1077,9 @@ __global__ void __launch_bounds__(256, 2) k_fwd_mma(SweepFwdArgs a)
     // partial rows rpart[(poff + d) * N + n]: lane holds n = 8 mb + g4, d = 8 nb + 2 t4 + {0,1}
 #pragma unroll
     for (int pass = 0; pass < 2; pass++) {
-        const int n = 8 * (warp + 8 * pass) + g4;
-        if (n >= N || (pass && !second)) continue;
+        const int nl = 8 * (warp + 8 * pass) + g4;
+        const int n = cbase + nl;
+        if (nl >= ncol || (pass && !second)) continue;
 #pragma unroll
         for (int nb = 0; nb < FWNB; nb++)
 #pragma unroll
@@ -1248,6 +1280,280 @@ __global__ void __launch_bounds__(256, 1) k_sweep_fused(SweepFusedArgs a)
     }
 }
 
+// ------------------------------------------------------------------------------ wide N
+// N > 128 (even, <= 1024): the gradient and the row projection become two kernels.
+//   k_grad_wide  CTA (bwd unit, column chunk of 128 outcomes): G = F_tile^T R_win[:, chunk] by
+//                DMMA (split-K slots per chunk as in k_bwd_mma), + gamma L Theta (Theta read from
+//                global / L2), G stored; regulariser pair partial per (tile, chunk).
+//   k_proj_wide  warp per Fock row (N / 32 values per lane): KKT, X = Theta -
+//                t_k G, Michelot threshold (reading R4), Theta_{k+1}.
+constexpr int RPW = 8 * 16 + 4;   // staged R row pitch for 128-column chunks (conflict-free B)
+size_t wide_grad_smem() { return (size_t)(2 * SKC * STP + 2 * SKC * RPW + 8) * sizeof(double); }
+
+__global__ void __launch_bounds__(256, 2) k_grad_wide(WideArgs a)
+{
+    constexpr int NB = 16;
+    extern __shared__ __align__(128) double sm[];
+    __shared__ __align__(8) uint64_t bars[2];
+    __shared__ double red[8];
+    __shared__ int s_last;
+    const DevState *st = a.state;
+    if (st && st->stop) return;
+    const int64_t it = st ? st->it : 0;
+    if (a.eval_gate && (it % a.kkt_every) != 0) return;
+    const bool fis = a.beta != nullptr && !a.eval;   // FISTA step: stencil of Y
+    const double beta = fis ? a.beta[it] : 0.0;
+    const int N = a.N, ncc = a.ncc;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g4 = lane >> 2, t4 = lane & 3;
+    const SwUnit u = a.units[blockIdx.x / ncc];
+    const int cc = blockIdx.x - (blockIdx.x / ncc) * ncc;
+    const int cbase = cc * 8 * NB, ncol = min(8 * NB, N - cbase);
+    const int k0 = u.tile * ST, Tt = min(ST, a.Ml - k0);
+    double *Fs = sm;
+    double *Rs = sm + 2 * SKC * STP;
+    const int W = u.p1 - u.p0, nch = (W + SKC - 1) / SKC;
+    const double *Fg = a.Fb + a.fb_off[u.tile] + (int64_t)(u.p0 - a.tile_dA[u.tile]) * STP;
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    auto issue = [&](int c) {
+        const int pb = c * SKC, kc = min(SKC, W - pb);
+        uint64_t *bar = &bars[c & 1];
+        const uint32_t fby = (uint32_t)kc * STP * 8, rby = (uint32_t)ncol * 8;
+        mbar_expect_tx(bar, fby + rby * kc);
+        bulk_g2s(Fs + (c & 1) * SKC * STP, Fg + (int64_t)pb * STP, fby, bar);
+        for (int j = 0; j < kc; j++)
+            bulk_g2s(Rs + (c & 1) * SKC * RPW + j * RPW, a.R + (int64_t)(u.p0 + pb + j) * N + cbase, rby, bar);
+    };
+    if (tid == 0 && nch > 0) issue(0);
+    double acc[NB][2];
+#pragma unroll
+    for (int nb = 0; nb < NB; nb++) acc[nb][0] = acc[nb][1] = 0.0;
+    for (int c = 0; c < nch; c++) {
+        if (tid == 0 && c + 1 < nch) issue(c + 1);
+        mbar_wait(&bars[c & 1], (c >> 1) & 1);
+        const int kc = min(SKC, W - c * SKC);
+        gemm_bwd<NB>(acc, Fs + (c & 1) * SKC * STP + 8 * warp + g4, Rs + (c & 1) * SKC * RPW + g4, kc, RPW, t4);
+        __syncthreads();
+    }
+    if (u.nsplit > 1) {
+        const int64_t fsz = (int64_t)8 * NB * 64;
+        double *slot = a.scratch + ((u.slot_base + u.slot) * ncc + cc) * fsz;
+#pragma unroll
+        for (int nb = 0; nb < NB; nb++)
+            __stcg(reinterpret_cast<double2 *>(slot + ((warp * NB + nb) * 32 + lane) * 2),
+                   make_double2(acc[nb][0], acc[nb][1]));
+        __threadfence();
+        __syncthreads();
+        int *ctr = a.counters + (int64_t)u.tile * ncc + cc;
+        if (tid == 0) s_last = (atomicAdd(ctr, 1) == u.nsplit - 1);
+        __syncthreads();
+        if (!s_last) return;
+        __threadfence();
+#pragma unroll
+        for (int nb = 0; nb < NB; nb++) acc[nb][0] = acc[nb][1] = 0.0;
+        for (int sl = 0; sl < u.nsplit; sl++) {
+            const double *sp = a.scratch + ((u.slot_base + sl) * ncc + cc) * fsz;
+#pragma unroll
+            for (int nb = 0; nb < NB; nb++) {
+                const double2 v = __ldcg(reinterpret_cast<const double2 *>(sp + ((warp * NB + nb) * 32 + lane) * 2));
+                acc[nb][0] += v.x;
+                acc[nb][1] += v.y;
+            }
+        }
+        if (tid == 0) *ctr = 0;
+    }
+    // G = acc + gamma L Y on this row's chunk columns; Y = Theta (+ beta (Theta - Theta_{k-1}))
+    const int r = 8 * warp + g4;
+    const int kl = k0 + r;
+    const int64_t kg = a.kb + kl;
+    const bool act = r < Tt, hp = kg > 0, hn = kg + 1 < a.M;
+    double sreg = 0.0;
+    if (act) {
+        const double *th = a.theta + (int64_t)kl * N + cbase;
+        double *gout = a.G + (int64_t)kl * N + cbase;
+#pragma unroll
+        for (int nb = 0; nb < NB; nb++) {
+            const int c = 8 * nb + 2 * t4;
+            if (c < ncol) {   // N even: the pair (c, c + 1) is valid together
+                double2 x = __ldg(reinterpret_cast<const double2 *>(th + c));
+                double2 y = hp ? __ldg(reinterpret_cast<const double2 *>(th + c - N)) : x;
+                double2 z = hn ? __ldg(reinterpret_cast<const double2 *>(th + c + N)) : x;
+                const double d20 = x.x - z.x, d21 = x.y - z.y;   // regulariser pair of Theta_k
+                sreg = fma(d20, d20, fma(d21, d21, sreg));
+                if (fis) {   // Y = Theta_k + beta (Theta_k - Theta_{k-1}) for the stencil
+                    const double *tq = a.theta_prev + (int64_t)kl * N + cbase;
+                    const double2 xq = __ldg(reinterpret_cast<const double2 *>(tq + c));
+                    const double2 yq = hp ? __ldg(reinterpret_cast<const double2 *>(tq + c - N)) : xq;
+                    const double2 zq = hn ? __ldg(reinterpret_cast<const double2 *>(tq + c + N)) : xq;
+                    const double2 xo = x;
+                    x = make_double2(fma(beta, x.x - xq.x, x.x), fma(beta, x.y - xq.y, x.y));
+                    y = hp ? make_double2(fma(beta, y.x - yq.x, y.x), fma(beta, y.y - yq.y, y.y)) : x;
+                    z = hn ? make_double2(fma(beta, z.x - zq.x, z.x), fma(beta, z.y - zq.y, z.y)) : x;
+                    (void)xo;
+                }
+                const double g0 = fma(a.gamma, (x.x - y.x) + (x.x - z.x), acc[nb][0]);
+                const double g1 = fma(a.gamma, (x.y - y.y) + (x.y - z.y), acc[nb][1]);
+                *reinterpret_cast<double2 *>(gout + c) = make_double2(g0, g1);
+            }
+        }
+    }
+    sreg = wsum(sreg);
+    if (lane == 0) red[warp] = sreg;
+    __syncthreads();
+    if (tid == 0) {
+        double v = 0.0;
+        for (int w = 0; w < 8; w++) v += red[w];
+        double *pp = a.part + ((int64_t)u.tile * ncc + cc) * NSC_TILE;
+        pp[SC_KKT] = 0.0;
+        pp[SC_KKTP] = 0.0;
+        pp[SC_REG] = v;
+        pp[SC_DTH] = 0.0;
+    }
+}
+
+template <int VM>
+__global__ void __launch_bounds__(256) k_proj_wide(WideArgs a)
+{
+    __shared__ double red[8 * 2];
+    const DevState *st = a.state;
+    if (st && st->stop) return;
+    const int64_t it = st ? st->it : 0;
+    const int N = a.N;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int kl = blockIdx.x * 8 + warp;
+    const bool act = kl < a.Ml;
+    if (a.eval_gate && (it % a.kkt_every) != 0) return;
+    const bool fis = a.beta != nullptr && !a.eval;   // FISTA step: X from Y, KKT in the eval pass
+    const double beta = fis ? a.beta[it] : 0.0;
+    const bool do_kkt = a.eval || (!fis && (it % a.kkt_every) == 0);
+    double th[VM], x[VM];
+    double mn = INFINITY, skkt = 0.0, skktp = 0.0;
+    if (act) {
+        const double *tr = a.theta + (int64_t)kl * N, *gr = a.G + (int64_t)kl * N;
+#pragma unroll
+        for (int v = 0; v < VM; v++) {
+            const int n = lane + 32 * v;
+            th[v] = n < N ? tr[n] : 0.0;
+            x[v] = n < N ? gr[n] : INFINITY;   // G for now
+            mn = fmin(mn, x[v]);
+        }
+    }
+    mn = 2.0 * wmin(mn);
+    const double lam = -mn, lamp = fmax(lam, 0.0);
+    const double tk = act ? a.tstep[kl] : 0.0;
+    double s = 0.0, xm = -INFINITY, xn = INFINITY;
+#pragma unroll
+    for (int v = 0; v < VM; v++) {
+        const bool ok = act && lane + 32 * v < N;
+        const double g = x[v];
+        if (ok && do_kkt) {
+            const double x1 = th[v] * fma(2.0, g, lam);
+            skkt = fma(x1, x1, skkt);
+            if (a.eval) {
+                const double x2 = th[v] * fma(2.0, g, lamp);
+                skktp = fma(x2, x2, skktp);
+            }
+        }
+        double yv = th[v];
+        if (fis && ok) yv = fma(beta, yv - a.theta_prev[(int64_t)kl * N + lane + 32 * v], yv);
+        const double xv = fma(-tk, g, yv);
+        x[v] = ok ? xv : -INFINITY;
+        if (ok) {
+            s += xv;
+            xm = fmax(xm, xv);
+            xn = fmin(xn, xv);
+        }
+    }
+    if (!a.eval) {
+        s = wsum(s);
+        xm = wmax(xm);
+        xn = wmin(xn);
+        double tau = (s - 1.0) / (double)N;
+        bool done = !act || xn > tau;
+        if (!done) tau = fmax(tau, xm - 1.0);
+        int cnt = N + 1;
+        for (int round = 0; round <= N && !done; round++) {   // warp-uniform: one row per warp
+            double ps = 0.0, mA = INFINITY;
+            int pc = 0;
+#pragma unroll
+            for (int v = 0; v < VM; v++)
+                if (x[v] > tau) {
+                    ps += x[v];
+                    pc++;
+                    mA = fmin(mA, x[v]);
+                }
+            ps = wsum(ps);
+            pc = wsum_i(pc);
+            mA = wmin(mA);
+            if (pc >= cnt) {
+                done = true;
+            } else {
+                cnt = pc;
+                tau = (ps - 1.0) / (double)pc;
+                done = mA > tau;
+            }
+        }
+        if (act) {
+            double *o = a.out + (int64_t)kl * N;
+#pragma unroll
+            for (int v = 0; v < VM; v++) {
+                const int n = lane + 32 * v;
+                if (n < N) {
+                    const double ov = x[v] - tau;
+                    o[n] = ov > 0.0 ? ov : 0.0;
+                }
+            }
+        }
+    }
+    skkt = wsum(skkt);
+    skktp = wsum(skktp);
+    if (lane == 0) {
+        red[warp * 2] = skkt;
+        red[warp * 2 + 1] = skktp;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double k0 = 0.0, k1 = 0.0;
+        for (int w = 0; w < 8; w++) {
+            k0 += red[w * 2];
+            k1 += red[w * 2 + 1];
+        }
+        double *pp = a.part + (a.part_b + (int64_t)blockIdx.x) * NSC_TILE;
+        if (do_kkt) {   // a FISTA step leaves the evaluation pass's KKT in place
+            pp[SC_KKT] = k0;
+            pp[SC_KKTP] = k1;
+        }
+        pp[SC_REG] = 0.0;
+        pp[SC_DTH] = 0.0;
+    }
+}
+
+cudaError_t launch_grad_wide(const WideArgs &a_in, int nunits, cudaStream_t s)
+{
+    if (nunits <= 0) return cudaSuccess;
+    WideArgs a = a_in;
+    a.ncc = (a.N + 127) / 128;
+    k_grad_wide<<<nunits * a.ncc, 256, wide_grad_smem(), s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_proj_wide(const WideArgs &a, cudaStream_t s)
+{
+    const int grid = (a.Ml + 7) / 8;
+    const int vm = (a.N + 31) / 32;
+    if (vm <= 8) k_proj_wide<8><<<grid, 256, 0, s>>>(a);
+    else if (vm <= 16) k_proj_wide<16><<<grid, 256, 0, s>>>(a);
+    else if (vm <= 24) k_proj_wide<24><<<grid, 256, 0, s>>>(a);
+    else if (vm <= 32) k_proj_wide<32><<<grid, 256, 0, s>>>(a);
+    else return cudaErrorInvalidValue;
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------------------ reduce R
 // Warp per probe: R[d,:] = sum_j rpart[rows_j] (list order = ascending Fock) - P[d,:]; the
 // block's ||R||^2 partial (warp order) goes to partR[blockIdx.x].
@@ -1385,6 +1691,8 @@ static cudaError_t prep_nb()
     cudaError_t e = cudaFuncSetAttribute(k_bwd_mma<NB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_bwd_mma<NB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    if (e == cudaSuccess && NB == 16)
+        e = cudaFuncSetAttribute(k_grad_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_bwd_split<NB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     if (e == cudaSuccess)
@@ -1475,10 +1783,13 @@ cudaError_t launch_bwd_split(const SweepArgs &a_in, int nunits, int NB, cudaStre
     return cudaGetLastError();
 }
 
-cudaError_t launch_fwd_mma(const SweepFwdArgs &a, int nunits, int NB, cudaStream_t s)
+cudaError_t launch_fwd_mma(const SweepFwdArgs &a_in, int nunits, int NB, cudaStream_t s)
 {
     if (nunits <= 0) return cudaSuccess;
+    SweepFwdArgs a = a_in;
+    a.ncc = (a.N + 8 * NB - 1) / (8 * NB);
     const size_t smem = sweep_fwd_smem(a.N, NB);
+    nunits *= a.ncc;
     switch (NB) {
 #define QDT_CASE(nb) \
     case nb: k_fwd_mma<nb><<<nunits, 256, smem, s>>>(a); break;

@@ -338,3 +338,25 @@ def test_stress_cut_solve_parity(q, ctx):
     assert _trace_ok(rg["trace"], ro["trace"], I.P)
     Th = rg["theta"]
     assert Th.min() >= 0 and np.abs(Th.sum(1) - 1).max() <= 4 * Th.shape[1] * EPS
+
+
+@pytest.mark.parametrize("N,accel", [(200, 0), (1000, 0), (151, 0), (250, 1)])
+def test_wide_sweep_parity(q, ctx, N, accel):
+    """N > 128: even N runs the wide sweep (128-column DMMA gradient chunks + warp-per-row
+    projection + column-chunked forward); odd N (151, the paper's outcome count) and FISTA the
+    general kernels.  25 iterations against the oracle."""
+    rng = np.random.default_rng(N)
+    D, M = 300, 6000
+    a2 = np.geomspace(0.5, 0.9 * M, D)
+    P = rng.dirichlet(np.ones(N) * 0.2, D)
+    gamma = 1e-3
+    Fo = oracle.Probes(a2, M)
+    Fg = q.qdt_build_probes(ctx, a2, M)
+    ro = oracle.solve(Fo, P, gamma, 0.0, 25, accel=accel, kkt_every=5 if accel else 1)
+    rg = q.qdt_solve(ctx, Fg, P, gamma, 0.0, 25, accel=bool(accel), kkt_every=5 if accel else 1)
+    assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9
+    assert _trace_ok(rg["trace"], ro["trace"], P)
+    m = ~np.isnan(ro["kkt"])
+    np.testing.assert_allclose(rg["kkt"][m], ro["kkt"][m], rtol=1e-8, atol=1e-15)
+    f, r = q.qdt_objective(ctx, Fg, P, rg["theta"], gamma)
+    assert f == pytest.approx(oracle.objective(Fo, P, rg["theta"], gamma), rel=1e-12)
