@@ -489,6 +489,50 @@ static bool sweep_enabled()
     return !(e && e[0] == '0');
 }
 
+// Forward units over tiles [t0, t1), emitted in ascending Fock order (so that every probe's
+// partial rows are listed in ascending Fock order):
+//  - narrow windows: runs of consecutive tiles whose union window is <= FWCAP probes (<= FW_MAXT
+//    tiles): one partial row per (run, probe);
+//  - runs of wide windows (> FWCAP probes, low Fock rows / wide N): probe-major, groups of FWCAP
+//    consecutive probes over the tiles their bands touch (<= FW_MAXT tiles per unit), so that a
+//    probe gets one partial row per group unit instead of one per tile.
+template <class Emit>
+static void plan_fwd_units(const qdt_probes *p, int t0, int t1, Emit &&emit)
+{
+    const std::vector<int32_t> &dA = p->sw_dA, &dB = p->sw_dB;
+    int t = t0;
+    while (t < t1) {
+        if (dB[t] <= dA[t]) {
+            t++;
+            continue;
+        }
+        if (dB[t] - dA[t] <= FWCAP) {
+            const int g0 = t, u0 = dA[t];
+            int u1 = dB[t];
+            t++;
+            while (t < t1 && dB[t] > dA[t] && dB[t] - dA[t] <= FWCAP && std::max(u1, (int)dB[t]) - u0 <= FWCAP &&
+                   t - g0 < FW_MAXT) {
+                u1 = std::max(u1, (int)dB[t]);
+                t++;
+            }
+            emit(g0, t, u0, u1);
+            continue;
+        }
+        const int r0 = t;
+        while (t < t1 && dB[t] - dA[t] > FWCAP) t++;
+        const int r1 = t;                       // wide run [r0, r1)
+        const int P0 = dA[r0], P1 = dB[r1 - 1];
+        int ta = r0;
+        for (int g0 = P0; g0 < P1; g0 += FWCAP) {
+            const int g1 = std::min(P1, g0 + FWCAP);
+            while (ta < r1 && dB[ta] <= g0) ta++;          // first tile meeting the group
+            int tb = ta;
+            while (tb < r1 && dA[tb] < g1) tb++;           // one past the last
+            for (int c0 = ta; c0 < tb; c0 += FW_MAXT) emit(c0, std::min(tb, c0 + FW_MAXT), g0, g1);
+        }
+    }
+}
+
 // Fused plan (single GPU): light tiles = the longest suffix of tiles whose window fits the ring
 // (cap probes), split into contiguous ranges, one persistent CTA each; the heavy prefix keeps
 // the unfused k_bwd_mma / k_fwd_mma units.  Partial rows: heavy fwd units first, then one row per
@@ -538,26 +582,7 @@ static qdt_status build_fused_plan(qdt_ctx *ctx, qdt_probes *p, Plan *pl, const 
         for (int d = u0; d < u1; d++) lists[d].push_back(poff + (d - u0));
         poff += u1 - u0;
     };
-    int g0 = -1, gu0 = 0, gu1 = 0;
-    for (int t = 0; t < ts; t++) {
-        const int dA = p->sw_dA[t], dB = p->sw_dB[t];
-        const bool empty = dB <= dA;
-        if (g0 >= 0 && !empty && std::max(gu1, dB) - gu0 <= FWCAP && t - g0 < FW_MAXT) {
-            gu1 = std::max(gu1, dB);
-            continue;
-        }
-        if (g0 >= 0) emit(g0, t, gu0, gu1);
-        g0 = -1;
-        if (empty) continue;
-        if (dB - dA > FWCAP) {
-            for (int a0 = dA; a0 < dB; a0 += FWCAP) emit(t, t + 1, a0, std::min(dB, a0 + FWCAP));
-            continue;
-        }
-        g0 = t;
-        gu0 = dA;
-        gu1 = dB;
-    }
-    if (g0 >= 0) emit(g0, ts, gu0, gu1);
+    plan_fwd_units(p, 0, ts, emit);
     std::vector<int64_t> cpoff(G);
     for (int c = 0; c < G; c++) {
         const int ta = range[2 * c], tb = range[2 * c + 1];
@@ -651,27 +676,7 @@ static qdt_status build_sweep_plan(qdt_ctx *ctx, qdt_probes *p, Plan *pl)
         for (int d = u0; d < u1; d++) lists[d].push_back(poff + (d - u0));
         poff += u1 - u0;
     };
-    int g0 = -1, gu0 = 0, gu1 = 0;
-    const int tend = nt;
-    for (int t = 0; t < tend; t++) {
-        const int dA = p->sw_dA[t], dB = p->sw_dB[t];
-        const bool empty = dB <= dA;
-        if (g0 >= 0 && !empty && std::max(gu1, dB) - gu0 <= FWCAP && t - g0 < FW_MAXT) {
-            gu1 = std::max(gu1, dB);
-            continue;
-        }
-        if (g0 >= 0) emit(g0, t, gu0, gu1);
-        g0 = -1;
-        if (empty) continue;
-        if (dB - dA > FWCAP) {
-            for (int a0 = dA; a0 < dB; a0 += FWCAP) emit(t, t + 1, a0, std::min(dB, a0 + FWCAP));
-            continue;
-        }
-        g0 = t;
-        gu0 = dA;
-        gu1 = dB;
-    }
-    if (g0 >= 0) emit(g0, tend, gu0, gu1);
+    plan_fwd_units(p, 0, nt, emit);
     pl->sw_nrpart = poff;
     std::vector<int64_t> red_beg(D + 1, 0), red_rows;
     for (int64_t d = 0; d < D; d++) red_beg[d + 1] = red_beg[d] + (int64_t)lists[d].size();
