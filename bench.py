@@ -401,7 +401,7 @@ def run_reference(args):
     v, dt, r = _oracle_sample_run(I, args.steps, args.warmup, rows)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (qdt_synth, seed 0)",
             "config": {"workload": args.config, "M": I.M, "N": I.N, "D": I.D, "gamma": I.gamma,
                        "step_mode": "SQS", "parallelism": "single-thread oracle"},
