@@ -201,15 +201,22 @@ __device__ __forceinline__ void pair_xchg(PairX &px, const double (&v)[K], doubl
 // NBA / CB (N-split kernel): the thread holds NBA column blocks starting at global block CB / 8;
 // global blocks >= NB are padding.  PAIR: the row is shared with the partner warp holding the
 // other column half; every row reduction is completed through PairX (fixed combination order).
+struct NoMid {
+    __device__ void operator()() const {}
+};
+// STASH: the row's own Theta values are kept in registers from pass 1, so that shared memory is
+// not read after pass 1 and mid() (called between the passes by every thread) may release the
+// tile (the persistent kernel issues the next unit's tile load there).
 template <int NB, bool FULL, bool EVEN, bool SMEM_OUT, bool FIS = false, int NBA = NB, int CB = 0,
-          bool PAIR = false>
+          bool PAIR = false, bool STASH = false, class Mid = NoMid>
 __device__ __forceinline__ void row_pass(double (&acc)[NBA][2], const double *thr, int N, int t4,
                                          bool act, bool has_prev, bool has_next, double gamma,
                                          double tk, bool do_kkt, bool want_kktp, double &sreg,
                                          double &skkt, double &skktp, double &s, double &xm,
                                          double &xn, const double *tpr = nullptr, double beta = 0.0,
-                                         PairX *px = nullptr)
+                                         PairX *px = nullptr, Mid mid = Mid())
 {
+    double keep[STASH ? NBA : 1][2];
     const int cl = 8 * (NB - 1) + 2 * t4;
     const bool v0 = cl < N, v1 = cl + 1 < N;
     const bool hp = FULL || has_prev, hn = FULL || has_next;
@@ -263,8 +270,10 @@ __device__ __forceinline__ void row_pass(double (&acc)[NBA][2], const double *th
                 mn = g < mn ? g : mn;
             }
             acc[nb][i] = g;
+            if (STASH) keep[STASH ? nb : 0][i] = a0;
         }
     }
+    mid();
     if (SMEM_OUT) __syncthreads();  // neighbour rows read: each row may now be overwritten by its owner
     double lam = 0.0, lamp = 0.0;
     if (do_kkt) {
@@ -283,7 +292,9 @@ __device__ __forceinline__ void row_pass(double (&acc)[NBA][2], const double *th
     for (int nb = 0; nb < NBA; nb++) {
         const int c = CB + 8 * nb + 2 * t4;
         double t0[2];
-        if (EVEN) {
+        if (STASH) {
+            t0[0] = keep[STASH ? nb : 0][0], t0[1] = keep[STASH ? nb : 0][1];
+        } else if (EVEN) {
             const double2 x = *reinterpret_cast<const double2 *>(thr + c);
             t0[0] = x.x, t0[1] = x.y;
         } else {
@@ -650,7 +661,19 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(Swe
             const bool ev = a.eval != 0;   // evaluation pass: KKT (both multipliers) + regulariser only
             const bool fast = full && even;
             const double *tpr = Tq + th_sh + (r + 1) * N;
-            if (fast)
+            // interior even-N tiles of plain steps: the own-row values stay in registers, the tile
+            // is released after pass 1 and the next unit's tile load overlaps pass 2 + Michelot
+            const bool stash = fast && !FIS && !ev;
+            auto release = [&]() {
+                __syncthreads();
+                if (tid == 0 && next < a.nunits && un.nsplit == 1) issue_theta(un);
+            };
+            if (stash)
+                row_pass<NB, true, true, false, false, NB, 0, false, true>(acc, thr, N, t4, act, has_prev, has_next,
+                                                                         a.gamma, tk, do_kkt, ev, sreg, skkt,
+                                                                         skktp, s, xm, xn, tpr, beta, nullptr,
+                                                                         release);
+            else if (fast)
                 row_pass<NB, true, true, false, FIS>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk,
                                                      do_kkt, ev, sreg, skkt, skktp, s, xm, xn, tpr, beta);
             else if (full)
@@ -659,8 +682,7 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(Swe
             else
                 row_pass<NB, false, false, false, FIS>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk,
                                                        do_kkt, ev, sreg, skkt, skktp, s, xm, xn, tpr, beta);
-            __syncthreads();  // Theta tile consumed: start the next unit's tile load
-            if (tid == 0 && next < a.nunits && un.nsplit == 1) issue_theta(un);
+            if (!stash) release();   // Theta tile consumed: start the next unit's tile load
             if (ev) {
             } else if (fast)
                 row_project<NB, true, true, false>(acc, thr, N, t4, act, s, xm, xn, orow);
