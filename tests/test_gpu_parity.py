@@ -360,3 +360,24 @@ def test_wide_sweep_parity(q, ctx, N, accel):
     np.testing.assert_allclose(rg["kkt"][m], ro["kkt"][m], rtol=1e-8, atol=1e-15)
     f, r = q.qdt_objective(ctx, Fg, P, rg["theta"], gamma)
     assert f == pytest.approx(oracle.objective(Fo, P, rg["theta"], gamma), rel=1e-12)
+
+
+@pytest.mark.parametrize("D,M,N", [(1, 1, 1), (1, 5, 128), (7, 40, 129), (9, 50, 130), (5, 300, 16),
+                                   (40, 64, 8), (40, 65, 8), (12, 130, 1)])
+def test_shape_edges(q, ctx, D, M, N):
+    """Boundary shapes: single probe / Fock row / outcome, the sweep's N limit (128 | 129 odd ->
+    general kernels | 130 even -> wide sweep), tile-multiple and tile-plus-one M, N = 1; probe means
+    beyond the cutoff (bands clipped to the last row) and repeated means."""
+    rng = np.random.default_rng(D * 1000 + M * 10 + N)
+    a2 = np.sort(np.concatenate([rng.uniform(0, 1.5 * M, D - D // 3), np.full(D // 3, 0.5 * M)]))
+    P = rng.dirichlet(np.ones(N), D) if N > 1 else np.ones((D, 1))
+    gamma = 1e-2
+    Fo = oracle.Probes(a2, M)
+    Fg = q.qdt_build_probes(ctx, a2, M)
+    for accel in (0, 1):
+        ro = oracle.solve(Fo, P, gamma, 0.0, 12, accel=accel)
+        rg = q.qdt_solve(ctx, Fg, P, gamma, 0.0, 12, accel=bool(accel))
+        assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9, accel
+        assert _trace_ok(rg["trace"], ro["trace"], P)
+        Th = rg["theta"]
+        assert Th.min() >= 0 and np.abs(Th.sum(1) - 1).max() <= 4 * max(N, 2) * EPS
