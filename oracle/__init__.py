@@ -81,6 +81,8 @@ def lib():
                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                                ctypes.POINTER(f64)]
         L.or_solve.restype = i64
+        L.or_smooth.argtypes = [_f64p, i64, i64, i64, i64, _f64p]
+        L.or_smooth.restype = None
         _lib = L
     return _lib
 
@@ -224,3 +226,11 @@ def solve(F: Probes, P, gamma: float, tol: float, iters: int, step: int = STEP_S
                           ctypes.byref(st))
     return dict(theta=Theta, trace=trace[:done + 1], kkt=kt[:done + 1], kkt_paper=kp[:done + 1],
                 iters_done=int(done), step=st.value)
+
+
+def smooth(Theta, exclude: int = 100, div: int = 50):
+    """Long-range smoothing of PAPER.md:307-314 (reading R13)."""
+    Theta = _f(Theta)
+    out = np.empty_like(Theta)
+    lib().or_smooth(Theta, Theta.shape[0], Theta.shape[1], int(exclude), int(div), out)
+    return out

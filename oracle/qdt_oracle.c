@@ -422,3 +422,29 @@ int64_t or_solve(const int64_t *lo, const int64_t *len, const int64_t *off, cons
     free(t);
     return k;
 }
+
+/* ------------------------------------------------------------------------------------
+ * Long-range smoothing (eq. smoothing):
+ *   Pi~_{i,n} = 1/(2 Ns(i) + 1) sum_{j = i - Ns(i)}^{i + Ns(i)} Pi_{j,n},   Ns(i) = floor(i / div)
+ * (the paper's N_smooth = i/50), rows i < exclude unchanged (the lowest ~100 photon numbers are
+ * excluded).  DESIGN.md reading R13: the window is clipped to the rows that exist,
+ * [max(0, i - Ns), min(M - 1, i + Ns)], and the average is over the rows in it, so every smoothed
+ * row is a convex combination of rows of Pi.
+ * ---------------------------------------------------------------------------------- */
+void or_smooth(const double *Theta, int64_t M, int64_t N, int64_t exclude, int64_t div, double *out)
+{
+    for (int64_t i = 0; i < M; i++) {
+        if (i < exclude || div <= 0) {
+            for (int64_t n = 0; n < N; n++) out[i * N + n] = Theta[i * N + n];
+            continue;
+        }
+        int64_t ns = i / div;
+        int64_t lo = i - ns < 0 ? 0 : i - ns;
+        int64_t hi = i + ns > M - 1 ? M - 1 : i + ns;
+        for (int64_t n = 0; n < N; n++) {
+            double s = 0.0;
+            for (int64_t j = lo; j <= hi; j++) s += Theta[j * N + n];
+            out[i * N + n] = s / (double)(hi - lo + 1);
+        }
+    }
+}

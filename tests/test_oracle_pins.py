@@ -423,3 +423,31 @@ def test_objective_sum_accuracy_many_terms():
     R = F.dense() @ Th - P
     ref = math.fsum((R * R).ravel())
     assert oracle.objective(F, P, Th, 0.0) == pytest.approx(ref, rel=1e-14)
+
+
+# ----------------------------------------------------------------------------- smoothing (f4)
+def test_smoothing_pins():
+    """eq. smoothing, reading R13: closed forms and invariants."""
+    rng = np.random.default_rng(8)
+    M, N = 400, 5
+    Th = oracle.project_rows(rng.normal(0.2, 0.3, (M, N)))
+    S = oracle.smooth(Th, exclude=100, div=50)
+    # rows below the exclusion are untouched; every row stays on the simplex (convex combination)
+    np.testing.assert_array_equal(S[:100], Th[:100])
+    assert S.min() >= 0 and np.abs(S.sum(1) - 1).max() <= 1e-13
+    # brute force of the definition with numpy (window [i - i//50, i + i//50] clipped to [0, M))
+    for i in [100, 149, 150, 250, 399]:
+        ns = i // 50
+        lo, hi = max(0, i - ns), min(M - 1, i + ns)
+        np.testing.assert_allclose(S[i], Th[lo:hi + 1].mean(0), rtol=1e-14, atol=1e-16)
+    # i = 150: Ns = 3, window rows 147..153 (7 rows, the paper's 2 Ns + 1)
+    np.testing.assert_allclose(S[150], Th[147:154].sum(0) / 7, rtol=1e-14)
+    # a column that is linear in i is reproduced where the window is symmetric (no clipping)
+    L = np.tile(np.arange(M, dtype=float)[:, None], (1, 2))
+    SL = oracle.smooth(L, exclude=0, div=50)
+    interior = [i for i in range(M) if i + i // 50 <= M - 1]
+    np.testing.assert_allclose(SL[interior], L[interior], rtol=1e-14)
+    # constant columns are fixed points; div <= 0 disables the smoothing
+    C = np.full((M, 3), 1.0 / 3)
+    np.testing.assert_allclose(oracle.smooth(C), C, rtol=1e-15)
+    np.testing.assert_array_equal(oracle.smooth(Th, div=0), Th)
