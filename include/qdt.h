@@ -154,6 +154,18 @@ qdt_status qdt_objective(qdt_ctx *ctx, const qdt_probes *F, const double *P, con
                          int64_t N, double gamma, int32_t mem_device, double *f_out,
                          double *kkt_out);
 
+/* Long-range smoothing (eq. smoothing; reading R13):
+ *   out_{i,n} = mean of theta_{j,n} over j in [i - Ns(i), i + Ns(i)] clipped to [0, M - 1],
+ *   Ns(i) = floor(i / div) (the paper's N_smooth = i/50: div = 50), rows i < exclude copied (the
+ *   paper excludes the lowest ~100 photon numbers: exclude = 100); div <= 0 copies everything.
+ * theta, out: M x N row-major, HOST pointers unless mem_device (then device pointers on ctx's
+ * device, ordered on ctx's stream; out may not alias theta).  Every output row is a convex
+ * combination of input rows (stays on the simplex).  The smoothed matrix is the warm start of a
+ * second solve (opts->theta0).  Single rank only (nranks > 1 -> QDT_ERR_INVALID_ARG).
+ * Errors: M, N < 1, exclude < 0, NULL pointers -> INVALID_ARG; non-finite host theta -> NONFINITE. */
+qdt_status qdt_smooth(qdt_ctx *ctx, const double *theta, int64_t M, int64_t N, int64_t exclude,
+                      int64_t div, int32_t mem_device, double *out);
+
 /* ------------------------------------------------------------------------------ kernel hooks
  * The individual steps of one iteration, for per-kernel parity tests.  They run the same
  * kernels as qdt_solve.  All arrays are HOST pointers, full (global) sizes, nranks == 1. */

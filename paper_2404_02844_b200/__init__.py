@@ -29,7 +29,8 @@ STATUS = {0: "QDT_OK", 1: "QDT_ERR_INVALID_ARG", 2: "QDT_ERR_UNSORTED", 3: "QDT_
 ABI_SYMBOLS = ["qdt_init", "qdt_finalize", "qdt_last_error", "qdt_build_probes", "qdt_probes_free",
                "qdt_probes_export", "qdt_solve", "qdt_objective", "qdt_residual", "qdt_gradient",
                "qdt_step", "qdt_project_rows", "qdt_step_setup", "qdt_profile_enable",
-               "qdt_profile_get", "qdt_launch_count", "qdt_nccl_unique_id", "qdt_shard_cuts"]
+               "qdt_profile_get", "qdt_launch_count", "qdt_nccl_unique_id", "qdt_shard_cuts",
+               "qdt_smooth"]
 
 
 class QdtError(RuntimeError):
@@ -99,6 +100,7 @@ def load_library(path: str = LIB_PATH):
     L.qdt_launch_count.argtypes = [vp, P(i64)]
     L.qdt_nccl_unique_id.argtypes = [vp]
     L.qdt_shard_cuts.argtypes = [vp, vp, i64, i64, i32, vp]
+    L.qdt_smooth.argtypes = [vp, vp, i64, i64, i64, i64, i32, vp]
     for s in ABI_SYMBOLS:
         if s != "qdt_last_error":
             getattr(L, s).restype = ctypes.c_int
@@ -315,3 +317,20 @@ def qdt_shard_cuts(lo, hi, M: int, nranks: int):
     if st != 0:
         raise QdtError(st, (load_library().qdt_last_error(None) or b"").decode())
     return cuts
+
+
+def qdt_smooth(ctx: Context, theta, exclude: int = 100, div: int = 50, out=None):
+    """Long-range smoothing: numpy in -> numpy out, CUDA tensor -> tensor."""
+    L = load_library()
+    if _is_cuda_tensor(theta):
+        import torch
+        th = theta.contiguous()
+        out = torch.empty_like(th) if out is None else out
+        _check(ctx, L.qdt_smooth(ctx.ptr, th.data_ptr(), th.shape[0], th.shape[1], int(exclude),
+                                 int(div), 1, out.data_ptr()))
+        return out
+    th = _host(theta)
+    out = np.empty_like(th) if out is None else out
+    _check(ctx, L.qdt_smooth(ctx.ptr, th.ctypes.data, th.shape[0], th.shape[1], int(exclude),
+                             int(div), 0, out.ctypes.data))
+    return out

@@ -1912,3 +1912,35 @@ extern "C" qdt_status qdt_project_rows(qdt_ctx *ctx, const double *X, int64_t M,
     CK(cudaStreamSynchronize(s));
     return QDT_OK;
 }
+
+// ------------------------------------------------------------------------------ smoothing
+extern "C" qdt_status qdt_smooth(qdt_ctx *ctx, const double *theta, int64_t M, int64_t N, int64_t exclude,
+                                 int64_t div, int32_t mem_device, double *out)
+{
+    if (!ctx) return fail(nullptr, QDT_ERR_INVALID_ARG, "qdt_smooth: ctx is NULL");
+    if (!theta || !out) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_smooth: NULL pointer");
+    if (M < 1 || N < 1 || N > INT32_MAX || exclude < 0)
+        return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_smooth: bad shape / exclude");
+    if (ctx->nranks != 1) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_smooth: single rank only");
+    const bool dev = mem_device != 0;
+    if (!dev) CKS(check_finite_host(ctx, theta, M * N, "theta"));
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    const int64_t nch = (M + 255) / 256;
+    double *X, *Y, *S, *T, *Tx;
+    CKS(ws_get(ctx, "sm_S", M * N, &S));
+    CKS(ws_get(ctx, "sm_T", nch * N, &T));
+    CKS(ws_get(ctx, "sm_Tx", (nch + 1) * N, &Tx));
+    if (dev) {
+        X = const_cast<double *>(theta);
+        Y = out;
+    } else {
+        CKS(ws_get(ctx, "sm_X", M * N, &X));
+        CKS(ws_get(ctx, "sm_Y", M * N, &Y));
+        CK(cudaMemcpyAsync(X, theta, sizeof(double) * M * N, cudaMemcpyHostToDevice, s));
+    }
+    CK(run_k(ctx, "smooth", 3, [&]() { return launch_smooth(X, M, (int)N, exclude, div, S, T, Tx, Y, s); }));
+    if (!dev) CK(cudaMemcpyAsync(out, Y, sizeof(double) * M * N, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return QDT_OK;
+}

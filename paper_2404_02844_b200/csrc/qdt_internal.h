@@ -187,6 +187,8 @@ constexpr int SW_FUSED_SMEM_MAX = 220 * 1024;
 size_t sweep_fused_smem(int N, int NB, int cap);
 cudaError_t launch_sweep_fused(const SweepFusedArgs &a, int nctas, int NB, cudaStream_t s);
 cudaError_t prepare_sweep_kernels();
+cudaError_t launch_smooth(const double *X, int64_t M, int N, int64_t exclude, int64_t div, double *S,
+                          double *T, double *Tx, double *Y, cudaStream_t s);
 cudaError_t launch_sqs_weights_tiled(int ntiles, int Ml, const int32_t *tile_dA,
                                      const int32_t *tile_dB, const int64_t *fb_off, const double *Fb,
                                      const double *s, double gamma, double *w, double *tstep,

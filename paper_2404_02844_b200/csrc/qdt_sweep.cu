@@ -1576,6 +1576,66 @@ cudaError_t launch_proj_wide(const WideArgs &a, cudaStream_t s)
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------------------ smoothing
+// Long-range smoothing (eq. smoothing; reading R13) by column prefix sums:
+// S(k) = sum_{j < k} Theta_j (per column), Theta~_i = (S(hi + 1) - S(lo)) / (hi - lo + 1) with
+// [lo, hi] = [i - Ns, i + Ns] clipped to [0, M - 1], Ns = floor(i / div); rows i < exclude copied.
+// Three kernels: chunk-local exclusive scans (SMC rows per chunk, thread per column), a scan of
+// the chunk totals (thread per column), the apply pass (thread per element).
+constexpr int SMC = 256;
+__global__ void k_scan_local(const double *X, int64_t M, int N, double *S, double *T)
+{
+    const int64_t c = blockIdx.x;
+    const int64_t r0 = c * SMC, r1 = min(M, r0 + SMC);
+    for (int n = threadIdx.x; n < N; n += blockDim.x) {
+        double run = 0.0;
+        for (int64_t r = r0; r < r1; r++) {
+            S[r * N + n] = run;
+            run += X[r * N + n];
+        }
+        T[c * N + n] = run;
+    }
+}
+__global__ void k_scan_chunks(const double *T, int64_t nch, int N, double *Tx)
+{
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    double run = 0.0;
+    for (int64_t c = 0; c < nch; c++) {
+        Tx[c * N + n] = run;
+        run += T[c * N + n];
+    }
+    Tx[nch * N + n] = run;
+}
+__global__ void k_smooth_apply(const double *X, const double *S, const double *Tx, int64_t M, int N,
+                               int64_t exclude, int64_t div, double *Y)
+{
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= M * N) return;
+    const int64_t i = e / N;
+    const int n = (int)(e - i * N);
+    if (i < exclude || div <= 0) {
+        Y[e] = X[e];
+        return;
+    }
+    const int64_t ns = i / div;
+    const int64_t lo = i - ns < 0 ? 0 : i - ns, hi = i + ns > M - 1 ? M - 1 : i + ns;
+    auto Sabs = [&](int64_t k) {   // sum of rows [0, k)
+        return k >= M ? Tx[((M + SMC - 1) / SMC) * N + n] : Tx[(k / SMC) * N + n] + S[k * N + n];
+    };
+    Y[e] = (Sabs(hi + 1) - Sabs(lo)) / (double)(hi - lo + 1);
+}
+
+cudaError_t launch_smooth(const double *X, int64_t M, int N, int64_t exclude, int64_t div, double *S,
+                          double *T, double *Tx, double *Y, cudaStream_t s)
+{
+    const int64_t nch = (M + SMC - 1) / SMC;
+    k_scan_local<<<(unsigned)nch, 128, 0, s>>>(X, M, N, S, T);
+    k_scan_chunks<<<(N + 127) / 128, 128, 0, s>>>(T, nch, N, Tx);
+    k_smooth_apply<<<(unsigned)((M * N + 255) / 256), 256, 0, s>>>(X, S, Tx, M, N, exclude, div, Y);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------------------ reduce R
 // Warp per probe: R[d,:] = sum_j rpart[rows_j] (list order = ascending Fock) - P[d,:]; the
 // block's ||R||^2 partial (warp order) goes to partR[blockIdx.x].

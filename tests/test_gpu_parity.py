@@ -381,3 +381,33 @@ def test_shape_edges(q, ctx, D, M, N):
         assert _trace_ok(rg["trace"], ro["trace"], P)
         Th = rg["theta"]
         assert Th.min() >= 0 and np.abs(Th.sum(1) - 1).max() <= 4 * max(N, 2) * EPS
+
+
+@pytest.mark.parametrize("M,N,exclude,div", [(400, 5, 100, 50), (3000, 100, 100, 50), (257, 8, 0, 7),
+                                             (1000, 33, 1001, 50), (50, 4, 10, 0)])
+def test_smoothing_parity(q, ctx, M, N, exclude, div):
+    """Long-range smoothing (reading R13) against the oracle; host and device."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(M + N)
+    Th = oracle.project_rows(rng.normal(0.2, 0.4, (M, N)))
+    ref = oracle.smooth(Th, exclude, div)
+    got = q.qdt_smooth(ctx, Th, exclude, div)
+    assert np.abs(got - ref).max() <= 1e-13
+    gd = q.qdt_smooth(ctx, torch.tensor(Th, device="cuda"), exclude, div)
+    np.testing.assert_array_equal(gd.cpu().numpy(), got)
+
+
+def test_smooth_then_restart_parity(q, ctx):
+    """The paper's refinement: solve, smooth, second solve from the smoothed
+    matrix (warm start through theta0), against the same sequence on the oracle."""
+    I = qs.medium()
+    Fo = oracle.Probes(I.alpha2, I.M)
+    Fg = q.qdt_build_probes(ctx, I.alpha2, I.M)
+    r1o = oracle.solve(Fo, I.P, I.gamma, 0.0, 60, accel=1, kkt_every=10)
+    r1g = q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, 60, accel=True, kkt_every=10)
+    so, sg = oracle.smooth(r1o["theta"]), q.qdt_smooth(ctx, r1g["theta"])
+    assert np.abs(sg - so).max() <= 1e-9
+    r2o = oracle.solve(Fo, I.P, I.gamma, 0.0, 40, theta0=so)
+    r2g = q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, 40, theta0=sg)
+    assert np.abs(r2g["theta"] - r2o["theta"]).max() <= 1e-9
+    assert _trace_ok(r2g["trace"], r2o["trace"], I.P)
