@@ -206,7 +206,7 @@ def power_iteration(F: Probes, k_pow: int = 100) -> float:
     return lib().or_power_iteration(*F._args(), F.M, int(k_pow))
 
 
-STEP_SQS, STEP_LIPSCHITZ = 0, 1
+STEP_SQS, STEP_LIPSCHITZ, STEP_BB = 0, 1, 2
 
 
 def solve(F: Probes, P, gamma: float, tol: float, iters: int, step: int = STEP_SQS,

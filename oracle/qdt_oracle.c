@@ -328,6 +328,11 @@ double or_power_iteration(const int64_t *lo, const int64_t *len, const int64_t *
  *   Theta_0 = 1/N or theta0.
  *   step 0: SQS      t_k = 1/w_k  (0 if w_k == 0: row frozen, reading R9)
  *   step 1: LIPSCHITZ t = 1/(1.01 rho + 4 gamma), rho from 100 power iterations
+ *   step 2: BB       Barzilai-Borwein scalar step (north_star "power-iteration Lipschitz bound
+ *            or Barzilai-Borwein"; reading R14): t_0 = t_LIP; for k >= 1 with s = Theta_k -
+ *            Theta_{k-1}: t_k = <s,s> / <s,Hs>, <s,Hs> = ||R_k - R_{k-1}||^2 + gamma ||D s||^2
+ *            (H = F^T F + gamma L, the Hessian of f/2), clamped to [t_LIP, 1e6 t_LIP];
+ *            t_LIP when <s,Hs> <= 0.  Plain projected gradient only (accel ignored).
  *   accel 1: FISTA extrapolation Y_k = Theta_k + (tau_k - 1)/tau_{k+1} (Theta_k - Theta_{k-1}),
  *            tau_0 = 1, tau_{k+1} = (1 + sqrt(1 + 4 tau_k^2))/2.
  *   iteration k (reading R3):
@@ -353,7 +358,16 @@ int64_t or_solve(const int64_t *lo, const int64_t *len, const int64_t *off, cons
     double *t = (double *)malloc((size_t)M * sizeof(double));
     if (kkt_every < 1) kkt_every = 1;
 
-    if (step_mode == 0) {
+    double t_lip = 0.0;
+    double *Rprev = NULL;
+    if (step_mode == 2) {
+        accel = 0;
+        double rho = or_power_iteration(lo, len, off, val, D, M, 100);
+        t_lip = 1.0 / (1.01 * rho + 4.0 * gamma);
+        for (int64_t k = 0; k < M; k++) t[k] = t_lip;
+        if (step_out) *step_out = t_lip;
+        Rprev = (double *)malloc((size_t)(D * N) * sizeof(double));
+    } else if (step_mode == 0) {
         or_sqs_weights(lo, len, off, val, D, M, gamma, t);
         for (int64_t k = 0; k < M; k++) t[k] = (t[k] > 0.0) ? 1.0 / t[k] : 0.0;
         if (step_out) *step_out = 0.0;
@@ -377,6 +391,33 @@ int64_t or_solve(const int64_t *lo, const int64_t *len, const int64_t *off, cons
         for (size_t i = 0; i < MN; i++) Y[i] = Theta[i] + beta * (Theta[i] - Tprev[i]);
         /* gradient at Y */
         or_forward(lo, len, off, val, D, Y, P, N, R);
+        if (step_mode == 2 && k >= 1) {
+            /* BB: s = Theta_k - Theta_{k-1} (Tprev), <s,Hs> = ||R_k - R_{k-1}||^2 + gamma ||D s||^2 */
+            long double ss = 0.0L, sh = 0.0L, sd = 0.0L;
+            for (size_t i = 0; i < MN; i++) {
+                double d = Theta[i] - Tprev[i];
+                ss += (long double)(d * d);
+            }
+            for (int64_t i = 0; i < D * N; i++) {
+                double d = R[i] - Rprev[i];
+                sh += (long double)(d * d);
+            }
+            for (int64_t r = 0; r + 1 < M; r++)
+                for (int64_t n = 0; n < N; n++) {
+                    double a = Theta[r * N + n] - Tprev[r * N + n];
+                    double b = Theta[(r + 1) * N + n] - Tprev[(r + 1) * N + n];
+                    sd += (long double)((a - b) * (a - b));
+                }
+            double shs = (double)sh + gamma * (double)sd;
+            double tb = t_lip;
+            if (shs > 0.0) {
+                tb = (double)ss / shs;
+                if (tb < t_lip) tb = t_lip;
+                if (tb > 1e6 * t_lip) tb = 1e6 * t_lip;
+            }
+            for (int64_t r = 0; r < M; r++) t[r] = tb;
+        }
+        if (step_mode == 2) memcpy(Rprev, R, (size_t)(D * N) * sizeof(double));
         or_backward(lo, len, off, val, D, M, R, Y, N, gamma, G);
         /* f(Theta_k) and r(Theta_k) */
         double fk, rk = NAN, rpk = NAN;
@@ -420,6 +461,7 @@ int64_t or_solve(const int64_t *lo, const int64_t *len, const int64_t *off, cons
     free(Gk);
     free(R);
     free(t);
+    free(Rprev);
     return k;
 }
 

@@ -451,3 +451,43 @@ def test_smoothing_pins():
     C = np.full((M, 3), 1.0 / 3)
     np.testing.assert_allclose(oracle.smooth(C), C, rtol=1e-15)
     np.testing.assert_array_equal(oracle.smooth(Th, div=0), Th)
+
+
+# ----------------------------------------------------------------------------- BB step (R14)
+@pytest.mark.parametrize("gamma", [1e-3, 1e-2])
+def test_bb_reaches_exact_qp_optimum(gamma):
+    """Barzilai-Borwein scalar step (reading R14) converges to the brute-force QP optimum (P11)."""
+    rng = np.random.default_rng(300)
+    M, N, D = 4, 3, 8
+    F = oracle.Probes(np.sort(rng.uniform(0.3, 3.0, D)), M)
+    P = rng.dirichlet(np.ones(N), size=D)
+    sols = _brute_qp(F.dense(), P, gamma)
+    assert len(sols) == 1
+    r = oracle.solve(F, P, gamma, 0.0, 3000, step=oracle.STEP_BB)
+    np.testing.assert_allclose(r["theta"], sols[0][0], atol=1e-12)
+    # the first step is the Lipschitz step, so iteration 1 matches LIPSCHITZ exactly
+    r1 = oracle.solve(F, P, gamma, 0.0, 1, step=oracle.STEP_BB)
+    l1 = oracle.solve(F, P, gamma, 0.0, 1, step=oracle.STEP_LIPSCHITZ)
+    np.testing.assert_array_equal(r1["theta"], l1["theta"])
+
+
+def test_bb_step_formula():
+    """Iteration 2 of BB uses t = <s,s>/(||F s||^2 + gamma ||D s||^2), s = Theta_1 - Theta_0:
+    reproduce it with dense numpy from the oracle's own iterates."""
+    rng = np.random.default_rng(301)
+    F = oracle.Probes(np.sort(rng.uniform(0.2, 6.0, 10)), 7)
+    P = rng.dirichlet(np.ones(4), 10)
+    g = 0.05
+    th0 = np.full((7, 4), 0.25)
+    th1 = oracle.solve(F, P, g, 0.0, 1, step=oracle.STEP_BB)["theta"]
+    s = th1 - th0
+    Fd = F.dense()
+    Ds = np.diff(s, axis=0)
+    t = np.sum(s * s) / (np.sum((Fd @ s) ** 2) + g * np.sum(Ds * Ds))
+    rho = oracle.power_iteration(F, 100)
+    tl = 1.0 / (1.01 * rho + 4 * g)
+    t = min(max(t, tl), 1e6 * tl)
+    G1 = oracle.backward(F, oracle.forward(F, th1, P), th1, g)
+    th2 = oracle.project_rows(th1 - t * G1)
+    np.testing.assert_allclose(oracle.solve(F, P, g, 0.0, 2, step=oracle.STEP_BB)["theta"], th2,
+                               atol=1e-14)
