@@ -56,7 +56,9 @@ typedef enum {
 
 typedef enum {
     QDT_STEP_SQS = 0,       /* row-constant diagonal majorizer, t_k = 1 / (F^T F 1 + 4 gamma)_k */
-    QDT_STEP_LIPSCHITZ = 1  /* scalar t = 1 / (1.01 rho + 4 gamma), rho: 100 power iterations   */
+    QDT_STEP_LIPSCHITZ = 1, /* scalar t = 1 / (1.01 rho + 4 gamma), rho: 100 power iterations   */
+    QDT_STEP_BB = 2         /* Barzilai-Borwein scalar step <s,s>/<s,Hs> clamped to [t_LIP, 1e6 t_LIP]
+                               (reading R14); plain PG (accel = 0), N <= 128 in this build */
 } qdt_step_mode;
 
 typedef struct qdt_ctx qdt_ctx;       /* device, stream, NCCL comm, workspace, last error  */

@@ -1085,6 +1085,7 @@ struct SolveBufs {
     double *sc2_stage = nullptr;
     int *sc2_arrive = nullptr;
     double *partS = nullptr;   // fused sweep: heavy-tile slots [0, tsplit) + CTA slots
+    double *bb_part = nullptr, *bb_vec = nullptr, *tbb = nullptr;  // BB step statistics / scalar
     double *Gw = nullptr;      // wide-N sweep: Ml x N gradient
 };
 
@@ -1096,6 +1097,8 @@ struct IterCfg {
     int fista;
     int kkt_every;
     int64_t trace_len;
+    int bb = 0;                // Barzilai-Borwein step (reading R14)
+    double tlip = 0.0;         // its safeguard / first step
 };
 
 static qdt_status fwd_reduce(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, const double *theta,
@@ -1267,6 +1270,7 @@ static SweepArgs sweep_args(const IterCfg &c, SolveBufs &b, const double *R, con
     a.theta = theta;
     a.out = out;
     a.tstep = b.tstep;
+    a.tscal = nullptr;
     a.gamma = c.gamma;
     a.scratch = b.scratch;
     a.counters = b.counters;
@@ -1324,6 +1328,25 @@ static qdt_status iteration(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, int64_
     cudaStream_t s = ctx->stream;
     Plan *pl = c.pl;
     int ntiles = pl->ntiles;
+    if (c.bb) {
+        // BB: R_k, the step statistics of s = Theta_k - Theta_{k-1} and R_k - R_{k-1}, t_k, the step
+        double *cur = b.theta[j % 2], *prv = b.theta[(j + 1) % 2];
+        double *Rk = b.R[j % 2], *Rkm1 = b.R[(j + 1) % 2];
+        qdt_probes *p = c.p;
+        CKS(fwd_reduce(ctx, c, b, cur, Rk, true));
+        CK(run_k(ctx, "bb_step", 2, [&]() {
+            return launch_bb_stats(cur, prv, p->Ml, p->kb, p->M, c.N, ctx->rank == 0 ? Rk : nullptr, Rkm1,
+                                   p->D * (int64_t)c.N, b.bb_part, b.bb_vec, b.state, s);
+        }));
+        CKS(allreduce(ctx, b.bb_vec, 3, "allreduce_scalars"));
+        CK(run_k(ctx, "bb_step", 1, [&]() { return launch_bb_step(b.bb_vec, c.gamma, c.tlip, b.tbb, b.state, s); }));
+        SweepArgs a = sweep_args(c, b, Rk, cur, b.theta[(j + 1) % 2]);
+        a.tscal = b.tbb;
+        CK(run_k(ctx, "bwd_step", 1, [&]() { return launch_bwd_mma(a, pl->sw_nbunits, pl->NB, s); }));
+        CKS(halo_exchange(ctx, c, b.theta[(j + 1) % 2]));
+        CKS(scalars(ctx, c, b, 0, c.p->sw_ntiles));
+        return QDT_OK;
+    }
     if (!c.fista && pl->NW) {
         double *cur = b.theta[j % 2], *nxt = b.theta[(j + 1) % 2];
         CKS(fwd_reduce(ctx, c, b, cur, b.R[0], true));
@@ -1550,8 +1573,10 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     if (iters < 0) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: iters < 0");
     qdt_solve_opts opt = {QDT_STEP_SQS, 0, nullptr, 16, 1, 0, 0, 1};
     if (o) opt = *o;
-    if (opt.step != QDT_STEP_SQS && opt.step != QDT_STEP_LIPSCHITZ)
+    if (opt.step != QDT_STEP_SQS && opt.step != QDT_STEP_LIPSCHITZ && opt.step != QDT_STEP_BB)
         return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: unknown step mode %d", opt.step);
+    if (opt.step == QDT_STEP_BB && opt.accel)
+        return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: the BB step is plain projected gradient (accel = 0)");
     if (opt.check_every < 1) opt.check_every = 16;
     if (opt.kkt_every < 1) opt.kkt_every = 1;
     const bool dev = opt.mem_device != 0;
@@ -1567,6 +1592,9 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     cudaStream_t s = ctx->stream;
     Plan *pl;
     CKS(build_plan(ctx, p, (int)N, &pl));
+    if (opt.step == QDT_STEP_BB && !pl->NB)
+        return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: the BB step needs N <= %d in this build", 8 * SW_NBMAX);
+    const bool bb = opt.step == QDT_STEP_BB;
     // memory plan (fails before allocating the big buffers)
     {
         const int nb = opt.accel ? 3 : 2;
@@ -1594,6 +1622,13 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
         CK(cudaMemsetAsync(t, 0, sizeof(double) * rowsz, s));
     }
     CKS(common_bufs(ctx, p, pl, N, b));
+    if (bb) {
+        CKS(ws_get(ctx, "R1", D * N + 4, &b.R[1]));
+        CK(cudaMemsetAsync(b.R[1], 0, sizeof(double) * D * N, s));
+        CKS(ws_get(ctx, "bb_part", 3 * BB_NBLK, &b.bb_part));
+        CKS(ws_get(ctx, "bb_vec", 3, &b.bb_vec));
+        CKS(ws_get(ctx, "tbb", 1, &b.tbb));
+    }
     if (fista) {
         CKS(ws_get(ctx, "R1", D * N + 4, &b.R[1]));
         CKS(ws_get(ctx, "RY", D * N + 4, &b.RY));
@@ -1640,7 +1675,10 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     if (pl->fz_on && !fista) CKS(fwd_reduce(ctx, c, b, b.theta[0], b.R[0], true));  // R_0
     if (fista) CK(cudaMemcpyAsync(b.theta[2] - N, b.theta[0] - N, sizeof(double) * rowsz, cudaMemcpyDeviceToDevice, s));
     double tscalar = 0.0;
-    CKS(step_setup(ctx, p, pl, opt.step, gamma, 100, b.tstep, nullptr, nullptr, &tscalar));
+    CKS(step_setup(ctx, p, pl, bb ? QDT_STEP_LIPSCHITZ : opt.step, gamma, 100, b.tstep, nullptr, nullptr,
+                   &tscalar));
+    c.bb = bb ? 1 : 0;
+    c.tlip = tscalar;
     DevState st0;
     memset(&st0, 0, sizeof st0);
     st0.iters_done = -1;

@@ -115,6 +115,7 @@ struct SweepArgs {
     const double *theta;        // local row 0; rows -1 and Ml readable
     double *out;
     const double *tstep;
+    const double *tscal;        // BB: one device scalar step for every row (nullptr: tstep)
     double gamma;
     double *scratch;
     int *counters;
@@ -187,6 +188,12 @@ constexpr int SW_FUSED_SMEM_MAX = 220 * 1024;
 size_t sweep_fused_smem(int N, int NB, int cap);
 cudaError_t launch_sweep_fused(const SweepFusedArgs &a, int nctas, int NB, cudaStream_t s);
 cudaError_t prepare_sweep_kernels();
+constexpr int BB_NBLK = 296;
+cudaError_t launch_bb_stats(const double *th, const double *tp, int64_t Ml, int64_t kb, int64_t M, int N,
+                            const double *R, const double *Rp, int64_t nR, double *part, double *vec3,
+                            const DevState *st, cudaStream_t s);
+cudaError_t launch_bb_step(const double *vec3, double gamma, double tlip, double *tout,
+                           const DevState *st, cudaStream_t s);
 cudaError_t launch_smooth(const double *X, int64_t M, int N, int64_t exclude, int64_t div, double *S,
                           double *T, double *Tx, double *Y, cudaStream_t s);
 cudaError_t launch_sqs_weights_tiled(int ntiles, int Ml, const int32_t *tile_dA,

@@ -592,8 +592,8 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(Swe
         const int next = unit + G;
         SwUnit un;
         if (next < a.nunits) un = a.units[next];
-        // the row's step weight, loaded before the GEMM so that its latency is hidden
-        const double tk = (8 * warp + g4 < Tt) ? __ldg(a.tstep + k0 + 8 * warp + g4) : 0.0;
+        // the row's step weight (or the BB scalar), loaded before the GEMM to hide its latency
+        const double tk = a.tscal ? *a.tscal : (8 * warp + g4 < Tt) ? __ldg(a.tstep + k0 + 8 * warp + g4) : 0.0;
         double acc[NB][2];
 #pragma unroll
         for (int nb = 0; nb < NB; nb++) acc[nb][0] = acc[nb][1] = 0.0;
@@ -816,7 +816,7 @@ __global__ void __launch_bounds__(512, 1) k_bwd_split(SweepArgs a)
         const int W = u.p1 - u.p0;
         const int nch = (W + SKC - 1) / SKC;
         const int next = unit + G;
-        const double tk = (8 * mb + g4 < Tt) ? __ldg(a.tstep + k0 + 8 * mb + g4) : 0.0;
+        const double tk = a.tscal ? *a.tscal : (8 * mb + g4 < Tt) ? __ldg(a.tstep + k0 + 8 * mb + g4) : 0.0;
         double acc[NBA][2];
 #pragma unroll
         for (int nb = 0; nb < NBA; nb++) acc[nb][0] = acc[nb][1] = 0.0;
@@ -1633,6 +1633,102 @@ cudaError_t launch_smooth(const double *X, int64_t M, int N, int64_t exclude, in
     k_scan_local<<<(unsigned)nch, 128, 0, s>>>(X, M, N, S, T);
     k_scan_chunks<<<(N + 127) / 128, 128, 0, s>>>(T, nch, N, Tx);
     k_smooth_apply<<<(unsigned)((M * N + 255) / 256), 256, 0, s>>>(X, S, Tx, M, N, exclude, div, Y);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------ BB step
+// Barzilai-Borwein scalar step (reading R14): block partials of <s,s>, ||D s||^2 (pairs (k, k+1)
+// with k + 1 < M, the slice's last row paired with its halo row) for s = Theta_k - Theta_{k-1},
+// and of ||R_k - R_{k-1}||^2; then one thread forms t_k.
+constexpr int BB_BLOCKS = 296;
+__global__ void __launch_bounds__(256) k_bb_stats(const double *th, const double *tp, int64_t Ml,
+                                                  int64_t kb, int64_t M, int N, const double *R,
+                                                  const double *Rp, int64_t nR, double *part,
+                                                  const DevState *st)
+{
+    __shared__ double red[8 * 3];
+    if (st && st->stop) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double ss = 0.0, sd = 0.0, sh = 0.0;
+    const int64_t tot = Ml * N, chunk = (tot + gridDim.x - 1) / gridDim.x;
+    const int64_t e0 = blockIdx.x * chunk, e1 = min(tot, e0 + chunk);
+    for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+        const double a = th[e] - tp[e];
+        ss = fma(a, a, ss);
+        const int64_t row = e / N;
+        if (kb + row + 1 < M) {
+            const double b = th[e + N] - tp[e + N];
+            sd = fma(a - b, a - b, sd);
+        }
+    }
+    if (R) {
+        const int64_t c2 = (nR + gridDim.x - 1) / gridDim.x, r0 = blockIdx.x * c2, r1 = min(nR, r0 + c2);
+        for (int64_t e = r0 + threadIdx.x; e < r1; e += blockDim.x) {
+            const double d = R[e] - Rp[e];
+            sh = fma(d, d, sh);
+        }
+    }
+    ss = wsum(ss);
+    sd = wsum(sd);
+    sh = wsum(sh);
+    if (lane == 0) {
+        red[warp * 3] = ss;
+        red[warp * 3 + 1] = sd;
+        red[warp * 3 + 2] = sh;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+        for (int w = 0; w < 8; w++) {
+            v0 += red[w * 3];
+            v1 += red[w * 3 + 1];
+            v2 += red[w * 3 + 2];
+        }
+        part[blockIdx.x * 3] = v0;
+        part[blockIdx.x * 3 + 1] = v1;
+        part[blockIdx.x * 3 + 2] = v2;
+    }
+}
+// sum the block partials in order (vec3 = <s,s>, ||Ds||^2, ||dR||^2; multi-GPU: allreduced by the
+// host between the two phases) -> t_k
+__global__ void k_bb_sum(const double *part, int nblk, double *vec3, const DevState *st)
+{
+    if (threadIdx.x || (st && st->stop)) return;
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+    for (int b = 0; b < nblk; b++) {
+        v0 += part[b * 3];
+        v1 += part[b * 3 + 1];
+        v2 += part[b * 3 + 2];
+    }
+    vec3[0] = v0;
+    vec3[1] = v1;
+    vec3[2] = v2;
+}
+__global__ void k_bb_step(const double *vec3, double gamma, double tlip, double *tout, const DevState *st)
+{
+    if (threadIdx.x || (st && st->stop)) return;
+    double t = tlip;
+    if (st->it > 0) {
+        const double shs = vec3[2] + gamma * vec3[1];
+        if (shs > 0.0) {
+            t = vec3[0] / shs;
+            t = t < tlip ? tlip : (t > 1e6 * tlip ? 1e6 * tlip : t);
+        }
+    }
+    *tout = t;
+}
+cudaError_t launch_bb_stats(const double *th, const double *tp, int64_t Ml, int64_t kb, int64_t M, int N,
+                            const double *R, const double *Rp, int64_t nR, double *part, double *vec3,
+                            const DevState *st, cudaStream_t s)
+{
+    k_bb_stats<<<BB_BLOCKS, 256, 0, s>>>(th, tp, Ml, kb, M, N, R, Rp, nR, part, st);
+    k_bb_sum<<<1, 32, 0, s>>>(part, BB_BLOCKS, vec3, st);
+    return cudaGetLastError();
+}
+cudaError_t launch_bb_step(const double *vec3, double gamma, double tlip, double *tout,
+                           const DevState *st, cudaStream_t s)
+{
+    k_bb_step<<<1, 32, 0, s>>>(vec3, gamma, tlip, tout, st);
     return cudaGetLastError();
 }
 

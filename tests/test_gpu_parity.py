@@ -411,3 +411,41 @@ def test_smooth_then_restart_parity(q, ctx):
     r2g = q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, 40, theta0=sg)
     assert np.abs(r2g["theta"] - r2o["theta"]).max() <= 1e-9
     assert _trace_ok(r2g["trace"], r2o["trace"], I.P)
+
+
+def test_bb_step_parity(q, ctx):
+    """Barzilai-Borwein step (reading R14): the first iterates match the oracle's BB iterates; at
+    convergence both reach the unique QP minimiser (gamma > 0, brute-force optimum of P11)."""
+    import itertools  # noqa: F401
+    from test_oracle_pins import _brute_qp
+    rng = np.random.default_rng(300)
+    M, N, D = 4, 3, 8
+    a2 = np.sort(rng.uniform(0.3, 3.0, D))
+    P = rng.dirichlet(np.ones(N), size=D)
+    gamma = 1e-2
+    Fo = oracle.Probes(a2, M)
+    Fg = q.qdt_build_probes(ctx, a2, M)
+    star = _brute_qp(Fo.dense(), P, gamma)[0][0]
+    rg = q.qdt_solve(ctx, Fg, P, gamma, 0.0, 3000, step=q.QDT_STEP_BB)
+    assert np.abs(rg["theta"] - star).max() <= 1e-9
+    I = qs.tiny()
+    Fo = oracle.Probes(I.alpha2, I.M)
+    Fg = q.qdt_build_probes(ctx, I.alpha2, I.M)
+    ro = oracle.solve(Fo, I.P, I.gamma, 0.0, 8, step=oracle.STEP_BB)
+    rg = q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, 8, step=q.QDT_STEP_BB)
+    assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9
+    assert _trace_ok(rg["trace"], ro["trace"], I.P)
+    assert rg["info"]["step_scalar"] == pytest.approx(ro["step"], rel=1e-12)
+    # long runs diverge iterate-wise (roundoff amplification, reading R5) but reach the same
+    # minimiser on a well-conditioned instance (gamma > 0)
+    rng = np.random.default_rng(302)
+    a2 = np.sort(rng.uniform(0.0, 12.0, 60))
+    P = rng.dirichlet(np.ones(6), 60)
+    Fo = oracle.Probes(a2, 20)
+    Fg2 = q.qdt_build_probes(ctx, a2, 20)
+    ro = oracle.solve(Fo, P, 1e-2, 0.0, 4000, step=oracle.STEP_BB)
+    rg = q.qdt_solve(ctx, Fg2, P, 1e-2, 0.0, 4000, step=q.QDT_STEP_BB)
+    assert ro["kkt"][-1] <= 1e-12 and rg["kkt"][-1] <= 1e-12
+    assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9
+    with pytest.raises(q.QdtError, match="INVALID_ARG"):
+        q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, 5, step=q.QDT_STEP_BB, accel=True)
