@@ -462,23 +462,28 @@ __device__ __forceinline__ void gemm_bwd(double (&acc)[NB][2], const double *F, 
     }
 }
 
-// SQS row weights from the tiled F (reading R2): w_k = sum_d F_{d,k} s_d + 4 gamma with d over the
-// tile's window in increasing order, t_k = 1/w_k (0 for a frozen row).  Block per tile, thread
-// per row: the window's F rows are read coalesced across the tile's rows.
-__global__ void k_sqs_weights_tiled(int Ml, const int32_t *tile_dA, const int32_t *tile_dB,
-                                    const int64_t *fb_off, const double *Fb, const double *s,
-                                    double gamma, double *w, double *tstep)
+// SQS row weights from the tiled F (reading R2): w_k = sum_d F_{d,k} s_d + 4 gamma over the
+// tile's window, t_k = 1/w_k (0 for a frozen row).  Block per tile: 64 rows x 4 probe slices
+// (fixed combination order, deterministic); the window's F rows are read coalesced.
+__global__ void __launch_bounds__(256) k_sqs_weights_tiled(int Ml, const int32_t *tile_dA,
+                                                            const int32_t *tile_dB, const int64_t *fb_off,
+                                                            const double *Fb, const double *s, double gamma,
+                                                            double *w, double *tstep)
 {
-    const int t = blockIdx.x, r = threadIdx.x;
-    const int k = t * ST + r;
-    if (k >= Ml) return;
+    // 64 rows x 4 probe slices (probes j = q mod 4); the slices are combined in a fixed order
+    __shared__ double part[4][ST];
+    const int t = blockIdx.x, r = threadIdx.x & (ST - 1), q = threadIdx.x >> 6;
     const int dA = tile_dA[t], W = tile_dB[t] - dA;
     const double *f = Fb + fb_off[t] + r;
     double acc = 0.0;
-    for (int j = 0; j < W; j++) acc += f[(int64_t)j * STP] * s[dA + j];
-    acc += 4.0 * gamma;
-    if (w) w[k] = acc;
-    if (tstep) tstep[k] = (acc > 0.0) ? 1.0 / acc : 0.0;
+    for (int j = q; j < W; j += 4) acc += f[(int64_t)j * STP] * s[dA + j];
+    part[q][r] = acc;
+    __syncthreads();
+    const int k = t * ST + r;
+    if (q || k >= Ml) return;
+    double v = ((part[0][r] + part[1][r]) + (part[2][r] + part[3][r])) + 4.0 * gamma;
+    if (w) w[k] = v;
+    if (tstep) tstep[k] = (v > 0.0) ? 1.0 / v : 0.0;
 }
 
 cudaError_t launch_sqs_weights_tiled(int ntiles, int Ml, const int32_t *tile_dA,
@@ -487,7 +492,7 @@ cudaError_t launch_sqs_weights_tiled(int ntiles, int Ml, const int32_t *tile_dA,
                                      cudaStream_t st)
 {
     if (ntiles <= 0) return cudaSuccess;
-    k_sqs_weights_tiled<<<ntiles, ST, 0, st>>>(Ml, tile_dA, tile_dB, fb_off, Fb, s, gamma, w, tstep);
+    k_sqs_weights_tiled<<<ntiles, 4 * ST, 0, st>>>(Ml, tile_dA, tile_dB, fb_off, Fb, s, gamma, w, tstep);
     return cudaGetLastError();
 }
 
