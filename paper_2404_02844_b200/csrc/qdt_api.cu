@@ -540,7 +540,7 @@ static void plan_fwd_units(const qdt_probes *p, int t0, int t1, Emit &&emit)
 static qdt_status build_fused_plan(qdt_ctx *ctx, qdt_probes *p, Plan *pl, const std::vector<SwUnit> &bu_all)
 {
     pl->fz_on = false;
-    if (ctx->nranks != 1 || pl->NB == 0) return QDT_OK;
+    if (ctx->nranks != 1 || pl->NB == 0 || pl->NB > SW_NBMAX) return QDT_OK;
     // the fused persistent sweep is opt-in (QDT_FUSED=1): at 8 warps per SM it is latency bound and
     // measured slower than the unfused sweep (profiles/r01_v2)
     const char *e = getenv("QDT_FUSED");
@@ -837,7 +837,8 @@ static qdt_status build_plan(qdt_ctx *ctx, qdt_probes *p, int N, Plan **out)
                            cudaMemcpyHostToDevice, s));
     CK(cudaStreamSynchronize(s));
     pl->NB = sweep_enabled() ? sweep_nb(N) : 0;
-    pl->NW = (sweep_enabled() && !pl->NB && N % 2 == 0 && N <= 1024) ? 1 : 0;
+    // wide kernels for N > 128 (even): the whole path, or (N <= 160) beside the NB > 16 plain step
+    pl->NW = (sweep_enabled() && (!pl->NB || pl->NB > SW_NBMAX) && N % 2 == 0 && N <= 1024) ? 1 : 0;
     if (pl->NB || pl->NW) CKS(build_sweep_plan(ctx, p, pl.get()));
     pl->nR = ctx->nranks == 1 ? (int)((D + 7) / 8) : ctx->nblkR;
     *out = pl.get();
@@ -1099,7 +1100,10 @@ struct IterCfg {
     int64_t trace_len;
     int bb = 0;                // Barzilai-Borwein step (reading R14)
     double tlip = 0.0;         // its safeguard / first step
+    int Nv = 0;                // outcomes when N is a padded pitch (pad_cols), else 0
 };
+
+static inline int nvalid(const IterCfg &c) { return c.Nv ? c.Nv : c.N; }
 
 static qdt_status fwd_reduce(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, const double *theta,
                              double *R, bool withP)
@@ -1109,7 +1113,7 @@ static qdt_status fwd_reduce(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, const
     qdt_probes *p = c.p;
     const bool multi = ctx->nranks > 1;
     if (pl->NB || pl->NW) {
-        const int fnb = pl->NB ? pl->NB : SW_NBMAX;   // wide N: 128-column chunks
+        const int fnb = pl->NW ? wide_nb(c.N) : pl->NB;   // wide N: balanced column chunks
         SweepFwdArgs fa;
         fa.N = c.N;
         fa.Ml = (int)p->Ml;
@@ -1232,13 +1236,13 @@ static qdt_status scalars(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, int fina
     const int ke = final_eval ? 1 : c.kkt_every;
     CK(run_k(ctx, "scalars", 1, [&]() {
         return launch_scalars2(b.partR, c.pl->nR, partT, ntiles, ctx->rank == 0, b.sc2_stage, b.sc2_arrive,
-                               b.vec, c.N, c.p->M, c.gamma, c.tol, final_eval, ke, b.trace, b.kkt, b.kktp,
+                               b.vec, nvalid(c), c.p->M, c.gamma, c.tol, final_eval, ke, b.trace, b.kkt, b.kktp,
                                c.trace_len, b.state, multi ? 0 : 1, s);
     }));
     if (!multi) return QDT_OK;
     CKS(allreduce(ctx, b.vec, NV, "allreduce_scalars"));
     CK(run_k(ctx, "scalars", 1, [&]() {
-        return launch_finalize(b.vec, c.N, c.p->M, c.gamma, c.tol, final_eval, ke, b.trace, b.kkt, b.kktp,
+        return launch_finalize(b.vec, nvalid(c), c.p->M, c.gamma, c.tol, final_eval, ke, b.trace, b.kkt, b.kktp,
                                c.trace_len, b.state, s);
     }));
     return QDT_OK;
@@ -1251,7 +1255,8 @@ static cudaError_t launch_bwd_any(const SweepArgs &a, int nunits, int NB, cudaSt
 {
     const int m = sweep_split_mode();
     const bool fis = a.beta != nullptr && !a.eval;
-    return (m == 1 || (m == 2 && fis)) ? launch_bwd_split(a, nunits, NB, s) : launch_bwd_mma(a, nunits, NB, s);
+    const bool split = NB <= SW_NBMAX && (m == 1 || (m == 2 && fis));
+    return split ? launch_bwd_split(a, nunits, NB, s) : launch_bwd_mma(a, nunits, NB, s);
 }
 
 static SweepArgs sweep_args(const IterCfg &c, SolveBufs &b, const double *R, const double *theta,
@@ -1290,6 +1295,7 @@ static WideArgs wide_args(const IterCfg &c, SolveBufs &b, const double *R, const
 {
     WideArgs w;
     w.N = c.N;
+    w.Nv = nvalid(c);
     w.Ml = (int)c.p->Ml;
     w.ncc = (c.N + 127) / 128;
     w.kb = c.p->kb;
@@ -1319,7 +1325,19 @@ static WideArgs wide_args(const IterCfg &c, SolveBufs &b, const double *R, const
 
 static int wide_nparts(const IterCfg &c)
 {
-    return c.p->sw_ntiles * ((c.N + 127) / 128) + (int)((c.p->Ml + 7) / 8);
+    return c.p->sw_ntiles * ((c.N + 127) / 128) + wide_proj_blocks((int)c.p->Ml);
+}
+
+// QDT_WIDE_PLAIN=1: plain steps at 128 < N <= 160 on the two wide kernels instead of k_bwd_mma
+// (A/B measurement)
+static bool wide_plain_forced()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("QDT_WIDE_PLAIN");
+        v = (e && e[0] == '1') ? 1 : 0;
+    }
+    return v == 1;
 }
 
 // one iteration with phase index j (buffer rotation)
@@ -1347,7 +1365,7 @@ static qdt_status iteration(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, int64_
         CKS(scalars(ctx, c, b, 0, c.p->sw_ntiles));
         return QDT_OK;
     }
-    if (!c.fista && pl->NW) {
+    if (!c.fista && pl->NW && (!pl->NB || wide_plain_forced())) {
         double *cur = b.theta[j % 2], *nxt = b.theta[(j + 1) % 2];
         CKS(fwd_reduce(ctx, c, b, cur, b.R[0], true));
         WideArgs w = wide_args(c, b, b.R[0], cur, nxt);
@@ -1559,7 +1577,28 @@ static qdt_status check_finite_host(qdt_ctx *ctx, const double *x, int64_t n, co
     return QDT_OK;
 }
 
-extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double *P, int64_t N,
+// Odd N in (128, 1024) (the paper's N = 151): the wide sweep needs an even row pitch, so solve
+// and objective run on an internal pitch N + 1 whose pad column is zero in P and Theta (hence in
+// R and G), and is excluded from the projection, the KKT sums and their M*N normalisation.
+static int64_t pad_cols(int64_t N)
+{
+    return (sweep_enabled() && N > 8 * SW_NBMAX && N < 1024 && (N & 1)) ? N + 1 : N;
+}
+
+// rows x ncols doubles between row pitches (in doubles)
+static qdt_status copy_cols(qdt_ctx *ctx, double *dst, int64_t dp, const double *src, int64_t sp,
+                            int64_t ncols, int64_t rows, cudaMemcpyKind k)
+{
+    if (rows <= 0) return QDT_OK;
+    if (dp == ncols && sp == ncols)
+        CK(cudaMemcpyAsync(dst, src, sizeof(double) * rows * ncols, k, ctx->stream));
+    else
+        CK(cudaMemcpy2DAsync(dst, sizeof(double) * dp, src, sizeof(double) * sp, sizeof(double) * ncols,
+                             rows, k, ctx->stream));
+    return QDT_OK;
+}
+
+extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double *P, int64_t Nu,
                                 double gamma, double tol, int64_t iters, const qdt_solve_opts *o,
                                 double *theta_out, double *trace_out, double *kkt_out,
                                 qdt_solve_info *info)
@@ -1567,7 +1606,8 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     if (!ctx) return fail(nullptr, QDT_ERR_INVALID_ARG, "qdt_solve: ctx is NULL");
     if (!F || !P || !theta_out) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: NULL pointer");
     if (F->ctx != ctx) return fail(ctx, QDT_ERR_STATE, "qdt_solve: probes built on another ctx");
-    if (N < 1 || N > 8192) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: N = %lld not in [1, 8192]", (long long)N);
+    if (Nu < 1 || Nu > 8192) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: N = %lld not in [1, 8192]", (long long)Nu);
+    const int64_t N = pad_cols(Nu);   // internal row pitch
     if (!(gamma >= 0.0) || !isfinite(gamma)) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: gamma must be finite and >= 0");
     if (!(tol >= 0.0)) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: tol must be >= 0");
     if (iters < 0) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: iters < 0");
@@ -1583,16 +1623,16 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     qdt_probes *p = const_cast<qdt_probes *>(F);
     const int64_t D = p->D, Ml = p->Ml, M = p->M;
     if (!dev) {
-        CKS(check_finite_host(ctx, P, D * N, "P"));
+        CKS(check_finite_host(ctx, P, D * Nu, "P"));
         if (opt.theta0)
-            CKS(check_finite_host(ctx, opt.theta0, (ctx->nranks > 1 && !opt.gather_theta ? Ml : M) * N,
+            CKS(check_finite_host(ctx, opt.theta0, (ctx->nranks > 1 && !opt.gather_theta ? Ml : M) * Nu,
                                   "theta0"));
     }
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
     Plan *pl;
     CKS(build_plan(ctx, p, (int)N, &pl));
-    if (opt.step == QDT_STEP_BB && !pl->NB)
+    if (opt.step == QDT_STEP_BB && (!pl->NB || pl->NB > SW_NBMAX))
         return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: the BB step needs N <= %d in this build", 8 * SW_NBMAX);
     const bool bb = opt.step == QDT_STEP_BB;
     // memory plan (fails before allocating the big buffers)
@@ -1642,11 +1682,12 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     CK(launch_fill(b.kkt, tl, NAN, s));
     CK(launch_fill(b.kktp, tl, NAN, s));
     ctx->launches += 3;
-    if (dev) {
+    if (dev && N == Nu) {
         b.P = const_cast<double *>(P);
     } else {
         CKS(ws_get(ctx, "P", D * N, &b.P));
-        CK(cudaMemcpyAsync(b.P, P, sizeof(double) * D * N, cudaMemcpyHostToDevice, s));
+        if (N != Nu) CK(cudaMemsetAsync(b.P, 0, sizeof(double) * D * N, s));
+        CKS(copy_cols(ctx, b.P, N, P, Nu, Nu, D, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
     }
     std::vector<double> betas;
     if (fista) {
@@ -1664,13 +1705,15 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     // !gather_theta)
     if (opt.theta0) {
         const double *src = opt.theta0;
-        if (ctx->nranks == 1 || opt.gather_theta) src += p->kb * N;
-        CKS(upload_rows(ctx, b.theta[0], src, Ml, (int)N, dev));
+        if (ctx->nranks == 1 || opt.gather_theta) src += p->kb * Nu;
+        CKS(copy_cols(ctx, b.theta[0], N, src, Nu, Nu, Ml, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
     } else {
-        CK(launch_fill(b.theta[0], Ml * N, 1.0 / (double)N, s));
+        CK(launch_fill(b.theta[0], Ml * N, 1.0 / (double)Nu, s));
         ctx->launches++;
+        if (N != Nu) CK(cudaMemset2DAsync(b.theta[0] + Nu, sizeof(double) * N, 0, sizeof(double), Ml, s));
     }
     IterCfg c{p, pl, (int)N, gamma, tol, fista, opt.kkt_every, tl};
+    c.Nv = (int)Nu;
     CKS(halo_exchange(ctx, c, b.theta[0]));
     if (pl->fz_on && !fista) CKS(fwd_reduce(ctx, c, b, b.theta[0], b.R[0], true));  // R_0
     if (fista) CK(cudaMemcpyAsync(b.theta[2] - N, b.theta[0] - N, sizeof(double) * rowsz, cudaMemcpyDeviceToDevice, s));
@@ -1767,11 +1810,9 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
         CK(cudaMemsetAsync(full, 0, sizeof(double) * M * N, s));
         CK(cudaMemcpyAsync(full + p->kb * N, res, sizeof(double) * Ml * N, cudaMemcpyDeviceToDevice, s));
         CKS(allreduce(ctx, full, (size_t)M * N, "gather"));
-        CK(cudaMemcpyAsync(theta_out, full, sizeof(double) * M * N,
-                           dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+        CKS(copy_cols(ctx, theta_out, Nu, full, N, Nu, M, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
     } else {
-        CK(cudaMemcpyAsync(theta_out, res, sizeof(double) * Ml * N,
-                           dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+        CKS(copy_cols(ctx, theta_out, Nu, res, N, Nu, Ml, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
     }
     std::vector<double> hk(tl);
     if (trace_out) CK(cudaMemcpyAsync(trace_out, b.trace, sizeof(double) * tl, cudaMemcpyDeviceToHost, s));
@@ -1809,20 +1850,21 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
 
 // ------------------------------------------------------------------------------ objective
 extern "C" qdt_status qdt_objective(qdt_ctx *ctx, const qdt_probes *F, const double *P,
-                                    const double *theta, int64_t N, double gamma,
+                                    const double *theta, int64_t Nu, double gamma,
                                     int32_t mem_device, double *f_out, double *kkt_out)
 {
     if (!ctx) return fail(nullptr, QDT_ERR_INVALID_ARG, "qdt_objective: ctx is NULL");
     if (!F || !P || !theta || !f_out) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_objective: NULL pointer");
     if (F->ctx != ctx) return fail(ctx, QDT_ERR_STATE, "probes built on another ctx");
-    if (N < 1 || N > 8192) return fail(ctx, QDT_ERR_INVALID_ARG, "N out of range");
+    if (Nu < 1 || Nu > 8192) return fail(ctx, QDT_ERR_INVALID_ARG, "N out of range");
+    const int64_t N = pad_cols(Nu);   // internal row pitch (qdt_solve)
     if (!(gamma >= 0.0) || !isfinite(gamma)) return fail(ctx, QDT_ERR_INVALID_ARG, "gamma must be finite >= 0");
     qdt_probes *p = const_cast<qdt_probes *>(F);
     const int64_t D = p->D, Ml = p->Ml;
     const bool dev = mem_device != 0;
     if (!dev) {
-        CKS(check_finite_host(ctx, P, D * N, "P"));
-        CKS(check_finite_host(ctx, theta, p->M * N, "theta"));
+        CKS(check_finite_host(ctx, P, D * Nu, "P"));
+        CKS(check_finite_host(ctx, theta, p->M * Nu, "theta"));
     }
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
@@ -1834,23 +1876,24 @@ extern "C" qdt_status qdt_objective(qdt_ctx *ctx, const qdt_probes *F, const dou
     CKS(ws_get(ctx, "theta0", rowsz + 2, &t));
     b.theta[0] = t + N;
     CK(cudaMemsetAsync(t, 0, sizeof(double) * rowsz, s));
-    CK(cudaMemcpyAsync(b.theta[0] - (p->kb > 0 ? N : 0), theta + (p->kb > 0 ? (p->kb - 1) * N : 0),
-                       sizeof(double) * (Ml + (p->kb > 0) + (p->ke < p->M)) * N,
-                       dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    CKS(copy_cols(ctx, b.theta[0] - (p->kb > 0 ? N : 0), N, theta + (p->kb > 0 ? (p->kb - 1) * Nu : 0), Nu, Nu,
+                  Ml + (p->kb > 0) + (p->ke < p->M), dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
     CKS(common_bufs(ctx, p, pl, N, b));
     CKS(ws_get(ctx, "trace", 1, &b.trace));
     CKS(ws_get(ctx, "kkt", 1, &b.kkt));
     CKS(ws_get(ctx, "kktp", 1, &b.kktp));
-    if (dev) {
+    if (dev && N == Nu) {
         b.P = const_cast<double *>(P);
     } else {
         CKS(ws_get(ctx, "P", D * N, &b.P));
-        CK(cudaMemcpyAsync(b.P, P, sizeof(double) * D * N, cudaMemcpyHostToDevice, s));
+        if (N != Nu) CK(cudaMemsetAsync(b.P, 0, sizeof(double) * D * N, s));
+        CKS(copy_cols(ctx, b.P, N, P, Nu, Nu, D, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
     }
     DevState st0;
     memset(&st0, 0, sizeof st0);
     CK(cudaMemcpyAsync(b.state, &st0, sizeof st0, cudaMemcpyHostToDevice, s));
     IterCfg c{p, pl, (int)N, gamma, 0.0, 0, 1, 1};
+    c.Nv = (int)Nu;
     CKS(eval_pass(ctx, c, b, b.theta[0]));
     double f = 0, r = 0;
     CK(cudaMemcpyAsync(&f, b.trace, sizeof(double), cudaMemcpyDeviceToHost, s));

@@ -94,7 +94,8 @@ constexpr int FWCAP = 48;       // fwd unit union-window cap (probes): 2 CTAs/SM
 constexpr int FWNB = FWCAP / 8; // fwd DMMA probe n-blocks per unit
 constexpr int FW_MAXT = 16;     // fwd unit length cap (tiles)
 constexpr int SC2_BLOCKS = 64;  // first-level blocks of the scalar reduction
-constexpr int SW_NBMAX = 16;    // sweep path: N <= 8 * SW_NBMAX outcomes
+constexpr int SW_NBMAX = 16;    // sweep path: N <= 8 * SW_NBMAX outcomes (every kernel variant)
+constexpr int SW_NBX = 20;      // plain steps up to N = 8 * SW_NBX (even) on k_bwd_mma alone
 
 struct SwUnit {                 // bwd unit: tile, probe range [p0, p1) of its window, split-K info
     int32_t tile, p0, p1, slot, nsplit, pad;
@@ -160,6 +161,7 @@ struct SweepFusedArgs {
 };
 struct WideArgs {               // wide-N sweep (N > 128): k_grad_wide + k_proj_wide
     int N, Ml, ncc;             // ncc: 128-column chunks (set by launch_grad_wide)
+    int Nv;                     // outcomes (< N when the row pitch N carries a zero pad column)
     int64_t kb, M;
     const SwUnit *units;
     const int64_t *fb_off;
@@ -184,6 +186,9 @@ struct WideArgs {               // wide-N sweep (N > 128): k_grad_wide + k_proj_
 };
 cudaError_t launch_grad_wide(const WideArgs &a, int nunits, cudaStream_t s);
 cudaError_t launch_proj_wide(const WideArgs &a, cudaStream_t s);
+int wide_nb(int N);                                  // balanced column-chunk width / 8 (N > 128)
+constexpr int PW_BLOCKS = 148 * 8;                   // k_proj_wide grid cap (contiguous row ranges)
+int wide_proj_blocks(int Ml);
 constexpr int SW_FUSED_SMEM_MAX = 220 * 1024;
 size_t sweep_fused_smem(int N, int NB, int cap);
 cudaError_t launch_sweep_fused(const SweepFusedArgs &a, int nctas, int NB, cudaStream_t s);

@@ -668,7 +668,8 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(Swe
             const double *tpr = Tq + th_sh + (r + 1) * N;
             // interior even-N tiles of plain steps: the own-row values stay in registers, the tile
             // is released after pass 1 and the next unit's tile load overlaps pass 2 + Michelot
-            const bool stash = fast && !FIS && !ev;
+            constexpr bool kStash = NB <= SW_NBMAX;   // register budget: 255 at NB = 16
+            const bool stash = kStash && fast && !FIS && !ev;
             auto release = [&]() {
                 __syncthreads();
                 if (tid == 0 && next < a.nunits && un.nsplit == 1) issue_theta(un);
@@ -1314,12 +1315,19 @@ __global__ void __launch_bounds__(256, 1) k_sweep_fused(SweepFusedArgs a)
 //                global / L2), G stored; regulariser pair partial per (tile, chunk).
 //   k_proj_wide  warp per Fock row (N / 32 values per lane): KKT, X = Theta -
 //                t_k G, Michelot threshold (reading R4), Theta_{k+1}.
-constexpr int RPW = 8 * 16 + 4;   // staged R row pitch for 128-column chunks (conflict-free B)
-size_t wide_grad_smem() { return (size_t)(2 * SKC * STP + 2 * SKC * RPW + 8) * sizeof(double); }
+// ncc = ceil(N / 128) column chunks of balanced width 8 NB (NB = wide_nb(N) in [9, 16]), so no
+// chunk is a thin remainder
+int wide_nb(int N)
+{
+    const int ncc = (N + 127) / 128;
+    return ((N + 7) / 8 + ncc - 1) / ncc;
+}
+size_t wide_grad_smem() { return (size_t)(2 * SKC * STP + 2 * SKC * (8 * 16 + 4) + 8) * sizeof(double); }
 
+template <int NB>
 __global__ void __launch_bounds__(256, 2) k_grad_wide(WideArgs a)
 {
-    constexpr int NB = 16;
+    constexpr int RPW = 8 * NB + 4;   // staged R row pitch (conflict-free B fragments)
     extern __shared__ __align__(128) double sm[];
     __shared__ __align__(8) uint64_t bars[2];
     __shared__ double red[8];
@@ -1450,23 +1458,28 @@ __global__ void __launch_bounds__(256) k_proj_wide(WideArgs a)
     const DevState *st = a.state;
     if (st && st->stop) return;
     const int64_t it = st ? st->it : 0;
-    const int N = a.N;
+    const int N = a.N, Nv = a.Nv;   // row pitch, outcomes (pad columns: excluded, written 0)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int kl = blockIdx.x * 8 + warp;
-    const bool act = kl < a.Ml;
     if (a.eval_gate && (it % a.kkt_every) != 0) return;
     const bool fis = a.beta != nullptr && !a.eval;   // FISTA step: X from Y, KKT in the eval pass
     const double beta = fis ? a.beta[it] : 0.0;
     const bool do_kkt = a.eval || (!fis && (it % a.kkt_every) == 0);
+    // CTA b owns the contiguous rows [b rpc, (b + 1) rpc) (grid fixed by Ml: deterministic sums);
+    // warp w its rows w, w + 8, ...; KKT partials accumulate per warp in row order
+    const int rpc = (int)(((a.Ml + gridDim.x - 1) / gridDim.x + 7) & ~7);
+    const int rbeg = blockIdx.x * rpc, rend = min(a.Ml, rbeg + rpc);
+    double skkt = 0.0, skktp = 0.0;
+    for (int kl = rbeg + warp; kl < rend; kl += 8) {
+    const bool act = true;
     double th[VM], x[VM];
-    double mn = INFINITY, skkt = 0.0, skktp = 0.0;
+    double mn = INFINITY;
     if (act) {
         const double *tr = a.theta + (int64_t)kl * N, *gr = a.G + (int64_t)kl * N;
 #pragma unroll
         for (int v = 0; v < VM; v++) {
             const int n = lane + 32 * v;
             th[v] = n < N ? tr[n] : 0.0;
-            x[v] = n < N ? gr[n] : INFINITY;   // G for now
+            x[v] = n < Nv ? gr[n] : INFINITY;   // G for now
             mn = fmin(mn, x[v]);
         }
     }
@@ -1476,7 +1489,7 @@ __global__ void __launch_bounds__(256) k_proj_wide(WideArgs a)
     double s = 0.0, xm = -INFINITY, xn = INFINITY;
 #pragma unroll
     for (int v = 0; v < VM; v++) {
-        const bool ok = act && lane + 32 * v < N;
+        const bool ok = act && lane + 32 * v < Nv;
         const double g = x[v];
         if (ok && do_kkt) {
             const double x1 = th[v] * fma(2.0, g, lam);
@@ -1500,11 +1513,11 @@ __global__ void __launch_bounds__(256) k_proj_wide(WideArgs a)
         s = wsum(s);
         xm = wmax(xm);
         xn = wmin(xn);
-        double tau = (s - 1.0) / (double)N;
+        double tau = (s - 1.0) / (double)Nv;
         bool done = !act || xn > tau;
         if (!done) tau = fmax(tau, xm - 1.0);
-        int cnt = N + 1;
-        for (int round = 0; round <= N && !done; round++) {   // warp-uniform: one row per warp
+        int cnt = Nv + 1;
+        for (int round = 0; round <= Nv && !done; round++) {   // warp-uniform: one row per warp
             double ps = 0.0, mA = INFINITY;
             int pc = 0;
 #pragma unroll
@@ -1537,6 +1550,7 @@ __global__ void __launch_bounds__(256) k_proj_wide(WideArgs a)
             }
         }
     }
+    }   // rows
     skkt = wsum(skkt);
     skktp = wsum(skktp);
     if (lane == 0) {
@@ -1564,14 +1578,23 @@ cudaError_t launch_grad_wide(const WideArgs &a_in, int nunits, cudaStream_t s)
 {
     if (nunits <= 0) return cudaSuccess;
     WideArgs a = a_in;
-    a.ncc = (a.N + 127) / 128;
-    k_grad_wide<<<nunits * a.ncc, 256, wide_grad_smem(), s>>>(a);
+    const int nb = wide_nb(a.N);
+    a.ncc = (a.N + 8 * nb - 1) / (8 * nb);
+    switch (nb) {
+#define QDT_CASE(n) \
+    case n: k_grad_wide<n><<<nunits * a.ncc, 256, wide_grad_smem(), s>>>(a); break;
+        QDT_CASE(9) QDT_CASE(10) QDT_CASE(11) QDT_CASE(12) QDT_CASE(13) QDT_CASE(14) QDT_CASE(15) QDT_CASE(16)
+#undef QDT_CASE
+        default: return cudaErrorInvalidValue;
+    }
     return cudaGetLastError();
 }
 
+int wide_proj_blocks(int Ml) { return (int)std::min<int64_t>((Ml + 7) / 8, PW_BLOCKS); }
+
 cudaError_t launch_proj_wide(const WideArgs &a, cudaStream_t s)
 {
-    const int grid = (a.Ml + 7) / 8;
+    const int grid = wide_proj_blocks(a.Ml);
     const int vm = (a.N + 31) / 32;
     if (vm <= 8) k_proj_wide<8><<<grid, 256, 0, s>>>(a);
     else if (vm <= 16) k_proj_wide<16><<<grid, 256, 0, s>>>(a);
@@ -1874,8 +1897,8 @@ static cudaError_t prep_nb()
     cudaError_t e = cudaFuncSetAttribute(k_bwd_mma<NB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_bwd_mma<NB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    if (e == cudaSuccess && NB == 16)
-        e = cudaFuncSetAttribute(k_grad_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    if (e == cudaSuccess && NB >= 9)
+        e = cudaFuncSetAttribute(k_grad_wide<NB < 9 ? 9 : NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_bwd_split<NB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     if (e == cudaSuccess)
@@ -1898,12 +1921,23 @@ cudaError_t prepare_sweep_kernels()
 #define QDT_PREP(nb) if (e == cudaSuccess) e = prep_nb<nb>();
     QDT_FOR_NB(QDT_PREP)
 #undef QDT_PREP
+#define QDT_PREP(nb) \
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_bwd_mma<nb, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+    QDT_PREP(17) QDT_PREP(18) QDT_PREP(19) QDT_PREP(20)
+#undef QDT_PREP
     done = e == cudaSuccess;
     return e;
 }
 
 // exact n-block count: only the last n-block of a row can hold padding columns
-int sweep_nb(int N) { return (N >= 1 && N <= 8 * SW_NBMAX) ? (N + 7) / 8 : 0; }
+// (N in (128, 160], even: plain steps only, k_bwd_mma without the register stash; the forward
+// pass and FISTA / evaluation passes take the wide kernels)
+int sweep_nb(int N)
+{
+    if (N >= 1 && N <= 8 * SW_NBMAX) return (N + 7) / 8;
+    if (N > 8 * SW_NBMAX && N <= 8 * SW_NBX && N % 2 == 0) return (N + 7) / 8;
+    return 0;
+}
 
 cudaError_t launch_bwd_mma(const SweepArgs &a_in, int nunits, int NB, cudaStream_t s)
 {
@@ -1924,6 +1958,13 @@ cudaError_t launch_bwd_mma(const SweepArgs &a_in, int nunits, int NB, cudaStream
             k_bwd_mma<nb, false><<<grid, 256, smem, s>>>(a);               \
         break;
         QDT_FOR_NB(QDT_CASE)
+#undef QDT_CASE
+#define QDT_CASE(nb)                                                       \
+    case nb:                                                               \
+        if (fis) return cudaErrorInvalidValue;                             \
+        k_bwd_mma<nb, false><<<grid, 256, smem, s>>>(a);                   \
+        break;
+        QDT_CASE(17) QDT_CASE(18) QDT_CASE(19) QDT_CASE(20)
 #undef QDT_CASE
         default: return cudaErrorInvalidValue;
     }

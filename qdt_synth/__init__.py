@@ -226,5 +226,77 @@ def random_instance(seed: int, D: int, M: int, N: int, mu_max: float | None = No
     return Instance(f"random{seed}", alpha2, M, P, gamma, 50, None)
 
 
+
+
+# ---------------------------------------------------------------- the paper's own detector
+TMD_R, TMD_ETA_LOOP, TMD_ETA_DET = 0.91644, 0.90524, 0.528   # fitted values
+
+
+def tmd_click_probs(i: np.ndarray, bins: int = 150) -> np.ndarray:
+    """Bin-click probabilities of the time-multiplexed detector for Fock inputs i (eq. pj_fock,
+    PAPER.md:208-217): p_1 = 1 - (1 - R eta_det)^i, p_j = 1 - [1 - (1-R)^2 R^-1 (R eta_loop)^(j-1)
+    eta_det]^i for j >= 2.  Returns (len(i), bins)."""
+    R, el, ed = TMD_R, TMD_ETA_LOOP, TMD_ETA_DET
+    j = np.arange(1, bins + 1, dtype=float)
+    q = np.where(j == 1, R * ed, (1 - R) ** 2 / R * (R * el) ** (j - 1) * ed)   # per-photon probability
+    i = np.asarray(i, dtype=float)[:, None]
+    return -np.expm1(i * np.log1p(-q)[None, :])
+
+
+def theta_tmd(M: int, bins: int = 150, block: int = 2048) -> np.ndarray:
+    """Analytic POVM of the detector: outcome n = number of clicked bins among
+    the first `bins` (N = bins + 1 = 151), the Poisson-binomial distribution of independent bin
+    clicks with probabilities p_j(i); computed by the exact DP over bins (after j bins only
+    counts <= j are reachable), blocks of rows on a thread pool (numpy releases the GIL)."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    N = bins + 1
+    T = np.empty((M, N))
+
+    def run(r0):
+        r1 = min(M, r0 + block)
+        p = tmd_click_probs(np.arange(r0, r1), bins)
+        q = 1.0 - p
+        dp = np.zeros((r1 - r0, N))
+        dp[:, 0] = 1.0
+        for j in range(bins):
+            pj, qj = p[:, j:j + 1], q[:, j:j + 1]
+            hi = dp[:, :j + 1] * pj
+            dp[:, :j + 1] *= qj
+            dp[:, 1:j + 2] += hi
+        T[r0:r1] = dp
+
+    with ThreadPoolExecutor(min(16, os.cpu_count() or 1)) as ex:
+        list(ex.map(run, range(0, M, block)))
+    return T
+
+
+def paper_tmd(D: int = 1076, seed: int = 0, trials: int = 5 * 10 ** 5, noiseless: bool = False,
+              gamma: float = 0.0) -> Instance:
+    """Paper-shaped synthetic workload: quadratic probes |alpha_d|^2 = d^2
+    (PAPER.md:112, 190), cutoff M covering the last probe's band, the analytic time-multiplexed
+    detector POVM with the paper's fitted parameters, multinomial noise at 5e5 trials per probe
+    (reading R6).  D = 1076 gives the paper's shape (M ~ 1.16e6, N = 151)."""
+    alpha2 = np.arange(D, dtype=float) ** 2
+    mu = alpha2[-1]
+    M = int(mu + 6 * np.sqrt(mu) + 100)
+    T = theta_tmd(M)
+    E = np.asarray(coherent_matrix(alpha2, M) @ T)
+    if noiseless:
+        P = E
+    else:
+        rng = np.random.Generator(np.random.PCG64(seed))
+        P = _multinomial_rows(rng, E, trials)
+    return Instance(f"paper_tmd{D}", alpha2, M, P, gamma, 300, T)
+
+
+def fidelities(theta: np.ndarray, theta_true: np.ndarray) -> np.ndarray:
+    """Per-outcome fidelity of diagonal POVM elements (eq. fidelities, diagonal
+    form): F_n = (sum_i sqrt(theta_in t_in))^2 / (sum_i theta_in sum_i t_in)."""
+    num = np.sum(np.sqrt(np.clip(theta, 0, None) * theta_true), axis=0) ** 2
+    den = theta.sum(0) * theta_true.sum(0)
+    return np.where(den > 0, num / np.where(den > 0, den, 1), np.nan)
+
+
 CONFIGS = {"tiny": tiny, "medium": medium, "large": large, "megascale": megascale,
-           "stress_cut": stress_cut}
+           "stress_cut": stress_cut, "paper_tmd": paper_tmd}

@@ -340,11 +340,14 @@ def test_stress_cut_solve_parity(q, ctx):
     assert Th.min() >= 0 and np.abs(Th.sum(1) - 1).max() <= 4 * Th.shape[1] * EPS
 
 
-@pytest.mark.parametrize("N,accel", [(200, 0), (1000, 0), (151, 0), (250, 1)])
+@pytest.mark.parametrize("N,accel", [(200, 0), (1000, 0), (151, 0), (250, 1), (151, 1), (129, 0),
+                                     (1023, 0), (152, 0), (160, 0), (137, 0), (162, 0)])
 def test_wide_sweep_parity(q, ctx, N, accel):
-    """N > 128: even N runs the wide sweep (128-column DMMA gradient chunks + warp-per-row
-    projection + column-chunked forward); odd N (151, the paper's outcome count) and FISTA the
-    general kernels.  25 iterations against the oracle."""
+    """N > 128: the wide sweep (balanced column-chunk DMMA gradient + warp-per-row projection +
+    column-chunked forward), plain and FISTA; plain steps at N <= 160 take k_bwd_mma with 17-20
+    n-blocks instead; odd N (151, the paper's outcome count) runs on a row pitch N + 1 with a
+    zero pad column excluded from the projection and the KKT.  25 iterations against the
+    oracle."""
     rng = np.random.default_rng(N)
     D, M = 300, 6000
     a2 = np.geomspace(0.5, 0.9 * M, D)
@@ -449,3 +452,48 @@ def test_bb_step_parity(q, ctx):
     assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9
     with pytest.raises(q.QdtError, match="INVALID_ARG"):
         q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, 5, step=q.QDT_STEP_BB, accel=True)
+
+
+def test_odd_wide_theta0_device_and_objective(q, ctx):
+    """Padded-pitch odd N through every entry: host theta0, device P/theta0/out, qdt_objective."""
+    import torch
+    rng = np.random.default_rng(7)
+    D, M, N = 90, 1500, 151
+    a2 = np.geomspace(0.5, 0.9 * M, D)
+    P = rng.dirichlet(np.ones(N) * 0.3, D)
+    th0 = rng.dirichlet(np.ones(N), M)
+    Fo = oracle.Probes(a2, M)
+    Fg = q.qdt_build_probes(ctx, a2, M)
+    ro = oracle.solve(Fo, P, 1e-3, 0.0, 12, theta0=th0)
+    rg = q.qdt_solve(ctx, Fg, P, 1e-3, 0.0, 12, theta0=th0)
+    assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9
+    Pd = torch.tensor(P, device="cuda")
+    td = torch.tensor(th0, device="cuda")
+    rd = q.qdt_solve(ctx, Fg, Pd, 1e-3, 0.0, 12, theta0=td)
+    th = rd["theta"].cpu().numpy() if hasattr(rd["theta"], "cpu") else rd["theta"]
+    assert np.array_equal(th, rg["theta"])
+    f, r = q.qdt_objective(ctx, Fg, P, ro["theta"], 1e-3)
+    assert f == pytest.approx(oracle.objective(Fo, P, ro["theta"], 1e-3), rel=1e-12)
+    # early stop on the KKT tolerance: same stopping iteration (post-stop evaluation pass)
+    full = oracle.solve(Fo, P, 1e-3, 0.0, 80)
+    tol = full["kkt"][41] * (1 + 1e-7)
+    ro2 = oracle.solve(Fo, P, 1e-3, tol, 80)
+    rg2 = q.qdt_solve(ctx, Fg, P, 1e-3, tol, 80, check_every=16)
+    assert rg2["info"]["iters_done"] == ro2["iters_done"] and rg2["info"]["converged"] == 1
+    assert np.abs(rg2["theta"] - ro2["theta"]).max() <= 1e-9
+    R = oracle.forward(Fo, ro["theta"], P)
+    G = oracle.backward(Fo, R, ro["theta"], 1e-3)
+    assert r == pytest.approx(oracle.kkt(ro["theta"], G)[0], rel=1e-8)
+
+
+def test_paper_tmd_parity(q, ctx):
+    """The paper's detector workload shape: quadratic probes, N = 151
+    outcomes of the analytic time-multiplexed-detector POVM, multinomial noise; D = 60."""
+    I = qs.paper_tmd(60)
+    Fo = oracle.Probes(I.alpha2, I.M)
+    Fg = q.qdt_build_probes(ctx, I.alpha2, I.M)
+    for accel in (0, 1):
+        ro = oracle.solve(Fo, I.P, 1e-4, 0.0, 20, accel=accel, kkt_every=5 if accel else 1)
+        rg = q.qdt_solve(ctx, Fg, I.P, 1e-4, 0.0, 20, accel=bool(accel), kkt_every=5 if accel else 1)
+        assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9
+        assert _trace_ok(rg["trace"], ro["trace"], I.P)
