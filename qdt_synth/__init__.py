@@ -272,14 +272,16 @@ def theta_tmd(M: int, bins: int = 150, block: int = 2048) -> np.ndarray:
 
 
 def paper_tmd(D: int = 1076, seed: int = 0, trials: int = 5 * 10 ** 5, noiseless: bool = False,
-              gamma: float = 0.0) -> Instance:
+              gamma: float = 1e-5, M: int | None = None) -> Instance:
     """Paper-shaped synthetic workload: quadratic probes |alpha_d|^2 = d^2
     (PAPER.md:112, 190), cutoff M covering the last probe's band, the analytic time-multiplexed
     detector POVM with the paper's fitted parameters, multinomial noise at 5e5 trials per probe
-    (reading R6).  D = 1076 gives the paper's shape (M ~ 1.16e6, N = 151)."""
+    (reading R6).  D = 1076 gives the paper's shape (M = 1 210 581, N = 151,
+    PAPER.md:124) with its nearest-neighbour gamma = 1e-5."""
     alpha2 = np.arange(D, dtype=float) ** 2
     mu = alpha2[-1]
-    M = int(mu + 6 * np.sqrt(mu) + 100)
+    if M is None:   # the paper's cutoff at its D (PAPER.md:124), else just past the last band
+        M = 1210581 if D == 1076 else int(mu + 6 * np.sqrt(mu) + 100)
     T = theta_tmd(M)
     E = np.asarray(coherent_matrix(alpha2, M) @ T)
     if noiseless:

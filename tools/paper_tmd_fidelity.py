@@ -3,7 +3,7 @@ through the C ABI to KKT tolerances and report the per-outcome fidelity of the r
 POVM against the analytic one (eq. fidelities, diagonal form), the figure
 the paper quotes (> 99 %), beside iterations and wall time.
 
-    python tools/paper_tmd_fidelity.py [--D 1076] [--gamma 0] [--tols 1e-3,1e-4,1e-5]
+    python tools/paper_tmd_fidelity.py [--D 1076] [--gamma 1e-5] [--tols 1e-3,1e-4,1e-5]
 """
 import argparse
 import json
@@ -21,7 +21,7 @@ import paper_2404_02844_b200 as q  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--D", type=int, default=1076)
-    ap.add_argument("--gamma", type=float, default=0.0)
+    ap.add_argument("--gamma", type=float, default=1e-5)
     ap.add_argument("--tols", default="1e-3,1e-4,1e-5")
     ap.add_argument("--cap", type=int, default=20000)
     ap.add_argument("--noiseless", action="store_true")
