@@ -18,7 +18,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqdt.so")
+LIB_PATH = os.environ.get("QDT_LIB") or os.path.join(_HERE, "libqdt.so")   # QDT_LIB: in-tree A/B build
 
 QDT_STEP_SQS, QDT_STEP_LIPSCHITZ, QDT_STEP_BB = 0, 1, 2
 STATUS = {0: "QDT_OK", 1: "QDT_ERR_INVALID_ARG", 2: "QDT_ERR_UNSORTED", 3: "QDT_ERR_NONFINITE",

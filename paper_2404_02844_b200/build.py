@@ -73,5 +73,27 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(tag: str, defines, src: str = "qdt_sweep.cu") -> str:
+    """A/B build: `src` recompiled with extra -D flags, linked with the main objects into
+    libqdt_<tag>.so (load it with QDT_LIB=<path>)."""
+    build()
+    out_dir = os.path.join(HERE, "build_" + tag)
+    os.makedirs(out_dir, exist_ok=True)
+    s = os.path.join(HERE, "csrc", src)
+    obj = os.path.join(out_dir, src.replace(".cu", ".o"))
+    r = subprocess.run([NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-c", s, "-o", obj],
+                       capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(r.stderr[-6000:])
+    with open(os.path.join(out_dir, "ptxas.log"), "w") as f:
+        f.write(r.stdout + r.stderr)
+    objs = [obj if os.path.basename(x) == src else _obj(x) for x in SRCS]
+    lib = os.path.join(HERE, f"libqdt_{tag}.so")
+    r = subprocess.run([NVCC, *ARCH, "-shared", "-o", lib, *objs, "-ldl"], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(r.stderr[-6000:])
+    return lib
+
+
 if __name__ == "__main__":
     build(force=True, verbose=True)

@@ -327,14 +327,20 @@ __device__ __forceinline__ void row_pass(double (&acc)[NBA][2], const double *th
             if (ok) {
                 s += x;
                 xm = x > xm ? x : xm;
+#ifndef QDT_NO_XN
                 xn = x < xn ? x : xn;
+#endif
             }
             acc[nb][i] = ok ? x : -INFINITY;
         }
     }
     s = quad_sum(s);
     xm = quad_max(xm);
+#ifndef QDT_NO_XN
     xn = quad_min(xn);
+#else
+    xn = -INFINITY;   // A/B: no all-active shortcut (the first Michelot round finds it)
+#endif
     if (PAIR) {
         double v[3] = {s, xm, xn}, o[3];
         pair_xchg<3>(*px, v, o);
@@ -363,6 +369,11 @@ __device__ __forceinline__ void row_project(double (&acc)[NBA][2], double *thr, 
     bool done = !ract || xn > tau;
     if (!done) tau = fmax(tau, xm - 1.0);
     int cnt = N + 1;
+#ifdef QDT_MICH_NOMIN
+    constexpr bool kMin = false;   // A/B: stop only when |A| stops shrinking (one more round, no min)
+#else
+    constexpr bool kMin = true;
+#endif
     for (int round = 0; round <= N; round++) {
         if (__all_sync(0xffffffffu, done)) break;
         double ps = 0.0, mA = INFINITY;
@@ -375,12 +386,12 @@ __device__ __forceinline__ void row_project(double (&acc)[NBA][2], double *thr, 
                 if (x > tau) {
                     ps += x;
                     pc++;
-                    mA = x < mA ? x : mA;
+                    if (kMin) mA = x < mA ? x : mA;
                 }
             }
         ps = quad_sum(ps);
         pc = quad_sum_i(pc);
-        mA = quad_min(mA);
+        if (kMin) mA = quad_min(mA);
         if (PAIR) {
             double v[3] = {ps, (double)pc, mA}, o[3];
             pair_xchg<3>(*px, v, o);
@@ -394,7 +405,7 @@ __device__ __forceinline__ void row_project(double (&acc)[NBA][2], double *thr, 
             } else {
                 cnt = pc;
                 tau = (ps - 1.0) / (double)pc;
-                done = mA > tau;
+                done = kMin && mA > tau;
             }
         }
     }
@@ -959,10 +970,11 @@ __global__ void __launch_bounds__(512, 1) k_bwd_split(SweepArgs a)
 // C[n][d] += sum_k Theta[k][n] F[d][k] for one outcome m-block (lane row n = 8 mb + g4) and NM
 // probe n-blocks (lane columns d = 8 nb + 2 t4 + {0,1}).  A fragment a = Theta[4 ks + t4][n],
 // B fragment b = F[8 nb + g4][4 ks + t4].  Tcol: Theta + t4 N + 8 mb + g4; Frow: F + g4 STP + t4.
-// Rows k >= Tt are masked (stale shared memory); probe masks are applied by the caller via fok.
+// Rows k >= Tt are masked (stale shared memory); probe rows outside the tile's window are zero
+// in shared memory (the caller zero-fills them), so the B fragments need no mask.
 template <int NM, bool MASKK, int MX>
 __device__ __forceinline__ void gemm_fwd_t(double (&cf)[MX][2], const double *Tcol, const double *Frow,
-                                           int N, int Tt, int t4, const bool (&fok)[MX])
+                                           int N, int Tt, int t4)
 {
     const int nks = (Tt + 3) >> 2;
     for (int ks = 0; ks < nks; ks++) {
@@ -971,25 +983,24 @@ __device__ __forceinline__ void gemm_fwd_t(double (&cf)[MX][2], const double *Tc
 #pragma unroll
         for (int nb = 0; nb < NM; nb++) {
             const double bv = Frow[8 * nb * STP + 4 * ks];
-            dmma(cf[nb][0], cf[nb][1], av, fok[nb] ? bv : 0.0);
+            dmma(cf[nb][0], cf[nb][1], av, bv);
         }
     }
 }
 
 template <bool MASKK, int MX>
 __device__ __forceinline__ void gemm_fwd_t_nm(int nm, double (&cf)[MX][2], const double *Tcol,
-                                              const double *Frow, int N, int Tt, int t4,
-                                              const bool (&fok)[MX])
+                                              const double *Frow, int N, int Tt, int t4)
 {
     switch (nm) {
-        case 1: gemm_fwd_t<1, MASKK, MX>(cf, Tcol, Frow, N, Tt, t4, fok); break;
-        case 2: gemm_fwd_t<(MX >= 2 ? 2 : 1), MASKK, MX>(cf, Tcol, Frow, N, Tt, t4, fok); break;
-        case 3: gemm_fwd_t<(MX >= 3 ? 3 : 1), MASKK, MX>(cf, Tcol, Frow, N, Tt, t4, fok); break;
-        case 4: gemm_fwd_t<(MX >= 4 ? 4 : 1), MASKK, MX>(cf, Tcol, Frow, N, Tt, t4, fok); break;
-        case 5: gemm_fwd_t<(MX >= 5 ? 5 : 1), MASKK, MX>(cf, Tcol, Frow, N, Tt, t4, fok); break;
-        case 6: gemm_fwd_t<(MX >= 6 ? 6 : 1), MASKK, MX>(cf, Tcol, Frow, N, Tt, t4, fok); break;
-        case 7: gemm_fwd_t<(MX >= 7 ? 7 : 1), MASKK, MX>(cf, Tcol, Frow, N, Tt, t4, fok); break;
-        case 8: gemm_fwd_t<(MX >= 8 ? 8 : 1), MASKK, MX>(cf, Tcol, Frow, N, Tt, t4, fok); break;
+        case 1: gemm_fwd_t<1, MASKK, MX>(cf, Tcol, Frow, N, Tt, t4); break;
+        case 2: gemm_fwd_t<(MX >= 2 ? 2 : 1), MASKK, MX>(cf, Tcol, Frow, N, Tt, t4); break;
+        case 3: gemm_fwd_t<(MX >= 3 ? 3 : 1), MASKK, MX>(cf, Tcol, Frow, N, Tt, t4); break;
+        case 4: gemm_fwd_t<(MX >= 4 ? 4 : 1), MASKK, MX>(cf, Tcol, Frow, N, Tt, t4); break;
+        case 5: gemm_fwd_t<(MX >= 5 ? 5 : 1), MASKK, MX>(cf, Tcol, Frow, N, Tt, t4); break;
+        case 6: gemm_fwd_t<(MX >= 6 ? 6 : 1), MASKK, MX>(cf, Tcol, Frow, N, Tt, t4); break;
+        case 7: gemm_fwd_t<(MX >= 7 ? 7 : 1), MASKK, MX>(cf, Tcol, Frow, N, Tt, t4); break;
+        case 8: gemm_fwd_t<(MX >= 8 ? 8 : 1), MASKK, MX>(cf, Tcol, Frow, N, Tt, t4); break;
         default: break;
     }
 }
@@ -1071,7 +1082,22 @@ __global__ void __launch_bounds__(256, 2) k_fwd_mma(SweepFwdArgs a)
             bulk_g2s(Fs + ((h >> 1) & 1) * FWCAP * STP + (ra - u.u0) * STP,
                      a.Fb + a.fb_off[t] + (int64_t)(ra - dA) * STP, fby, bar);
     };
+    // union probes outside a tile's window [ra, rb) would hold stale F rows: zero them in the
+    // tile's F buffer (disjoint from the rows the bulk copy writes), so B fragments need no mask
+    auto zfill = [&](int h) {
+        const int t = u.t0 + (h >> 1);
+        int ra = max(a.tile_dA[t], u.u0) - u.u0, rb = min(a.tile_dB[t], u.u1) - u.u0;
+        if (rb <= ra) ra = rb = 0;
+        double *Fz = Fs + ((h >> 1) & 1) * FWCAP * STP;
+        const int nz = ra + (Wu - rb);
+        for (int i = tid; i < nz * ST; i += 256) {
+            const int r = i / ST, c = i - r * ST;
+            Fz[(r < ra ? r : rb + (r - ra)) * STP + c] = 0.0;
+        }
+    };
     if (tid == 0) issue(0);
+    zfill(0);
+    __syncthreads();
 
     double cA[FWNB][2], cB[FWNB][2];
 #pragma unroll
@@ -1079,25 +1105,21 @@ __global__ void __launch_bounds__(256, 2) k_fwd_mma(SweepFwdArgs a)
 
     for (int h = 0; h < nh; h++) {
         if (tid == 0 && h + 1 < nh) issue(h + 1);
+        if (h + 1 < nh && !((h + 1) & 1)) zfill(h + 1);   // buffer last read at step h - 2
         mbar_wait(&bars[h & 1], (h >> 1) & 1);
         const int t = u.t0 + (h >> 1), half = h & 1;
         const int k0 = t * ST + half * FH;
         const int rows = min(FH, a.Ml - k0);
         if (rows > 0) {
             const int sh = ncc > 1 ? 0 : (int)(((uintptr_t)(a.theta + (int64_t)k0 * N) & 15) >> 3);
-            // union probes outside this tile's window hold stale F rows: their B fragments -> 0
-            const int ra = max(a.tile_dA[t], u.u0) - u.u0, rb = min(a.tile_dB[t], u.u1) - u.u0;
-            bool fok[FWNB];
-#pragma unroll
-            for (int nb = 0; nb < FWNB; nb++) fok[nb] = 8 * nb + g4 >= ra && 8 * nb + g4 < rb;
             const double *T = Ts + (h & 1) * tsz + sh + t4 * TP + g4;
             const double *Frow = Fs + ((h >> 1) & 1) * FWCAP * STP + g4 * STP + t4 + half * FH;
             if (rows == FH) {
-                gemm_fwd_t_nm<false>(nm, cA, T + 8 * warp, Frow, TP, FH, t4, fok);
-                if (second) gemm_fwd_t_nm<false>(nm, cB, T + 8 * (warp + 8), Frow, TP, FH, t4, fok);
+                gemm_fwd_t_nm<false>(nm, cA, T + 8 * warp, Frow, TP, FH, t4);
+                if (second) gemm_fwd_t_nm<false>(nm, cB, T + 8 * (warp + 8), Frow, TP, FH, t4);
             } else {
-                gemm_fwd_t_nm<true>(nm, cA, T + 8 * warp, Frow, TP, rows, t4, fok);
-                if (second) gemm_fwd_t_nm<true>(nm, cB, T + 8 * (warp + 8), Frow, TP, rows, t4, fok);
+                gemm_fwd_t_nm<true>(nm, cA, T + 8 * warp, Frow, TP, rows, t4);
+                if (second) gemm_fwd_t_nm<true>(nm, cB, T + 8 * (warp + 8), Frow, TP, rows, t4);
             }
         }
         __syncthreads();
@@ -1247,7 +1269,6 @@ __global__ void __launch_bounds__(256, 1) k_sweep_fused(SweepFusedArgs a)
             for (int nb = 0; nb < 4; nb++)
 #pragma unroll
                 for (int i = 0; i < 2; i++) slot[nb][i] = ((dA + 8 * nb + 2 * t4 + i) % cap) * RP;
-            const bool fok[4] = {true, true, true, true};
             const double *Frow = Fs + g4 * STP + t4;
             for (int mbo = warp; mbo < NB; mbo += 8) {
                 double cf[4][2];
@@ -1255,9 +1276,9 @@ __global__ void __launch_bounds__(256, 1) k_sweep_fused(SweepFusedArgs a)
                 for (int nb = 0; nb < 4; nb++) cf[nb][0] = cf[nb][1] = 0.0;
                 const double *Tcol = Th + N + t4 * N + 8 * mbo + g4;   // Theta_{k+1}, tile row 0
                 if (Tt == ST)
-                    gemm_fwd_t_nm<false>(nm, cf, Tcol, Frow, N, Tt, t4, fok);
+                    gemm_fwd_t_nm<false>(nm, cf, Tcol, Frow, N, Tt, t4);
                 else
-                    gemm_fwd_t_nm<true>(nm, cf, Tcol, Frow, N, Tt, t4, fok);
+                    gemm_fwd_t_nm<true>(nm, cf, Tcol, Frow, N, Tt, t4);
                 const int n = 8 * mbo + g4;
                 if (n < N) {
 #pragma unroll

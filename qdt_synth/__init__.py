@@ -280,8 +280,13 @@ def paper_tmd(D: int = 1076, seed: int = 0, trials: int = 5 * 10 ** 5, noiseless
     PAPER.md:124) with its nearest-neighbour gamma = 1e-5."""
     alpha2 = np.arange(D, dtype=float) ** 2
     mu = alpha2[-1]
-    if M is None:   # the paper's cutoff at its D (PAPER.md:124), else just past the last band
-        M = 1210581 if D == 1076 else int(mu + 6 * np.sqrt(mu) + 100)
+    if M is None and D == 1076:
+        M = 1210581                  # the paper's cutoff at its D (PAPER.md:124)
+    if M is None:                    # just past the last probe's band
+        M = int(mu + 6 * np.sqrt(mu) + 100)
+    else:                            # |alpha_d|^2 ~ d^2 scaled so the last band reaches M - 100
+        mu_top = (-3.0 + np.sqrt(9.0 + M - 100)) ** 2
+        alpha2 = alpha2 * (mu_top / max(mu, 1.0))
     T = theta_tmd(M)
     E = np.asarray(coherent_matrix(alpha2, M) @ T)
     if noiseless:
