@@ -83,6 +83,18 @@ def lib():
         L.or_solve.restype = i64
         L.or_smooth.argtypes = [_f64p, i64, i64, i64, i64, _f64p]
         L.or_smooth.restype = None
+        L.or_hess_diag.argtypes = [_i64p, _i64p, _i64p, _f64p, i64, i64, f64, _f64p]
+        L.or_hess_diag.restype = None
+        L.or_row_argmax.argtypes = [_f64p, i64, i64, _i64p]
+        L.or_row_argmax.restype = None
+        L.or_newton_direction.argtypes = [_i64p, _i64p, _i64p, _f64p, i64, i64, _f64p, i64, f64, _f64p,
+                                          ctypes.c_void_p, f64, i64, _f64p, ctypes.POINTER(f64)]
+        L.or_newton_direction.restype = i64
+        L.or_newton.argtypes = [_i64p, _i64p, _i64p, _f64p, i64, i64, _f64p, i64, f64, _f64p, i64, f64,
+                                f64, i64, f64, i64, _f64p, _f64p, _i64p, _i64p, _f64p, ctypes.POINTER(i64)]
+        L.or_newton.restype = i64
+        L.or_newton_set_cg_rtol.argtypes = [f64]
+        L.or_newton_set_cg_rtol.restype = None
         _lib = L
     return _lib
 
@@ -234,3 +246,56 @@ def smooth(Theta, exclude: int = 100, div: int = 50):
     out = np.empty_like(Theta)
     lib().or_smooth(Theta, Theta.shape[0], Theta.shape[1], int(exclude), int(div), out)
     return out
+
+
+def hess_diag(F: Probes, gamma: float):
+    """h_i = 2 (sum_d F_{d,i}^2 + gamma L_ii): Hessian diagonal per Fock row (Table 1)."""
+    h = np.empty(F.M)
+    lib().or_hess_diag(F.lo, F.len, F.off, F.val, F.D, F.M, float(gamma), h)
+    return h
+
+
+def row_argmax(Theta):
+    Theta = _f(Theta)
+    m = np.empty(Theta.shape[0], dtype=np.int64)
+    lib().or_row_argmax(Theta, Theta.shape[0], Theta.shape[1], m)
+    return m
+
+
+NEWTON_DEFAULTS = dict(eps_active=1e-8, cg_max=50, switch_tol=1e-4, max_ls=60)
+
+
+def newton_direction(F: Probes, P, gamma: float, Theta, m=None, eps_active: float = 1e-8,
+                     cg_max: int = 50, cg_rtol: float = -1.0):
+    """One two-metric Newton direction (stage 1: m None; stage 2: row maxima m).
+    cg_rtol >= 0 replaces CG's forcing term (pins).  Returns (p, slope, cg_iterations)."""
+    P, Theta = _f(P), _f(Theta)
+    lib().or_newton_set_cg_rtol(float(cg_rtol))
+    p = np.empty_like(Theta)
+    sl = ctypes.c_double()
+    mp = None if m is None else np.ascontiguousarray(m, dtype=np.int64)
+    it = lib().or_newton_direction(F.lo, F.len, F.off, F.val, F.D, F.M, P, P.shape[1], float(gamma),
+                                   Theta, None if mp is None else mp.ctypes.data, float(eps_active),
+                                   int(cg_max), p, ctypes.byref(sl))
+    return p, sl.value, int(it)
+
+
+def newton(F: Probes, P, gamma: float, max_iter: int, eps_kkt: float = 0.0, theta0=None,
+           eps_active: float = 1e-8, cg_max: int = 50, switch_tol: float = 1e-4, max_ls: int = 60):
+    """Two-stage two-metric projected truncated Newton (reading R16)."""
+    P = _f(P)
+    N = P.shape[1]
+    Theta = np.full((F.M, N), 1.0 / N) if theta0 is None else _f(theta0).copy()
+    tr = np.full(max_iter + 1, np.nan)
+    kk = np.full(max_iter + 1, np.nan)
+    st = np.zeros(max_iter + 1, dtype=np.int64)
+    cg = np.zeros(max_iter + 1, dtype=np.int64)
+    al = np.full(max_iter + 1, np.nan)
+    sw = ctypes.c_int64()
+    lib().or_newton_set_cg_rtol(-1.0)
+    k = lib().or_newton(F.lo, F.len, F.off, F.val, F.D, F.M, P, N, float(gamma), Theta, int(max_iter),
+                        float(eps_kkt), float(eps_active), int(cg_max), float(switch_tol), int(max_ls),
+                        tr, kk, st, cg, al, ctypes.byref(sw))
+    return dict(theta=Theta, trace=tr[:k + 1], kkt=kk[:k + 1], stage=st[:k], cg=cg[:k], alpha=al[:k],
+                iters_done=int(k), switch=int(sw.value))
+

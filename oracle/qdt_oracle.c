@@ -490,3 +490,352 @@ void or_smooth(const double *Theta, int64_t M, int64_t N, int64_t exclude, int64
         }
     }
 }
+
+/* ------------------------------------------------------------------------------------
+ * Two-stage, two-metric projected truncated Newton (Alg. 3 of PAPER.md:536-544: stage 1 =
+ * Alg. 2, stage 2 = Alg. 1), SURVEY 8(f) row 1.
+ * Readings (R16): f is the paper's objective incl. gamma * regul; df = 2G (R0);
+ * H d = 2 (F^T F d + gamma L d) acts on each column of d independently (Table 1 "Hessian
+ * products"); its diagonal h_i = 2 (sum_d F_{d,i}^2 + gamma L_ii) (Table 1,
+ * PAPER.md:245).  The metric D of eq. 2metric D / I: entries in the active
+ * set I = {x <= eps, df > 0} keep only their diagonal, the others the Hessian restricted to
+ * the free set; D p = -df is solved by diagonally preconditioned CG from p = 0,
+ * truncated at cg_max iterations or ||r|| <= min(0.5, sqrt||b||) ||b|| (Nocedal-Wright's
+ * forcing sequence; the paper only says "truncated").  Line search alpha = beta^m, beta = 3/4,
+ * c = 1/10 with Bertsekas' Armijo rule along the projection arc:
+ * f(x(alpha)) <= f(x) + c df . (x(alpha) - x).  Stage switch when the
+ * one-sided derivative of the stage-1 arc at alpha = 0, df . d0 with d0 the projection of p
+ * onto the simplex tangent cone at Theta, satisfies |df . d0| <= switch_tol.  Stop when the
+ * KKT measure (R7, unclamped multiplier) <= eps_kkt, or when no step length is accepted in
+ * stage 2; a stage-1 iteration that admits none switches to stage 2 (stage 1 carries no
+ * convergence proof).
+ * ---------------------------------------------------------------------------------- */
+typedef struct {
+    const int64_t *lo, *len, *off;
+    const double *val;
+    int64_t D, M, N;
+    const double *P;
+    double gamma;
+} or_prob;
+
+/* H v = 2 (F^T (F v) + gamma L v) */
+static void nt_hess(const or_prob *q, const double *v, double *out, double *Rw)
+{
+    or_forward(q->lo, q->len, q->off, q->val, q->D, v, NULL, q->N, Rw);
+    or_backward(q->lo, q->len, q->off, q->val, q->D, q->M, Rw, v, q->N, q->gamma, out);
+    for (int64_t i = 0; i < q->M * q->N; i++) out[i] *= 2.0;
+}
+
+/* df = 2 G(Theta) */
+static void nt_grad(const or_prob *q, const double *Th, double *g, double *Rw)
+{
+    or_forward(q->lo, q->len, q->off, q->val, q->D, Th, q->P, q->N, Rw);
+    or_backward(q->lo, q->len, q->off, q->val, q->D, q->M, Rw, Th, q->N, q->gamma, g);
+    for (int64_t i = 0; i < q->M * q->N; i++) g[i] *= 2.0;
+}
+
+static double nt_f(const or_prob *q, const double *Th)
+{
+    return or_objective(q->lo, q->len, q->off, q->val, q->D, q->M, q->P, Th, q->N, q->gamma);
+}
+
+static double dotl(const double *a, const double *b, int64_t n)
+{
+    long double s = 0.0L;
+    for (int64_t i = 0; i < n; i++) s += (long double)a[i] * (long double)b[i];
+    return (double)s;
+}
+
+/* Hessian diagonal per Fock row: h_i = 2 (sum_d F_{d,i}^2 + gamma L_ii) */
+void or_hess_diag(const int64_t *lo, const int64_t *len, const int64_t *off, const double *val,
+                  int64_t D, int64_t M, double gamma, double *h)
+{
+    for (int64_t i = 0; i < M; i++) h[i] = 0.0;
+    for (int64_t d = 0; d < D; d++)
+        for (int64_t j = 0; j < len[d]; j++) {
+            double f = val[off[d] + j];
+            h[lo[d] + j] += f * f;
+        }
+    for (int64_t i = 0; i < M; i++) {
+        double lii = (M > 1) ? ((i > 0) + (i < M - 1)) : 0.0;
+        h[i] = 2.0 * (h[i] + gamma * lii);
+    }
+}
+
+/* Tangent-cone projection of p at a point Theta of the simplex (one row):
+ * d = argmin ||d - p|| s.t. sum d = 0, d_j >= 0 where Theta_j = 0.  d_j = p_j - mu on the
+ * support, max(p_j - mu, 0) on the zeros; mu solves sum d(mu) = 0 (sort of the breakpoints). */
+static void nt_tangent_row(const double *th, const double *p, int64_t N, double *d, double *work)
+{
+    int64_t nf = 0, nz = 0;
+    double sf = 0.0;
+    for (int64_t j = 0; j < N; j++) {
+        if (th[j] > 0.0) { sf += p[j]; nf++; } else work[nz++] = p[j];
+    }
+    qsort(work, (size_t)nz, sizeof(double), cmp_desc);
+    /* h(mu) = sf - nf mu + sum_{zeros} max(p_j - mu, 0), decreasing; find the root */
+    double mu;
+    if (nf == 0 && nz == 0) return;
+    double cum = 0.0;
+    int64_t k = 0;       /* number of zero-entries above mu */
+    mu = (nf > 0) ? sf / (double)nf : work[0];
+    if (nf > 0) {
+        /* candidate with the k largest zero entries active: mu = (sf + cum_k) / (nf + k) */
+        for (k = 0; k <= nz; k++) {
+            if (k > 0) cum += work[k - 1];
+            double m = (sf + cum) / (double)(nf + k);
+            double upper = (k > 0) ? work[k - 1] : INFINITY;   /* active ones must exceed mu */
+            double lower = (k < nz) ? work[k] : -INFINITY;     /* inactive ones must not */
+            if (m < upper && m >= lower) { mu = m; break; }
+        }
+    } else {
+        for (k = 1; k <= nz; k++) {
+            cum += work[k - 1];
+            double m = cum / (double)k;
+            double lower = (k < nz) ? work[k] : -INFINITY;
+            if (m >= lower) { mu = m; break; }
+        }
+    }
+    for (int64_t j = 0; j < N; j++) {
+        double v = p[j] - mu;
+        d[j] = (th[j] > 0.0) ? v : (v > 0.0 ? v : 0.0);
+    }
+}
+
+/* CG stopping rule override for the pins: rtol >= 0 replaces the forcing term (-1: default) */
+static double nt_cg_rtol = -1.0;
+void or_newton_set_cg_rtol(double rtol) { nt_cg_rtol = rtol; }
+
+/* Truncated PCG for the masked system: free entries (mask 0) solve H_FF x_F = b_F, active
+ * entries (mask 1) x = b / hdiag.  Stage 2 (m != NULL) works in the reduced variables of the
+ * transformation Theta_{i,m(i)} = 1 - sum_{n != m(i)} x_{i,n} (entries n = m(i) are held at 0)
+ * with H~ = Z^T H Z and diagonal 2 h_i.  Returns the CG iteration count. */
+static int64_t nt_pcg(const or_prob *q, const int64_t *m, const unsigned char *act, const double *hrow,
+                      const double *b, int64_t cg_max, double *x, double *ws)
+{
+    const int64_t M = q->M, N = q->N, n = M * N;
+    double *r = ws, *z = ws + n, *d = ws + 2 * n, *Hd = ws + 3 * n, *u = ws + 4 * n, *Rw = ws + 5 * n;
+    int64_t it = 0;
+    for (int64_t i = 0; i < n; i++) {
+        const int64_t k = i / N, c = i % N;
+        const double hd = m ? 2.0 * hrow[k] : hrow[k];
+        const int fixed = m && c == m[k];
+        x[i] = 0.0;
+        r[i] = 0.0;
+        if (fixed) continue;
+        if (act[i]) x[i] = hd > 0.0 ? b[i] / hd : 0.0;
+        else r[i] = b[i];
+    }
+    const double bn = sqrt(dotl(r, r, n));
+    const double tol = (nt_cg_rtol >= 0.0 ? nt_cg_rtol : fmin(0.5, sqrt(bn))) * bn;
+    for (int64_t i = 0; i < n; i++) {
+        const double hd = m ? 2.0 * hrow[i / N] : hrow[i / N];
+        z[i] = hd > 0.0 ? r[i] / hd : 0.0;
+        d[i] = z[i];
+    }
+    double rz = dotl(r, z, n);
+    for (it = 0; it < cg_max && bn > 0.0; it++) {
+        if (rz <= 0.0) break;
+        /* Hd = mask_F (H~ d) */
+        if (m) {
+            for (int64_t k = 0; k < M; k++) {
+                double s = 0.0;
+                for (int64_t c = 0; c < N; c++)
+                    if (c != m[k]) { u[k * N + c] = d[k * N + c]; s += d[k * N + c]; }
+                u[k * N + m[k]] = -s;
+            }
+            nt_hess(q, u, Hd, Rw);
+            for (int64_t k = 0; k < M; k++) {
+                const double hm = Hd[k * N + m[k]];
+                for (int64_t c = 0; c < N; c++) Hd[k * N + c] -= hm;
+                Hd[k * N + m[k]] = 0.0;
+            }
+        } else {
+            nt_hess(q, d, Hd, Rw);
+        }
+        for (int64_t i = 0; i < n; i++)
+            if (act[i]) Hd[i] = 0.0;
+        const double dHd = dotl(d, Hd, n);
+        if (dHd <= 0.0) break;
+        const double a = rz / dHd;
+        for (int64_t i = 0; i < n; i++) {
+            x[i] += a * d[i];
+            r[i] -= a * Hd[i];
+        }
+        if (sqrt(dotl(r, r, n)) <= tol) { it++; break; }
+        for (int64_t i = 0; i < n; i++) {
+            const double hd = m ? 2.0 * hrow[i / N] : hrow[i / N];
+            z[i] = hd > 0.0 ? r[i] / hd : 0.0;
+        }
+        const double rz2 = dotl(r, z, n);
+        const double beta = rz2 / rz;
+        rz = rz2;
+        for (int64_t i = 0; i < n; i++) d[i] = z[i] + beta * d[i];
+    }
+    return it;
+}
+
+/* One Newton direction (exposed for the pins): stage 1 (m == NULL) or stage 2 (row maxima m).
+ * g: df at Theta (stage 2: at the transformed Theta~); out p (M x N; stage 2: 0 at n = m(i));
+ * returns the CG iteration count; *slope = df . d0 (stage 1: d0 = tangent-cone projection of
+ * p; stage 2: d0 = p with p_j -> 0 where x_j = 0 and p_j < 0, in reduced variables). */
+int64_t or_newton_direction(const int64_t *lo, const int64_t *len, const int64_t *off,
+                            const double *val, int64_t D, int64_t M, const double *P, int64_t N,
+                            double gamma, const double *Theta, const int64_t *m, double eps_active,
+                            int64_t cg_max, double *p, double *slope)
+{
+    or_prob q = {lo, len, off, val, D, M, N, P, gamma};
+    const int64_t n = M * N;
+    double *g = malloc(sizeof(double) * n), *gr = malloc(sizeof(double) * n), *b = malloc(sizeof(double) * n);
+    double *h = malloc(sizeof(double) * M), *ws = malloc(sizeof(double) * (5 * n + D * N + N));
+    unsigned char *act = malloc((size_t)n);
+    or_hess_diag(lo, len, off, val, D, M, gamma, h);
+    nt_grad(&q, Theta, g, ws);
+    for (int64_t i = 0; i < n; i++) {
+        const int64_t k = i / N, c = i % N;
+        gr[i] = m ? (c == m[k] ? 0.0 : g[i] - g[k * N + m[k]]) : g[i];
+        act[i] = (!m || c != m[k]) && Theta[i] <= eps_active && gr[i] > 0.0;
+        b[i] = -gr[i];
+    }
+    const int64_t it = nt_pcg(&q, m, act, h, b, cg_max, p, ws);
+    if (slope) {
+        double s = 0.0;
+        if (!m) {
+            double *d0 = ws, *work = ws + n;
+            for (int64_t k = 0; k < M; k++) nt_tangent_row(Theta + k * N, p + k * N, N, d0 + k * N, work);
+            s = dotl(g, d0, n);
+        } else {
+            long double t = 0.0L;
+            for (int64_t i = 0; i < n; i++) {
+                const double pj = (Theta[i] <= 0.0 && p[i] < 0.0) ? 0.0 : p[i];
+                t += (long double)gr[i] * pj;
+            }
+            s = (double)t;
+        }
+        *slope = s;
+    }
+    free(g); free(gr); free(b); free(h); free(ws); free(act);
+    return it;
+}
+
+/* Row maxima m(i) = argmax_n Theta_{i,n}, first index on ties (Table 1 "row-maxima"). */
+void or_row_argmax(const double *Theta, int64_t M, int64_t N, int64_t *m)
+{
+    for (int64_t k = 0; k < M; k++) {
+        int64_t a = 0;
+        for (int64_t c = 1; c < N; c++)
+            if (Theta[k * N + c] > Theta[k * N + a]) a = c;
+        m[k] = a;
+    }
+}
+
+/* The two-stage solve.  Theta (M x N) in: start (rows on the simplex), out: result.
+ * Logs (length max_iter + 1): trace f_k, kkt r_KKT(Theta_k) (R7), stage of step k (1/2),
+ * CG iterations of step k, accepted alpha of step k.  Returns the iterations done (k of the
+ * returned Theta); *switch_out = first stage-2 iteration (-1 if none). */
+int64_t or_newton(const int64_t *lo, const int64_t *len, const int64_t *off, const double *val,
+                  int64_t D, int64_t M, const double *P, int64_t N, double gamma, double *Theta,
+                  int64_t max_iter, double eps_kkt, double eps_active, int64_t cg_max,
+                  double switch_tol, int64_t max_ls, double *trace, double *kkt, int64_t *stage_log,
+                  int64_t *cg_log, double *alpha_log, int64_t *switch_out)
+{
+    or_prob q = {lo, len, off, val, D, M, N, P, gamma};
+    const int64_t n = M * N;
+    const double beta = 0.75, c_arm = 0.1;
+    double *g = malloc(sizeof(double) * n), *G2 = malloc(sizeof(double) * n), *p = malloc(sizeof(double) * n);
+    double *T1 = malloc(sizeof(double) * n), *X = malloc(sizeof(double) * n), *Rw = malloc(sizeof(double) * D * N);
+    int64_t *mrow = malloc(sizeof(int64_t) * M);
+    int stage = 1;
+    int64_t k = 0;
+    if (switch_out) *switch_out = -1;
+    for (k = 0;; k++) {
+        nt_grad(&q, Theta, g, Rw);
+        for (int64_t i = 0; i < n; i++) G2[i] = 0.5 * g[i];
+        const double f = nt_f(&q, Theta);
+        double kp;
+        const double r = or_kkt(Theta, G2, M, N, &kp);
+        trace[k] = f;
+        kkt[k] = r;
+        if (r <= eps_kkt || k >= max_iter) break;
+        double slope = 0.0;
+        int64_t it = 0;
+        if (stage == 1) {
+            it = or_newton_direction(lo, len, off, val, D, M, P, N, gamma, Theta, NULL, eps_active, cg_max,
+                                     p, &slope);
+            if (fabs(slope) <= switch_tol) {
+                stage = 2;
+                if (switch_out) *switch_out = k;
+            }
+        }
+        int64_t used_stage = stage;
+        if (stage == 2) {
+            or_row_argmax(Theta, M, N, mrow);
+            for (int64_t i = 0; i < M; i++) {   /* transformation step (Alg. 1) */
+                double s = 0.0;
+                for (int64_t c = 0; c < N; c++)
+                    if (c != mrow[i]) s += Theta[i * N + c];
+                Theta[i * N + mrow[i]] = 1.0 - s;
+            }
+            it = or_newton_direction(lo, len, off, val, D, M, P, N, gamma, Theta, mrow, eps_active, cg_max,
+                                     p, &slope);
+            nt_grad(&q, Theta, g, Rw);   /* df at Theta~ (reduced gradient for the Armijo term) */
+        }
+        const double f0 = (stage == 2) ? nt_f(&q, Theta) : f;
+        double alpha = 0.0;
+        int accepted = 0;
+        for (int64_t l = 0; l < max_ls && !accepted; l++) {
+            const double a = pow(beta, (double)l);
+            if (used_stage == 1) {
+                for (int64_t i = 0; i < n; i++) X[i] = Theta[i] + a * p[i];
+                or_project_rows(X, M, N, T1);
+            } else {
+                for (int64_t i = 0; i < M; i++) {
+                    double s = 0.0;
+                    for (int64_t c = 0; c < N; c++) {
+                        if (c == mrow[i]) continue;
+                        double v = Theta[i * N + c] + a * p[i * N + c];
+                        v = v > 0.0 ? v : 0.0;   /* P_{0,inf} */
+                        T1[i * N + c] = v;
+                        s += v;
+                    }
+                    T1[i * N + mrow[i]] = 1.0 - s;
+                }
+                int ok = 1;
+                for (int64_t i = 0; i < M; i++)
+                    if (T1[i * N + mrow[i]] < 0.0) ok = 0;
+                if (!ok) continue;
+            }
+            /* Armijo along the arc: f(T1) <= f0 + c df . (T1 - Theta) (stage 2: reduced df) */
+            long double dd = 0.0L;
+            for (int64_t i = 0; i < n; i++) {
+                const int64_t rr = i / N, cc = i % N;
+                double gi = g[i];
+                if (used_stage == 2) {
+                    if (cc == mrow[rr]) continue;
+                    gi = g[i] - g[rr * N + mrow[rr]];
+                }
+                dd += (long double)gi * (long double)(T1[i] - Theta[i]);
+            }
+            const double f1 = nt_f(&q, T1);
+            if (f1 <= f0 + c_arm * (double)dd) {
+                accepted = 1;
+                alpha = a;
+            }
+        }
+        if (!accepted && used_stage == 1) {
+            /* stage 1 has no convergence guarantee: when its arc admits no
+             * step length, switch to the globally convergent stage 2 and redo iteration k */
+            stage = 2;
+            if (switch_out) *switch_out = k;
+            k--;
+            continue;
+        }
+        stage_log[k] = used_stage;
+        cg_log[k] = it;
+        alpha_log[k] = alpha;
+        if (!accepted) break;   /* no admissible step length: stalled */
+        memcpy(Theta, T1, sizeof(double) * n);
+    }
+    free(g); free(G2); free(p); free(T1); free(X); free(Rw); free(mrow);
+    return k;
+}

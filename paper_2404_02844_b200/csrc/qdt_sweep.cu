@@ -415,8 +415,13 @@ __device__ __forceinline__ void row_project(double (&acc)[NBA][2], double *thr, 
             const int gb = CB / 8 + nb;
             const int c = CB + 8 * nb + 2 * t4;
             double o0 = acc[nb][0] - tau, o1 = acc[nb][1] - tau;
+#ifdef QDT_CLAMP_ARITH
+            o0 = (o0 + fabs(o0)) * 0.5;   // A/B: max(o, 0) on the fp64 pipe (exact: 2o * 0.5 = o)
+            o1 = (o1 + fabs(o1)) * 0.5;
+#else
             o0 = o0 > 0.0 ? o0 : 0.0;
             o1 = o1 > 0.0 ? o1 : 0.0;
+#endif
             if (EVEN) {
                 if (gb < NB - 1 || (gb == NB - 1 && v0)) {
                     *reinterpret_cast<double2 *>(orow + c) = make_double2(o0, o1);
