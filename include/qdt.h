@@ -168,6 +168,45 @@ qdt_status qdt_objective(qdt_ctx *ctx, const qdt_probes *F, const double *P, con
 qdt_status qdt_smooth(qdt_ctx *ctx, const double *theta, int64_t M, int64_t N, int64_t exclude,
                       int64_t div, int32_t mem_device, double *out);
 
+/* Two-stage, two-metric projected truncated Newton (the paper's optimiser: Alg. 2 = stage 1,
+ * Alg. 1 = stage 2, Alg. 3 = the two stages; reading R16).
+ * Per outer iteration: df = 2 (F^T (F Theta - P) + gamma L Theta); the metric D of eq. 2metric
+ * (active set I = {theta <= eps_active, df > 0} keeps only the Hessian diagonal
+ * h_i = 2 (sum_d F_{d,i}^2 + gamma L_ii)); D p = -df by diagonally preconditioned CG from 0
+ * (H d = 2 (F^T F d + gamma L d), <= cg_max iterations, ||r|| <= min(1/2, sqrt||b||) ||b||);
+ * Armijo along the projection arc (beta = 3/4, c = 1/10, <= max_ls step lengths); stage 1
+ * arcs P_{S^M}[Theta + alpha p], stage 2 (row maxima m(i) eliminated by the sum constraint)
+ * arcs max(x + alpha p, 0); switch to stage 2 when |df . Pi_T(p)| <= switch_tol or when a
+ * stage-1 iteration admits no step length.  Stops when r_KKT (reading R7) <= eps_kkt, after
+ * max_iter iterations, or when stage 2 admits no step length.  Single rank only.
+ *   P, theta0: host (mem_device = 0) or device pointers, D x N / M x N row-major; theta0 NULL:
+ *   Theta_0 = 1/N.  theta_out: M x N (same memory kind).  trace_out / kkt_out: host arrays of
+ *   max_iter + 1 (NaN past the last iteration); stage_out / cg_out / alpha_out: host arrays of
+ *   max_iter (per accepted step), any may be NULL.  Errors: QDT_ERR_INVALID_ARG (shapes,
+ *   options, nranks > 1), QDT_ERR_NONFINITE, QDT_ERR_OOM, QDT_ERR_CUDA. */
+typedef struct {
+    int32_t max_iter;          /* outer iterations */
+    int32_t cg_max;            /* CG iterations per direction (default 50) */
+    int32_t max_ls;            /* step lengths tried per line search (default 60) */
+    int32_t mem_device;        /* 1: P / theta0 / theta_out are device pointers */
+    double eps_active;         /* active-set threshold (default 1e-8) */
+    double switch_tol;         /* stage switch |df . Pi_T(p)| (default 1e-4) */
+    const double *theta0;      /* optional start (rows on the simplex) */
+} qdt_newton_opts;
+
+typedef struct {
+    int64_t iters_done;        /* k of the returned Theta */
+    int64_t switch_iter;       /* first stage-2 iteration (-1: none) */
+    int64_t cg_total;          /* CG iterations (Hessian products) over the solve */
+    double f_final, kkt;       /* f and r_KKT of the returned Theta */
+    double loop_ms;            /* device time of the iterations (CUDA events) */
+} qdt_newton_info;
+
+qdt_status qdt_solve_newton(qdt_ctx *ctx, const qdt_probes *F, const double *P, int64_t N, double gamma,
+                            double eps_kkt, const qdt_newton_opts *opts, double *theta_out,
+                            double *trace_out, double *kkt_out, int32_t *stage_out, int32_t *cg_out,
+                            double *alpha_out, qdt_newton_info *info);
+
 /* ------------------------------------------------------------------------------ kernel hooks
  * The individual steps of one iteration, for per-kernel parity tests.  They run the same
  * kernels as qdt_solve.  All arrays are HOST pointers, full (global) sizes, nranks == 1. */

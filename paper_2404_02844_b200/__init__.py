@@ -30,7 +30,7 @@ ABI_SYMBOLS = ["qdt_init", "qdt_finalize", "qdt_last_error", "qdt_build_probes",
                "qdt_probes_export", "qdt_solve", "qdt_objective", "qdt_residual", "qdt_gradient",
                "qdt_step", "qdt_project_rows", "qdt_step_setup", "qdt_profile_enable",
                "qdt_profile_get", "qdt_launch_count", "qdt_nccl_unique_id", "qdt_shard_cuts",
-               "qdt_smooth"]
+               "qdt_smooth", "qdt_solve_newton"]
 
 
 class QdtError(RuntimeError):
@@ -54,6 +54,20 @@ class SolveOpts(ctypes.Structure):
                 ("check_every", ctypes.c_int32), ("kkt_every", ctypes.c_int32),
                 ("mem_device", ctypes.c_int32), ("gather_theta", ctypes.c_int32),
                 ("use_graph", ctypes.c_int32)]
+
+
+class NewtonOpts(ctypes.Structure):
+    _fields_ = [("max_iter", ctypes.c_int32), ("cg_max", ctypes.c_int32), ("max_ls", ctypes.c_int32),
+                ("mem_device", ctypes.c_int32), ("eps_active", ctypes.c_double),
+                ("switch_tol", ctypes.c_double), ("theta0", ctypes.c_void_p)]
+
+
+class NewtonInfo(ctypes.Structure):
+    _fields_ = [("iters_done", ctypes.c_int64), ("switch_iter", ctypes.c_int64), ("cg_total", ctypes.c_int64),
+                ("f_final", ctypes.c_double), ("kkt", ctypes.c_double), ("loop_ms", ctypes.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
 
 
 class SolveInfo(ctypes.Structure):
@@ -101,6 +115,8 @@ def load_library(path: str = LIB_PATH):
     L.qdt_nccl_unique_id.argtypes = [vp]
     L.qdt_shard_cuts.argtypes = [vp, vp, i64, i64, i32, vp]
     L.qdt_smooth.argtypes = [vp, vp, i64, i64, i64, i64, i32, vp]
+    L.qdt_solve_newton.argtypes = [vp, vp, vp, i64, f64, f64, P(NewtonOpts), vp, vp, vp, vp, vp, vp,
+                                   P(NewtonInfo)]
     for s in ABI_SYMBOLS:
         if s != "qdt_last_error":
             getattr(L, s).restype = ctypes.c_int
@@ -334,3 +350,31 @@ def qdt_smooth(ctx: Context, theta, exclude: int = 100, div: int = 50, out=None)
     _check(ctx, L.qdt_smooth(ctx.ptr, th.ctypes.data, th.shape[0], th.shape[1], int(exclude),
                              int(div), 0, out.ctypes.data))
     return out
+
+
+def qdt_solve_newton(ctx: Context, F: Probes, P, gamma: float, eps_kkt: float = 0.0, max_iter: int = 100,
+                     cg_max: int = 50, max_ls: int = 60, eps_active: float = 1e-8, switch_tol: float = 1e-4,
+                     theta0=None):
+    """Two-stage two-metric projected truncated Newton (include/qdt.h qdt_solve_newton; reading R16).
+    Host numpy P / theta0 (single rank).  Returns dict(theta, trace, kkt, stage, cg, alpha, info)."""
+    L = load_library()
+    P = _host(P)
+    D, N = P.shape
+    M = F.M
+    t0 = _host(theta0) if theta0 is not None else None
+    o = NewtonOpts(int(max_iter), int(cg_max), int(max_ls), 0, float(eps_active), float(switch_tol),
+                   t0.ctypes.data if t0 is not None else None)
+    theta = np.empty((M, N))
+    tr = np.full(max_iter + 1, np.nan)
+    kk = np.full(max_iter + 1, np.nan)
+    st = np.zeros(max(1, max_iter), dtype=np.int32)
+    cg = np.zeros(max(1, max_iter), dtype=np.int32)
+    al = np.full(max(1, max_iter), np.nan)
+    info = NewtonInfo()
+    _check(ctx, L.qdt_solve_newton(ctx.ptr, F.ptr, P.ctypes.data, N, float(gamma), float(eps_kkt),
+                                   ctypes.byref(o), theta.ctypes.data, tr.ctypes.data, kk.ctypes.data,
+                                   st.ctypes.data, cg.ctypes.data, al.ctypes.data, ctypes.byref(info)))
+    k = int(info.iters_done)
+    return dict(theta=theta, trace=tr[:k + 1], kkt=kk[:k + 1], stage=st[:k], cg=cg[:k], alpha=al[:k],
+                info=info.as_dict())
+

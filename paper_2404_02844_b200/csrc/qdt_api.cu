@@ -2025,3 +2025,275 @@ extern "C" qdt_status qdt_smooth(qdt_ctx *ctx, const double *theta, int64_t M, i
     CK(cudaStreamSynchronize(s));
     return QDT_OK;
 }
+
+// ------------------------------------------------------------------------------ Newton solve
+// Host orchestration of the two-stage two-metric projected truncated Newton (include/qdt.h;
+// reading R16), step for step as the oracle's or_newton: every vector operation, Hessian
+// product, projection and reduction runs in kernels; the host holds the scalars of CG and the
+// line search (one device->host copy per scalar decision).
+namespace {
+struct NtBufs {
+    double *theta, *T1, *X, *g, *gr, *x, *r, *z, *d, *Hd, *u, *Rd, *h, *part, *scal, *d0;
+    uint8_t *act;
+    int32_t *m;
+    int *neg;
+};
+}  // namespace
+
+extern "C" qdt_status qdt_solve_newton(qdt_ctx *ctx, const qdt_probes *F, const double *P, int64_t N,
+                                       double gamma, double eps_kkt, const qdt_newton_opts *o,
+                                       double *theta_out, double *trace_out, double *kkt_out,
+                                       int32_t *stage_out, int32_t *cg_out, double *alpha_out,
+                                       qdt_newton_info *info)
+{
+    if (!ctx) return fail(nullptr, QDT_ERR_INVALID_ARG, "qdt_solve_newton: ctx is NULL");
+    if (!F || !P || !theta_out || !o) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve_newton: NULL pointer");
+    if (F->ctx != ctx) return fail(ctx, QDT_ERR_STATE, "qdt_solve_newton: probes built on another ctx");
+    if (ctx->nranks != 1) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve_newton: single rank only");
+    if (N < 1 || N > 8192) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve_newton: N out of range");
+    if (!(gamma >= 0.0) || !isfinite(gamma)) return fail(ctx, QDT_ERR_INVALID_ARG, "gamma must be finite >= 0");
+    if (o->max_iter < 0 || o->cg_max < 1 || o->max_ls < 1 || !(eps_kkt >= 0.0))
+        return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve_newton: bad options");
+    qdt_probes *p = const_cast<qdt_probes *>(F);
+    const int64_t D = p->D, M = p->Ml, n = M * N;
+    const bool dev = o->mem_device != 0;
+    if (!dev) {
+        CKS(check_finite_host(ctx, P, D * N, "P"));
+        if (o->theta0) CKS(check_finite_host(ctx, o->theta0, n, "theta0"));
+    }
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    Plan *pl;
+    CKS(build_plan(ctx, p, (int)N, &pl));
+    {
+        const double need = 8.0 * (14.0 * (M + 2) * N + 3.0 * D * N) + (double)n;
+        size_t fr = 0, tot = 0;
+        CK(cudaMemGetInfo(&fr, &tot));
+        size_t have = fr;
+        for (auto &kv : ctx->ws) have += kv.second.n;
+        if (need > 0.97 * (double)have)
+            return fail(ctx, QDT_ERR_OOM, "newton memory plan: need %.2f GB, %.2f GB available", need / 1e9,
+                        have / 1e9);
+    }
+    SolveBufs b;
+    NtBufs v;
+    const size_t hz = (size_t)(M + 2) * N + 2;   // halo rows -1 and M (zero) + bulk-copy slack
+    auto halo = [&](const char *name, double **out) -> qdt_status {
+        double *t;
+        CKS(ws_get(ctx, name, hz, &t));
+        CK(cudaMemsetAsync(t, 0, sizeof(double) * hz, s));
+        *out = t + N;
+        return QDT_OK;
+    };
+    CKS(halo("theta0", &v.theta));
+    b.theta[0] = v.theta;
+    CKS(halo("nt_T1", &v.T1));
+    CKS(halo("nt_d", &v.d));
+    CKS(halo("nt_u", &v.u));
+    CKS(halo("nt_X", &v.X));
+    CKS(ws_get(ctx, "nt_g", n + 2, &v.g));
+    CKS(ws_get(ctx, "nt_gr", n + 2, &v.gr));
+    CKS(ws_get(ctx, "nt_x", n + 2, &v.x));
+    CKS(ws_get(ctx, "nt_r", n + 2, &v.r));
+    CKS(ws_get(ctx, "nt_z", n + 2, &v.z));
+    CKS(ws_get(ctx, "nt_Hd", n + 2, &v.Hd));
+    CKS(ws_get(ctx, "nt_d0", n + 2, &v.d0));
+    CKS(ws_get(ctx, "nt_Rd", D * N + 4, &v.Rd));
+    CKS(ws_get(ctx, "nt_h", M + 2, &v.h));
+    CKS(ws_get(ctx, "nt_part", 4 * NT_BLK + 8, &v.part));
+    CKS(ws_get(ctx, "nt_scal", 8, &v.scal));
+    CKS(ws_get(ctx, "nt_act", n + 8, &v.act));
+    CKS(ws_get(ctx, "nt_m", M + 2, &v.m));
+    CKS(ws_get(ctx, "nt_neg", 2, &v.neg));
+    CKS(common_bufs(ctx, p, pl, N, b));
+    if (dev) {
+        b.P = const_cast<double *>(P);
+    } else {
+        CKS(ws_get(ctx, "P", D * N, &b.P));
+        CK(cudaMemcpyAsync(b.P, P, sizeof(double) * D * N, cudaMemcpyHostToDevice, s));
+    }
+    if (o->theta0)
+        CK(cudaMemcpyAsync(v.theta, o->theta0, sizeof(double) * n,
+                           dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    else
+        CK(launch_fill(v.theta, n, 1.0 / (double)N, s));
+    IterCfg c{p, pl, (int)N, gamma, 0.0, 0, 1, 1};
+    // Hessian diagonal h_k = 2 (sum_d F_{d,k}^2 + gamma L_kk) from the tiled F (once)
+    CKS(build_sweep_tiling(ctx, p));
+    CK(run_k(ctx, "nt_setup", 1, [&]() {
+        return nt_hdiag(p->sw_ntiles, (int)M, p->kb, p->M, p->d_sw_dA, p->d_sw_dB, p->d_fb_off, p->d_Fb, gamma,
+                        v.h, s);
+    }));
+    double *hs = nullptr;
+    CK(cudaMallocHost(&hs, sizeof(double) * 8));
+    auto fetch = [&](int k) -> double {
+        cudaMemcpyAsync(hs, v.scal, sizeof(double) * k, cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        return hs[0];
+    };
+    auto hess = [&](const double *vin, double *out) -> qdt_status {
+        CKS(fwd_reduce(ctx, c, b, vin, v.Rd, false));
+        BwdArgs a = bwd_args(ctx, c, b, v.Rd, vin, nullptr, out, false);
+        a.state = nullptr;
+        CK(run_k(ctx, "nt_hess", 1, [&]() { return launch_bwd(a, pl->nbunits, pl->TC, BWD_GRAD, s); }));
+        return QDT_OK;
+    };
+    auto grad = [&](const double *th) -> qdt_status {   // g = 2 G(th); R[0] = F th - P
+        CKS(fwd_reduce(ctx, c, b, th, b.R[0], true));
+        BwdArgs a = bwd_args(ctx, c, b, b.R[0], th, nullptr, v.g, false);
+        a.state = nullptr;
+        CK(run_k(ctx, "nt_grad", 1, [&]() { return launch_bwd(a, pl->nbunits, pl->TC, BWD_GRAD, s); }));
+        CK(nt_scale_mask(v.g, nullptr, 2.0, n, s));
+        return QDT_OK;
+    };
+    auto fval = [&](const double *th, const double *R, const double *g, double *kk) -> double {
+        nt_fparts(R, D * N, th, g, M, (int)N, v.part, v.scal, s);
+        cudaMemcpyAsync(hs, v.scal, sizeof(double) * 4, cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        if (kk) *kk = sqrt(hs[2] / ((double)N * (double)M));
+        return hs[0] + gamma * hs[1];
+    };
+    // direction: PCG on the metric (stage 2 when mrow != nullptr); x = p, returns CG iterations
+    auto direction = [&](const int32_t *mrow, const double *th, int64_t *it_out) -> qdt_status {
+        CK(nt_pcg_init(v.g, th, v.h, mrow, (int)N, n, o->eps_active, v.gr, v.act, v.x, v.r, v.z, v.d, v.part,
+                       v.scal, s));
+        const double bn = sqrt(fetch(1));
+        const double tol = fmin(0.5, sqrt(bn)) * bn;
+        CK(nt_dot(v.r, v.z, nullptr, nullptr, 0, n, v.part, v.scal, s));
+        double rz = fetch(1);
+        int64_t it = 0;
+        for (it = 0; it < o->cg_max && bn > 0.0; it++) {
+            if (rz <= 0.0) break;
+            if (mrow) {
+                CK(nt_zexp(v.d, mrow, M, (int)N, v.u, s));
+                CKS(hess(v.u, v.Hd));
+                CK(nt_scale_mask(v.Hd, nullptr, 2.0, n, s));
+                CK(nt_zred(v.Hd, mrow, v.act, M, (int)N, s));
+            } else {
+                CKS(hess(v.d, v.Hd));
+                CK(nt_scale_mask(v.Hd, v.act, 2.0, n, s));
+            }
+            CK(nt_dot(v.d, v.Hd, nullptr, nullptr, 0, n, v.part, v.scal, s));
+            const double dHd = fetch(1);
+            if (dHd <= 0.0) break;
+            const double a = rz / dHd;
+            CK(nt_cg_update(v.x, v.r, v.z, v.d, v.Hd, a, v.h, mrow, (int)N, n, v.part, v.scal, s));
+            cudaMemcpyAsync(hs, v.scal, sizeof(double) * 2, cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            if (sqrt(hs[0]) <= tol) {
+                it++;
+                break;
+            }
+            const double rz2 = hs[1];
+            const double beta = rz2 / rz;
+            rz = rz2;
+            CK(nt_cg_dir(v.d, v.z, beta, n, s));
+        }
+        *it_out = it;
+        return QDT_OK;
+    };
+    const int64_t K = o->max_iter;
+    std::vector<double> tr(K + 1, NAN), kt(K + 1, NAN), al(K, NAN);
+    std::vector<int32_t> stg(K, 0), cgl(K, 0);
+    int stage = 1;
+    int64_t k = 0, sw = -1, cg_total = 0;
+    double f_last = NAN, kkt_last = NAN;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, s));
+    for (k = 0;; k++) {
+        CKS(grad(v.theta));
+        double r;
+        const double f = fval(v.theta, b.R[0], v.g, &r);
+        tr[k] = f;
+        kt[k] = r;
+        f_last = f;
+        kkt_last = r;
+        if (!isfinite(f)) return fail(ctx, QDT_ERR_NONFINITE, "newton: non-finite objective at %lld", (long long)k);
+        if (r <= eps_kkt || k >= K) break;
+        int64_t it = 0;
+        const int used = stage;
+        double f0 = f;
+        if (stage == 1) {
+            CKS(direction(nullptr, v.theta, &it));
+            CK(nt_tangent(v.theta, v.x, M, (int)N, v.d0, s));
+            CK(nt_dot(v.g, v.d0, nullptr, nullptr, 0, n, v.part, v.scal, s));
+            const double slope = fetch(1);
+            if (fabs(slope) <= o->switch_tol) {
+                stage = 2;
+                sw = k;
+            }
+        }
+        const int us = stage;   // the stage this iteration steps with
+        if (us == 2) {
+            CK(nt_transform(v.theta, M, (int)N, v.m, s));
+            CKS(grad(v.theta));
+            CKS(direction(v.m, v.theta, &it));
+            f0 = fval(v.theta, b.R[0], nullptr, nullptr);
+        }
+        (void)used;
+        double alpha = 0.0;
+        bool accepted = false;
+        for (int64_t l = 0; l < o->max_ls && !accepted; l++) {
+            const double a = pow(0.75, (double)l);
+            if (us == 1) {
+                CK(nt_axpy(v.theta, v.x, a, n, v.X, s));
+                CK(launch_project_rows(v.X, M, (int)N, v.T1, s));
+            } else {
+                CK(cudaMemsetAsync(v.neg, 0, sizeof(int), s));
+                CK(nt_clamp_arc(v.theta, v.x, a, v.m, M, (int)N, v.T1, v.neg, s));
+                int hneg = 0;
+                CK(cudaMemcpyAsync(&hneg, v.neg, sizeof(int), cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                if (hneg) continue;
+            }
+            CK(nt_dotdiff(us == 2 ? v.gr : v.g, v.T1, v.theta, us == 2 ? v.m : nullptr, (int)N, n, v.part,
+                          v.scal, s));
+            const double dd = fetch(1);
+            CKS(fwd_reduce(ctx, c, b, v.T1, v.Rd, true));
+            const double f1 = fval(v.T1, v.Rd, nullptr, nullptr);
+            if (f1 <= f0 + 0.1 * dd) {
+                accepted = true;
+                alpha = a;
+            }
+        }
+        if (!accepted && us == 1) {   // stage 1 carries no convergence proof: switch, redo k
+            stage = 2;
+            sw = k;
+            k--;
+            continue;
+        }
+        if (k < K) {
+            stg[k] = us;
+            cgl[k] = (int32_t)it;
+            al[k] = alpha;
+        }
+        cg_total += it;
+        if (!accepted) break;
+        CK(cudaMemcpyAsync(v.theta, v.T1, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+    }
+    CK(cudaEventRecord(e1, s));
+    CK(cudaMemcpyAsync(theta_out, v.theta, sizeof(double) * n,
+                       dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    cudaFreeHost(hs);
+    if (trace_out) memcpy(trace_out, tr.data(), sizeof(double) * (K + 1));
+    if (kkt_out) memcpy(kkt_out, kt.data(), sizeof(double) * (K + 1));
+    if (stage_out && K) memcpy(stage_out, stg.data(), sizeof(int32_t) * K);
+    if (cg_out && K) memcpy(cg_out, cgl.data(), sizeof(int32_t) * K);
+    if (alpha_out && K) memcpy(alpha_out, al.data(), sizeof(double) * K);
+    if (info) {
+        info->iters_done = k;
+        info->switch_iter = sw;
+        info->cg_total = cg_total;
+        info->f_final = f_last;
+        info->kkt = kkt_last;
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        info->loop_ms = ms;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return QDT_OK;
+}

@@ -270,4 +270,30 @@ cudaError_t launch_fista_rcomb(double *RY, const double *Rk, const double *Rkm1,
                                const double *beta, int64_t n, const DevState *st,
                                cudaStream_t s);
 
+
+// ---- two-stage two-metric projected truncated Newton (qdt_newton.cu; reading R16)
+constexpr int NT_BLK = 296;    // reduction grid (block partials, then one warp)
+cudaError_t nt_pcg_init(const double *g, const double *theta, const double *h, const int32_t *m, int N,
+                        int64_t n, double eps, double *gr, uint8_t *act, double *x, double *r, double *z, double *d,
+                        double *part, double *out, cudaStream_t s);
+cudaError_t nt_dot(const double *a, const double *b, const uint8_t *act, const double *theta, int mode, int64_t n,
+                   double *part, double *out, cudaStream_t s);
+cudaError_t nt_dotdiff(const double *g, const double *T, const double *theta, const int32_t *m, int N, int64_t n,
+                       double *part, double *out, cudaStream_t s);
+cudaError_t nt_scale_mask(double *x, const uint8_t *act, double sc, int64_t n, cudaStream_t s);
+cudaError_t nt_cg_update(double *x, double *r, double *z, const double *d, const double *Hd, double a,
+                         const double *h, const int32_t *m, int N, int64_t n, double *part, double *out,
+                         cudaStream_t s);
+cudaError_t nt_cg_dir(double *d, const double *z, double beta, int64_t n, cudaStream_t s);
+cudaError_t nt_zexp(const double *v, const int32_t *m, int64_t M, int N, double *u, cudaStream_t s);
+cudaError_t nt_zred(double *w, const int32_t *m, const uint8_t *act, int64_t M, int N, cudaStream_t s);
+cudaError_t nt_tangent(const double *theta, const double *p, int64_t M, int N, double *d0, cudaStream_t s);
+cudaError_t nt_axpy(const double *theta, const double *p, double a, int64_t n, double *X, cudaStream_t s);
+cudaError_t nt_clamp_arc(const double *theta, const double *p, double a, const int32_t *m, int64_t M, int N,
+                         double *T, int *neg, cudaStream_t s);
+cudaError_t nt_transform(double *theta, int64_t M, int N, int32_t *m, cudaStream_t s);
+cudaError_t nt_hdiag(int ntiles, int Ml, int64_t kb, int64_t M, const int32_t *tile_dA, const int32_t *tile_dB,
+                     const int64_t *fb_off, const double *Fb, double gamma, double *h, cudaStream_t s);
+cudaError_t nt_fparts(const double *R, int64_t nR, const double *theta, const double *g, int64_t M, int N,
+                      double *part, double *out, cudaStream_t s);
 }  // namespace qdt

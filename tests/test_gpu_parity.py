@@ -497,3 +497,36 @@ def test_paper_tmd_parity(q, ctx):
         rg = q.qdt_solve(ctx, Fg, I.P, 1e-4, 0.0, 20, accel=bool(accel), kkt_every=5 if accel else 1)
         assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9
         assert _trace_ok(rg["trace"], ro["trace"], I.P)
+
+
+# ------------------------------------------------------------------ 8(f) row 1: Newton solve
+@pytest.mark.parametrize("seed,D,M,N,gamma,conv", [(1, 30, 60, 5, 1e-3, 1), (2, 20, 30, 3, 1e-2, 1),
+                                                   (3, 80, 40, 6, 1e-4, 1), (4, 200, 700, 37, 1e-4, 0)])
+def test_newton_parity(q, ctx, seed, D, M, N, gamma, conv):
+    """qdt_solve_newton against the oracle's or_newton (reading R16): the first iterations
+    step for step (same stage, CG count and step length; Theta to 1e-9), then (well-posed
+    cases) the same minimiser (objective 1e-12 relative) at the KKT tolerance; the
+    ill-conditioned case (M > D, small gamma) only step for step."""
+    rng = np.random.default_rng(seed)
+    a2 = np.sort(rng.uniform(0.0, 0.8 * M, D))
+    P = rng.dirichlet(np.ones(N), D)
+    Fo = oracle.Probes(a2, M)
+    Fg = q.qdt_build_probes(ctx, a2, M)
+    for k in (1, 3):
+        ro = oracle.newton(Fo, P, gamma, k)
+        rg = q.qdt_solve_newton(ctx, Fg, P, gamma, 0.0, k)
+        assert rg["info"]["iters_done"] == ro["iters_done"]
+        np.testing.assert_array_equal(rg["stage"], ro["stage"])
+        np.testing.assert_array_equal(rg["cg"], ro["cg"])
+        np.testing.assert_allclose(rg["alpha"], ro["alpha"], rtol=0)
+        assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9
+        assert _trace_ok(rg["trace"], ro["trace"], P)
+    if not conv:
+        return
+    ro = oracle.newton(Fo, P, gamma, 400, eps_kkt=1e-12)
+    rg = q.qdt_solve_newton(ctx, Fg, P, gamma, 1e-12, 400)
+    assert rg["kkt"][-1] <= 1e-12
+    assert rg["trace"][-1] == pytest.approx(ro["trace"][-1], rel=1e-12)
+    assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-6
+    Th = rg["theta"]
+    assert Th.min() >= 0 and np.abs(Th.sum(1) - 1).max() <= 1e-12
