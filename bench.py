@@ -147,6 +147,7 @@ def run_qdt(args):
     th_out = torch.empty((rows_local, N), dtype=torch.float64, device="cuda")
 
     def solve(iters, **kw):
+        kw.setdefault("kkt_every", args.kkt_every)
         return q.qdt_solve(ctx, F, Pd, I.gamma, 0.0, iters, theta_out=th_out, **kw)
 
     # warm-up (untimed): plans, graphs, workspace; repeated right before the timed region
@@ -220,7 +221,8 @@ def run_qdt(args):
         t0 = time.perf_counter()
         e0.record(stream)
         F2 = q.qdt_build_probes(ctx, a_host.numpy(), M)
-        q.qdt_solve(ctx, F2, P_host.numpy(), I.gamma, 0.0, args.steps, theta_out=th_host.numpy())
+        q.qdt_solve(ctx, F2, P_host.numpy(), I.gamma, 0.0, args.steps, theta_out=th_host.numpy(),
+                    kkt_every=args.kkt_every)
         e1.record(stream)
         barrier()
         e2e_ms = max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3)
@@ -245,7 +247,7 @@ def run_qdt(args):
         "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (qdt_synth, seed 0)",
-        "config": {"workload": args.config, "M": M, "N": N, "D": D, "gamma": I.gamma,
+        "config": {"workload": args.config, "M": M, "N": N, "D": D, "gamma": I.gamma, "kkt_every": args.kkt_every,
                    "nnz": int(nnz_local) if world == 1 else None, "step_mode": "SQS",
                    "parallelism": f"fock-shard{world}" if world > 1 else "single",
                    "l2": "Theta (8*M*N bytes) > 126 MB L2; no flush needed"},
@@ -429,6 +431,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-tol leg")
+    ap.add_argument("--kkt-every", type=int, default=1,
+                    help="evaluate r_KKT every k-th iteration in the timed loop (f is traced every iteration)")
     args = ap.parse_args()
     if args.config not in CONFIG_NAMES:
         ap.error(f"--config must be one of {CONFIG_NAMES}")
