@@ -305,6 +305,34 @@ def time_to_tol(q, ctx, I, stream, barrier, rhos=(1e-2, 1e-3, 1e-4), cap=4000):
             if not inf["converged"]:
                 break
         res["modes"][name] = rows
+    # objective-gap ladder: (f_k - f_ref) / (f_0 - f_ref) <= 1e-3, 1e-6 with f_ref the
+    # minimum f of a 10x longer SQS-FISTA run; iterations from the trace of one call per mode at
+    # tol = 0, seconds = that call's wall time scaled by the iteration fraction (cost per
+    # iteration is constant), reported as derived
+    fista_it = max([r["iters"] for r in res["modes"].get("SQS-FISTA", {}).values()] or [200])
+    long_it = min(10 * fista_it, 4000)
+    gap = {"f_ref_iters": long_it, "ladder": (1e-3, 1e-6), "modes": {}}
+    traces = {}
+    for name, accel, iters in [("SQS-FISTA", True, long_it), ("SQS", False, cap)]:
+        barrier()
+        t0 = time.perf_counter()
+        F = q.qdt_build_probes(ctx, a_host, I.M)
+        o = q.qdt_solve(ctx, F, P_host, I.gamma, 0.0, iters, accel=accel, kkt_every=5 if accel else 1,
+                        theta_out=th_host)
+        barrier()
+        traces[name] = (np.asarray(o["trace"]), time.perf_counter() - t0)
+        del F
+    f_ref = float(np.nanmin(traces["SQS-FISTA"][0]))
+    gap["f_ref"] = f_ref
+    for name, (tr, dt) in traces.items():
+        g = (tr - f_ref) / (tr[0] - f_ref)
+        rows = {}
+        for lv in gap["ladder"]:
+            hit = np.nonzero(g <= lv)[0]
+            k = int(hit[0]) if len(hit) else None
+            rows[f"{lv:g}"] = {"iters": k, "seconds_derived": (dt * k / (len(tr) - 1)) if k else None}
+        gap["modes"][name] = rows
+    res["objective_gap"] = gap
     return res
 
 

@@ -501,7 +501,8 @@ def test_paper_tmd_parity(q, ctx):
 
 # ------------------------------------------------------------------ 8(f) row 1: Newton solve
 @pytest.mark.parametrize("seed,D,M,N,gamma,conv", [(1, 30, 60, 5, 1e-3, 1), (2, 20, 30, 3, 1e-2, 1),
-                                                   (3, 80, 40, 6, 1e-4, 1), (4, 200, 700, 37, 1e-4, 0)])
+                                                   (3, 80, 40, 6, 1e-4, 1), (4, 200, 700, 37, 1e-4, 0),
+                                                   (5, 120, 80, 151, 1e-3, 0), (6, 120, 80, 200, 1e-3, 0)])
 def test_newton_parity(q, ctx, seed, D, M, N, gamma, conv):
     """qdt_solve_newton against the oracle's or_newton (reading R16): the first iterations
     step for step (same stage, CG count and step length; Theta to 1e-9), then (well-posed
@@ -530,3 +531,21 @@ def test_newton_parity(q, ctx, seed, D, M, N, gamma, conv):
     assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-6
     Th = rg["theta"]
     assert Th.min() >= 0 and np.abs(Th.sum(1) - 1).max() <= 1e-12
+
+
+def test_newton_theta0_and_errors(q, ctx):
+    """Newton from a given start (a few PG iterations) matches the oracle from the same start;
+    bad options are rejected."""
+    rng = np.random.default_rng(9)
+    D, M, N, gamma = 40, 50, 4, 1e-3
+    a2 = np.sort(rng.uniform(0.0, 40.0, D))
+    P = rng.dirichlet(np.ones(N), D)
+    Fo = oracle.Probes(a2, M)
+    Fg = q.qdt_build_probes(ctx, a2, M)
+    th0 = oracle.solve(Fo, P, gamma, 0.0, 20)["theta"]
+    ro = oracle.newton(Fo, P, gamma, 4, theta0=th0)
+    rg = q.qdt_solve_newton(ctx, Fg, P, gamma, 0.0, 4, theta0=th0)
+    np.testing.assert_array_equal(rg["cg"], ro["cg"])
+    assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9
+    with pytest.raises(q.QdtError):
+        q.qdt_solve_newton(ctx, Fg, P, gamma, 0.0, 4, cg_max=0)
