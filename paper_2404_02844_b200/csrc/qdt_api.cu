@@ -12,6 +12,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <map>
 #include <memory>
 #include <numeric>
@@ -93,9 +94,17 @@ struct qdt_ctx {
     int64_t launches = 0;
     std::map<std::string, DevBuf> ws;  // grow-only workspace
     int nblkR = 148 * 4;
+    // the last instantiated solve-loop graph and the key it was captured under (configuration
+    // + every device pointer it bakes in): a repeated qdt_solve with the same key replays it
+    cudaGraphExec_t gexec = nullptr;
+    std::vector<uint64_t> gkey;
+    int64_t glaunches = 0;
 };
 
+static std::atomic<uint64_t> g_serial{1};   // unique ids of probe handles / plans (graph keys)
+
 struct Plan {
+    uint64_t serial = g_serial++;
     int N = 0, T = 0, CG = 0, RG = 0, TC = 0, KC = 0, KR = 0, TF = 0, nthr = 0, SEG = 32;
     int ntiles = 0;
     int32_t *d_tile_dA = nullptr, *d_tile_dB = nullptr;
@@ -151,6 +160,7 @@ struct Plan {
 };
 
 struct qdt_probes {
+    uint64_t serial = g_serial++;
     qdt_ctx *ctx = nullptr;
     int64_t D = 0, M = 0, kb = 0, ke = 0, Ml = 0;
     double c_sigma = 6.0;
@@ -347,6 +357,7 @@ extern "C" qdt_status qdt_finalize(qdt_ctx *ctx)
     if (!ctx) return QDT_OK;
     cudaSetDevice(ctx->device);
     flush_profile(ctx);
+    if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
     for (auto &kv : ctx->ws) cudaFree(kv.second.p);
     if (ctx->comm) g_nccl.commDestroy(ctx->comm);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -1675,9 +1686,12 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
         CK(cudaMemsetAsync(b.R[1], 0, sizeof(double) * D * N, s));
     }
     const int64_t tl = iters + 1;
-    CKS(ws_get(ctx, "trace", tl, &b.trace));
-    CKS(ws_get(ctx, "kkt", tl, &b.kkt));
-    CKS(ws_get(ctx, "kktp", tl, &b.kktp));
+    // trace buffers sized by capacity (>= 4096 entries), so that calls of different lengths keep
+    // the same buffers and the captured loop graph stays valid (the host bounds the iterations)
+    const int64_t tcap = std::max<int64_t>(4096, tl);
+    CKS(ws_get(ctx, "trace", tcap, &b.trace));
+    CKS(ws_get(ctx, "kkt", tcap, &b.kkt));
+    CKS(ws_get(ctx, "kktp", tcap, &b.kktp));
     CK(launch_fill(b.trace, tl, NAN, s));
     CK(launch_fill(b.kkt, tl, NAN, s));
     CK(launch_fill(b.kktp, tl, NAN, s));
@@ -1691,7 +1705,7 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     }
     std::vector<double> betas;
     if (fista) {
-        CKS(ws_get(ctx, "beta", tl, &b.beta));
+        CKS(ws_get(ctx, "beta", tcap, &b.beta));
         betas.resize(tl);
         double tau = 1.0;
         for (int64_t k = 0; k < tl; k++) {
@@ -1712,7 +1726,7 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
         ctx->launches++;
         if (N != Nu) CK(cudaMemset2DAsync(b.theta[0] + Nu, sizeof(double) * N, 0, sizeof(double), Ml, s));
     }
-    IterCfg c{p, pl, (int)N, gamma, tol, fista, opt.kkt_every, tl};
+    IterCfg c{p, pl, (int)N, gamma, tol, fista, opt.kkt_every, tcap};
     c.Nv = (int)Nu;
     CKS(halo_exchange(ctx, c, b.theta[0]));
     if (pl->fz_on && !fista) CKS(fwd_reduce(ctx, c, b, b.theta[0], b.R[0], true));  // R_0
@@ -1736,18 +1750,49 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     cudaGraphExec_t gexec = nullptr;
     int64_t graph_launches = 0;
     if (use_graph) {
-        cudaGraph_t g;
-        int64_t l0 = ctx->launches;
-        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-        qdt_status cs = QDT_OK;
-        for (int j = 0; j < period && cs == QDT_OK; j++) cs = iteration(ctx, c, b, j);
-        cudaError_t ee = cudaStreamEndCapture(s, &g);
-        if (cs != QDT_OK) return cs;
-        CK(ee);
-        graph_launches = ctx->launches - l0;
-        ctx->launches = l0;
-        CK(cudaGraphInstantiate(&gexec, g, 0));
-        cudaGraphDestroy(g);
+        std::vector<uint64_t> key;
+        auto put = [&](const void *x, size_t n) {
+            const size_t k0 = key.size();
+            key.resize(k0 + (n + 7) / 8, 0);
+            memcpy(key.data() + k0, x, n);
+        };
+        put(&c.p->serial, sizeof c.p->serial);   // ids, not addresses: a freed handle's address may
+        put(&c.pl->serial, sizeof c.pl->serial); // be reused by a different one
+        put(&c.N, sizeof c.N);
+        put(&c.gamma, sizeof c.gamma);
+        put(&c.tol, sizeof c.tol);
+        put(&c.fista, sizeof c.fista);
+        put(&c.kkt_every, sizeof c.kkt_every);
+        put(&c.trace_len, sizeof c.trace_len);
+        put(&c.bb, sizeof c.bb);
+        put(&c.tlip, sizeof c.tlip);
+        put(&c.Nv, sizeof c.Nv);
+        put(&b, sizeof b);   // every device pointer the loop reads or writes (pointer-only struct)
+        put(&period, sizeof period);
+        put(&ctx->stream, sizeof ctx->stream);
+        if (ctx->gexec && key == ctx->gkey) {
+            gexec = ctx->gexec;
+            graph_launches = ctx->glaunches;
+        } else {
+            if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
+            ctx->gexec = nullptr;
+            ctx->gkey.clear();
+            cudaGraph_t g;
+            int64_t l0 = ctx->launches;
+            CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            qdt_status cs = QDT_OK;
+            for (int j = 0; j < period && cs == QDT_OK; j++) cs = iteration(ctx, c, b, j);
+            cudaError_t ee = cudaStreamEndCapture(s, &g);
+            if (cs != QDT_OK) return cs;
+            CK(ee);
+            graph_launches = ctx->launches - l0;
+            ctx->launches = l0;
+            CK(cudaGraphInstantiate(&gexec, g, 0));
+            cudaGraphDestroy(g);
+            ctx->gexec = gexec;
+            ctx->gkey = key;
+            ctx->glaunches = graph_launches;
+        }
     }
     cudaEvent_t ev0, ev1;
     CK(cudaEventCreate(&ev0));
@@ -1777,7 +1822,6 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
         }
     }
     CK(cudaEventRecord(ev1, s));
-    if (gexec) cudaGraphExecDestroy(gexec);
     // ---- final evaluation at Theta_iters (if no early stop)
     CK(cudaMemcpyAsync(&hst, b.state, sizeof hst, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));

@@ -214,8 +214,9 @@ __device__ __forceinline__ void row_pass(double (&acc)[NBA][2], const double *th
                                          double tk, bool do_kkt, bool want_kktp, double &sreg,
                                          double &skkt, double &skktp, double &s, double &xm,
                                          double &xn, const double *tpr = nullptr, double beta = 0.0,
-                                         PairX *px = nullptr, Mid mid = Mid())
+                                         PairX *px = nullptr, Mid mid = Mid(), int pitch = -1)
 {
+    const int TPp = pitch < 0 ? N : pitch;   // row pitch of the staged Theta tile(s)
     double keep[STASH ? NBA : 1][2];
     const int cl = 8 * (NB - 1) + 2 * t4;
     const bool v0 = cl < N, v1 = cl + 1 < N;
@@ -231,23 +232,23 @@ __device__ __forceinline__ void row_pass(double (&acc)[NBA][2], const double *th
         double t0[2], tp[2], tn[2];
         if (EVEN) {
             const double2 x = *reinterpret_cast<const double2 *>(thr + c);
-            const double2 y = *reinterpret_cast<const double2 *>(thr + c - N);
-            const double2 z = *reinterpret_cast<const double2 *>(thr + c + N);
+            const double2 y = *reinterpret_cast<const double2 *>(thr + c - TPp);
+            const double2 z = *reinterpret_cast<const double2 *>(thr + c + TPp);
             t0[0] = x.x, t0[1] = x.y, tp[0] = y.x, tp[1] = y.y, tn[0] = z.x, tn[1] = z.y;
         } else {
 #pragma unroll
-            for (int i = 0; i < 2; i++) t0[i] = thr[c + i], tp[i] = thr[c + i - N], tn[i] = thr[c + i + N];
+            for (int i = 0; i < 2; i++) t0[i] = thr[c + i], tp[i] = thr[c + i - TPp], tn[i] = thr[c + i + TPp];
         }
         double q0[2], qp[2], qn[2];   // Theta_{k-1} (FISTA only)
         if (FIS) {
             if (EVEN) {
                 const double2 x = *reinterpret_cast<const double2 *>(tpr + c);
-                const double2 y = *reinterpret_cast<const double2 *>(tpr + c - N);
-                const double2 z = *reinterpret_cast<const double2 *>(tpr + c + N);
+                const double2 y = *reinterpret_cast<const double2 *>(tpr + c - TPp);
+                const double2 z = *reinterpret_cast<const double2 *>(tpr + c + TPp);
                 q0[0] = x.x, q0[1] = x.y, qp[0] = y.x, qp[1] = y.y, qn[0] = z.x, qn[1] = z.y;
             } else {
 #pragma unroll
-                for (int i = 0; i < 2; i++) q0[i] = tpr[c + i], qp[i] = tpr[c + i - N], qn[i] = tpr[c + i + N];
+                for (int i = 0; i < 2; i++) q0[i] = tpr[c + i], qp[i] = tpr[c + i - TPp], qn[i] = tpr[c + i + TPp];
             }
         }
 #pragma unroll
@@ -514,12 +515,24 @@ cudaError_t launch_sqs_weights_tiled(int ntiles, int Ml, const int32_t *tile_dA,
 
 // ------------------------------------------------------------------------------ bwd sweep
 // Smem: Theta tile (ST+2 rows incl. halo) | F chunks 2 x SKC x STP | R chunks 2 x (SKC*N + pad)
+// Theta-tile row pitch in shared memory.  QDT_TH_PAD (A/B): even N padded to a pitch = 8 mod 16
+// doubles, so the two row segments a quarter-warp reads (rows g, g + 1: 64 B each) fall in
+// disjoint bank halves; the tile then arrives as one bulk copy per row (warp 0 issues them).
+__device__ __host__ __forceinline__ int th_pitch(int N)
+{
+#ifdef QDT_TH_PAD
+    return (N & 1) ? N : N + ((8 - N % 16 + 16) % 16);
+#else
+    return N;
+#endif
+}
+
 template <int NB>
 struct SwLayout {
     int thsz, rsz;
     __device__ __host__ SwLayout(int N)
     {
-        thsz = (((ST + 2) * N + 8 * NB + 16) + 1) & ~1;
+        thsz = (((ST + 2) * th_pitch(N) + 8 * NB + 16) + 1) & ~1;
         rsz = ((SKC * N + 8 * NB + 16) + 1) & ~1;
     }
     __device__ __host__ size_t bytes() const
@@ -530,7 +543,7 @@ struct SwLayout {
 
 size_t sweep_bwd_smem(int N, int NB, bool fista)
 {
-    const int thsz = (((ST + 2) * N + 8 * NB + 16) + 1) & ~1;
+    const int thsz = (((ST + 2) * th_pitch(N) + 8 * NB + 16) + 1) & ~1;
     const int rsz = ((SKC * N + 8 * NB + 16) + 1) & ~1;
     return (size_t)((fista ? 2 : 1) * thsz + 2 * SKC * STP + 2 * rsz) * sizeof(double);
 }
@@ -575,15 +588,30 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(Swe
     __syncthreads();
     // issue helpers (thread 0 only); chunk stage / parity follow a running chunk counter
     uint32_t c_issue = 0, c_use = 0, th_use = 0;
+    const int TPB = th_pitch(N);   // staged tile pitch (== N: one contiguous copy)
+    // warp 0 (converged) issues the tile: one copy, or one per row at the padded pitch
     auto issue_theta = [&](const SwUnit &v) {
         const int k0 = v.tile * ST, Tt = min(ST, a.Ml - k0);
-        const double *src;
-        int sh;
-        uint32_t by;
-        aligned_span(a.theta + (int64_t)(k0 - 1) * N, (int64_t)(Tt + 2) * N, &src, &sh, &by);
-        mbar_expect_tx(&bars[0], FIS ? 2 * by : by);
-        bulk_g2s(Th, src, by, &bars[0]);
-        if (FIS) bulk_g2s(Tq, a.theta_prev + (src - a.theta), by, &bars[0]);
+        if (TPB == N) {
+            if (lane == 0) {
+                const double *src;
+                int sh;
+                uint32_t by;
+                aligned_span(a.theta + (int64_t)(k0 - 1) * N, (int64_t)(Tt + 2) * N, &src, &sh, &by);
+                mbar_expect_tx(&bars[0], FIS ? 2 * by : by);
+                bulk_g2s(Th, src, by, &bars[0]);
+                if (FIS) bulk_g2s(Tq, a.theta_prev + (src - a.theta), by, &bars[0]);
+            }
+            return;
+        }
+        const uint32_t rb = (uint32_t)N * 8;
+        if (lane == 0) mbar_expect_tx(&bars[0], (FIS ? 2u : 1u) * rb * (uint32_t)(Tt + 2));
+        __syncwarp();
+        for (int j = lane; j < Tt + 2; j += 32) {
+            const int64_t off = (int64_t)(k0 - 1 + j) * N;
+            bulk_g2s(Th + j * TPB, a.theta + off, rb, &bars[0]);
+            if (FIS) bulk_g2s(Tq + j * TPB, a.theta_prev + off, rb, &bars[0]);
+        }
     };
     auto issue_chunk = [&](const SwUnit &v, int c) {
         const int W = v.p1 - v.p0, pb = c * SKC, kc = min(SKC, W - pb);
@@ -601,10 +629,8 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(Swe
         c_issue++;
     };
     SwUnit u = a.units[unit];
-    if (tid == 0) {
-        if (u.nsplit == 1) issue_theta(u);
-        if (u.p1 > u.p0) issue_chunk(u, 0);
-    }
+    if (warp == 0 && u.nsplit == 1) issue_theta(u);
+    if (tid == 0 && u.p1 > u.p0) issue_chunk(u, 0);
     while (true) {
         const int k0 = u.tile * ST;
         const int Tt = min(ST, a.Ml - k0);
@@ -650,7 +676,7 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(Swe
             epi = s_last;
             if (epi) {
                 __threadfence();
-                if (tid == 0) issue_theta(u);
+                if (warp == 0) issue_theta(u);
 #pragma unroll
                 for (int nb = 0; nb < NB; nb++) acc[nb][0] = acc[nb][1] = 0.0;
                 for (int sl = 0; sl < u.nsplit; sl++) {
@@ -669,41 +695,41 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(Swe
         if (epi) {
             mbar_wait(&bars[0], th_use & 1);
             th_use++;
-            const int th_sh = (int)(((uintptr_t)(a.theta + (int64_t)(k0 - 1) * N) & 15) >> 3);
+            const int th_sh = TPB != N ? 0 : (int)(((uintptr_t)(a.theta + (int64_t)(k0 - 1) * N) & 15) >> 3);
             const int r = 8 * warp + g4;
             const bool act = r < Tt;
             const int kl = k0 + r;
             const int64_t kg = a.kb + kl;
             const bool has_prev = kg > 0, has_next = kg + 1 < a.M;
-            double *thr = Th + th_sh + (r + 1) * N;
+            double *thr = Th + th_sh + (r + 1) * TPB;
             double sreg = 0.0, skkt = 0.0, skktp = 0.0, s, xm, xn;
             double *orow = a.out + (int64_t)kl * N;
             const bool full = Tt == ST && a.kb + k0 > 0 && a.kb + k0 + ST < a.M;
             const bool ev = a.eval != 0;   // evaluation pass: KKT (both multipliers) + regulariser only
             const bool fast = full && even;
-            const double *tpr = Tq + th_sh + (r + 1) * N;
+            const double *tpr = Tq + th_sh + (r + 1) * TPB;
             // interior even-N tiles of plain steps: the own-row values stay in registers, the tile
             // is released after pass 1 and the next unit's tile load overlaps pass 2 + Michelot
             constexpr bool kStash = NB <= SW_NBMAX;   // register budget: 255 at NB = 16
             const bool stash = kStash && fast && !FIS && !ev;
             auto release = [&]() {
                 __syncthreads();
-                if (tid == 0 && next < a.nunits && un.nsplit == 1) issue_theta(un);
+                if (warp == 0 && next < a.nunits && un.nsplit == 1) issue_theta(un);
             };
             if (stash)
                 row_pass<NB, true, true, false, false, NB, 0, false, true>(acc, thr, N, t4, act, has_prev, has_next,
                                                                          a.gamma, tk, do_kkt, ev, sreg, skkt,
                                                                          skktp, s, xm, xn, tpr, beta, nullptr,
-                                                                         release);
+                                                                         release, TPB);
             else if (fast)
                 row_pass<NB, true, true, false, FIS>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk,
-                                                     do_kkt, ev, sreg, skkt, skktp, s, xm, xn, tpr, beta);
+                                                     do_kkt, ev, sreg, skkt, skktp, s, xm, xn, tpr, beta, nullptr, NoMid(), TPB);
             else if (full)
                 row_pass<NB, true, false, false, FIS>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk,
-                                                      do_kkt, ev, sreg, skkt, skktp, s, xm, xn, tpr, beta);
+                                                      do_kkt, ev, sreg, skkt, skktp, s, xm, xn, tpr, beta, nullptr, NoMid(), TPB);
             else
                 row_pass<NB, false, false, false, FIS>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk,
-                                                       do_kkt, ev, sreg, skkt, skktp, s, xm, xn, tpr, beta);
+                                                       do_kkt, ev, sreg, skkt, skktp, s, xm, xn, tpr, beta, nullptr, NoMid(), TPB);
             if (!stash) release();   // Theta tile consumed: start the next unit's tile load
             if (ev) {
             } else if (fast)
@@ -737,7 +763,7 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(Swe
                 p[SC_REG] = v2;
                 p[SC_DTH] = 0.0;
             }
-        } else if (tid == 0 && next < a.nunits && un.nsplit == 1) {
+        } else if (warp == 0 && next < a.nunits && un.nsplit == 1) {
             issue_theta(un);
         }
         if (next >= a.nunits) break;

@@ -549,3 +549,28 @@ def test_newton_theta0_and_errors(q, ctx):
     assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9
     with pytest.raises(q.QdtError):
         q.qdt_solve_newton(ctx, Fg, P, gamma, 0.0, 4, cg_max=0)
+
+
+def test_graph_cache_keys(q, ctx):
+    """The solve loop's CUDA graph is reused across calls with the same key (configuration,
+    handle ids, device buffers); alternating handles / gammas / lengths must each match the
+    oracle, and a repeated call must reproduce its first result bitwise."""
+    rng = np.random.default_rng(11)
+    D, M, N = 120, 400, 12
+    cases = []
+    for j in range(2):
+        a2 = np.sort(rng.uniform(0.0, 0.8 * M, D))
+        cases.append((a2, rng.dirichlet(np.ones(N), D)))
+    Fg = [q.qdt_build_probes(ctx, a2, M) for a2, _ in cases]
+    first = {}
+    for rep in range(2):
+        for j, (a2, P) in enumerate(cases):
+            for gamma, iters in ((1e-3, 40), (1e-4, 33)):
+                rg = q.qdt_solve(ctx, Fg[j], P, gamma, 0.0, iters, use_graph=True)
+                key = (j, gamma, iters)
+                if rep == 0:
+                    ro = oracle.solve(oracle.Probes(a2, M), P, gamma, 0.0, iters)
+                    assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9
+                    first[key] = rg["theta"].copy()
+                else:
+                    assert np.array_equal(rg["theta"], first[key])
