@@ -1,6 +1,7 @@
 // qdt_internal.h -- declarations shared by the host runtime (qdt_api.cu) and the sm_100a
 // kernels (qdt_kernels.cu).  Not part of the public ABI (include/qdt.h is).
 #pragma once
+#include <cuda.h>   // CUtensorMap (type only; the encoder is fetched through the runtime)
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -128,6 +129,9 @@ struct SweepArgs {
     const double *theta_prev;   // FISTA step: Theta_{k-1} (same layout as theta)
     const double *beta;         // FISTA step: beta_k indexed by state->it (nullptr: plain PG)
     const DevState *state;
+    int tm_on;                  // set by launch_bwd_mma: the Theta tile arrives by 2-D tensor copy
+    alignas(64) CUtensorMap tm_theta;   // box (tp_pitch(NB) x 66) over rows -1 .. Ml of theta
+    alignas(64) CUtensorMap tm_prev;    // same over theta_prev (FISTA)
 };
 struct SweepFwdArgs {
     int N, Ml;
@@ -206,7 +210,7 @@ cudaError_t launch_sqs_weights_tiled(int ntiles, int Ml, const int32_t *tile_dA,
                                      const double *s, double gamma, double *w, double *tstep,
                                      cudaStream_t st);
 int sweep_nb(int N);            // DMMA n-blocks instantiated for N (0: N too wide, general path)
-size_t sweep_bwd_smem(int N, int NB, bool fista);
+size_t sweep_bwd_smem(int N, int NB, bool fista, bool tp = false);
 size_t sweep_fwd_smem(int N, int NB);
 cudaError_t launch_tile_F(Band b, int64_t kb, int Ml, int ntiles, const int32_t *tile_dA,
                           const int32_t *tile_dB, const int64_t *fb_off, double *Fb,

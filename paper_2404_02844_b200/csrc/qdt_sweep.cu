@@ -14,6 +14,7 @@
 // buffered.  F is pre-tiled once per probe handle (k_tile_F): for every Fock tile a dense block of
 // (window probes) x STP doubles, zero outside each band, so a staged chunk is one contiguous copy.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -60,6 +61,16 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
             smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+// 2-D tensor copy (TMA): box at coordinates (x, y) of the tensor map into shared memory;
+// out-of-bounds elements (columns >= N of the padded box, rows past the array) arrive as zeros
+__device__ __forceinline__ void tma_2d(void *dst, const CUtensorMap *tm, int x, int y, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(smem_u32(bar))
         : "memory");
 }
 // bulk prefetch of a global range into L2 (no shared memory, no completion tracking)
@@ -515,24 +526,19 @@ cudaError_t launch_sqs_weights_tiled(int ntiles, int Ml, const int32_t *tile_dA,
 
 // ------------------------------------------------------------------------------ bwd sweep
 // Smem: Theta tile (ST+2 rows incl. halo) | F chunks 2 x SKC x STP | R chunks 2 x (SKC*N + pad)
-// Theta-tile row pitch in shared memory.  QDT_TH_PAD (A/B): even N padded to a pitch = 8 mod 16
-// doubles, so the two row segments a quarter-warp reads (rows g, g + 1: 64 B each) fall in
-// disjoint bank halves; the tile then arrives as one bulk copy per row (warp 0 issues them).
-__device__ __host__ __forceinline__ int th_pitch(int N)
-{
-#ifdef QDT_TH_PAD
-    return (N & 1) ? N : N + ((8 - N % 16 + 16) % 16);
-#else
-    return N;
-#endif
-}
+// Theta-tile row pitch in shared memory: N (one contiguous bulk copy of the rows), or with TP
+// (tensor-map tile, even N) the compile-time pitch tp_pitch(NB) = 8 NB (+ 8 for even NB), which
+// is = 8 mod 16 doubles: the two 64-byte row segments a quarter-warp reads (rows g, g + 1) fall
+// in disjoint bank halves, so the row pass's tile loads are free of bank conflicts; the tile
+// arrives by one 2-D TMA copy whose box columns >= N are zero-filled.
+__device__ __host__ constexpr int tp_pitch(int NB) { return 8 * NB + ((NB & 1) ? 0 : 8); }
 
 template <int NB>
 struct SwLayout {
     int thsz, rsz;
-    __device__ __host__ SwLayout(int N)
+    __device__ __host__ SwLayout(int N, int pitch)
     {
-        thsz = (((ST + 2) * th_pitch(N) + 8 * NB + 16) + 1) & ~1;
+        thsz = (((ST + 2) * pitch + 8 * NB + 16) + 15) & ~15;   // 128-byte aligned tiles
         rsz = ((SKC * N + 8 * NB + 16) + 1) & ~1;
     }
     __device__ __host__ size_t bytes() const
@@ -541,9 +547,9 @@ struct SwLayout {
     }
 };
 
-size_t sweep_bwd_smem(int N, int NB, bool fista)
+size_t sweep_bwd_smem(int N, int NB, bool fista, bool tp)
 {
-    const int thsz = (((ST + 2) * th_pitch(N) + 8 * NB + 16) + 1) & ~1;
+    const int thsz = (((ST + 2) * (tp ? tp_pitch(NB) : N) + 8 * NB + 16) + 15) & ~15;
     const int rsz = ((SKC * N + 8 * NB + 16) + 1) & ~1;
     return (size_t)((fista ? 2 : 1) * thsz + 2 * SKC * STP + 2 * rsz) * sizeof(double);
 }
@@ -552,8 +558,8 @@ size_t sweep_bwd_smem(int N, int NB, bool fista)
 // the next unit are refilled as soon as this unit's GEMM is done, the Theta tile as soon as the
 // epilogue has read it (before the Michelot rounds and stores), so the next unit's loads overlap
 // the current unit's epilogue.
-template <int NB, bool FIS>
-__global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(SweepArgs a)
+template <int NB, bool FIS, bool TP = false>
+__global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(const __grid_constant__ SweepArgs a)
 {
     extern __shared__ __align__(128) double sm[];
     __shared__ __align__(8) uint64_t bars[3];
@@ -568,7 +574,8 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(Swe
     const int G = gridDim.x;
     int unit = blockIdx.x;
     if (unit >= a.nunits) return;
-    const SwLayout<NB> L(N);
+    const int TPB = TP ? tp_pitch(NB) : N;          // staged tile pitch
+    const SwLayout<NB> L(N, TPB);
     double *Th = sm;
     double *Tq = sm + L.thsz;                       // FISTA: Theta_{k-1} tile (same rows)
     double *Fs = sm + (FIS ? 2 : 1) * L.thsz;
@@ -588,30 +595,25 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(Swe
     __syncthreads();
     // issue helpers (thread 0 only); chunk stage / parity follow a running chunk counter
     uint32_t c_issue = 0, c_use = 0, th_use = 0;
-    const int TPB = th_pitch(N);   // staged tile pitch (== N: one contiguous copy)
-    // warp 0 (converged) issues the tile: one copy, or one per row at the padded pitch
+    // the tile load (lane 0 of the calling warp): one contiguous bulk copy, or (TP) one 2-D tensor
+    // copy of rows k0 - 1 .. k0 + 64 at pitch TPB with the pad columns zero-filled
     auto issue_theta = [&](const SwUnit &v) {
+        if (lane != 0) return;
         const int k0 = v.tile * ST, Tt = min(ST, a.Ml - k0);
-        if (TPB == N) {
-            if (lane == 0) {
-                const double *src;
-                int sh;
-                uint32_t by;
-                aligned_span(a.theta + (int64_t)(k0 - 1) * N, (int64_t)(Tt + 2) * N, &src, &sh, &by);
-                mbar_expect_tx(&bars[0], FIS ? 2 * by : by);
-                bulk_g2s(Th, src, by, &bars[0]);
-                if (FIS) bulk_g2s(Tq, a.theta_prev + (src - a.theta), by, &bars[0]);
-            }
+        if (TP) {
+            const uint32_t bb = (uint32_t)TPB * (ST + 2) * 8;
+            mbar_expect_tx(&bars[0], FIS ? 2 * bb : bb);
+            tma_2d(Th, &a.tm_theta, 0, k0, &bars[0]);
+            if (FIS) tma_2d(Tq, &a.tm_prev, 0, k0, &bars[0]);
             return;
         }
-        const uint32_t rb = (uint32_t)N * 8;
-        if (lane == 0) mbar_expect_tx(&bars[0], (FIS ? 2u : 1u) * rb * (uint32_t)(Tt + 2));
-        __syncwarp();
-        for (int j = lane; j < Tt + 2; j += 32) {
-            const int64_t off = (int64_t)(k0 - 1 + j) * N;
-            bulk_g2s(Th + j * TPB, a.theta + off, rb, &bars[0]);
-            if (FIS) bulk_g2s(Tq + j * TPB, a.theta_prev + off, rb, &bars[0]);
-        }
+        const double *src;
+        int sh;
+        uint32_t by;
+        aligned_span(a.theta + (int64_t)(k0 - 1) * N, (int64_t)(Tt + 2) * N, &src, &sh, &by);
+        mbar_expect_tx(&bars[0], FIS ? 2 * by : by);
+        bulk_g2s(Th, src, by, &bars[0]);
+        if (FIS) bulk_g2s(Tq, a.theta_prev + (src - a.theta), by, &bars[0]);
     };
     auto issue_chunk = [&](const SwUnit &v, int c) {
         const int W = v.p1 - v.p0, pb = c * SKC, kc = min(SKC, W - pb);
@@ -695,7 +697,7 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(Swe
         if (epi) {
             mbar_wait(&bars[0], th_use & 1);
             th_use++;
-            const int th_sh = TPB != N ? 0 : (int)(((uintptr_t)(a.theta + (int64_t)(k0 - 1) * N) & 15) >> 3);
+            const int th_sh = TP ? 0 : (int)(((uintptr_t)(a.theta + (int64_t)(k0 - 1) * N) & 15) >> 3);
             const int r = 8 * warp + g4;
             const bool act = r < Tt;
             const int kl = k0 + r;
@@ -795,7 +797,7 @@ __global__ void __launch_bounds__(512, 1) k_bwd_split(SweepArgs a)
     const int G = gridDim.x;
     int unit = blockIdx.x;
     if (unit >= a.nunits) return;
-    const SwLayout<NB> L(N);
+    const SwLayout<NB> L(N, N);
     double *Th = sm;
     double *Tq = sm + L.thsz;
     double *Fs = sm + 2 * L.thsz;                   // two tiles: double buffer or Theta_{k-1}
@@ -1948,6 +1950,8 @@ static cudaError_t prep_nb()
     const int big = 210 * 1024;  // fwd at N = 128 needs 203 KB; the opt-in cap (227 KB) includes static smem
     cudaError_t e = cudaFuncSetAttribute(k_bwd_mma<NB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_bwd_mma<NB, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_bwd_mma<NB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     if (e == cudaSuccess && NB >= 9)
         e = cudaFuncSetAttribute(k_grad_wide<NB < 9 ? 9 : NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
@@ -1991,13 +1995,59 @@ int sweep_nb(int N)
     return 0;
 }
 
+// Tensor maps of the Theta buffers for the TP tile copies (box tp_pitch(NB) x 66 over rows
+// -1 .. Ml); the encoder comes from the driver through the runtime (no libcuda link).  Returns
+// false (TP not used) for odd N (row stride not a multiple of 16 bytes) or without an encoder.
+static bool sweep_tensor_maps(SweepArgs &a, int NB)
+{
+    a.tm_on = 0;
+    const int N = a.N, P = tp_pitch(NB);
+    if ((N & 1) || P < N) return false;
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        void *fp = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &qr) != cudaSuccess ||
+            qr != cudaDriverEntryPointSuccess)
+            return false;
+        enc = (PFN_cuTensorMapEncodeTiled_v12000)fp;
+    }
+    auto encode = [&](CUtensorMap *tm, const double *base) {
+        cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)a.Ml + 2};
+        cuuint64_t strides[1] = {(cuuint64_t)N * sizeof(double)};
+        cuuint32_t box[2] = {(cuuint32_t)P, (cuuint32_t)(ST + 2)};
+        cuuint32_t es[2] = {1, 1};
+        return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void *)(base - N), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    };
+    bool ok = encode(&a.tm_theta, a.theta);
+    if (ok && a.theta_prev) ok = encode(&a.tm_prev, a.theta_prev);
+    a.tm_on = ok ? 1 : 0;
+    return ok;
+}
+
+// QDT_TMA_TILE: 1 (default) plain steps at even N <= 128 stage the Theta tile by tensor copy at
+// the bank-conflict-free pitch; 0 keeps the contiguous bulk copy (A/B)
+static bool tma_tile_on()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("QDT_TMA_TILE");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 cudaError_t launch_bwd_mma(const SweepArgs &a_in, int nunits, int NB, cudaStream_t s)
 {
     if (nunits <= 0) return cudaSuccess;
     SweepArgs a = a_in;
+    a.tm_on = 0;
     a.nunits = nunits;
     const bool fis = a.beta != nullptr && !a.eval;
-    const size_t smem = sweep_bwd_smem(a.N, NB, fis);
+    const bool tp = !fis && NB <= SW_NBMAX && tma_tile_on() && sweep_tensor_maps(a, NB);
+    const size_t smem = sweep_bwd_smem(a.N, NB, fis, tp);
     static int nsm = 0;
     if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
     const int grid = std::min(nunits, (NB <= 13 && !fis ? 2 : 1) * nsm);
@@ -2006,6 +2056,8 @@ cudaError_t launch_bwd_mma(const SweepArgs &a_in, int nunits, int NB, cudaStream
     case nb:                                                               \
         if (fis)                                                           \
             k_bwd_mma<nb, true><<<grid, 256, smem, s>>>(a);                \
+        else if (tp)                                                       \
+            k_bwd_mma<nb, false, true><<<grid, 256, smem, s>>>(a);         \
         else                                                               \
             k_bwd_mma<nb, false><<<grid, 256, smem, s>>>(a);               \
         break;
@@ -2040,7 +2092,7 @@ cudaError_t launch_bwd_split(const SweepArgs &a_in, int nunits, int NB, cudaStre
     SweepArgs a = a_in;
     a.nunits = nunits;
     const bool fis = a.beta != nullptr && !a.eval;
-    const size_t smem = sweep_bwd_smem(a.N, NB, true);   // two tiles: double buffer or Theta_{k-1}
+    const size_t smem = sweep_bwd_smem(a.N, NB, true, false);   // two tiles: double buffer or Theta_{k-1}
     static int nsm = 0;
     if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
     const int grid = std::min(nunits, nsm);
