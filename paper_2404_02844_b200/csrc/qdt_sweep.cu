@@ -778,8 +778,8 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(con
 // the column half w >> 3 (NBA = ceil(NB/2) column blocks; the last block of an odd NB is padding),
 // so that each thread holds half a row and two CTAs (32 warps) fit an SM; the two halves of a row
 // complete every row reduction through a named-barrier pair exchange (PairX).
-template <int NB, bool FIS>
-__global__ void __launch_bounds__(512, 1) k_bwd_split(SweepArgs a)
+template <int NB, bool FIS, bool TP = false>
+__global__ void __launch_bounds__(512, 1) k_bwd_split(const __grid_constant__ SweepArgs a)
 {
     constexpr int NBA = (NB + 1) / 2;
     extern __shared__ __align__(128) double sm[];
@@ -797,7 +797,8 @@ __global__ void __launch_bounds__(512, 1) k_bwd_split(SweepArgs a)
     const int G = gridDim.x;
     int unit = blockIdx.x;
     if (unit >= a.nunits) return;
-    const SwLayout<NB> L(N, N);
+    const int TPB = TP ? tp_pitch(NB) : N;          // staged tile pitch (TP: tensor-copy tile)
+    const SwLayout<NB> L(N, TPB);
     double *Th = sm;
     double *Tq = sm + L.thsz;
     double *Fs = sm + 2 * L.thsz;                   // two tiles: double buffer or Theta_{k-1}
@@ -825,11 +826,19 @@ __global__ void __launch_bounds__(512, 1) k_bwd_split(SweepArgs a)
     auto th_par = [&](uint32_t n) -> uint32_t { return FIS ? (n & 1) : ((n >> 1) & 1); };
     auto issue_theta = [&](const SwUnit &v) {
         const int k0 = v.tile * ST, Tt = min(ST, a.Ml - k0);
+        uint64_t *bar = th_bar(th_issue);
+        if (TP) {   // one 2-D tensor copy per tile at the conflict-free pitch (see k_bwd_mma)
+            const uint32_t bb = (uint32_t)TPB * (ST + 2) * 8;
+            mbar_expect_tx(bar, FIS ? 2 * bb : bb);
+            tma_2d(th_buf(th_issue), &a.tm_theta, 0, k0, bar);
+            if (FIS) tma_2d(Tq, &a.tm_prev, 0, k0, bar);
+            th_issue++;
+            return;
+        }
         const double *src;
         int sh;
         uint32_t by;
         aligned_span(a.theta + (int64_t)(k0 - 1) * N, (int64_t)(Tt + 2) * N, &src, &sh, &by);
-        uint64_t *bar = th_bar(th_issue);
         mbar_expect_tx(bar, FIS ? 2 * by : by);
         bulk_g2s(th_buf(th_issue), src, by, bar);
         if (FIS) bulk_g2s(Tq, a.theta_prev + (src - a.theta), by, bar);
@@ -921,14 +930,14 @@ __global__ void __launch_bounds__(512, 1) k_bwd_split(SweepArgs a)
             double *Thc = th_buf(th_use);
             mbar_wait(th_bar(th_use), th_par(th_use));
             th_use++;
-            const int th_sh = (int)(((uintptr_t)(a.theta + (int64_t)(k0 - 1) * N) & 15) >> 3);
+            const int th_sh = TP ? 0 : (int)(((uintptr_t)(a.theta + (int64_t)(k0 - 1) * N) & 15) >> 3);
             const int r = 8 * mb + g4;
             const bool act = r < Tt;
             const int kl = k0 + r;
             const int64_t kg = a.kb + kl;
             const bool has_prev = kg > 0, has_next = kg + 1 < a.M;
-            double *thr = Thc + th_sh + (r + 1) * N;
-            const double *tpr = Tq + th_sh + (r + 1) * N;
+            double *thr = Thc + th_sh + (r + 1) * TPB;
+            const double *tpr = Tq + th_sh + (r + 1) * TPB;
             double sreg = 0.0, skkt = 0.0, skktp = 0.0, s, xm, xn;
             double *orow = a.out + (int64_t)kl * N;
             const bool full = Tt == ST && a.kb + k0 > 0 && a.kb + k0 + ST < a.M;
@@ -936,7 +945,8 @@ __global__ void __launch_bounds__(512, 1) k_bwd_split(SweepArgs a)
             const bool ev = a.eval != 0;
 #define QDT_SPLIT_PASS(CBV, FU, EV)                                                                    \
     row_pass<NB, FU, EV, false, FIS, NBA, CBV, true>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk, \
-                                                     do_kkt, ev, sreg, skkt, skktp, s, xm, xn, tpr, beta, &px)
+                                                     do_kkt, ev, sreg, skkt, skktp, s, xm, xn, tpr, beta, &px, \
+                                                     NoMid(), TPB)
 #define QDT_SPLIT_PROJ(CBV, FU, EV) \
     row_project<NB, FU, EV, false, NBA, CBV, true>(acc, thr, N, t4, act, s, xm, xn, orow, &px)
             if (hh == 0) {
@@ -1960,6 +1970,8 @@ static cudaError_t prep_nb()
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_bwd_split<NB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_bwd_split<NB, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
+    if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_fwd_mma<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_sweep_fused<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -2090,16 +2102,20 @@ cudaError_t launch_bwd_split(const SweepArgs &a_in, int nunits, int NB, cudaStre
 {
     if (nunits <= 0) return cudaSuccess;
     SweepArgs a = a_in;
+    a.tm_on = 0;
     a.nunits = nunits;
     const bool fis = a.beta != nullptr && !a.eval;
-    const size_t smem = sweep_bwd_smem(a.N, NB, true, false);   // two tiles: double buffer or Theta_{k-1}
+    const bool tp = fis && NB <= SW_NBMAX && tma_tile_on() && sweep_tensor_maps(a, NB);   // FISTA steps
+    const size_t smem = sweep_bwd_smem(a.N, NB, true, tp);   // two tiles: double buffer or Theta_{k-1}
     static int nsm = 0;
     if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
     const int grid = std::min(nunits, nsm);
     switch (NB) {
 #define QDT_CASE(nb)                                                       \
     case nb:                                                               \
-        if (fis)                                                           \
+        if (fis && tp)                                                     \
+            k_bwd_split<nb, true, true><<<grid, 512, smem, s>>>(a);        \
+        else if (fis)                                                      \
             k_bwd_split<nb, true><<<grid, 512, smem, s>>>(a);              \
         else                                                               \
             k_bwd_split<nb, false><<<grid, 512, smem, s>>>(a);             \
