@@ -86,6 +86,13 @@ typedef struct {
     int32_t mem_device;    /* 1: P / theta0 / theta_out are device pointers                    */
     int32_t gather_theta;  /* nranks>1: 1 -> theta_out is the full M x N on every rank         */
     int32_t use_graph;     /* 1 (default): replay the iteration as a CUDA graph                */
+    /* FISTA resume state (accel = 1; the paper restarts its second stage from a given
+     * Pi): a solve stopped at Theta_k continues bit for bit as the uninterrupted one
+     * when called with theta0 = Theta_k, theta_prev = Theta_{k-1} and fista_t = tau_k.          */
+    const double *theta_prev; /* Theta_{k-1}, same layout as theta0; NULL -> Theta_{-1} = Theta_0  */
+    double fista_t;        /* tau_k of the Beck-Teboulle sequence at the resume point (>= 1); 0 -> 1 */
+    double *theta_prev_out;/* receives Theta_{k-1} of the returned Theta_k (layout of theta_out);
+                              may be NULL; FISTA only                                            */
 } qdt_solve_opts;
 
 typedef struct {
@@ -101,6 +108,7 @@ typedef struct {
     double min_row_mass;   /* min_d sum_k F_{d,k} over stored bands (truncation diagnostic)    */
     int64_t uncovered_rows;/* Fock rows (this rank) touched by no probe band (reading R9)      */
     double loop_ms;        /* CUDA-event time of the iteration loop on ctx's stream            */
+    double fista_t;        /* FISTA: tau of the returned iterate (resume state), 0 otherwise    */
 } qdt_solve_info;
 
 /* ------------------------------------------------------------------------------ context */
@@ -129,6 +137,16 @@ const char *qdt_last_error(const qdt_ctx *ctx);
  * decreasing mu -> UNSORTED; strict_mass and a clipped band -> TRUNCATED. */
 qdt_status qdt_build_probes(qdt_ctx *ctx, const double *alpha2, int64_t D, int64_t M,
                             const qdt_probe_opts *opts, qdt_probes **out);
+/* Test hook: a probe handle from an arbitrary banded F instead of the Poisson
+ * generator.  Probe d stores rows [lo[d], lo[d] + len[d]) (global Fock indices) with values
+ * vals[off_d + j], off_d = sum_{e<d} len_e (probe-major, host pointers, copied: the caller keeps
+ * ownership).  Requirements: len[d] >= 1, 0 <= lo[d], lo[d] + len[d] <= M, and both band edges
+ * nondecreasing in d (the structure the S0 bands of sorted probes have; the tile planner relies
+ * on contiguous probe windows).  Collective when nranks > 1 (every rank passes the full bands).
+ * Errors: bad sizes / edges -> INVALID_ARG; decreasing edges -> UNSORTED; non-finite values ->
+ * NONFINITE. */
+qdt_status qdt_probes_from_banded(qdt_ctx *ctx, int64_t D, int64_t M, const int64_t *lo,
+                                  const int64_t *len, const double *vals, qdt_probes **out);
 qdt_status qdt_probes_free(qdt_probes *probes);
 /* Band tables and sizes of this rank: any output pointer may be NULL.  lo/len: host
  * int64[D] (global first row and length of the locally stored band), val: host double[nnz]
@@ -174,7 +192,8 @@ qdt_status qdt_smooth(qdt_ctx *ctx, const double *theta, int64_t M, int64_t N, i
  * (active set I = {theta <= eps_active, df > 0} keeps only the Hessian diagonal
  * h_i = 2 (sum_d F_{d,i}^2 + gamma L_ii)); D p = -df by diagonally preconditioned CG from 0
  * (H d = 2 (F^T F d + gamma L d), <= cg_max iterations, ||r|| <= min(1/2, sqrt||b||) ||b||);
- * Armijo along the projection arc (beta = 3/4, c = 1/10, <= max_ls step lengths); stage 1
+ * Armijo along the projection arc (beta = 3/4, c = 1/10, <= max_ls step lengths; the test is
+ * opts->armijo's); stage 1
  * arcs P_{S^M}[Theta + alpha p], stage 2 (row maxima m(i) eliminated by the sum constraint)
  * arcs max(x + alpha p, 0); switch to stage 2 when |df . Pi_T(p)| <= switch_tol or when a
  * stage-1 iteration admits no step length.  Stops when r_KKT (reading R7) <= eps_kkt, after
@@ -192,6 +211,12 @@ typedef struct {
     double eps_active;         /* active-set threshold (default 1e-8) */
     double switch_tol;         /* stage switch |df . Pi_T(p)| (default 1e-4) */
     const double *theta0;      /* optional start (rows on the simplex) */
+    int32_t armijo;            /* line-search test.  0 (default): the paper's printed condition
+                                  f(P[Pi + beta^m p]) <= f(Pi) + c beta^m d/dalpha f(P[Pi + alpha p])|_0
+                                  (the one-sided arc derivative at alpha = 0, the
+                                  same slope as the stage switch; a direction with slope >= 0 admits
+                                  no step length); 1: Bertsekas' secant form
+                                  f(Pi(alpha)) <= f(Pi) + c df . (Pi(alpha) - Pi)                 */
 } qdt_newton_opts;
 
 typedef struct {

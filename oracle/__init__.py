@@ -4,8 +4,10 @@ Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline``
 ``--impl reference`` legs may import this package.  The product package
 ``paper_2404_02844_b200`` never imports it, and the two share no code.
 
-This module is a ctypes shim around ``qdt_oracle.c`` (plain fp64 C, one thread,
-``-O2 -ffp-contract=off``): argument marshalling only, every number is computed in C.
+This module is a ctypes shim around ``qdt_oracle.c`` (plain fp64 C, ``-O2
+-ffp-contract=off``, OpenMP with a thread-count-independent deterministic split: results are
+bit-identical for any ``set_threads(n)``): argument marshalling only, every number is
+computed in C.
 Each C function cites the PAPER.md passage it follows.
 
 Parity status: every function below is pinned by a
@@ -32,8 +34,8 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(
-            ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=gnu11", "-shared",
-             "-fPIC", _SRC, "-o", tmp, "-lquadmath", "-lm"])
+            ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=gnu11", "-fopenmp",
+             "-shared", "-fPIC", _SRC, "-o", tmp, "-lquadmath", "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -79,6 +81,7 @@ def lib():
         L.or_solve.argtypes = [_i64p, _i64p, _i64p, _f64p, i64, i64, _f64p, i64, f64, f64, i64,
                                ctypes.c_int, ctypes.c_int, i64, ctypes.c_void_p, _f64p,
                                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                               ctypes.POINTER(f64), ctypes.c_void_p, f64, ctypes.c_void_p,
                                ctypes.POINTER(f64)]
         L.or_solve.restype = i64
         L.or_smooth.argtypes = [_f64p, i64, i64, i64, i64, _f64p]
@@ -91,8 +94,13 @@ def lib():
                                           ctypes.c_void_p, f64, i64, _f64p, ctypes.POINTER(f64)]
         L.or_newton_direction.restype = i64
         L.or_newton.argtypes = [_i64p, _i64p, _i64p, _f64p, i64, i64, _f64p, i64, f64, _f64p, i64, f64,
-                                f64, i64, f64, i64, _f64p, _f64p, _i64p, _i64p, _f64p, ctypes.POINTER(i64)]
+                                f64, i64, f64, i64, ctypes.c_int, _f64p, _f64p, _i64p, _i64p, _f64p,
+                                ctypes.POINTER(i64)]
         L.or_newton.restype = i64
+        L.or_set_threads.argtypes = [ctypes.c_int]
+        L.or_set_threads.restype = None
+        L.or_get_threads.argtypes = []
+        L.or_get_threads.restype = ctypes.c_int
         L.or_newton_set_cg_rtol.argtypes = [f64]
         L.or_newton_set_cg_rtol.restype = None
         _lib = L
@@ -123,6 +131,20 @@ class Probes:
         self.val = np.zeros(self.nnz, np.float64)
         L.or_build_probes(alpha2, D, self.M, c_sigma, margin, self.lo, self.len, self.off,
                           self.val.ctypes.data)
+
+    @classmethod
+    def from_banded(cls, lo, length, val, M: int):
+        """A banded F given directly (the test hook qdt_probes_from_banded's counterpart)."""
+        self = cls.__new__(cls)
+        self.lo = np.ascontiguousarray(lo, dtype=np.int64)
+        self.len = np.ascontiguousarray(length, dtype=np.int64)
+        self.D, self.M = int(self.lo.shape[0]), int(M)
+        self.alpha2 = None
+        self.off = np.concatenate([[0], np.cumsum(self.len)]).astype(np.int64)
+        self.nnz = int(self.off[-1])
+        self.val = _f(val).copy()
+        assert self.val.shape[0] == self.nnz
+        return self
 
     @property
     def hi(self):
@@ -222,22 +244,36 @@ STEP_SQS, STEP_LIPSCHITZ, STEP_BB = 0, 1, 2
 
 
 def solve(F: Probes, P, gamma: float, tol: float, iters: int, step: int = STEP_SQS,
-          accel: int = 0, kkt_every: int = 1, theta0=None):
-    """Projected-gradient solve; returns dict(theta, trace, kkt, kkt_paper, iters_done, step)."""
+          accel: int = 0, kkt_every: int = 1, theta0=None, theta_prev=None, fista_t: float = 0.0):
+    """Projected-gradient solve; returns dict(theta, trace, kkt, kkt_paper, iters_done, step,
+    theta_prev, fista_t).  FISTA resume: theta_prev = Theta_{k-1}, fista_t = tau_k."""
     P = _f(P)
     N = P.shape[1]
     Theta = np.empty((F.M, N))
+    Tprev = np.empty((F.M, N))
     trace = np.full(iters + 1, np.nan)
     kt = np.full(iters + 1, np.nan)
     kp = np.full(iters + 1, np.nan)
     st = ctypes.c_double()
+    tau = ctypes.c_double()
     t0 = None if theta0 is None else _f(theta0)
+    tp = None if theta_prev is None else _f(theta_prev)
     done = lib().or_solve(*F._args(), F.M, P, N, float(gamma), float(tol), int(iters), int(step),
                           int(accel), int(kkt_every), None if t0 is None else t0.ctypes.data,
                           Theta, trace.ctypes.data, kt.ctypes.data, kp.ctypes.data,
-                          ctypes.byref(st))
+                          ctypes.byref(st), None if tp is None else tp.ctypes.data, float(fista_t),
+                          Tprev.ctypes.data, ctypes.byref(tau))
     return dict(theta=Theta, trace=trace[:done + 1], kkt=kt[:done + 1], kkt_paper=kp[:done + 1],
-                iters_done=int(done), step=st.value)
+                iters_done=int(done), step=st.value, theta_prev=Tprev, fista_t=tau.value)
+
+
+def set_threads(n: int = 0):
+    """Thread count of the oracle (0: all cores).  Results do not depend on it."""
+    lib().or_set_threads(int(n))
+
+
+def get_threads() -> int:
+    return int(lib().or_get_threads())
 
 
 def smooth(Theta, exclude: int = 100, div: int = 50):
@@ -281,8 +317,10 @@ def newton_direction(F: Probes, P, gamma: float, Theta, m=None, eps_active: floa
 
 
 def newton(F: Probes, P, gamma: float, max_iter: int, eps_kkt: float = 0.0, theta0=None,
-           eps_active: float = 1e-8, cg_max: int = 50, switch_tol: float = 1e-4, max_ls: int = 60):
-    """Two-stage two-metric projected truncated Newton (reading R16)."""
+           eps_active: float = 1e-8, cg_max: int = 50, switch_tol: float = 1e-4, max_ls: int = 60,
+           armijo: int = 0):
+    """Two-stage two-metric projected truncated Newton (reading R16).
+    armijo 0: the paper's printed line-search test; 1: the secant form."""
     P = _f(P)
     N = P.shape[1]
     Theta = np.full((F.M, N), 1.0 / N) if theta0 is None else _f(theta0).copy()
@@ -295,7 +333,7 @@ def newton(F: Probes, P, gamma: float, max_iter: int, eps_kkt: float = 0.0, thet
     lib().or_newton_set_cg_rtol(-1.0)
     k = lib().or_newton(F.lo, F.len, F.off, F.val, F.D, F.M, P, N, float(gamma), Theta, int(max_iter),
                         float(eps_kkt), float(eps_active), int(cg_max), float(switch_tol), int(max_ls),
-                        tr, kk, st, cg, al, ctypes.byref(sw))
+                        int(armijo), tr, kk, st, cg, al, ctypes.byref(sw))
     return dict(theta=Theta, trace=tr[:k + 1], kkt=kk[:k + 1], stage=st[:k], cg=cg[:k], alpha=al[:k],
                 iters_done=int(k), switch=int(sw.value))
 

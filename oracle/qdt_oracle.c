@@ -21,12 +21,103 @@
  * power-iteration norms) accumulate in x87 extended precision: a plain double running sum
  * of 10^7 - 10^8 nonnegative terms carries a biased rounding error (measured 5e-10 relative
  * on the Large config) that would exceed the objective gate of reading R5.
+ *
+ * Threads (oracle-MT): the file builds with OpenMP.  Work is split only where
+ * the split leaves every floating-point operation and its order unchanged -- a probe row of
+ * F Theta, a block of Fock rows of F^T R (each element still sums over probes d in increasing
+ * order), elementwise and per-row work -- and every scalar reduction is summed in a FIXED chunk
+ * order (OR_CHUNK elements / OR_RCHUNK rows per chunk, chunk partials in extended precision,
+ * then added in chunk order) that does not depend on the thread count.  So the result is
+ * bit-identical for any number of threads (tests/test_oracle_mt.py); or_set_threads(1) is the
+ * single-thread parity reference.
  */
 #include <math.h>
 #include <quadmath.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#define OR_CHUNK 8192   /* elements per partial sum of a flat reduction */
+#define OR_RCHUNK 64    /* rows per partial sum of a row-structured reduction */
+#define OR_RB 256       /* Fock rows per block of the backward product */
+
+void or_set_threads(int n)
+{
+#ifdef _OPENMP
+    omp_set_num_threads(n > 0 ? n : omp_get_num_procs());
+#else
+    (void)n;
+#endif
+}
+
+int or_get_threads(void)
+{
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+/* sum_i x_i^2 in fixed chunks (chunk partials in extended precision, added in chunk order) */
+static double sumsq(const double *x, int64_t n)
+{
+    const int64_t nc = (n + OR_CHUNK - 1) / OR_CHUNK;
+    long double *part = (long double *)malloc((size_t)(nc > 0 ? nc : 1) * sizeof(long double));
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < nc; c++) {
+        long double s = 0.0L;
+        const int64_t e = (c + 1) * OR_CHUNK < n ? (c + 1) * OR_CHUNK : n;
+        for (int64_t i = c * OR_CHUNK; i < e; i++) s += (long double)(x[i] * x[i]);
+        part[c] = s;
+    }
+    long double t = 0.0L;
+    for (int64_t c = 0; c < nc; c++) t += part[c];
+    free(part);
+    return (double)t;
+}
+
+/* sum_i (a_i - b_i)^2, same chunking */
+static double sumsq_diff(const double *a, const double *b, int64_t n)
+{
+    const int64_t nc = (n + OR_CHUNK - 1) / OR_CHUNK;
+    long double *part = (long double *)malloc((size_t)(nc > 0 ? nc : 1) * sizeof(long double));
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < nc; c++) {
+        long double s = 0.0L;
+        const int64_t e = (c + 1) * OR_CHUNK < n ? (c + 1) * OR_CHUNK : n;
+        for (int64_t i = c * OR_CHUNK; i < e; i++) {
+            const double d = a[i] - b[i];
+            s += (long double)(d * d);
+        }
+        part[c] = s;
+    }
+    long double t = 0.0L;
+    for (int64_t c = 0; c < nc; c++) t += part[c];
+    free(part);
+    return (double)t;
+}
+
+/* sum_i a_i b_i in extended precision, same chunking */
+static double dotl(const double *a, const double *b, int64_t n)
+{
+    const int64_t nc = (n + OR_CHUNK - 1) / OR_CHUNK;
+    long double *part = (long double *)malloc((size_t)(nc > 0 ? nc : 1) * sizeof(long double));
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < nc; c++) {
+        long double s = 0.0L;
+        const int64_t e = (c + 1) * OR_CHUNK < n ? (c + 1) * OR_CHUNK : n;
+        for (int64_t i = c * OR_CHUNK; i < e; i++) s += (long double)a[i] * (long double)b[i];
+        part[c] = s;
+    }
+    long double t = 0.0L;
+    for (int64_t c = 0; c < nc; c++) t += part[c];
+    free(part);
+    return (double)t;
+}
 
 #define OR_OK 0
 #define OR_EINVAL 1
@@ -156,9 +247,13 @@ double or_project_simplex(const double *x, int64_t n, double *y, double *work)
 /* Row-wise generalisation P_{S^M} (eq. Mp1_proj). */
 void or_project_rows(const double *X, int64_t M, int64_t N, double *Y)
 {
-    double *work = (double *)malloc((size_t)N * sizeof(double));
-    for (int64_t k = 0; k < M; k++) or_project_simplex(X + k * N, N, Y + k * N, work);
-    free(work);
+#pragma omp parallel
+    {
+        double *work = (double *)malloc((size_t)N * sizeof(double));
+#pragma omp for schedule(static)
+        for (int64_t k = 0; k < M; k++) or_project_simplex(X + k * N, N, Y + k * N, work);
+        free(work);
+    }
 }
 
 /* ------------------------------------------------------------------------------------
@@ -169,7 +264,8 @@ void or_project_rows(const double *X, int64_t M, int64_t N, double *Y)
 void or_forward(const int64_t *lo, const int64_t *len, const int64_t *off, const double *val,
                 int64_t D, const double *Theta, const double *P, int64_t N, double *R)
 {
-    for (int64_t d = 0; d < D; d++) {
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t d = 0; d < D; d++) {   /* probe rows are independent */
         double *r = R + d * N;
         for (int64_t n = 0; n < N; n++) r[n] = 0.0;
         for (int64_t j = 0; j < len[d]; j++) {
@@ -187,6 +283,7 @@ void or_forward(const int64_t *lo, const int64_t *len, const int64_t *off, const
  * (M-1) x M forward difference, free ends (reading R8).  grad g = 2 gamma L Theta. */
 void or_laplacian(const double *Theta, int64_t M, int64_t N, double *LT)
 {
+#pragma omp parallel for schedule(static)
     for (int64_t k = 0; k < M; k++)
         for (int64_t n = 0; n < N; n++) {
             double v = 0.0;
@@ -198,45 +295,45 @@ void or_laplacian(const double *Theta, int64_t M, int64_t N, double *LT)
 
 /* Half gradient G = F^T R + gamma L Theta  (gradient row of Table 1, PAPER.md:243;
  * grad f = 2G, reading R0).  For each d in order and each k in its band:
- * G[k,:] += F[d,k] R[d,:]; then gamma L Theta is added. */
+ * G[k,:] += F[d,k] R[d,:]; then gamma L Theta is added.  Threads take blocks of OR_RB Fock rows;
+ * inside a block the probe loop runs in the same increasing order, so every element of G is the
+ * same sequence of operations as in the single loop over d. */
 void or_backward(const int64_t *lo, const int64_t *len, const int64_t *off, const double *val,
                  int64_t D, int64_t M, const double *R, const double *Theta, int64_t N,
                  double gamma, double *G)
 {
-    memset(G, 0, (size_t)(M * N) * sizeof(double));
-    for (int64_t d = 0; d < D; d++)
-        for (int64_t j = 0; j < len[d]; j++) {
-            double f = val[off[d] + j];
-            double *g = G + (lo[d] + j) * N;
-            const double *r = R + d * N;
-            for (int64_t n = 0; n < N; n++) g[n] += f * r[n];
+    const int64_t nb = (M + OR_RB - 1) / OR_RB;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t b = 0; b < nb; b++) {
+        const int64_t r0 = b * OR_RB, r1 = (r0 + OR_RB < M) ? r0 + OR_RB : M;
+        memset(G + r0 * N, 0, (size_t)((r1 - r0) * N) * sizeof(double));
+        for (int64_t d = 0; d < D; d++) {
+            const int64_t a = lo[d] > r0 ? lo[d] : r0;
+            const int64_t e = (lo[d] + len[d] < r1) ? lo[d] + len[d] : r1;
+            for (int64_t k = a; k < e; k++) {
+                double f = val[off[d] + (k - lo[d])];
+                double *g = G + k * N;
+                const double *r = R + d * N;
+                for (int64_t n = 0; n < N; n++) g[n] += f * r[n];
+            }
         }
+    }
     if (gamma != 0.0 && M > 1) {
         double *LT = (double *)malloc((size_t)(M * N) * sizeof(double));
         or_laplacian(Theta, M, N, LT);
+#pragma omp parallel for schedule(static)
         for (int64_t i = 0; i < M * N; i++) G[i] += gamma * LT[i];
         free(LT);
     }
 }
 
-/* sum_n sum_{i=0}^{M-2} (Theta_{i,n} - Theta_{i+1,n})^2   (eq. regul) */
+/* sum_n sum_{i=0}^{M-2} (Theta_{i,n} - Theta_{i+1,n})^2   (eq. regul):
+ * the pairs (i, i+1) with i < M-1, i.e. sum (a - b)^2 over the first (M-1) N entries against the
+ * entries one row below (fixed chunks, see the header) */
 double or_regul(const double *Theta, int64_t M, int64_t N)
 {
-    long double s = 0.0L; /* long scalar sums accumulate in extended precision (see header) */
-    for (int64_t k = 0; k + 1 < M; k++)
-        for (int64_t n = 0; n < N; n++) {
-            double d = Theta[k * N + n] - Theta[(k + 1) * N + n];
-            s += (long double)(d * d);
-        }
-    return (double)s;
-}
-
-/* ||R||_F^2 over D x N entries, extended-precision accumulator */
-static double sumsq(const double *R, int64_t n)
-{
-    long double s = 0.0L;
-    for (int64_t i = 0; i < n; i++) s += (long double)(R[i] * R[i]);
-    return (double)s;
+    if (M < 2) return 0.0;
+    return sumsq_diff(Theta, Theta + N, (M - 1) * N);
 }
 
 /* f(Theta) = ||P - F Theta||_2^2 + gamma * regul   (eq. min_obj2 PAPER.md:70 + eq. regul) */
@@ -257,8 +354,13 @@ double or_objective(const int64_t *lo, const int64_t *len, const int64_t *off, c
  * df = 2G (reading R0).  Returns the unclamped value; *paper_out gets the clamped one. */
 double or_kkt(const double *Theta, const double *G, int64_t M, int64_t N, double *paper_out)
 {
+    const int64_t nc = (M + OR_RCHUNK - 1) / OR_RCHUNK;
+    long double *ps = (long double *)malloc((size_t)nc * 2 * sizeof(long double));
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < nc; c++) {
     long double s = 0.0L, sp = 0.0L;
-    for (int64_t k = 0; k < M; k++) {
+    const int64_t k1 = ((c + 1) * OR_RCHUNK < M) ? (c + 1) * OR_RCHUNK : M;
+    for (int64_t k = c * OR_RCHUNK; k < k1; k++) {
         double mn = INFINITY;
         for (int64_t n = 0; n < N; n++) {
             double df = 2.0 * G[k * N + n];
@@ -274,6 +376,15 @@ double or_kkt(const double *Theta, const double *G, int64_t M, int64_t N, double
             sp += (long double)(b * b);
         }
     }
+    ps[2 * c] = s;
+    ps[2 * c + 1] = sp;
+    }
+    long double s = 0.0L, sp = 0.0L;
+    for (int64_t c = 0; c < nc; c++) {
+        s += ps[2 * c];
+        sp += ps[2 * c + 1];
+    }
+    free(ps);
     if (paper_out) *paper_out = sqrt((double)sp / ((double)N * (double)M));
     return sqrt((double)s / ((double)N * (double)M));
 }
@@ -286,13 +397,25 @@ double or_kkt(const double *Theta, const double *G, int64_t M, int64_t N, double
 void or_sqs_weights(const int64_t *lo, const int64_t *len, const int64_t *off, const double *val,
                     int64_t D, int64_t M, double gamma, double *w)
 {
-    for (int64_t k = 0; k < M; k++) w[k] = 0.0;
+    double *sd = (double *)malloc((size_t)D * sizeof(double));
     for (int64_t d = 0; d < D; d++) {
         double s = 0.0;
         for (int64_t j = 0; j < len[d]; j++) s += val[off[d] + j];
-        for (int64_t j = 0; j < len[d]; j++) w[lo[d] + j] += val[off[d] + j] * s;
+        sd[d] = s;
     }
-    for (int64_t k = 0; k < M; k++) w[k] += 4.0 * gamma;
+    const int64_t nb = (M + OR_RB - 1) / OR_RB;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t b = 0; b < nb; b++) {   /* w[k] sums over d in increasing order (as one loop) */
+        const int64_t r0 = b * OR_RB, r1 = (r0 + OR_RB < M) ? r0 + OR_RB : M;
+        for (int64_t k = r0; k < r1; k++) w[k] = 0.0;
+        for (int64_t d = 0; d < D; d++) {
+            const int64_t a = lo[d] > r0 ? lo[d] : r0;
+            const int64_t e = (lo[d] + len[d] < r1) ? lo[d] + len[d] : r1;
+            for (int64_t k = a; k < e; k++) w[k] += val[off[d] + (k - lo[d])] * sd[d];
+        }
+        for (int64_t k = r0; k < r1; k++) w[k] += 4.0 * gamma;
+    }
+    free(sd);
 }
 
 /* Power iteration for rho ~ lambda_max(F^T F): v0 = 1/sqrt(M); exactly K_pow iterations of
@@ -334,7 +457,10 @@ double or_power_iteration(const int64_t *lo, const int64_t *len, const int64_t *
  *            (H = F^T F + gamma L, the Hessian of f/2), clamped to [t_LIP, 1e6 t_LIP];
  *            t_LIP when <s,Hs> <= 0.  Plain projected gradient only (accel ignored).
  *   accel 1: FISTA extrapolation Y_k = Theta_k + (tau_k - 1)/tau_{k+1} (Theta_k - Theta_{k-1}),
- *            tau_0 = 1, tau_{k+1} = (1 + sqrt(1 + 4 tau_k^2))/2.
+ *            tau_0 = 1, tau_{k+1} = (1 + sqrt(1 + 4 tau_k^2))/2 (Beck-Teboulle).  Resume state
+ *            (SURVEY 8(b)): theta_prev = Theta_{-1} (NULL: Theta_0) and tau0 = tau_0 (< 1: 1);
+ *            theta_prev_out / tau_out (may be NULL) receive Theta_{k-1} and tau_k of the returned
+ *            iterate k.
  *   iteration k (reading R3):
  *     R = F Y - P;  G = F^T R + gamma L Y;  Theta_{k+1} = P_{S^M}(Y - t o G);
  *     trace[k] = f(Theta_k);  kkt[k] = r(Theta_k) (G at Theta_k; for FISTA an extra pass);
@@ -346,7 +472,8 @@ int64_t or_solve(const int64_t *lo, const int64_t *len, const int64_t *off, cons
                  int64_t D, int64_t M, const double *P, int64_t N, double gamma, double tol,
                  int64_t iters, int step_mode, int accel, int64_t kkt_every, const double *theta0,
                  double *Theta, double *trace, double *kkt_trace, double *kkt_paper_trace,
-                 double *step_out)
+                 double *step_out, const double *theta_prev, double tau0, double *theta_prev_out,
+                 double *tau_out)
 {
     size_t MN = (size_t)(M * N);
     double *Tprev = (double *)malloc(MN * sizeof(double));
@@ -379,8 +506,11 @@ int64_t or_solve(const int64_t *lo, const int64_t *len, const int64_t *off, cons
     }
 
     for (size_t i = 0; i < MN; i++) Theta[i] = theta0 ? theta0[i] : 1.0 / (double)N;
-    memcpy(Tprev, Theta, MN * sizeof(double));
-    double tau = 1.0;
+    if (accel && theta_prev)
+        memcpy(Tprev, theta_prev, MN * sizeof(double));
+    else
+        memcpy(Tprev, Theta, MN * sizeof(double));
+    double tau = (accel && tau0 >= 1.0) ? tau0 : 1.0;
     int64_t k;
     for (k = 0; k < iters; k++) {
         double beta = 0.0, tau_next = tau;
@@ -388,30 +518,22 @@ int64_t or_solve(const int64_t *lo, const int64_t *len, const int64_t *off, cons
             tau_next = (1.0 + sqrt(1.0 + 4.0 * tau * tau)) / 2.0;
             beta = (tau - 1.0) / tau_next;
         }
+#pragma omp parallel for schedule(static)
         for (size_t i = 0; i < MN; i++) Y[i] = Theta[i] + beta * (Theta[i] - Tprev[i]);
         /* gradient at Y */
         or_forward(lo, len, off, val, D, Y, P, N, R);
         if (step_mode == 2 && k >= 1) {
             /* BB: s = Theta_k - Theta_{k-1} (Tprev), <s,Hs> = ||R_k - R_{k-1}||^2 + gamma ||D s||^2 */
-            long double ss = 0.0L, sh = 0.0L, sd = 0.0L;
-            for (size_t i = 0; i < MN; i++) {
-                double d = Theta[i] - Tprev[i];
-                ss += (long double)(d * d);
-            }
-            for (int64_t i = 0; i < D * N; i++) {
-                double d = R[i] - Rprev[i];
-                sh += (long double)(d * d);
-            }
-            for (int64_t r = 0; r + 1 < M; r++)
-                for (int64_t n = 0; n < N; n++) {
-                    double a = Theta[r * N + n] - Tprev[r * N + n];
-                    double b = Theta[(r + 1) * N + n] - Tprev[(r + 1) * N + n];
-                    sd += (long double)((a - b) * (a - b));
-                }
-            double shs = (double)sh + gamma * (double)sd;
+            /* s = Theta_k - Theta_{k-1} (X as scratch); ||D s||^2 = regulariser sum of s */
+#pragma omp parallel for schedule(static)
+            for (size_t i = 0; i < MN; i++) X[i] = Theta[i] - Tprev[i];
+            const double ss = sumsq(X, (int64_t)MN);
+            const double sh = sumsq_diff(R, Rprev, D * N);
+            const double sd = or_regul(X, M, N);
+            double shs = sh + gamma * sd;
             double tb = t_lip;
             if (shs > 0.0) {
-                tb = (double)ss / shs;
+                tb = ss / shs;
                 if (tb < t_lip) tb = t_lip;
                 if (tb > 1e6 * t_lip) tb = 1e6 * t_lip;
             }
@@ -438,6 +560,7 @@ int64_t or_solve(const int64_t *lo, const int64_t *len, const int64_t *off, cons
         if (kkt_paper_trace) kkt_paper_trace[k] = rpk;
         if (k % kkt_every == 0 && rk <= tol) break; /* NaN compares false */
         /* step + projection */
+#pragma omp parallel for schedule(static)
         for (int64_t r = 0; r < M; r++)
             for (int64_t n = 0; n < N; n++) X[r * N + n] = Y[r * N + n] - t[r] * G[r * N + n];
         memcpy(Tprev, Theta, MN * sizeof(double));
@@ -454,6 +577,8 @@ int64_t or_solve(const int64_t *lo, const int64_t *len, const int64_t *off, cons
         if (kkt_trace) kkt_trace[iters] = r;
         if (kkt_paper_trace) kkt_paper_trace[iters] = rp;
     }
+    if (theta_prev_out) memcpy(theta_prev_out, Tprev, MN * sizeof(double));
+    if (tau_out) *tau_out = tau;
     free(Tprev);
     free(Y);
     free(X);
@@ -502,8 +627,13 @@ void or_smooth(const double *Theta, int64_t M, int64_t N, int64_t exclude, int64
  * the free set; D p = -df is solved by diagonally preconditioned CG from p = 0,
  * truncated at cg_max iterations or ||r|| <= min(0.5, sqrt||b||) ||b|| (Nocedal-Wright's
  * forcing sequence; the paper only says "truncated").  Line search alpha = beta^m, beta = 3/4,
- * c = 1/10 with Bertsekas' Armijo rule along the projection arc:
- * f(x(alpha)) <= f(x) + c df . (x(alpha) - x).  Stage switch when the
+ * c = 1/10.  armijo = 0 (default): the paper's printed condition
+ *   f(P[x + beta^m p]) <= f(x) + c beta^m d/dalpha f(P[x + alpha p])|_{alpha=0},
+ * the derivative being the one-sided arc slope at 0 (stage 1: df . Pi_T(p); stage 2: the reduced
+ * gradient . p with p_j -> 0 where x_j = 0 and p_j < 0); a direction whose slope is >= 0 admits no
+ * step length (the condition cannot certify descent: DESIGN.md reading R16).  armijo = 1:
+ * Bertsekas' secant form along the projection arc f(x(alpha)) <= f(x) + c df . (x(alpha) - x).
+ * Stage switch when the
  * one-sided derivative of the stage-1 arc at alpha = 0, df . d0 with d0 the projection of p
  * onto the simplex tangent cone at Theta, satisfies |df . d0| <= switch_tol.  Stop when the
  * KKT measure (R7, unclamped multiplier) <= eps_kkt, or when no step length is accepted in
@@ -539,12 +669,6 @@ static double nt_f(const or_prob *q, const double *Th)
     return or_objective(q->lo, q->len, q->off, q->val, q->D, q->M, q->P, Th, q->N, q->gamma);
 }
 
-static double dotl(const double *a, const double *b, int64_t n)
-{
-    long double s = 0.0L;
-    for (int64_t i = 0; i < n; i++) s += (long double)a[i] * (long double)b[i];
-    return (double)s;
-}
 
 /* Hessian diagonal per Fock row: h_i = 2 (sum_d F_{d,i}^2 + gamma L_ii) */
 void or_hess_diag(const int64_t *lo, const int64_t *len, const int64_t *off, const double *val,
@@ -736,7 +860,7 @@ void or_row_argmax(const double *Theta, int64_t M, int64_t N, int64_t *m)
 int64_t or_newton(const int64_t *lo, const int64_t *len, const int64_t *off, const double *val,
                   int64_t D, int64_t M, const double *P, int64_t N, double gamma, double *Theta,
                   int64_t max_iter, double eps_kkt, double eps_active, int64_t cg_max,
-                  double switch_tol, int64_t max_ls, double *trace, double *kkt, int64_t *stage_log,
+                  double switch_tol, int64_t max_ls, int armijo, double *trace, double *kkt, int64_t *stage_log,
                   int64_t *cg_log, double *alpha_log, int64_t *switch_out)
 {
     or_prob q = {lo, len, off, val, D, M, N, P, gamma};
@@ -805,7 +929,18 @@ int64_t or_newton(const int64_t *lo, const int64_t *len, const int64_t *off, con
                     if (T1[i * N + mrow[i]] < 0.0) ok = 0;
                 if (!ok) continue;
             }
-            /* Armijo along the arc: f(T1) <= f0 + c df . (T1 - Theta) (stage 2: reduced df) */
+            if (armijo == 0) {
+                /* the paper's condition: f(P[Theta + a p]) <= f0 + c a slope,
+                 * slope = one-sided arc derivative at alpha = 0 (this iteration's stage) */
+                if (!(slope < 0.0)) break;   /* no descent certified: no admissible step length */
+                const double f1 = nt_f(&q, T1);
+                if (f1 <= f0 + c_arm * a * slope) {
+                    accepted = 1;
+                    alpha = a;
+                }
+                continue;
+            }
+            /* secant form along the arc: f(T1) <= f0 + c df . (T1 - Theta) (stage 2: reduced df) */
             long double dd = 0.0L;
             for (int64_t i = 0; i < n; i++) {
                 const int64_t rr = i / N, cc = i % N;

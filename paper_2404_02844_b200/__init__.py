@@ -30,7 +30,7 @@ ABI_SYMBOLS = ["qdt_init", "qdt_finalize", "qdt_last_error", "qdt_build_probes",
                "qdt_probes_export", "qdt_solve", "qdt_objective", "qdt_residual", "qdt_gradient",
                "qdt_step", "qdt_project_rows", "qdt_step_setup", "qdt_profile_enable",
                "qdt_profile_get", "qdt_launch_count", "qdt_nccl_unique_id", "qdt_shard_cuts",
-               "qdt_smooth", "qdt_solve_newton"]
+               "qdt_smooth", "qdt_solve_newton", "qdt_probes_from_banded"]
 
 
 class QdtError(RuntimeError):
@@ -53,13 +53,14 @@ class SolveOpts(ctypes.Structure):
     _fields_ = [("step", ctypes.c_int32), ("accel", ctypes.c_int32), ("theta0", ctypes.c_void_p),
                 ("check_every", ctypes.c_int32), ("kkt_every", ctypes.c_int32),
                 ("mem_device", ctypes.c_int32), ("gather_theta", ctypes.c_int32),
-                ("use_graph", ctypes.c_int32)]
+                ("use_graph", ctypes.c_int32), ("theta_prev", ctypes.c_void_p),
+                ("fista_t", ctypes.c_double), ("theta_prev_out", ctypes.c_void_p)]
 
 
 class NewtonOpts(ctypes.Structure):
     _fields_ = [("max_iter", ctypes.c_int32), ("cg_max", ctypes.c_int32), ("max_ls", ctypes.c_int32),
                 ("mem_device", ctypes.c_int32), ("eps_active", ctypes.c_double),
-                ("switch_tol", ctypes.c_double), ("theta0", ctypes.c_void_p)]
+                ("switch_tol", ctypes.c_double), ("theta0", ctypes.c_void_p), ("armijo", ctypes.c_int32)]
 
 
 class NewtonInfo(ctypes.Structure):
@@ -76,7 +77,7 @@ class SolveInfo(ctypes.Structure):
                 ("f_final", ctypes.c_double), ("step_scalar", ctypes.c_double),
                 ("k_begin", ctypes.c_int64), ("k_end", ctypes.c_int64), ("nnz", ctypes.c_int64),
                 ("min_row_mass", ctypes.c_double), ("uncovered_rows", ctypes.c_int64),
-                ("loop_ms", ctypes.c_double)]
+                ("loop_ms", ctypes.c_double), ("fista_t", ctypes.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -101,6 +102,7 @@ def load_library(path: str = LIB_PATH):
     L.qdt_last_error.restype = ctypes.c_char_p
     L.qdt_build_probes.argtypes = [vp, vp, i64, i64, P(ProbeOpts), P(vp)]
     L.qdt_probes_free.argtypes = [vp]
+    L.qdt_probes_from_banded.argtypes = [vp, i64, i64, vp, vp, vp, P(vp)]
     L.qdt_probes_export.argtypes = [vp, vp, P(i64), P(i64), P(i64), vp, vp, vp]
     L.qdt_solve.argtypes = [vp, vp, vp, i64, f64, f64, i64, P(SolveOpts), vp, vp, vp, P(SolveInfo)]
     L.qdt_objective.argtypes = [vp, vp, vp, vp, i64, f64, i32, P(f64), P(f64)]
@@ -131,8 +133,9 @@ def _check(ctx, status):
 
 
 class Context:
-    def __init__(self, ptr):
+    def __init__(self, ptr, device=0):
         self.ptr = ptr
+        self.device = device
 
     def __del__(self):
         if getattr(self, "ptr", None) and _lib is not None:
@@ -158,6 +161,30 @@ def _is_cuda_tensor(x):
     return hasattr(x, "is_cuda") and x.is_cuda
 
 
+def _dev_arg(ctx: Context, x, name: str, shape=None):
+    """A CUDA tensor argument: float64, contiguous, on ctx's device, of the given shape (the
+    library reads raw fp64 memory).  Raises instead of converting silently."""
+    import torch
+    if not _is_cuda_tensor(x):
+        raise TypeError(f"{name}: expected a CUDA tensor (P is one)")
+    if x.dtype != torch.float64:
+        raise TypeError(f"{name}: dtype {x.dtype}, the library computes in float64")
+    if x.device.index != ctx.device:
+        raise ValueError(f"{name}: on {x.device}, the context is on cuda:{ctx.device}")
+    if shape is not None and tuple(x.shape) != tuple(shape):
+        raise ValueError(f"{name}: shape {tuple(x.shape)}, expected {tuple(shape)}")
+    if not x.is_contiguous():
+        raise ValueError(f"{name}: not contiguous")
+    return x
+
+
+def _order_after_torch(ctx: Context):
+    """Device pointers are read on the library's own stream: finish the work torch queued on
+    its current stream (the producer of P / theta0) before the call."""
+    import torch
+    torch.cuda.current_stream(ctx.device).synchronize()
+
+
 def qdt_init(device: int = 0, rank: int = 0, nranks: int = 1, nccl_unique_id: bytes | None = None,
              cuda_stream: int | None = None) -> Context:
     L = load_library()
@@ -168,7 +195,7 @@ def qdt_init(device: int = 0, rank: int = 0, nranks: int = 1, nccl_unique_id: by
     st = L.qdt_init(ctypes.byref(p), ctypes.byref(o))
     if st != 0:
         raise QdtError(st, (L.qdt_last_error(None) or b"").decode())
-    return Context(p)
+    return Context(p, device)
 
 
 def qdt_finalize(ctx: Context):
@@ -185,6 +212,16 @@ def qdt_build_probes(ctx: Context, alpha2, M: int, c_sigma: float = 6.0, margin:
     _check(ctx, load_library().qdt_build_probes(ctx.ptr, a.ctypes.data, a.shape[0], int(M),
                                                 ctypes.byref(o), ctypes.byref(p)))
     return Probes(ctx, p, a.shape[0], int(M))
+
+
+def qdt_probes_from_banded(ctx: Context, lo, length, vals, M: int) -> Probes:
+    """Test hook: a probe handle from an arbitrary banded F (include/qdt.h)."""
+    lo_, ln_ = _host(lo, np.int64), _host(length, np.int64)
+    v = _host(vals)
+    p = ctypes.c_void_p()
+    _check(ctx, load_library().qdt_probes_from_banded(ctx.ptr, lo_.shape[0], int(M), lo_.ctypes.data,
+                                                      ln_.ctypes.data, v.ctypes.data, ctypes.byref(p)))
+    return Probes(ctx, p, lo_.shape[0], int(M))
 
 
 def qdt_probes_export(ctx: Context, F: Probes, values: bool = True):
@@ -204,47 +241,68 @@ def qdt_probes_export(ctx: Context, F: Probes, values: bool = True):
 def qdt_solve(ctx: Context, F: Probes, P, gamma: float, tol: float = 0.0, iters: int = 100,
               step: int = QDT_STEP_SQS, accel: bool = False, theta0=None, check_every: int = 16,
               kkt_every: int = 1, gather_theta: bool = False, use_graph: bool = True,
-              theta_out=None):
+              theta_out=None, theta_prev=None, fista_t: float = 0.0, want_prev: bool = False):
     """Projected-gradient solve.  P: numpy (host) or CUDA tensor (device, then theta0 and
-    theta_out are device tensors too).  Returns dict(theta, trace, kkt, info)."""
+    theta_out are device tensors too).  FISTA resume: theta_prev = Theta_{k-1}, fista_t = tau_k;
+    want_prev returns Theta_{k-1} of the result as 'theta_prev'.  Returns dict(theta, trace,
+    kkt, info[, theta_prev])."""
     L = load_library()
     dev = _is_cuda_tensor(P)
+    prev_out = None
     if dev:
         import torch
         D, N = P.shape
-        Pp = P.contiguous()
+        _dev_arg(ctx, P, "P", (F.D, N))
         rows = F.M
         if theta_out is None:
             theta_out = torch.empty((rows, N), dtype=torch.float64, device=P.device)
-        t0 = theta0.contiguous() if theta0 is not None else None
-        p_ptr, out_ptr = Pp.data_ptr(), theta_out.data_ptr()
+        _dev_arg(ctx, theta_out, "theta_out", (rows, N))
+        t0 = _dev_arg(ctx, theta0, "theta0", (rows, N)) if theta0 is not None else None
+        tp = _dev_arg(ctx, theta_prev, "theta_prev", (rows, N)) if theta_prev is not None else None
+        if want_prev:
+            prev_out = torch.empty((rows, N), dtype=torch.float64, device=P.device)
+        p_ptr, out_ptr = P.data_ptr(), theta_out.data_ptr()
         t0_ptr = t0.data_ptr() if t0 is not None else None
+        tp_ptr = tp.data_ptr() if tp is not None else None
+        po_ptr = prev_out.data_ptr() if prev_out is not None else None
+        _order_after_torch(ctx)
     else:
         Pp = _host(P)
         D, N = Pp.shape
         if theta_out is None:
             theta_out = np.empty((F.M, N))
         t0 = _host(theta0) if theta0 is not None else None
+        tp = _host(theta_prev) if theta_prev is not None else None
+        if want_prev:
+            prev_out = np.empty((F.M, N))
         p_ptr, out_ptr = Pp.ctypes.data, theta_out.ctypes.data
         t0_ptr = t0.ctypes.data if t0 is not None else None
+        tp_ptr = tp.ctypes.data if tp is not None else None
+        po_ptr = prev_out.ctypes.data if prev_out is not None else None
     trace = np.full(iters + 1, np.nan)
     kkt = np.full(iters + 1, np.nan)
     o = SolveOpts(step, int(accel), t0_ptr, check_every, kkt_every, int(dev), int(gather_theta),
-                  int(use_graph))
+                  int(use_graph), tp_ptr, float(fista_t), po_ptr)
     info = SolveInfo()
     _check(ctx, L.qdt_solve(ctx.ptr, F.ptr, p_ptr, N, float(gamma), float(tol), int(iters),
                             ctypes.byref(o), out_ptr, trace.ctypes.data, kkt.ctypes.data,
                             ctypes.byref(info)))
     k = info.iters_done
-    return dict(theta=theta_out, trace=trace[:k + 1], kkt=kkt[:k + 1], info=info.as_dict())
+    out = dict(theta=theta_out, trace=trace[:k + 1], kkt=kkt[:k + 1], info=info.as_dict())
+    if want_prev:
+        out["theta_prev"] = prev_out
+    return out
 
 
 def qdt_objective(ctx: Context, F: Probes, P, theta, gamma: float):
     L = load_library()
     dev = _is_cuda_tensor(P)
     if dev:
-        Pp, Tp = P.contiguous(), theta.contiguous()
-        pp, tp, N = Pp.data_ptr(), Tp.data_ptr(), Pp.shape[1]
+        N = P.shape[1]
+        Pp = _dev_arg(ctx, P, "P", (F.D, N))
+        Tp = _dev_arg(ctx, theta, "theta", (F.M, N))
+        pp, tp = Pp.data_ptr(), Tp.data_ptr()
+        _order_after_torch(ctx)
     else:
         Pp, Tp = _host(P), _host(theta)
         pp, tp, N = Pp.ctypes.data, Tp.ctypes.data, Pp.shape[1]
@@ -340,8 +398,9 @@ def qdt_smooth(ctx: Context, theta, exclude: int = 100, div: int = 50, out=None)
     L = load_library()
     if _is_cuda_tensor(theta):
         import torch
-        th = theta.contiguous()
-        out = torch.empty_like(th) if out is None else out
+        th = _dev_arg(ctx, theta, "theta")
+        out = torch.empty_like(th) if out is None else _dev_arg(ctx, out, "out", tuple(th.shape))
+        _order_after_torch(ctx)
         _check(ctx, L.qdt_smooth(ctx.ptr, th.data_ptr(), th.shape[0], th.shape[1], int(exclude),
                                  int(div), 1, out.data_ptr()))
         return out
@@ -354,7 +413,7 @@ def qdt_smooth(ctx: Context, theta, exclude: int = 100, div: int = 50, out=None)
 
 def qdt_solve_newton(ctx: Context, F: Probes, P, gamma: float, eps_kkt: float = 0.0, max_iter: int = 100,
                      cg_max: int = 50, max_ls: int = 60, eps_active: float = 1e-8, switch_tol: float = 1e-4,
-                     theta0=None):
+                     theta0=None, armijo: int = 0):
     """Two-stage two-metric projected truncated Newton (include/qdt.h qdt_solve_newton; reading R16).
     Host numpy P / theta0 (single rank).  Returns dict(theta, trace, kkt, stage, cg, alpha, info)."""
     L = load_library()
@@ -363,7 +422,7 @@ def qdt_solve_newton(ctx: Context, F: Probes, P, gamma: float, eps_kkt: float = 
     M = F.M
     t0 = _host(theta0) if theta0 is not None else None
     o = NewtonOpts(int(max_iter), int(cg_max), int(max_ls), 0, float(eps_active), float(switch_tol),
-                   t0.ctypes.data if t0 is not None else None)
+                   t0.ctypes.data if t0 is not None else None, int(armijo))
     theta = np.empty((M, N))
     tr = np.full(max_iter + 1, np.nan)
     kk = np.full(max_iter + 1, np.nan)

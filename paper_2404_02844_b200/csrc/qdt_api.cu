@@ -172,6 +172,7 @@ struct qdt_probes {
     int64_t nnz = 0;
     std::vector<int32_t> lo_g, hi_g, lo_l, len_l;
     std::vector<int64_t> off;
+    std::vector<int64_t> cuts;   // Fock-axis shard cuts of every rank (nranks + 1)
     double min_row_mass = 1.0;
     int64_t uncovered = 0;
     std::map<int, std::unique_ptr<Plan>> plans;
@@ -194,6 +195,21 @@ struct qdt_probes {
         cudaFree(d_len);
         cudaFree(d_off);
         cudaFree(d_val);
+    }
+};
+
+// two CUDA events destroyed with their owner (every early return of a solve releases them)
+struct EventPair {
+    cudaEvent_t a = nullptr, b = nullptr;
+    cudaError_t create()
+    {
+        cudaError_t e = cudaEventCreate(&a);
+        return e == cudaSuccess ? cudaEventCreate(&b) : e;
+    }
+    ~EventPair()
+    {
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
     }
 };
 
@@ -409,6 +425,29 @@ static qdt_status allreduce(qdt_ctx *ctx, double *buf, size_t n, const char *nam
     });
     (void)e;
     if (r != 0) return fail(ctx, QDT_ERR_NCCL, "ncclAllReduce(%s): %s", name, g_nccl.getErrorString(r));
+    return QDT_OK;
+}
+
+// All-gather of the row slices: full (M x N, pitch N) receives every rank's slice rows
+// [cuts[g], cuts[g+1]) at its place; src: this rank's local rows.  NCCL: grouped send/recv of
+// the slices (no zero-padded allreduce of the whole matrix).
+static qdt_status gather_rows(qdt_ctx *ctx, const qdt_probes *p, const double *src, int64_t N, double *full)
+{
+    CK(cudaMemcpyAsync(full + p->kb * N, src, sizeof(double) * p->Ml * N, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (ctx->nranks == 1) return QDT_OK;
+    nccl_result_t e = 0;
+    run_k(ctx, "gather", 1, [&]() {
+        g_nccl.groupStart();
+        for (int q = 0; q < ctx->nranks; q++) {
+            if (q == ctx->rank) continue;
+            const int64_t qb = p->cuts[q], qe = p->cuts[q + 1];
+            e |= g_nccl.send(src, (size_t)(p->Ml * N), NCCL_FLOAT64, q, ctx->comm, ctx->stream);
+            e |= g_nccl.recv(full + qb * N, (size_t)((qe - qb) * N), NCCL_FLOAT64, q, ctx->comm, ctx->stream);
+        }
+        e |= g_nccl.groupEnd();
+        return cudaSuccess;
+    });
+    if (e != 0) return fail(ctx, QDT_ERR_NCCL, "row gather failed");
     return QDT_OK;
 }
 
@@ -857,6 +896,76 @@ static qdt_status build_plan(qdt_ctx *ctx, qdt_probes *p, int N, Plan **out)
     return QDT_OK;
 }
 
+// Shard, local band tables and values of a probe handle whose global edges lo_g / hi_g are set:
+// values from the S0 kernel (vals == nullptr: p->d_alpha2 holds mu) or copied from host vals
+// (global probe-major bands, qdt_probes_from_banded).
+static qdt_status finish_probes(qdt_ctx *ctx, qdt_probes *p, const double *vals)
+{
+    cudaStream_t s = ctx->stream;
+    const int64_t D = p->D, M = p->M;
+    // shard the Fock axis
+    std::vector<int64_t> &cuts = p->cuts;
+    shard_bounds(p->lo_g, p->hi_g, M, ctx->nranks, cuts);
+    p->kb = cuts[ctx->rank];
+    p->ke = cuts[ctx->rank + 1];
+    p->Ml = p->ke - p->kb;
+    if (p->Ml < 1) return fail(ctx, QDT_ERR_INVALID_ARG, "rank %d owns no Fock rows (M too small)", ctx->rank);
+    p->lo_l.resize(D);
+    p->len_l.resize(D);
+    p->off.resize(D + 1);
+    p->off[0] = 0;
+    for (int64_t d = 0; d < D; d++) {
+        int64_t a = std::max<int64_t>(p->lo_g[d], p->kb), b = std::min<int64_t>(p->hi_g[d], p->ke - 1);
+        p->lo_l[d] = (int32_t)a;
+        p->len_l[d] = b >= a ? (int32_t)(b - a + 1) : 0;
+        p->off[d + 1] = p->off[d] + p->len_l[d];
+    }
+    p->nnz = p->off[D];
+    {   // uncovered rows of this slice (reading R9)
+        std::vector<int32_t> diff(p->Ml + 1, 0);
+        for (int64_t d = 0; d < D; d++)
+            if (p->len_l[d]) {
+                diff[p->lo_l[d] - p->kb] += 1;
+                diff[p->lo_l[d] - p->kb + p->len_l[d]] -= 1;
+            }
+        int64_t c = 0, unc = 0;
+        for (int64_t k = 0; k < p->Ml; k++) {
+            c += diff[k];
+            unc += (c == 0);
+        }
+        p->uncovered = unc;
+    }
+    CK(cudaMemcpyAsync(p->d_lo, p->lo_l.data(), sizeof(int32_t) * D, cudaMemcpyHostToDevice, s));
+    CK(cudaMalloc(&p->d_len, sizeof(int32_t) * D));
+    CK(cudaMemcpyAsync(p->d_len, p->len_l.data(), sizeof(int32_t) * D, cudaMemcpyHostToDevice, s));
+    CK(cudaMalloc(&p->d_off, sizeof(int64_t) * (D + 1)));
+    CK(cudaMemcpyAsync(p->d_off, p->off.data(), sizeof(int64_t) * (D + 1), cudaMemcpyHostToDevice, s));
+    CK(cudaMalloc(&p->d_val, sizeof(double) * std::max<int64_t>(1, p->nnz)));
+    if (vals) {   // host values of the global bands: keep this slice's part of each band
+        std::vector<double> hv(std::max<int64_t>(1, p->nnz));
+        int64_t go = 0;
+        for (int64_t d = 0; d < D; d++) {
+            if (p->len_l[d]) memcpy(hv.data() + p->off[d], vals + go + (p->lo_l[d] - p->lo_g[d]), sizeof(double) * p->len_l[d]);
+            go += (int64_t)p->hi_g[d] - p->lo_g[d] + 1;
+        }
+        CK(cudaMemcpyAsync(p->d_val, hv.data(), sizeof(double) * p->nnz, cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));
+    } else {   // S0 (b): values on the device
+        CK(run_k(ctx, "probe_values", 1, [&]() { return launch_probe_values(p->d_alpha2, D, p->band(), s); }));
+    }
+    // stored mass per probe (diagnostic; summed over ranks)
+    double *d_s = nullptr;
+    CKS(ws_get(ctx, "probe_s", D, &d_s));
+    CK(run_k(ctx, "probe_rowsum", 1, [&]() { return launch_probe_rowsum(D, p->band(), d_s, s); }));
+    CKS(allreduce(ctx, d_s, D, "allreduce_s"));
+    std::vector<double> hs(D);
+    CK(cudaMemcpyAsync(hs.data(), d_s, sizeof(double) * D, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    p->min_row_mass = *std::min_element(hs.begin(), hs.end());
+    return QDT_OK;
+}
+
+
 // ------------------------------------------------------------------------------ probes
 extern "C" qdt_status qdt_build_probes(qdt_ctx *ctx, const double *alpha2, int64_t D, int64_t M,
                                        const qdt_probe_opts *o, qdt_probes **out)
@@ -910,55 +1019,47 @@ extern "C" qdt_status qdt_build_probes(qdt_ctx *ctx, const double *alpha2, int64
                             (long long)d, mu, (long long)M);
         }
     }
-    // shard the Fock axis
-    std::vector<int64_t> cuts;
-    shard_bounds(p->lo_g, p->hi_g, M, ctx->nranks, cuts);
-    p->kb = cuts[ctx->rank];
-    p->ke = cuts[ctx->rank + 1];
-    p->Ml = p->ke - p->kb;
-    if (p->Ml < 1) return fail(ctx, QDT_ERR_INVALID_ARG, "rank %d owns no Fock rows (M too small)", ctx->rank);
-    p->lo_l.resize(D);
-    p->len_l.resize(D);
-    p->off.resize(D + 1);
-    p->off[0] = 0;
+    CKS(finish_probes(ctx, p.get(), nullptr));
+    *out = p.release();
+    return QDT_OK;
+}
+
+// Test hook: a banded F given directly.  lo[d], len[d] (global rows, len >= 1,
+// lo + len <= M, both edges nondecreasing in d like the Poisson bands of S0), vals probe-major
+// (band of probe d at off_d = sum_{e<d} len_e).  Values are copied (host pointers).
+extern "C" qdt_status qdt_probes_from_banded(qdt_ctx *ctx, int64_t D, int64_t M, const int64_t *lo,
+                                             const int64_t *len, const double *vals, qdt_probes **out)
+{
+    if (!ctx) return fail(nullptr, QDT_ERR_INVALID_ARG, "qdt_probes_from_banded: ctx is NULL");
+    if (!out || !lo || !len || !vals) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_probes_from_banded: NULL pointer");
+    *out = nullptr;
+    if (D < 1 || D > INT32_MAX) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_probes_from_banded: D = %lld", (long long)D);
+    if (M < 1 || M > INT32_MAX - 64)
+        return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_probes_from_banded: M = %lld out of range", (long long)M);
+    int64_t nnz = 0;
     for (int64_t d = 0; d < D; d++) {
-        int64_t a = std::max<int64_t>(p->lo_g[d], p->kb), b = std::min<int64_t>(p->hi_g[d], p->ke - 1);
-        p->lo_l[d] = (int32_t)a;
-        p->len_l[d] = b >= a ? (int32_t)(b - a + 1) : 0;
-        p->off[d + 1] = p->off[d] + p->len_l[d];
+        if (len[d] < 1 || lo[d] < 0 || lo[d] + len[d] > M)
+            return fail(ctx, QDT_ERR_INVALID_ARG, "band %lld = [%lld, +%lld) outside [0, M)", (long long)d,
+                        (long long)lo[d], (long long)len[d]);
+        if (d > 0 && (lo[d] < lo[d - 1] || lo[d] + len[d] < lo[d - 1] + len[d - 1]))
+            return fail(ctx, QDT_ERR_UNSORTED, "band edges not nondecreasing at d = %lld", (long long)d);
+        nnz += len[d];
     }
-    p->nnz = p->off[D];
-    {   // uncovered rows of this slice (reading R9)
-        std::vector<int32_t> diff(p->Ml + 1, 0);
-        for (int64_t d = 0; d < D; d++)
-            if (p->len_l[d]) {
-                diff[p->lo_l[d] - p->kb] += 1;
-                diff[p->lo_l[d] - p->kb + p->len_l[d]] -= 1;
-            }
-        int64_t c = 0, unc = 0;
-        for (int64_t k = 0; k < p->Ml; k++) {
-            c += diff[k];
-            unc += (c == 0);
-        }
-        p->uncovered = unc;
+    for (int64_t i = 0; i < nnz; i++)
+        if (!isfinite(vals[i])) return fail(ctx, QDT_ERR_NONFINITE, "vals[%lld] is not finite", (long long)i);
+    CK(cudaSetDevice(ctx->device));
+    std::unique_ptr<qdt_probes> p(new qdt_probes());
+    p->ctx = ctx;
+    p->D = D;
+    p->M = M;
+    p->lo_g.resize(D);
+    p->hi_g.resize(D);
+    for (int64_t d = 0; d < D; d++) {
+        p->lo_g[d] = (int32_t)lo[d];
+        p->hi_g[d] = (int32_t)(lo[d] + len[d] - 1);
     }
-    CK(cudaMemcpyAsync(p->d_lo, p->lo_l.data(), sizeof(int32_t) * D, cudaMemcpyHostToDevice, s));
-    CK(cudaMalloc(&p->d_len, sizeof(int32_t) * D));
-    CK(cudaMemcpyAsync(p->d_len, p->len_l.data(), sizeof(int32_t) * D, cudaMemcpyHostToDevice, s));
-    CK(cudaMalloc(&p->d_off, sizeof(int64_t) * (D + 1)));
-    CK(cudaMemcpyAsync(p->d_off, p->off.data(), sizeof(int64_t) * (D + 1), cudaMemcpyHostToDevice, s));
-    CK(cudaMalloc(&p->d_val, sizeof(double) * std::max<int64_t>(1, p->nnz)));
-    // S0 (b): values on the device
-    CK(run_k(ctx, "probe_values", 1, [&]() { return launch_probe_values(p->d_alpha2, D, p->band(), s); }));
-    // stored mass per probe (diagnostic; summed over ranks)
-    double *d_s = nullptr;
-    CKS(ws_get(ctx, "probe_s", D, &d_s));
-    CK(run_k(ctx, "probe_rowsum", 1, [&]() { return launch_probe_rowsum(D, p->band(), d_s, s); }));
-    CKS(allreduce(ctx, d_s, D, "allreduce_s"));
-    std::vector<double> hs(D);
-    CK(cudaMemcpyAsync(hs.data(), d_s, sizeof(double) * D, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    p->min_row_mass = *std::min_element(hs.begin(), hs.end());
+    CK(cudaMalloc(&p->d_lo, sizeof(int32_t) * D));
+    CKS(finish_probes(ctx, p.get(), vals));
     *out = p.release();
     return QDT_OK;
 }
@@ -1275,6 +1376,7 @@ static SweepArgs sweep_args(const IterCfg &c, SolveBufs &b, const double *R, con
 {
     SweepArgs a;
     a.N = c.N;
+    a.Nv = nvalid(c);
     a.Ml = (int)c.p->Ml;
     a.kb = c.p->kb;
     a.M = c.p->M;
@@ -1622,8 +1724,15 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     if (!(gamma >= 0.0) || !isfinite(gamma)) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: gamma must be finite and >= 0");
     if (!(tol >= 0.0)) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: tol must be >= 0");
     if (iters < 0) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: iters < 0");
-    qdt_solve_opts opt = {QDT_STEP_SQS, 0, nullptr, 16, 1, 0, 0, 1};
+    qdt_solve_opts opt;
+    memset(&opt, 0, sizeof opt);
+    opt.step = QDT_STEP_SQS;
+    opt.check_every = 16;
+    opt.kkt_every = 1;
+    opt.use_graph = 1;
     if (o) opt = *o;
+    if (opt.fista_t != 0.0 && !(opt.fista_t >= 1.0 && isfinite(opt.fista_t)))
+        return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: fista_t must be 0 or a finite value >= 1");
     if (opt.step != QDT_STEP_SQS && opt.step != QDT_STEP_LIPSCHITZ && opt.step != QDT_STEP_BB)
         return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: unknown step mode %d", opt.step);
     if (opt.step == QDT_STEP_BB && opt.accel)
@@ -1638,6 +1747,9 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
         if (opt.theta0)
             CKS(check_finite_host(ctx, opt.theta0, (ctx->nranks > 1 && !opt.gather_theta ? Ml : M) * Nu,
                                   "theta0"));
+        if (opt.theta_prev && opt.accel)
+            CKS(check_finite_host(ctx, opt.theta_prev, (ctx->nranks > 1 && !opt.gather_theta ? Ml : M) * Nu,
+                                  "theta_prev"));
     }
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
@@ -1703,16 +1815,21 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
         if (N != Nu) CK(cudaMemsetAsync(b.P, 0, sizeof(double) * D * N, s));
         CKS(copy_cols(ctx, b.P, N, P, Nu, Nu, D, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
     }
-    std::vector<double> betas;
+    std::vector<double> betas, taus;
     if (fista) {
+        // Beck-Teboulle momentum: tau_{k+1} = (1 + sqrt(1 + 4 tau_k^2)) / 2, beta_k = (tau_k - 1) / tau_{k+1},
+        // from tau_0 = 1 or the resume state opts.fista_t
         CKS(ws_get(ctx, "beta", tcap, &b.beta));
         betas.resize(tl);
-        double tau = 1.0;
+        taus.resize(tl + 1);
+        double tau = opt.fista_t >= 1.0 ? opt.fista_t : 1.0;
         for (int64_t k = 0; k < tl; k++) {
+            taus[k] = tau;
             double tn_ = (1.0 + sqrt(1.0 + 4.0 * tau * tau)) / 2.0;
             betas[k] = (tau - 1.0) / tn_;
             tau = tn_;
         }
+        taus[tl] = tau;
         CK(cudaMemcpyAsync(b.beta, betas.data(), sizeof(double) * tl, cudaMemcpyHostToDevice, s));
     }
     // Theta_0 = 1/N or theta0 (full M x N; local rows when nranks > 1 and
@@ -1730,7 +1847,17 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     c.Nv = (int)Nu;
     CKS(halo_exchange(ctx, c, b.theta[0]));
     if (pl->fz_on && !fista) CKS(fwd_reduce(ctx, c, b, b.theta[0], b.R[0], true));  // R_0
-    if (fista) CK(cudaMemcpyAsync(b.theta[2] - N, b.theta[0] - N, sizeof(double) * rowsz, cudaMemcpyDeviceToDevice, s));
+    if (fista && opt.theta_prev) {
+        // resume: Theta_{k-1} given (same layout as theta0); R_{k-1} = F Theta_{k-1} - P for the
+        // first extrapolated residual R(Y) = (1 + beta) R_k - beta R_{k-1}
+        const double *src = opt.theta_prev;
+        if (ctx->nranks == 1 || opt.gather_theta) src += p->kb * Nu;
+        CKS(copy_cols(ctx, b.theta[2], N, src, Nu, Nu, Ml, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
+        CKS(halo_exchange(ctx, c, b.theta[2]));
+        CKS(fwd_reduce(ctx, c, b, b.theta[2], b.R[1], true));
+    } else if (fista) {
+        CK(cudaMemcpyAsync(b.theta[2] - N, b.theta[0] - N, sizeof(double) * rowsz, cudaMemcpyDeviceToDevice, s));
+    }
     double tscalar = 0.0;
     CKS(step_setup(ctx, p, pl, bb ? QDT_STEP_LIPSCHITZ : opt.step, gamma, 100, b.tstep, nullptr, nullptr,
                    &tscalar));
@@ -1794,9 +1921,9 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
             ctx->glaunches = graph_launches;
         }
     }
-    cudaEvent_t ev0, ev1;
-    CK(cudaEventCreate(&ev0));
-    CK(cudaEventCreate(&ev1));
+    EventPair evp;
+    CK(evp.create());
+    cudaEvent_t ev0 = evp.a, ev1 = evp.b;
     CK(cudaEventRecord(ev0, s));
     const int64_t check = tol > 0.0 ? std::max<int64_t>(period, (opt.check_every / period) * period) : INT64_MAX;
     int64_t since = 0;
@@ -1826,7 +1953,7 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     CK(cudaMemcpyAsync(&hst, b.state, sizeof hst, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     stopped = hst.stop != 0;
-    if (stopped && hst.converged && !hst.nonfinite && pl->NB && !fista) {
+    if (stopped && hst.converged && !hst.nonfinite && (pl->NB || pl->NW) && !fista) {
         // the sweep loop evaluates the unclamped KKT only; re-evaluate Theta_kd once with the
         // general kernels so that trace/kkt/kkt_paper at kd come from one consistent pass
         DevState sr = hst;
@@ -1848,15 +1975,24 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     // ---- outputs
     const bool gather = ctx->nranks > 1 && opt.gather_theta;
     if (gather) {
-        // assemble the full M x N on every rank (allreduce of zero-padded slices)
+        // assemble the full M x N on every rank: each rank's slice broadcast into place
         double *full;
         CKS(ws_get(ctx, "gather", M * N, &full));
-        CK(cudaMemsetAsync(full, 0, sizeof(double) * M * N, s));
-        CK(cudaMemcpyAsync(full + p->kb * N, res, sizeof(double) * Ml * N, cudaMemcpyDeviceToDevice, s));
-        CKS(allreduce(ctx, full, (size_t)M * N, "gather"));
+        CKS(gather_rows(ctx, p, res, N, full));
         CKS(copy_cols(ctx, theta_out, Nu, full, N, Nu, M, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
     } else {
         CKS(copy_cols(ctx, theta_out, Nu, res, N, Nu, Ml, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
+    }
+    if (fista && opt.theta_prev_out) {   // resume state: Theta_{kd-1} (the initial Theta_{-1} when kd = 0)
+        const double *prv = b.theta[(kd + 2) % 3];
+        if (gather) {
+            double *full;
+            CKS(ws_get(ctx, "gather", M * N, &full));
+            CKS(gather_rows(ctx, p, prv, N, full));
+            CKS(copy_cols(ctx, opt.theta_prev_out, Nu, full, N, Nu, M, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
+        } else {
+            CKS(copy_cols(ctx, opt.theta_prev_out, Nu, prv, N, Nu, Ml, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
+        }
     }
     std::vector<double> hk(tl);
     if (trace_out) CK(cudaMemcpyAsync(trace_out, b.trace, sizeof(double) * tl, cudaMemcpyDeviceToHost, s));
@@ -1877,6 +2013,7 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
         CK(cudaStreamSynchronize(s));
         info->f_final = fl;
         info->step_scalar = tscalar;
+        info->fista_t = fista ? taus[kd] : 0.0;
         info->k_begin = p->kb;
         info->k_end = p->ke;
         info->nnz = p->nnz;
@@ -1886,8 +2023,6 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
         cudaEventElapsedTime(&lm, ev0, ev1);
         info->loop_ms = lm;
     }
-    cudaEventDestroy(ev0);
-    cudaEventDestroy(ev1);
     (void)stopped;
     return QDT_OK;
 }
@@ -2170,6 +2305,7 @@ extern "C" qdt_status qdt_solve_newton(qdt_ctx *ctx, const qdt_probes *F, const 
     }));
     double *hs = nullptr;
     CK(cudaMallocHost(&hs, sizeof(double) * 8));
+    std::unique_ptr<double, decltype(&cudaFreeHost)> hs_guard(hs, &cudaFreeHost);   // freed on every return
     auto fetch = [&](int k) -> double {
         cudaMemcpyAsync(hs, v.scal, sizeof(double) * k, cudaMemcpyDeviceToHost, s);
         cudaStreamSynchronize(s);
@@ -2242,9 +2378,9 @@ extern "C" qdt_status qdt_solve_newton(qdt_ctx *ctx, const qdt_probes *F, const 
     int stage = 1;
     int64_t k = 0, sw = -1, cg_total = 0;
     double f_last = NAN, kkt_last = NAN;
-    cudaEvent_t e0, e1;
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
+    EventPair ev;
+    CK(ev.create());
+    cudaEvent_t e0 = ev.a, e1 = ev.b;
     CK(cudaEventRecord(e0, s));
     for (k = 0;; k++) {
         CKS(grad(v.theta));
@@ -2257,13 +2393,13 @@ extern "C" qdt_status qdt_solve_newton(qdt_ctx *ctx, const qdt_probes *F, const 
         if (!isfinite(f)) return fail(ctx, QDT_ERR_NONFINITE, "newton: non-finite objective at %lld", (long long)k);
         if (r <= eps_kkt || k >= K) break;
         int64_t it = 0;
-        const int used = stage;
         double f0 = f;
+        double slope = 0.0;   // one-sided arc derivative at alpha = 0 of the stage that steps
         if (stage == 1) {
             CKS(direction(nullptr, v.theta, &it));
             CK(nt_tangent(v.theta, v.x, M, (int)N, v.d0, s));
             CK(nt_dot(v.g, v.d0, nullptr, nullptr, 0, n, v.part, v.scal, s));
-            const double slope = fetch(1);
+            slope = fetch(1);
             if (fabs(slope) <= o->switch_tol) {
                 stage = 2;
                 sw = k;
@@ -2274,9 +2410,12 @@ extern "C" qdt_status qdt_solve_newton(qdt_ctx *ctx, const qdt_probes *F, const 
             CK(nt_transform(v.theta, M, (int)N, v.m, s));
             CKS(grad(v.theta));
             CKS(direction(v.m, v.theta, &it));
+            // stage-2 arc slope: reduced gradient . p with p_j -> 0 where theta_j <= 0 and p_j < 0
+            CK(nt_dot(v.gr, v.x, nullptr, v.theta, 2, n, v.part, v.scal, s));
+            slope = fetch(1);
             f0 = fval(v.theta, b.R[0], nullptr, nullptr);
         }
-        (void)used;
+        const bool paper_armijo = o->armijo == 0;
         double alpha = 0.0;
         bool accepted = false;
         for (int64_t l = 0; l < o->max_ls && !accepted; l++) {
@@ -2291,6 +2430,18 @@ extern "C" qdt_status qdt_solve_newton(qdt_ctx *ctx, const qdt_probes *F, const 
                 CK(cudaMemcpyAsync(&hneg, v.neg, sizeof(int), cudaMemcpyDeviceToHost, s));
                 CK(cudaStreamSynchronize(s));
                 if (hneg) continue;
+            }
+            if (paper_armijo) {
+                // f(P[Theta + a p]) <= f(Theta) + c a slope; no descent certified
+                // (slope >= 0): no admissible step length
+                if (!(slope < 0.0)) break;
+                CKS(fwd_reduce(ctx, c, b, v.T1, v.Rd, true));
+                const double f1 = fval(v.T1, v.Rd, nullptr, nullptr);
+                if (f1 <= f0 + 0.1 * a * slope) {
+                    accepted = true;
+                    alpha = a;
+                }
+                continue;
             }
             CK(nt_dotdiff(us == 2 ? v.gr : v.g, v.T1, v.theta, us == 2 ? v.m : nullptr, (int)N, n, v.part,
                           v.scal, s));
@@ -2321,7 +2472,6 @@ extern "C" qdt_status qdt_solve_newton(qdt_ctx *ctx, const qdt_probes *F, const 
     CK(cudaMemcpyAsync(theta_out, v.theta, sizeof(double) * n,
                        dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    cudaFreeHost(hs);
     if (trace_out) memcpy(trace_out, tr.data(), sizeof(double) * (K + 1));
     if (kkt_out) memcpy(kkt_out, kt.data(), sizeof(double) * (K + 1));
     if (stage_out && K) memcpy(stage_out, stg.data(), sizeof(int32_t) * K);
@@ -2337,7 +2487,5 @@ extern "C" qdt_status qdt_solve_newton(qdt_ctx *ctx, const qdt_probes *F, const 
         cudaEventElapsedTime(&ms, e0, e1);
         info->loop_ms = ms;
     }
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
     return QDT_OK;
 }

@@ -108,6 +108,7 @@ struct FwUnit {                 // fwd unit: tiles [t0, t1), union window [u0, u
 };
 struct SweepArgs {
     int N, Ml;
+    int Nv;                     // outcomes (< N when the row pitch N carries a zero pad column; 0: N)
     int64_t kb, M;
     const SwUnit *units;
     const int64_t *fb_off;
@@ -249,6 +250,7 @@ cudaError_t launch_scale(double *v, const double *u, const double *nrm2, int64_t
 cudaError_t launch_fill(double *x, int64_t n, double v, cudaStream_t s);
 
 cudaError_t prepare_kernels();
+int device_sm_count();            // SM count of the current device (cached per ordinal)
 int fwd_threads(int N, int *CG, int *RG, int *TC);
 int bwd_threads(int N, int *CG, int *RG, int *TC);
 constexpr int TR = 4;  // rows (bwd) / probes (fwd) per thread

@@ -1062,16 +1062,32 @@ static cudaError_t prep_tc()
     if (e == cudaSuccess) e = prep_bwd<TC, 0>();
     return e;
 }
+int device_sm_count()
+{
+    static int cache[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cache[dev]) cudaDeviceGetAttribute(&cache[dev], cudaDevAttrMultiProcessorCount, dev);
+    return cache[dev] > 0 ? cache[dev] : 148;
+}
+
 cudaError_t prepare_kernels()
 {
-    static bool done = false;
-    if (done) return cudaSuccess;
+    // the shared-memory attribute is per device: prepare each device ordinal once
+    static uint64_t done_mask = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = dev < 64 ? (1ull << dev) : 0;
+    if (done_mask & bit) return cudaSuccess;
+    bool done = false;
     cudaError_t e = prep_tc<1>();
     if (e == cudaSuccess) e = prep_tc<2>();
     if (e == cudaSuccess) e = prep_tc<4>();
     if (e == cudaSuccess) e = prep_tc<5>();
     if (e == cudaSuccess) e = prep_tc<8>();
     done = e == cudaSuccess;
+    if (done) done_mask |= bit;
     return e;
 }
 

@@ -569,6 +569,7 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(con
     if (st && st->stop) return;
     const int64_t it = st ? st->it : 0;
     const int N = a.N;
+    const int Nv = a.Nv > 0 ? a.Nv : N;   // valid outcomes: a padded pitch's zero column is no coordinate
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g4 = lane >> 2, t4 = lane & 3;
     const int G = gridDim.x;
@@ -719,27 +720,27 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(con
                 if (warp == 0 && next < a.nunits && un.nsplit == 1) issue_theta(un);
             };
             if (stash)
-                row_pass<NB, true, true, false, false, NB, 0, false, true>(acc, thr, N, t4, act, has_prev, has_next,
+                row_pass<NB, true, true, false, false, NB, 0, false, true>(acc, thr, Nv, t4, act, has_prev, has_next,
                                                                          a.gamma, tk, do_kkt, ev, sreg, skkt,
                                                                          skktp, s, xm, xn, tpr, beta, nullptr,
                                                                          release, TPB);
             else if (fast)
-                row_pass<NB, true, true, false, FIS>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk,
+                row_pass<NB, true, true, false, FIS>(acc, thr, Nv, t4, act, has_prev, has_next, a.gamma, tk,
                                                      do_kkt, ev, sreg, skkt, skktp, s, xm, xn, tpr, beta, nullptr, NoMid(), TPB);
             else if (full)
-                row_pass<NB, true, false, false, FIS>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk,
+                row_pass<NB, true, false, false, FIS>(acc, thr, Nv, t4, act, has_prev, has_next, a.gamma, tk,
                                                       do_kkt, ev, sreg, skkt, skktp, s, xm, xn, tpr, beta, nullptr, NoMid(), TPB);
             else
-                row_pass<NB, false, false, false, FIS>(acc, thr, N, t4, act, has_prev, has_next, a.gamma, tk,
+                row_pass<NB, false, false, false, FIS>(acc, thr, Nv, t4, act, has_prev, has_next, a.gamma, tk,
                                                        do_kkt, ev, sreg, skkt, skktp, s, xm, xn, tpr, beta, nullptr, NoMid(), TPB);
             if (!stash) release();   // Theta tile consumed: start the next unit's tile load
             if (ev) {
             } else if (fast)
-                row_project<NB, true, true, false>(acc, thr, N, t4, act, s, xm, xn, orow);
+                row_project<NB, true, true, false>(acc, thr, Nv, t4, act, s, xm, xn, orow);
             else if (full)
-                row_project<NB, true, false, false>(acc, thr, N, t4, act, s, xm, xn, orow);
+                row_project<NB, true, false, false>(acc, thr, Nv, t4, act, s, xm, xn, orow);
             else
-                row_project<NB, false, false, false>(acc, thr, N, t4, act, s, xm, xn, orow);
+                row_project<NB, false, false, false>(acc, thr, Nv, t4, act, s, xm, xn, orow);
             // per-tile scalar partials (fixed order: lanes, then warps)
             sreg = wsum(sreg);
             skkt = wsum(skkt);
@@ -1983,8 +1984,13 @@ static cudaError_t prep_nb()
 
 cudaError_t prepare_sweep_kernels()
 {
-    static bool done = false;
-    if (done) return cudaSuccess;
+    // the shared-memory attribute is per device: prepare each device ordinal once
+    static uint64_t done_mask = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = dev < 64 ? (1ull << dev) : 0;
+    if (done_mask & bit) return cudaSuccess;
+    bool done = false;
     cudaError_t e = cudaSuccess;
 #define QDT_PREP(nb) if (e == cudaSuccess) e = prep_nb<nb>();
     QDT_FOR_NB(QDT_PREP)
@@ -1994,6 +2000,7 @@ cudaError_t prepare_sweep_kernels()
     QDT_PREP(17) QDT_PREP(18) QDT_PREP(19) QDT_PREP(20)
 #undef QDT_PREP
     done = e == cudaSuccess;
+    if (done) done_mask |= bit;
     return e;
 }
 
@@ -2060,8 +2067,7 @@ cudaError_t launch_bwd_mma(const SweepArgs &a_in, int nunits, int NB, cudaStream
     const bool fis = a.beta != nullptr && !a.eval;
     const bool tp = !fis && NB <= SW_NBMAX && tma_tile_on() && sweep_tensor_maps(a, NB);
     const size_t smem = sweep_bwd_smem(a.N, NB, fis, tp);
-    static int nsm = 0;
-    if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    const int nsm = device_sm_count();
     const int grid = std::min(nunits, (NB <= 13 && !fis ? 2 : 1) * nsm);
     switch (NB) {
 #define QDT_CASE(nb)                                                       \
@@ -2107,8 +2113,7 @@ cudaError_t launch_bwd_split(const SweepArgs &a_in, int nunits, int NB, cudaStre
     const bool fis = a.beta != nullptr && !a.eval;
     const bool tp = fis && NB <= SW_NBMAX && tma_tile_on() && sweep_tensor_maps(a, NB);   // FISTA steps
     const size_t smem = sweep_bwd_smem(a.N, NB, true, tp);   // two tiles: double buffer or Theta_{k-1}
-    static int nsm = 0;
-    if (!nsm) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    const int nsm = device_sm_count();
     const int grid = std::min(nunits, nsm);
     switch (NB) {
 #define QDT_CASE(nb)                                                       \

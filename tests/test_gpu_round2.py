@@ -1,0 +1,182 @@
+"""GPU parity, round 2 additions (-m gpu): the padded-pitch projection with unnormalised rows,
+the banded-F test hook, FISTA resume, the binding's argument checks, and full-size parity at
+the iteration counts of SURVEY 8(c) (slow; the oracle runs on all host cores, oracle-MT,
+bit-identical to one thread)."""
+import numpy as np
+import pytest
+
+import oracle
+import qdt_synth as qs
+
+pytestmark = pytest.mark.gpu
+EPS = 2.220446049250313e-16
+
+
+@pytest.fixture(scope="module")
+def q():
+    import paper_2404_02844_b200 as q
+    from paper_2404_02844_b200 import build
+    build.build()
+    oracle.set_threads(0)
+    return q
+
+
+@pytest.fixture(scope="module")
+def ctx(q):
+    return q.qdt_init(0)
+
+
+def _trace_ok(tg, to, P):
+    tg, to = np.asarray(tg), np.asarray(to)
+    floor = 4 * EPS * np.sqrt(np.sum(P ** 2)) * np.sqrt(np.abs(to))
+    return np.all(np.abs(tg - to) <= 1e-10 * np.abs(to) + floor + 1e-300)
+
+
+@pytest.mark.parametrize("N", [151, 137, 159])
+def test_odd_pitch_rows_off_the_simplex(q, ctx, N):
+    """at odd 128 < N <= 160 the plain step runs k_bwd_mma on the padded pitch N + 1;
+    the zero pad column is no simplex coordinate.  theta0 rows summing to 0.9 (and P rows to
+    0.95) make tau < 0, where a pad counted as a coordinate would take mass."""
+    rng = np.random.default_rng(N)
+    D, M = 80, 1200
+    a2 = np.geomspace(0.5, 0.9 * M, D)
+    P = 0.95 * rng.dirichlet(np.ones(N) * 0.3, D)
+    th0 = 0.9 * rng.dirichlet(np.ones(N), M)
+    Fo = oracle.Probes(a2, M)
+    Fg = q.qdt_build_probes(ctx, a2, M)
+    for iters in (1, 7):
+        ro = oracle.solve(Fo, P, 1e-3, 0.0, iters, theta0=th0)
+        rg = q.qdt_solve(ctx, Fg, P, 1e-3, 0.0, iters, theta0=th0)
+        assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9
+        assert np.abs(rg["theta"].sum(1) - 1.0).max() <= 8 * N * EPS
+        assert _trace_ok(rg["trace"], ro["trace"], P)
+
+
+def _random_banded(seed, D, M):
+    rng = np.random.default_rng(seed)
+    lo = np.sort(rng.integers(0, M - 40, D))
+    hi = np.sort(np.minimum(M - 1, lo + rng.integers(0, 60, D)))
+    hi = np.maximum(hi, lo)
+    hi = np.maximum.accumulate(hi)
+    ln = hi - lo + 1
+    val = rng.uniform(0.0, 0.3, int(ln.sum()))
+    return lo, ln, val
+
+
+@pytest.mark.parametrize("N,accel", [(6, 0), (100, 1), (300, 0)])
+def test_probes_from_banded_hook(q, ctx, N, accel):
+    """Arbitrary (non-Poisson) banded F through qdt_probes_from_banded: same tables, and the
+    solve matches the oracle run on the same bands."""
+    D, M = 150, 700
+    lo, ln, val = _random_banded(N, D, M)
+    Fo = oracle.Probes.from_banded(lo, ln, val, M)
+    Fg = q.qdt_probes_from_banded(ctx, lo, ln, val, M)
+    ex = q.qdt_probes_export(ctx, Fg)
+    np.testing.assert_array_equal(ex["lo"], lo)
+    np.testing.assert_array_equal(ex["len"], ln)
+    assert np.array_equal(ex["val"], val)
+    rng = np.random.default_rng(1)
+    P = rng.dirichlet(np.ones(N), D) * 0.5
+    ro = oracle.solve(Fo, P, 1e-3, 0.0, 25, accel=accel)
+    rg = q.qdt_solve(ctx, Fg, P, 1e-3, 0.0, 25, accel=accel)
+    assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9
+    assert _trace_ok(rg["trace"], ro["trace"], P)
+    # validation
+    with pytest.raises(q.QdtError, match="UNSORTED"):
+        q.qdt_probes_from_banded(ctx, lo[::-1].copy(), ln, val, M)
+    bad = ln.copy()
+    bad[3] = 0
+    with pytest.raises(q.QdtError, match="INVALID_ARG"):
+        q.qdt_probes_from_banded(ctx, lo, bad, val, M)
+
+
+@pytest.mark.parametrize("N", [10, 100, 200])
+def test_fista_resume(q, ctx, N):
+    """FISTA resume state: solve(K1) -> (Theta_K1, Theta_K1-1, tau_K1) ->
+    solve(K2) from it equals the uninterrupted solve(K1 + K2) bit for bit, and the oracle's
+    resumed sequence to 1e-9."""
+    rng = np.random.default_rng(N)
+    D, M = 120, 900
+    a2 = np.sort(rng.uniform(0, 0.8 * M, D))
+    P = rng.dirichlet(np.ones(N), D)
+    Fg = q.qdt_build_probes(ctx, a2, M)
+    Fo = oracle.Probes(a2, M)
+    full = q.qdt_solve(ctx, Fg, P, 1e-3, 0.0, 40, accel=True)
+    a = q.qdt_solve(ctx, Fg, P, 1e-3, 0.0, 17, accel=True, want_prev=True)
+    assert a["info"]["fista_t"] > 1.0
+    b = q.qdt_solve(ctx, Fg, P, 1e-3, 0.0, 23, accel=True, theta0=a["theta"], theta_prev=a["theta_prev"],
+                    fista_t=a["info"]["fista_t"])
+    assert np.array_equal(b["theta"], full["theta"])
+    ao = oracle.solve(Fo, P, 1e-3, 0.0, 17, accel=1)
+    assert ao["fista_t"] == a["info"]["fista_t"]
+    assert np.abs(a["theta_prev"] - ao["theta_prev"]).max() <= 1e-9
+    bo = oracle.solve(Fo, P, 1e-3, 0.0, 23, accel=1, theta0=ao["theta"], theta_prev=ao["theta_prev"],
+                      fista_t=ao["fista_t"])
+    assert np.abs(b["theta"] - bo["theta"]).max() <= 1e-9
+    assert _trace_ok(b["trace"], bo["trace"], P)
+
+
+def test_binding_checks_device_arguments(q, ctx):
+    import torch
+    I = qs.tiny()
+    F = q.qdt_build_probes(ctx, I.alpha2, I.M)
+    P = torch.tensor(I.P, device="cuda")
+    with pytest.raises(TypeError, match="float64"):
+        q.qdt_solve(ctx, F, P.float(), I.gamma, 0.0, 3)
+    with pytest.raises(ValueError, match="shape"):
+        q.qdt_solve(ctx, F, P, I.gamma, 0.0, 3, theta0=torch.zeros((I.M + 1, I.P.shape[1]), dtype=torch.float64,
+                                                                   device="cuda"))
+    with pytest.raises(ValueError, match="contiguous"):
+        q.qdt_objective(ctx, F, P, torch.full((I.P.shape[1], I.M), 0.1, dtype=torch.float64, device="cuda").t(),
+                        I.gamma)
+    # producer on torch's stream right before the call: the binding orders the library after it
+    P2 = (P * 1.0).contiguous()
+    r = q.qdt_solve(ctx, F, P2, I.gamma, 0.0, 5)
+    rh = q.qdt_solve(ctx, F, I.P, I.gamma, 0.0, 5)
+    assert np.array_equal(r["theta"].cpu().numpy(), rh["theta"])
+
+
+# ------------------------------------------------------------- SURVEY 8(c) iteration counts
+def _full(q, ctx, I, iters, accel=0, kkt_every=1, step=0):
+    Fo = oracle.Probes(I.alpha2, I.M)
+    Fg = q.qdt_build_probes(ctx, I.alpha2, I.M)
+    ro = oracle.solve(Fo, I.P, I.gamma, 0.0, iters, step=step, accel=accel, kkt_every=kkt_every)
+    rg = q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, iters, step=step, accel=bool(accel), kkt_every=kkt_every)
+    d = np.abs(rg["theta"] - ro["theta"]).max()
+    assert d <= 1e-9, d
+    assert _trace_ok(rg["trace"], ro["trace"], I.P)
+    m = np.isfinite(ro["kkt"])
+    np.testing.assert_allclose(rg["kkt"][m], ro["kkt"][m], rtol=1e-8, atol=1e-15)
+    Th = rg["theta"]
+    assert Th.min() >= 0 and np.abs(Th.sum(1) - 1).max() <= 4 * Th.shape[1] * EPS
+    if not accel:   # plain SQS majorises: monotone up to roundoff (P9)
+        tr = rg["trace"]
+        assert np.all(tr[1:] <= tr[:-1] * (1 + 1e-12))
+    return d
+
+
+@pytest.mark.slow
+def test_medium_2000_iterations(q, ctx):
+    _full(q, ctx, qs.medium(), 2000)
+
+
+@pytest.mark.slow
+def test_medium_lipschitz_2000_iterations(q, ctx):
+    _full(q, ctx, qs.medium(), 2000, step=1)
+
+
+@pytest.mark.slow
+def test_large_200_iterations(q, ctx):
+    _full(q, ctx, qs.large(), 200)
+
+
+@pytest.mark.slow
+def test_megascale_sqs_100_iterations(q, ctx):
+    _full(q, ctx, qs.megascale(), 100)
+
+
+@pytest.mark.slow
+def test_megascale_fista_60_iterations(q, ctx):
+    """SQS-FISTA, the mode of the time-to-tol ladder, with the KKT recorded every 5 iterations
+    (bench.py's time_to_tol setting)."""
+    _full(q, ctx, qs.megascale(), 60, accel=1, kkt_every=5)

@@ -150,3 +150,73 @@ def test_newton_reaches_the_projected_gradient_minimiser(seed, D, M, N, gamma):
 def test_row_argmax_first_on_ties():
     T = np.array([[0.2, 0.4, 0.4], [1.0, 0.0, 0.0], [0.3, 0.3, 0.4]])
     np.testing.assert_array_equal(oracle.row_argmax(T), [1, 0, 2])
+
+
+def _np_project_rows(X):
+    U = -np.sort(-X, axis=1)
+    css = np.cumsum(U, axis=1) - 1.0
+    j = np.arange(1, X.shape[1] + 1)
+    rho = (U - css / j > 0).sum(axis=1)
+    tau = css[np.arange(X.shape[0]), rho - 1] / rho
+    return np.maximum(X - tau[:, None], 0.0)
+
+
+def _np_f(A, P, T, gamma):
+    R = A @ T - P
+    return float(np.sum(R * R) + gamma * np.sum((T[:-1] - T[1:]) ** 2))
+
+
+@pytest.mark.parametrize("seed,D,M,N", [(10, 20, 40, 4), (12, 20, 40, 4), (10, 30, 24, 3)])
+def test_line_search_is_the_papers_armijo_rule(seed, D, M, N):
+    """armijo = 0: every accepted step length alpha_k = beta^m is the smallest m >= 0 with
+    f(P[Theta + beta^m p]) <= f(Theta) + c beta^m slope (beta = 3/4,
+    c = 1/10), slope the one-sided arc derivative at 0 (pinned by finite differences above);
+    the objective and the arcs are re-evaluated here in dense NumPy.  Stage 2 arcs are the
+    clamped transformed arcs of Alg. 1 (infeasible lengths are skipped)."""
+    F, P, g = _instance(seed, D, M, N, 1e-3)
+    A = F.dense()
+    K = 8
+    run = oracle.newton(F, P, g, K, armijo=0)
+    ks = len(run["alpha"])
+    assert ks >= 4
+    seen = set()
+    for k in range(ks):
+        Th = oracle.newton(F, P, g, k, armijo=0)["theta"]
+        Tn = oracle.newton(F, P, g, k + 1, armijo=0)["theta"]
+        st, al = int(run["stage"][k]), float(run["alpha"][k])
+        seen.add(st)
+        m_acc = int(round(np.log(al) / np.log(0.75)))
+        assert al == 0.75 ** m_acc
+        if st == 1:
+            p, slope, _ = oracle.newton_direction(F, P, g, Th)
+            arc = lambda a: _np_project_rows(Th + a * p)
+            T0 = Th
+        else:
+            m = oracle.row_argmax(Th)
+            T0 = Th.copy()
+            rows = np.arange(T0.shape[0])
+            T0[rows, m] = 0.0
+            T0[rows, m] = 1.0 - T0.sum(1)
+            p, slope, _ = oracle.newton_direction(F, P, g, T0, m=m)
+
+            def arc(a, T0=T0, p=p, m=m, rows=rows):
+                T = np.maximum(T0 + a * p, 0.0)
+                T[rows, m] = 0.0
+                T[rows, m] = 1.0 - T.sum(1)
+                return T if T[rows, m].min() >= 0.0 else None
+        f0 = _np_f(A, P, T0, g)
+        assert slope < 0.0
+        T1 = arc(al)
+        np.testing.assert_allclose(Tn, T1, rtol=0, atol=1e-13)
+        assert _np_f(A, P, T1, g) <= f0 + 0.1 * al * slope + 1e-13 * abs(f0)
+        for mm in range(m_acc):   # every shorter exponent (longer step) fails the test
+            a = 0.75 ** mm
+            Ta = arc(a)
+            if Ta is None:
+                continue
+            assert _np_f(A, P, Ta, g) > f0 + 0.1 * a * slope - 1e-13 * abs(f0)
+    # the secant form of R16 (armijo = 1) is a different rule: on the first two instances it
+    # accepts other lengths (so the checks above discriminate the two)
+    sec = oracle.newton(F, P, g, K, armijo=1)
+    if M == 40:
+        assert not np.array_equal(sec["alpha"][:ks], run["alpha"][:ks])

@@ -491,3 +491,85 @@ def test_bb_step_formula():
     th2 = oracle.project_rows(th1 - t * G1)
     np.testing.assert_allclose(oracle.solve(F, P, g, 0.0, 2, step=oracle.STEP_BB)["theta"], th2,
                                atol=1e-14)
+
+
+# ---------------------------------------------------------------------------- FISTA (P13 gap)
+def _np_project_rows(X):
+    """Sort-based Euclidean projection of every row onto the simplex, written here in NumPy."""
+    U = -np.sort(-X, axis=1)
+    css = np.cumsum(U, axis=1) - 1.0
+    j = np.arange(1, X.shape[1] + 1)
+    rho = (U - css / j > 0).sum(axis=1)
+    tau = css[np.arange(X.shape[0]), rho - 1] / rho
+    return np.maximum(X - tau[:, None], 0.0)
+
+
+def _np_L(T):
+    """(L Theta) of eq. regul with free ends (reading R8), dense NumPy."""
+    L = np.zeros_like(T)
+    L[1:] += T[1:] - T[:-1]
+    L[:-1] += T[:-1] - T[1:]
+    return L
+
+
+def test_fista_coefficients_beck_teboulle():
+    """Iterations 1-3 of the oracle's SQS-FISTA equal a dense NumPy run of the Beck-Teboulle
+    recurrence tau_{k+1} = (1 + sqrt(1 + 4 tau_k^2)) / 2, beta_k = (tau_k - 1) / tau_{k+1},
+    Y_k = Theta_k + beta_k (Theta_k - Theta_{k-1}) (SURVEY 8(c) algorithm step 4.1), with the
+    SQS step of reading R2; a plausible wrong recurrence beta_k = (tau_k - 1) / tau_k misses."""
+    rng = np.random.default_rng(11)
+    M, N, D, gamma = 30, 4, 25, 1e-3
+    a2 = np.sort(rng.uniform(0.0, 22.0, D))
+    F = oracle.Probes(a2, M)
+    A = F.dense()
+    P = rng.dirichlet(np.ones(N), D)
+    w = A.T @ (A @ np.ones(M)) + 4.0 * gamma
+    t = 1.0 / w
+
+    def run(beta_of, K):
+        th = np.full((M, N), 1.0 / N)
+        prev = th.copy()
+        tau = 1.0
+        out = []
+        for _ in range(K):
+            tn = (1.0 + np.sqrt(1.0 + 4.0 * tau * tau)) / 2.0
+            b = beta_of(tau, tn)
+            Y = th + b * (th - prev)
+            G = A.T @ (A @ Y - P) + gamma * _np_L(Y)
+            prev, th = th, _np_project_rows(Y - t[:, None] * G)
+            tau = tn
+            out.append(th)
+        return out
+
+    good = run(lambda tau, tn: (tau - 1.0) / tn, 3)
+    wrong = run(lambda tau, tn: (tau - 1.0) / tau, 3)
+    for k in (1, 2, 3):
+        ref = oracle.solve(F, P, gamma, 0.0, k, accel=1)
+        np.testing.assert_allclose(ref["theta"], good[k - 1], rtol=0, atol=1e-13)
+        if k >= 2:   # beta_0 = 0 either way; from k = 2 the sequences separate
+            assert np.abs(ref["theta"] - wrong[k - 1]).max() > 1e-6
+    # the returned resume state: tau_3 and Theta_2
+    r3 = oracle.solve(F, P, gamma, 0.0, 3, accel=1)
+    tau = 1.0
+    for _ in range(3):
+        tau = (1.0 + np.sqrt(1.0 + 4.0 * tau * tau)) / 2.0
+    assert r3["fista_t"] == tau
+    np.testing.assert_allclose(r3["theta_prev"], good[1], rtol=0, atol=1e-13)
+
+
+def test_fista_resume_continues_the_sequence():
+    """solve(K1) then solve(K2) from (Theta_K1, Theta_K1-1, tau_K1) is the uninterrupted
+    solve(K1 + K2) bit for bit (the resume state of SURVEY 8(b))."""
+    rng = np.random.default_rng(12)
+    M, N, D, gamma = 40, 5, 30, 1e-3
+    F = oracle.Probes(np.sort(rng.uniform(0.0, 30.0, D)), M)
+    P = rng.dirichlet(np.ones(N), D)
+    full = oracle.solve(F, P, gamma, 0.0, 9, accel=1)
+    a = oracle.solve(F, P, gamma, 0.0, 4, accel=1)
+    b = oracle.solve(F, P, gamma, 0.0, 5, accel=1, theta0=a["theta"], theta_prev=a["theta_prev"],
+                     fista_t=a["fista_t"])
+    assert np.array_equal(b["theta"], full["theta"])
+    assert np.array_equal(b["trace"], full["trace"][4:])
+    # a fresh restart from Theta_4 (momentum reset) is a different sequence
+    c = oracle.solve(F, P, gamma, 0.0, 5, accel=1, theta0=a["theta"])
+    assert np.abs(c["theta"] - full["theta"]).max() > 1e-9
