@@ -189,6 +189,40 @@ struct WideArgs {               // wide-N sweep (N > 128): k_grad_wide + k_proj_
     const double *beta;         // FISTA step: beta_k by state->it (nullptr: plain)
     const DevState *state;
 };
+// ---- fused wide-row step (qdt_wide.cu): N > 160, one cluster of C CTAs per 32-row tile
+constexpr int WT = 32;          // Fock rows per wide tile (half of a 64-row sweep tile)
+constexpr int WKC = 8;          // probes per staged chunk
+constexpr int WSTAGES = 4;      // chunk ring depth
+constexpr int WFP = 36;         // staged F row pitch (32 rows + 4: conflict-free A fragments)
+constexpr int W_NBW_MAX = 10;   // n-blocks per warp: <= 640 columns per CTA
+constexpr int W_THREADS = 512;
+constexpr int W_CMAX = 16;      // CTAs per cluster (non-portable above 8)
+struct WStepArgs {
+    int N, Nv, Ml;
+    int C, Wc;                  // CTAs per cluster, columns per CTA (multiple of 8)
+    int64_t kb, M;
+    const int32_t *trange;      // per cluster: tiles [trange[c], trange[c + 1])
+    const int64_t *fb_off;
+    const int32_t *tile_dA, *tile_dB;   // 64-row sweep tiles (tile tt uses sweep tile tt >> 1)
+    const double *Fb;
+    const double *R;
+    const double *theta;        // local row 0; rows -1 and Ml readable
+    const double *theta_prev;   // FISTA step: Theta_{k-1}
+    const double *beta;         // FISTA step: beta_k by state->it (nullptr: plain)
+    double *out;
+    const double *tstep;
+    const double *tscal;        // one device scalar step (nullptr: tstep per row)
+    double gamma;
+    double *part;               // [grid x NSC_TILE] scalar partials
+    int kkt_every;
+    int eval, eval_gate;
+    const DevState *state;
+};
+size_t wide_step_smem(int Wc);
+int wide_nbw(int Wc);
+int wide_max_clusters(int C, int Wc);
+cudaError_t prepare_wide_kernels();
+cudaError_t launch_wide_step(const WStepArgs &a, int nclusters, cudaStream_t s);
 cudaError_t launch_grad_wide(const WideArgs &a, int nunits, cudaStream_t s);
 cudaError_t launch_proj_wide(const WideArgs &a, cudaStream_t s);
 int wide_nb(int N);                                  // balanced column-chunk width / 8 (N > 128)

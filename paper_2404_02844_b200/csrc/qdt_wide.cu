@@ -1,0 +1,525 @@
+// qdt_wide.cu -- fused step kernel of the hot path for wide rows (N > 160 outcomes, up to
+// N = 10 240: BASELINE's Stress configuration has N = 10^4, 80 KB per Fock row).
+//
+// One thread-block cluster of C CTAs owns a 32-row Fock tile across ALL N columns: CTA r of the
+// cluster holds the column chunk [r Wc, (r + 1) Wc) (SURVEY 8(a) "Per-config kernel shape",
+// Stress: "a 16-CTA cluster ... each CTA owning a 625-column chunk; X stays on chip; tau by
+// cluster-wide Michelot reductions").  Per tile, in one kernel:
+//   S3  G = F_tile^T R_win          fp64 tensor cores (mma.sync m8n8k4 f64 -> SASS DMMA), operands
+//                                   staged by bulk copies (TMA engine) in a 4-stage mbarrier ring
+//   S4  G += gamma L Y              eq. regul, free ends (reading R8)
+//   S6  KKT / regulariser partials  PAPER.md:563-567 (reading R7)
+//   S5  X = Y - t o G, row-wise simplex projection (eq. Mp1_proj) by Michelot
+//       rounds whose per-row sums / counts are combined over the cluster through distributed
+//       shared memory (reading R4), Theta_{k+1} = max(X - tau, 0) stored from registers.
+// G and X never reach HBM: per element the kernel reads Theta_k once from DRAM (plus Theta_{k-1}
+// for FISTA) and writes Theta_{k+1} once; the R rows of the window come from L2.
+//
+// Layout of a CTA (512 threads, 16 warps): warp w = (mp, ng), mp = w & 1 owns the m-blocks
+// {2 mp, 2 mp + 1} (rows 16 mp .. 16 mp + 15 of the tile), ng = w >> 1 the n-blocks
+// [ng NBW, (ng + 1) NBW) of the chunk (8 columns each).  In the DMMA accumulator layout a 4-lane
+// quad (lane = 4 g + t) holds columns 8 nb + 2 t, 8 nb + 2 t + 1 of row g of an m-block, so a row's
+// values are spread over one quad in each of the 8 n-group warps and over the C CTAs: row
+// reductions go quad (shuffles) -> CTA (shared memory, fixed n-group order) -> cluster (DSMEM,
+// fixed CTA order).  Every CTA of the cluster combines the same partials in the same order, so
+// all of them take identical tau / stop decisions and the result is bitwise deterministic.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "qdt_internal.h"
+#include "qdt_ptx.cuh"
+
+namespace qdt {
+
+__device__ __forceinline__ void fence_proxy_async_smem()
+{
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+size_t wide_step_smem(int Wc)
+{
+    return (size_t)WSTAGES * WKC * ((Wc + 4) + WFP) * sizeof(double);
+}
+
+template <int NBW>
+__global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ WStepArgs a)
+{
+    extern __shared__ __align__(128) double sm[];
+    __shared__ __align__(8) uint64_t bars[WSTAGES];
+    __shared__ double rowp[WT][8][4];   // per row and n-group warp: quad-reduced partials
+    __shared__ double xb[2][WT][4];     // exchange slots (read by the cluster peers)
+    __shared__ double trow[WT][3];      // per row: tau, lambda (unclamped), lambda (clamped)
+    __shared__ int tcnt[WT];            // per row: |A| of the last Michelot round
+    __shared__ int tdone[WT];
+    __shared__ int s_alldone;
+    __shared__ double red[16][3];
+
+    const DevState *st = a.state;
+    if (st && st->stop) return;                    // cluster-uniform exits only
+    const int64_t it = st ? st->it : 0;
+    if (a.eval_gate && (it % a.kkt_every) != 0) return;
+    const bool ev = a.eval != 0;
+    const bool fis = a.beta != nullptr && !ev;     // FISTA step: Y = Theta_k + beta (Theta_k - Theta_{k-1})
+    const double beta = fis ? a.beta[it] : 0.0;
+    const bool do_kkt = ev || (!fis && (it % a.kkt_every) == 0);
+    const int N = a.N, Nv = a.Nv, C = a.C;
+    const int crank = C > 1 ? (int)cluster_ctarank() : 0;
+    const int cid = blockIdx.x / C;
+    const int cbase = crank * a.Wc;
+    const int ncol = min(a.Wc, N - cbase);         // even (N even), > 0 (planner)
+    const int Pr = a.Wc + 4;                       // staged R row pitch: = 4 mod 16 doubles
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    const int mp = warp & 1, ng = warp >> 1;
+    double *Rs = sm;                               // WSTAGES x WKC x Pr
+    double *Fs = sm + WSTAGES * WKC * Pr;          // WSTAGES x WKC x WFP
+    const int ta = a.trange[cid], tb = a.trange[cid + 1];
+
+    // zero the stages once: a masked tail k-step then multiplies stale but finite values by 0
+    for (int i = tid; i < WSTAGES * WKC * (Pr + WFP); i += W_THREADS) sm[i] = 0.0;
+    if (tid == 0) {
+        for (int s = 0; s < WSTAGES; s++) mbar_init(&bars[s], 1);
+        fence_barrier_init();
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+
+    // ---- producer (warp 0): the chunk stream of the cluster's tile range, WSTAGES ahead
+    int pt = ta, pc = 0;                           // next chunk to issue: tile, chunk
+    uint32_t issued = 0, used = 0;
+    auto nchunks = [&](int tt) {
+        const int t64 = tt >> 1;
+        return (a.tile_dB[t64] - a.tile_dA[t64] + WKC - 1) / WKC;
+    };
+    auto issue_next = [&]() {                      // warp 0, all lanes
+        while (pt < tb && pc >= nchunks(pt)) {
+            pt++;
+            pc = 0;
+        }
+        if (pt >= tb) return;
+        const int t64 = pt >> 1, half = pt & 1;
+        const int dA = a.tile_dA[t64], W = a.tile_dB[t64] - dA;
+        const int p0 = pc * WKC, kc = min(WKC, W - p0);
+        const int stg = issued % WSTAGES;
+        uint64_t *bar = &bars[stg];
+        if (lane == 0) mbar_expect_tx(bar, (uint32_t)kc * (WFP + ncol) * 8u);
+        __syncwarp();
+        if (lane < kc) {
+            bulk_g2s(Fs + (stg * WKC + lane) * WFP, a.Fb + a.fb_off[t64] + (int64_t)(p0 + lane) * STP + half * WT,
+                     WFP * 8u, bar);
+            bulk_g2s(Rs + (stg * WKC + lane) * Pr, a.R + (int64_t)(dA + p0 + lane) * N + cbase, (uint32_t)ncol * 8u,
+                     bar);
+        }
+        issued++;
+        pc++;
+    };
+    if (warp == 0)
+        for (int s = 0; s < WSTAGES; s++) issue_next();
+
+    double sreg = 0.0, skkt = 0.0, skktp = 0.0;    // per-thread running partials (fixed order)
+    int slot = 0;
+    const double *Fw = Fs + t * WFP + 16 * mp + g;            // A fragment: F[4 ks + t][8 mb + g]
+    const double *Rw = Rs + t * Pr + 8 * ng * NBW + g;        // B fragment: R[4 ks + t][8 nb + g]
+
+    // cluster-wide combination of the 32 rows' partials in xb[slot]: fixed CTA order
+    auto exchange = [&]() {
+        if (C > 1)
+            cluster_sync_all();
+        else
+            __syncthreads();
+    };
+
+    for (int tt = ta; tt < tb; tt++) {
+        const int t64 = tt >> 1;
+        const int k0 = tt * WT;                    // local first row of the tile
+        const int Tt = min(WT, a.Ml - k0);
+        const int W = a.tile_dB[t64] - a.tile_dA[t64];
+        const int nch = (W + WKC - 1) / WKC;
+        if (warp == 1) {                           // Theta rows of the epilogue -> L2 while the GEMM runs
+            for (int r = lane; r < Tt + 2; r += 32) {
+                bulk_prefetch_l2(a.theta + (int64_t)(k0 - 1 + r) * N + cbase, (uint32_t)ncol * 8u);
+                if (fis) bulk_prefetch_l2(a.theta_prev + (int64_t)(k0 - 1 + r) * N + cbase, (uint32_t)ncol * 8u);
+            }
+        }
+        double acc[2][NBW][2];
+#pragma unroll
+        for (int i = 0; i < 2; i++)
+#pragma unroll
+            for (int j = 0; j < NBW; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+        // ---- S3: G = F_tile^T R_win
+        for (int c = 0; c < nch; c++) {
+            const int stg = used % WSTAGES;
+            mbar_wait(&bars[stg], (used / WSTAGES) & 1);
+            used++;
+            const int kc = min(WKC, W - c * WKC);
+            const double *Fc = Fw + stg * WKC * WFP;
+            const double *Rc = Rw + stg * WKC * Pr;
+#pragma unroll
+            for (int ks = 0; ks < WKC / 4; ks++) {
+                if (4 * ks < kc) {
+                    const bool ok = 4 * ks + t < kc;
+                    const double a0 = ok ? Fc[4 * ks * WFP] : 0.0;
+                    const double a1 = ok ? Fc[4 * ks * WFP + 8] : 0.0;
+#pragma unroll
+                    for (int j = 0; j < NBW; j++) {
+                        const double b = Rc[4 * ks * Pr + 8 * j];
+                        dmma(acc[0][j][0], acc[0][j][1], a0, b);
+                        dmma(acc[1][j][0], acc[1][j][1], a1, b);
+                    }
+                }
+            }
+            __syncthreads();                       // stage consumed
+            if (warp == 0) issue_next();
+        }
+
+        // ---- S4 + pass 1: G = acc + gamma L Y; row min of G, sum / max / min of X = Y - t G
+        double tk[2];
+        double pmn[2], ps[2], pxm[2], pxn[2];
+#pragma unroll
+        for (int i = 0; i < 2; i++) {
+            const int rl = 16 * mp + 8 * i + g;
+            const int kl = k0 + rl;
+            const bool act = rl < Tt;
+            const int64_t kg = a.kb + kl;
+            const bool hp = kg > 0, hn = kg + 1 < a.M;
+            tk[i] = act ? (a.tscal ? *a.tscal : __ldg(a.tstep + kl)) : 0.0;
+            double mn = INFINITY, s = 0.0, xm = -INFINITY, xn = INFINITY;
+            if (act) {
+                const double *th = a.theta + (int64_t)kl * N + cbase;
+                const double *tq = fis ? a.theta_prev + (int64_t)kl * N + cbase : nullptr;
+#pragma unroll
+                for (int j = 0; j < NBW; j++) {
+                    const int lc = 8 * (ng * NBW + j) + 2 * t;
+                    if (lc < ncol) {
+                        const double2 x = __ldg(reinterpret_cast<const double2 *>(th + lc));
+                        const double2 y = hp ? __ldg(reinterpret_cast<const double2 *>(th + lc - N)) : x;
+                        const double2 z = hn ? __ldg(reinterpret_cast<const double2 *>(th + lc + N)) : x;
+                        double y0[2] = {x.x, x.y}, yp[2] = {y.x, y.y}, yn[2] = {z.x, z.y};
+                        const double d20 = x.x - z.x, d21 = x.y - z.y;   // regulariser pair of Theta_k
+                        const bool v0 = cbase + lc < Nv, v1 = cbase + lc + 1 < Nv;
+                        if (v0) sreg = fma(d20, d20, sreg);
+                        if (v1) sreg = fma(d21, d21, sreg);
+                        if (fis) {
+                            const double2 xq = __ldg(reinterpret_cast<const double2 *>(tq + lc));
+                            const double2 yq = hp ? __ldg(reinterpret_cast<const double2 *>(tq + lc - N)) : xq;
+                            const double2 zq = hn ? __ldg(reinterpret_cast<const double2 *>(tq + lc + N)) : xq;
+                            y0[0] = fma(beta, x.x - xq.x, x.x), y0[1] = fma(beta, x.y - xq.y, x.y);
+                            yp[0] = hp ? fma(beta, y.x - yq.x, y.x) : y0[0];
+                            yp[1] = hp ? fma(beta, y.y - yq.y, y.y) : y0[1];
+                            yn[0] = hn ? fma(beta, z.x - zq.x, z.x) : y0[0];
+                            yn[1] = hn ? fma(beta, z.y - zq.y, z.y) : y0[1];
+                        }
+#pragma unroll
+                        for (int e = 0; e < 2; e++) {
+                            const double gv = fma(a.gamma, (y0[e] - yp[e]) + (y0[e] - yn[e]), acc[i][j][e]);
+                            acc[i][j][e] = gv;
+                            if (e ? v1 : v0) {
+                                mn = fmin(mn, gv);
+                                const double xv = fma(-tk[i], gv, y0[e]);
+                                s += xv;
+                                xm = fmax(xm, xv);
+                                xn = fmin(xn, xv);
+                            }
+                        }
+                    }
+                }
+            }
+            pmn[i] = quad_min(mn);
+            ps[i] = quad_sum(s);
+            pxm[i] = quad_max(xm);
+            pxn[i] = quad_min(xn);
+        }
+        if (t == 0) {
+#pragma unroll
+            for (int i = 0; i < 2; i++) {
+                double *rp = rowp[16 * mp + 8 * i + g][ng];
+                rp[0] = pmn[i], rp[1] = ps[i], rp[2] = pxm[i], rp[3] = pxn[i];
+            }
+        }
+        __syncthreads();
+        if (tid < WT) {                            // CTA partial of row tid (n-group order)
+            double mn = INFINITY, s = 0.0, xm = -INFINITY, xn = INFINITY;
+            for (int w = 0; w < 8; w++) {
+                mn = fmin(mn, rowp[tid][w][0]);
+                s += rowp[tid][w][1];
+                xm = fmax(xm, rowp[tid][w][2]);
+                xn = fmin(xn, rowp[tid][w][3]);
+            }
+            xb[slot][tid][0] = mn, xb[slot][tid][1] = s, xb[slot][tid][2] = xm, xb[slot][tid][3] = xn;
+        }
+        exchange();
+        if (tid < WT) {                            // cluster totals (CTA order) -> lambda, tau_0
+            double mn = INFINITY, s = 0.0, xm = -INFINITY, xn = INFINITY;
+            for (int r = 0; r < C; r++) {
+                const double *x4 = xb[slot][tid];
+                const double v0 = C > 1 ? ld_dsmem(x4 + 0, r) : x4[0];
+                const double v1 = C > 1 ? ld_dsmem(x4 + 1, r) : x4[1];
+                const double v2 = C > 1 ? ld_dsmem(x4 + 2, r) : x4[2];
+                const double v3 = C > 1 ? ld_dsmem(x4 + 3, r) : x4[3];
+                mn = fmin(mn, v0);
+                s += v1;
+                xm = fmax(xm, v2);
+                xn = fmin(xn, v3);
+            }
+            const double lam = -2.0 * mn;
+            trow[tid][1] = lam;
+            trow[tid][2] = fmax(lam, 0.0);
+            // tau_0 = (sum X - 1) / N is exact when every entry stays active; otherwise Michelot
+            // from the lower bound max(tau_0, max X - 1) (reading R4)
+            double tau = (s - 1.0) / (double)Nv;
+            bool done = tid >= Tt || xn > tau;
+            if (!done) tau = fmax(tau, xm - 1.0);
+            trow[tid][0] = tau;
+            tdone[tid] = done ? 1 : 0;
+            tcnt[tid] = Nv + 1;
+            const unsigned all = __ballot_sync(0xffffffffu, done);
+            if (tid == 0) s_alldone = (all == 0xffffffffu);
+        }
+        __syncthreads();
+        slot ^= 1;
+
+        // ---- pass 2: KKT terms with lambda; X = Y - t G in the accumulators
+#pragma unroll
+        for (int i = 0; i < 2; i++) {
+            const int rl = 16 * mp + 8 * i + g;
+            const int kl = k0 + rl;
+            const bool act = rl < Tt;
+            const double lam = trow[rl][1], lamp = trow[rl][2];
+            const double *th = a.theta + (int64_t)kl * N + cbase;
+            const double *tq = fis ? a.theta_prev + (int64_t)kl * N + cbase : nullptr;
+#pragma unroll
+            for (int j = 0; j < NBW; j++) {
+                const int lc = 8 * (ng * NBW + j) + 2 * t;
+                const bool in = act && lc < ncol;
+                double2 x = make_double2(0.0, 0.0);
+                if (in) x = __ldg(reinterpret_cast<const double2 *>(th + lc));
+                double y0[2] = {x.x, x.y};
+                if (fis && in) {
+                    const double2 xq = __ldg(reinterpret_cast<const double2 *>(tq + lc));
+                    y0[0] = fma(beta, x.x - xq.x, x.x), y0[1] = fma(beta, x.y - xq.y, x.y);
+                }
+                const double th2[2] = {x.x, x.y};
+#pragma unroll
+                for (int e = 0; e < 2; e++) {
+                    const bool v = in && cbase + lc + e < Nv;
+                    const double gv = acc[i][j][e];
+                    if (do_kkt && v) {
+                        const double k1 = th2[e] * fma(2.0, gv, lam);
+                        skkt = fma(k1, k1, skkt);
+                        if (ev) {
+                            const double k2 = th2[e] * fma(2.0, gv, lamp);
+                            skktp = fma(k2, k2, skktp);
+                        }
+                    }
+                    acc[i][j][e] = v ? fma(-tk[i], gv, y0[e]) : -INFINITY;
+                }
+            }
+        }
+        if (ev) continue;                          // evaluation pass: no step
+
+        // ---- S5: Michelot rounds, all rows of the tile in lockstep over the cluster
+        while (!s_alldone) {
+            double rps[2], rpc[2], rmA[2];
+#pragma unroll
+            for (int i = 0; i < 2; i++) {
+                const int rl = 16 * mp + 8 * i + g;
+                const double tau = trow[rl][0];
+                double sA = 0.0, mA = INFINITY;
+                int cA = 0;
+                if (!tdone[rl]) {
+#pragma unroll
+                    for (int j = 0; j < NBW; j++)
+#pragma unroll
+                        for (int e = 0; e < 2; e++) {
+                            const double x = acc[i][j][e];
+                            if (x > tau) {
+                                sA += x;
+                                cA++;
+                                mA = fmin(mA, x);
+                            }
+                        }
+                }
+                rps[i] = quad_sum(sA);
+                rpc[i] = (double)quad_sum_i(cA);
+                rmA[i] = quad_min(mA);
+            }
+            if (t == 0) {
+#pragma unroll
+                for (int i = 0; i < 2; i++) {
+                    double *rp = rowp[16 * mp + 8 * i + g][ng];
+                    rp[0] = rps[i], rp[1] = rpc[i], rp[2] = rmA[i];
+                }
+            }
+            __syncthreads();
+            if (tid < WT) {
+                double s = 0.0, cnt = 0.0, mA = INFINITY;
+                for (int w = 0; w < 8; w++) {
+                    s += rowp[tid][w][0];
+                    cnt += rowp[tid][w][1];
+                    mA = fmin(mA, rowp[tid][w][2]);
+                }
+                xb[slot][tid][0] = s, xb[slot][tid][1] = cnt, xb[slot][tid][2] = mA;
+            }
+            exchange();
+            if (tid < WT) {
+                double s = 0.0, cntd = 0.0, mA = INFINITY;
+                for (int r = 0; r < C; r++) {
+                    const double *x4 = xb[slot][tid];
+                    s += C > 1 ? ld_dsmem(x4 + 0, r) : x4[0];
+                    cntd += C > 1 ? ld_dsmem(x4 + 1, r) : x4[1];
+                    mA = fmin(mA, C > 1 ? ld_dsmem(x4 + 2, r) : x4[2]);
+                }
+                bool done = tdone[tid] != 0;
+                if (!done) {
+                    const int cnt = (int)cntd;
+                    if (cnt >= tcnt[tid]) {
+                        done = true;
+                    } else {
+                        tcnt[tid] = cnt;
+                        const double tau = (s - 1.0) / (double)cnt;
+                        trow[tid][0] = tau;
+                        done = mA > tau;
+                    }
+                }
+                tdone[tid] = done ? 1 : 0;
+                const unsigned all = __ballot_sync(0xffffffffu, done);
+                if (tid == 0) s_alldone = (all == 0xffffffffu);
+            }
+            __syncthreads();
+            slot ^= 1;
+        }
+        // ---- Theta_{k+1} = max(X - tau, 0), stored from registers
+#pragma unroll
+        for (int i = 0; i < 2; i++) {
+            const int rl = 16 * mp + 8 * i + g;
+            if (rl >= Tt) continue;
+            const double tau = trow[rl][0];
+            double *o = a.out + (int64_t)(k0 + rl) * N + cbase;
+#pragma unroll
+            for (int j = 0; j < NBW; j++) {
+                const int lc = 8 * (ng * NBW + j) + 2 * t;
+                if (lc < ncol) {
+                    const double o0 = acc[i][j][0] - tau, o1 = acc[i][j][1] - tau;
+                    *reinterpret_cast<double2 *>(o + lc) = make_double2(o0 > 0.0 ? o0 : 0.0, o1 > 0.0 ? o1 : 0.0);
+                }
+            }
+        }
+    }
+    // ---- per-CTA scalar partials (fixed order: lanes, then warps)
+    sreg = wsum(sreg);
+    skkt = wsum(skkt);
+    skktp = wsum(skktp);
+    if (lane == 0) {
+        red[warp][0] = skkt;
+        red[warp][1] = skktp;
+        red[warp][2] = sreg;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+        for (int w = 0; w < 16; w++) {
+            v0 += red[w][0];
+            v1 += red[w][1];
+            v2 += red[w][2];
+        }
+        double *p = a.part + (int64_t)blockIdx.x * NSC_TILE;
+        if (do_kkt) {
+            p[SC_KKT] = v0;
+            p[SC_KKTP] = v1;
+        }
+        p[SC_REG] = v2;
+        p[SC_DTH] = 0.0;
+    }
+    if (C > 1) cluster_sync_all();                 // no CTA leaves while a peer may read its slots
+}
+
+// ---- host side
+template <int NBW>
+static cudaError_t launch_nbw(const WStepArgs &a, int grid, size_t smem, cudaStream_t s)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(W_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = a.C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_wstep<NBW>, a);
+}
+
+#define QDT_FOR_NBW(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10)
+
+int wide_nbw(int Wc) { return (Wc / 8 + 7) / 8; }
+
+cudaError_t prepare_wide_kernels()
+{
+    static uint64_t done_mask = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = dev < 64 ? (1ull << dev) : 0;
+    if (done_mask & bit) return cudaSuccess;
+    cudaError_t e = cudaSuccess;
+    const int smax = (int)wide_step_smem(8 * 8 * W_NBW_MAX);
+#define QDT_PREP(n)                                                                                         \
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_wstep<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax); \
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_wstep<n>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    QDT_FOR_NBW(QDT_PREP)
+#undef QDT_PREP
+    if (e == cudaSuccess) done_mask |= bit;
+    return e;
+}
+
+// Clusters of C CTAs that can be co-resident (0 on error)
+int wide_max_clusters(int C, int Wc)
+{
+    const int nbw = wide_nbw(Wc);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(C * 256);
+    cfg.blockDim = dim3(W_THREADS);
+    cfg.dynamicSmemBytes = wide_step_smem(Wc);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    cudaError_t e = cudaErrorInvalidValue;
+    switch (nbw) {
+#define QDT_CASE(k) \
+    case k: e = cudaOccupancyMaxActiveClusters(&n, k_wstep<k>, &cfg); break;
+        QDT_FOR_NBW(QDT_CASE)
+#undef QDT_CASE
+        default: break;
+    }
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+cudaError_t launch_wide_step(const WStepArgs &a, int nclusters, cudaStream_t s)
+{
+    if (nclusters <= 0) return cudaSuccess;
+    const int grid = nclusters * a.C;
+    const size_t smem = wide_step_smem(a.Wc);
+    switch (wide_nbw(a.Wc)) {
+#define QDT_CASE(k) \
+    case k: return launch_nbw<k>(a, grid, smem, s);
+        QDT_FOR_NBW(QDT_CASE)
+#undef QDT_CASE
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace qdt
