@@ -16,9 +16,15 @@ CUDA-event time of K iterations bracketed by barrier + synchronize, max over ran
 GPUs the Fock axis is sharded (NCCL allreduce of the D x N residual, halo rows): strong
 scaling of one reconstruction.
 
---impl reference runs the CPU oracle (oracle/, plain fp64 C, one thread) on the same
-workload; each step is one oracle iteration on a bounded sample of the Fock rows (S evenly
-spaced row slabs), sized so that the run ends within a few minutes.
+--impl reference runs the CPU oracle (oracle/, plain fp64 C, OpenMP on all host cores with a
+thread-count-independent deterministic split) on the same workload; each step is one oracle
+iteration on a bounded sample of the Fock rows (S evenly spaced row slabs), sized so that the
+run ends within a few minutes.
+
+Roofline: each kernel's algorithmic bytes B and flops F give t_hbm = B / HBM peak
+(MEASURED_PEAKS.json) and t_fp64 = F / fp64 tensor-core peak (profiles/fp64_peak.json, the DMMA
+microbenchmark); the bound is the larger one ("hbm" in GB/s or "tensor" in TFLOP/s), frac its
+achieved rate over the peak.  Megascale is HBM-bound, Large / Stress / Medium fp64-bound.
 """
 import argparse
 import json
@@ -29,7 +35,7 @@ import sys
 import threading
 import time
 
-CONFIG_NAMES = ["tiny", "medium", "large", "megascale", "stress_cut", "paper_tmd"]   # qdt_synth.CONFIGS
+CONFIG_NAMES = ["tiny", "medium", "large", "megascale", "stress", "stress_cut", "paper_tmd"]   # qdt_synth.CONFIGS
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -50,6 +56,31 @@ def peaks():
         return float(p["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def fp64_peak():
+    """fp64 tensor-core (DMMA) peak, TFLOP/s: our own microbenchmark (MEASURED_PEAKS.json has no
+    fp64 entry); fallback the datasheet figure."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
+            return float(json.load(f)["dmma_tflops"]), "measured (profiles/fp64_peak.json, DMMA microbenchmark)"
+    except Exception:
+        return 37.0, "fallback (datasheet fp64 tensor core)"
+
+
+def roofline_of(bytes_, flops, ms, hbm, fp64):
+    """Roofline of one kernel / the iteration: the binding resource is the one whose ideal time
+    is larger; frac = achieved rate of that resource / its peak."""
+    t_h = bytes_ / (hbm * 1e9)
+    t_f = flops / (fp64 * 1e12)
+    s = ms / 1e3
+    if t_f > t_h:
+        return {"bound": "tensor", "unit": "TFLOP/s", "achieved": flops / s / 1e12, "peak": fp64,
+                "frac": flops / s / 1e12 / fp64, "alg_flops": flops, "alg_bytes": bytes_,
+                "hbm_frac": bytes_ / s / 1e9 / hbm}
+    return {"bound": "hbm", "unit": "GB/s", "achieved": bytes_ / s / 1e9, "peak": hbm,
+            "frac": bytes_ / s / 1e9 / hbm, "alg_bytes": bytes_, "alg_flops": flops,
+            "tensor_frac": flops / s / 1e12 / fp64}
 
 
 class ClockSampler:
@@ -100,6 +131,13 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def algorithmic_flops(M, N, D, nnz):
+    """Per-kernel algorithmic fp64 flops per launch (SURVEY 8d F_alg: 2 flops per F entry and
+    column in each contraction, 12 per element for stencil, step and projection)."""
+    return {"bwd_step": 2.0 * nnz * N + 12.0 * M * N, "fwd_partial": 2.0 * nnz * N,
+            "reduce_R": 2.0 * D * N, "iteration": 4.0 * nnz * N + 12.0 * M * N}
+
+
 def algorithmic_bytes(M, N, D, nnz):
     """Per-kernel algorithmic bytes per launch."""
     return {
@@ -144,11 +182,13 @@ def run_qdt(args):
     nnz_local = ex["nnz"]
     Pd = torch.tensor(I.P, device="cuda")
     rows_local = ex["k_end"] - ex["k_begin"]
-    th_out = torch.empty((rows_local, N), dtype=torch.float64, device="cuda")
+    big = 8.0 * rows_local * N > 20e9   # Stress: the library's two Theta buffers fill HBM; the
+    # device-timed solves then copy no result out (theta_out = None), the e2e leg copies it to host
+    th_out = None if big else torch.empty((rows_local, N), dtype=torch.float64, device="cuda")
 
     def solve(iters, **kw):
         kw.setdefault("kkt_every", args.kkt_every)
-        return q.qdt_solve(ctx, F, Pd, I.gamma, 0.0, iters, theta_out=th_out, **kw)
+        return q.qdt_solve(ctx, F, Pd, I.gamma, 0.0, iters, theta_out=th_out, no_theta=big, **kw)
 
     # warm-up (untimed): plans, graphs, workspace; repeated right before the timed region.  At
     # least 16 iterations, the loop-graph period, so the graph the timed call replays is
@@ -193,16 +233,18 @@ def run_qdt(args):
             kern[name] = {"count": c, "avg_ms": t / c}
     q.qdt_profile_enable(ctx, False)
     if "proj_step" in kern and "bwd_step" in kern:
-        # wide N (> 128): the step is two kernels (gradient, projection); its roofline is theirs
+        # QDT_WIDE=old A/B: the step is two kernels (gradient, projection); its roofline is theirs
         kern["bwd_step"]["grad_ms"] = kern["bwd_step"]["avg_ms"]
         kern["bwd_step"]["avg_ms"] += kern["proj_step"]["avg_ms"]
         kern["bwd_step"]["note"] = "k_grad_wide + k_proj_wide"
-    # dominant kernel roofline (HBM bound; achieved = algorithmic bytes / avg launch time)
+    # dominant kernel roofline (achieved = algorithmic bytes or flops / avg launch time)
     hbm, src = peaks()
+    f64, f64src = fp64_peak()
     ab = algorithmic_bytes(rows_local, N, D, nnz_local)
+    af = algorithmic_flops(rows_local, N, D, nnz_local)
     dom = max(("bwd_step", "fwd_partial"), key=lambda k: kern.get(k, {}).get("avg_ms", 0))
     dom_ms = kern[dom]["avg_ms"] if dom in kern else float("nan")
-    achieved = ab[dom] / (dom_ms / 1e3) / 1e9
+    roof = roofline_of(ab[dom], af[dom], dom_ms, hbm, f64)
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
@@ -212,7 +254,9 @@ def run_qdt(args):
         pass
     for k in kern:
         if k in ab:
-            kern[k]["achieved_gbs"] = ab[k] / (kern[k]["avg_ms"] / 1e3) / 1e9
+            r = roofline_of(ab[k], af[k], kern[k]["avg_ms"], hbm, f64)
+            kern[k].update({"bound": r["bound"], "frac": r["frac"], "achieved_gbs": ab[k] / (kern[k]["avg_ms"] / 1e3) / 1e9,
+                            "achieved_tflops": af[k] / (kern[k]["avg_ms"] / 1e3) / 1e12})
 
     # ---- end to end through the public API with HOST buffers (pinned), per solve call
     e2e = None
@@ -221,7 +265,7 @@ def run_qdt(args):
         a_host = torch.tensor(I.alpha2).pin_memory()
         th_host = torch.empty((rows_local, N), dtype=torch.float64).pin_memory()
         samples = []
-        for _ in range(3):   # three calls, each with a fresh probe handle; the median is reported
+        for _ in range(1 if big else 3):   # calls with a fresh probe handle each; the median is reported
             barrier()
             t0 = time.perf_counter()
             e0.record(stream)
@@ -245,7 +289,7 @@ def run_qdt(args):
                        "theta (pinned); bytes are per call"}
 
     ttt = None
-    if not args.no_ttt and world == 1:
+    if not args.no_ttt and world == 1 and not big:
         ttt = time_to_tol(q, ctx, I, stream, barrier)
 
     line = {
@@ -259,13 +303,10 @@ def run_qdt(args):
                    "parallelism": f"fock-shard{world}" if world > 1 else "single",
                    "l2": "Theta (8*M*N bytes) > 126 MB L2; no flush needed"},
         "loop_ms_per_step": loop_ms / args.steps,
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm,
-                     "peak_source": src, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": traffic, "alg_bytes_per_launch": ab[dom]},
+        "roofline": dict(roof, kernel=dom, traffic=traffic,
+                         peak_source=(src + " (MEASURED_PEAKS.json hbm_gbs)") if roof["bound"] == "hbm" else f64src),
         "kernels": kern,
-        "iteration_roofline": {"alg_bytes": ab["iteration"],
-                               "achieved_gbs": ab["iteration"] / (ms / args.steps / 1e3) / 1e9,
-                               "frac": ab["iteration"] / (ms / args.steps / 1e3) / 1e9 / hbm},
+        "iteration_roofline": roofline_of(ab["iteration"], af["iteration"], ms / args.steps, hbm, f64),
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "e2e": e2e,
@@ -408,17 +449,27 @@ def _oracle_sample_run(I, steps, warmup, rows_total, n_slabs=20):
 
 
 def cpu_baseline(I, args):
-    """Oracle timed on this host (one thread), bounded sample (~10-30 s of CPU work)."""
+    """The oracle timed on this host's cores (oracle-MT: every core, deterministic split, bit-
+    identical to one thread), bounded sample (~10 s of CPU work); oracle-1T beside it."""
+    import oracle as o
     try:
-        # ~10-15 s of single-thread oracle work (measured ~10 us per row-iteration at N = 100)
-        rows = min(I.M, int(700000 * 100 / max(1, I.N)))
-        v, dt, r = _oracle_sample_run(I, 4, 1, rows)
-        return {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                "sample": f"4 oracle iterations (SQS) on {r} Fock rows = 20 evenly spaced slabs of "
-                          f"the {args.config} instance ({dt:.1f} s)",
-                "host_cpu": _cpu_model(), "nproc": os.cpu_count()}
+        ncpu = os.cpu_count() or 1
+        # measured ~10 us per row-iteration single-threaded at N = 100
+        rows1 = min(I.M, int(500000 * 100 / max(1, I.N)))
+        o.set_threads(1)
+        v1, dt1, r1 = _oracle_sample_run(I, 3, 1, rows1)
+        o.set_threads(0)
+        nt = o.get_threads()
+        rowsm = min(I.M, rows1 * max(1, nt // 2))
+        vm, dtm, rm = _oracle_sample_run(I, 3, 1, rowsm)
+        return {"value": vm, "unit": UNIT, "cores": nt, "kind": "oracle",
+                "sample": f"3 oracle-MT iterations (SQS) on {rm} Fock rows = 20 evenly spaced slabs of "
+                          f"the {args.config} instance ({dtm:.1f} s, {nt} threads)",
+                "oracle_1t": {"value": v1, "cores": 1,
+                              "sample": f"3 iterations on {r1} Fock rows ({dt1:.1f} s)"},
+                "host_cpu": _cpu_model(), "nproc": ncpu}
     except Exception as e:  # pragma: no cover
-        return {"value": None, "unit": UNIT, "cores": 1, "kind": "oracle", "error": repr(e)}
+        return {"value": None, "unit": UNIT, "cores": None, "kind": "oracle", "error": repr(e)}
 
 
 def _cpu_model():
@@ -435,11 +486,15 @@ def run_reference(args):
     rank, _, world = env_rank()
     if rank != 0:
         return
+    import oracle as o
     import qdt_synth as qs
     I = qs.CONFIGS[args.config]()
-    # size the per-step sample so that (steps + warmup) steps take ~150 s single-threaded
-    # (measured oracle cost ~8.5 us per row-iteration at N = 100)
-    per_row = 8.5e-6 * I.N / 100
+    o.set_threads(0)
+    nt = o.get_threads()
+    # size the per-step sample so that (steps + warmup) steps take ~150 s of CPU work on this
+    # host (measured oracle cost ~8.5 us per row-iteration per thread at N = 100; ~half-linear
+    # scaling assumed over the threads)
+    per_row = 8.5e-6 * I.N / 100 / max(1.0, nt / 2)
     rows = int(150.0 / max(1, args.steps + args.warmup) / per_row)
     rows = max(20 * 64, min(I.M, rows))
     v, dt, r = _oracle_sample_run(I, args.steps, args.warmup, rows)
@@ -448,10 +503,10 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (qdt_synth, seed 0)",
             "config": {"workload": args.config, "M": I.M, "N": I.N, "D": I.D, "gamma": I.gamma,
-                       "step_mode": "SQS", "parallelism": "single-thread oracle"},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                       "step_mode": "SQS", "parallelism": f"oracle-MT, {nt} threads"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": nt, "kind": "oracle",
                              "sample": f"each step = one oracle iteration on {r} Fock rows "
-                                       f"(20 evenly spaced slabs)", "host_cpu": _cpu_model()},
+                                       f"(20 evenly spaced slabs), {nt} threads", "host_cpu": _cpu_model()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

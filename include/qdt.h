@@ -157,9 +157,11 @@ qdt_status qdt_probes_export(qdt_ctx *ctx, const qdt_probes *probes, int64_t *nn
 
 /* ------------------------------------------------------------------------------ solve */
 /* Projected-gradient solve.  P: D x N (host, or device if
- * opts->mem_device).  N >= 1, gamma >= 0 finite, tol >= 0, iters >= 0.
+ * opts->mem_device).  1 <= N <= 10 240 (N > 1024: sweep kernels only), gamma >= 0 finite, tol >= 0,
+ * iters >= 0.
  * theta_out: M x N (or the local (k_end-k_begin) x N rows when nranks > 1 and
- * !gather_theta) receiving Theta_{iters_done}.  trace_out (may be NULL): host double[iters+1],
+ * !gather_theta) receiving Theta_{iters_done}; NULL: no copy of the result (trace / info only,
+ * e.g. when Theta fills the device and the caller times the iterations).  trace_out (may be NULL): host double[iters+1],
  * trace_out[k] = f(Theta_k) for k <= iters_done (reading R3); kkt_out (may be NULL): host
  * double[iters+1] with r_KKT(Theta_k) (NaN where not evaluated).  Early stop at the first
  * k with r_KKT(Theta_k) <= tol returns Theta_k.  info may be NULL.  Collective. */

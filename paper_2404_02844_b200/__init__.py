@@ -241,11 +241,12 @@ def qdt_probes_export(ctx: Context, F: Probes, values: bool = True):
 def qdt_solve(ctx: Context, F: Probes, P, gamma: float, tol: float = 0.0, iters: int = 100,
               step: int = QDT_STEP_SQS, accel: bool = False, theta0=None, check_every: int = 16,
               kkt_every: int = 1, gather_theta: bool = False, use_graph: bool = True,
-              theta_out=None, theta_prev=None, fista_t: float = 0.0, want_prev: bool = False):
+              theta_out=None, theta_prev=None, fista_t: float = 0.0, want_prev: bool = False,
+              no_theta: bool = False):
     """Projected-gradient solve.  P: numpy (host) or CUDA tensor (device, then theta0 and
     theta_out are device tensors too).  FISTA resume: theta_prev = Theta_{k-1}, fista_t = tau_k;
-    want_prev returns Theta_{k-1} of the result as 'theta_prev'.  Returns dict(theta, trace,
-    kkt, info[, theta_prev])."""
+    want_prev returns Theta_{k-1} of the result as 'theta_prev'; no_theta copies no result out
+    (theta None).  Returns dict(theta, trace, kkt, info[, theta_prev])."""
     L = load_library()
     dev = _is_cuda_tensor(P)
     prev_out = None
@@ -254,14 +255,15 @@ def qdt_solve(ctx: Context, F: Probes, P, gamma: float, tol: float = 0.0, iters:
         D, N = P.shape
         _dev_arg(ctx, P, "P", (F.D, N))
         rows = F.M
-        if theta_out is None:
+        if theta_out is None and not no_theta:
             theta_out = torch.empty((rows, N), dtype=torch.float64, device=P.device)
-        _dev_arg(ctx, theta_out, "theta_out", (rows, N))
+        if theta_out is not None:
+            _dev_arg(ctx, theta_out, "theta_out", (theta_out.shape[0], N))
         t0 = _dev_arg(ctx, theta0, "theta0", (rows, N)) if theta0 is not None else None
         tp = _dev_arg(ctx, theta_prev, "theta_prev", (rows, N)) if theta_prev is not None else None
         if want_prev:
             prev_out = torch.empty((rows, N), dtype=torch.float64, device=P.device)
-        p_ptr, out_ptr = P.data_ptr(), theta_out.data_ptr()
+        p_ptr, out_ptr = P.data_ptr(), (theta_out.data_ptr() if theta_out is not None else None)
         t0_ptr = t0.data_ptr() if t0 is not None else None
         tp_ptr = tp.data_ptr() if tp is not None else None
         po_ptr = prev_out.data_ptr() if prev_out is not None else None
@@ -269,13 +271,13 @@ def qdt_solve(ctx: Context, F: Probes, P, gamma: float, tol: float = 0.0, iters:
     else:
         Pp = _host(P)
         D, N = Pp.shape
-        if theta_out is None:
+        if theta_out is None and not no_theta:
             theta_out = np.empty((F.M, N))
         t0 = _host(theta0) if theta0 is not None else None
         tp = _host(theta_prev) if theta_prev is not None else None
         if want_prev:
             prev_out = np.empty((F.M, N))
-        p_ptr, out_ptr = Pp.ctypes.data, theta_out.ctypes.data
+        p_ptr, out_ptr = Pp.ctypes.data, (theta_out.ctypes.data if theta_out is not None else None)
         t0_ptr = t0.ctypes.data if t0 is not None else None
         tp_ptr = tp.ctypes.data if tp is not None else None
         po_ptr = prev_out.ctypes.data if prev_out is not None else None

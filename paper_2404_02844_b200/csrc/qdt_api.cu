@@ -118,6 +118,11 @@ struct Plan {
     // sweep path (DMMA kernels, N <= 128): NB n-blocks; bwd/fwd units; reduce lists
     int NB = 0;
     int NW = 0;                       // wide-N sweep (N > 128, even, <= 1024): 128-column chunks
+    // fused wide step (N > 128, even pitch): clusters of wx_C CTAs x wx_Wc columns per 32-row tile
+    int NX = 0;
+    int wx_C = 1, wx_Wc = 0, wx_ncl = 0;
+    int32_t *d_wx_trange = nullptr;
+    bool gen = true;                  // general (CUDA-core) plan built (N <= 1024)
     int nR = 0;                       // partR entries written by the residual reduction
     int sw_nbunits = 0;
     SwUnit *d_swunits = nullptr;
@@ -140,6 +145,7 @@ struct Plan {
     int64_t *d_fz_red_beg = nullptr, *d_fz_red_rows = nullptr;
     ~Plan()
     {
+        cudaFree(d_wx_trange);
         cudaFree(d_fz_range);
         cudaFree(d_fz_poff);
         cudaFree(d_fz_bunits);
@@ -353,6 +359,7 @@ extern "C" qdt_status qdt_init(qdt_ctx **out, const qdt_init_opts *o)
     c->nblkR = nsm * 4;
     CK(prepare_kernels());
     CK(prepare_sweep_kernels());
+    CK(prepare_wide_kernels());
     if (c->nranks > 1) {
         if (!o->nccl_unique_id)
             return fail(nullptr, QDT_ERR_INVALID_ARG, "qdt_init: nranks > 1 needs nccl_unique_id");
@@ -751,6 +758,72 @@ static qdt_status build_sweep_plan(qdt_ctx *ctx, qdt_probes *p, Plan *pl)
     return build_fused_plan(ctx, p, pl, bu);
 }
 
+// QDT_WIDE=old: N > 128 on the two-kernel wide sweep (k_grad_wide + k_proj_wide, N <= 1024)
+// instead of the fused cluster step (A/B measurement)
+static bool wide_old_forced()
+{
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("QDT_WIDE");
+        v = (e && !strcmp(e, "old")) ? 1 : 0;
+    }
+    return v == 1;
+}
+
+// Fused wide step (qdt_wide.cu): C CTAs per cluster, Wc columns each (multiple of 8, <= 640), the
+// 32-row tiles of the slice split over the co-resident clusters in contiguous ranges of equal cost
+// (window probes + a fixed epilogue share per tile).  C: the fewest CTAs with Wc <= 640, raised
+// while the slice has at least ~6 tiles per cluster and the per-CTA chunk stays >= 128 columns,
+// so that small-M / wide-N problems still fill the GPU.
+static qdt_status build_wide_plan(qdt_ctx *ctx, qdt_probes *p, Plan *pl)
+{
+    const int N = pl->N;
+    const int nbt = (N + 7) / 8;                                   // n-blocks of the row
+    const int ntw = (int)((p->Ml + WT - 1) / WT);
+    auto wc_of = [&](int C) { return 8 * ((nbt + C - 1) / C); };
+    int C = (nbt + 8 * W_NBW_MAX - 1) / (8 * W_NBW_MAX);
+    if (C > W_CMAX) return fail(ctx, QDT_ERR_INVALID_ARG, "N = %d exceeds the fused wide step (max %d)", N,
+                                W_CMAX * 64 * W_NBW_MAX);
+    const int nsm = device_sm_count();
+    while (C < W_CMAX && wc_of(C + 1) >= 128 && (int64_t)ntw < 6LL * (nsm / C)) C++;
+    while (C > 1 && (int64_t)(C - 1) * wc_of(C) >= N) C--;           // every CTA owns >= 1 column pair
+    const int Wc = wc_of(C);
+    int ncl = wide_max_clusters(C, Wc);
+    if (ncl <= 0) return fail(ctx, QDT_ERR_CUDA, "fused wide step: no co-resident cluster of %d CTAs", C);
+    ncl = std::min(ncl, std::max(1, ntw));
+    std::vector<int64_t> cost(ntw + 1, 0);
+    for (int tt = 0; tt < ntw; tt++) {
+        const int t64 = tt >> 1;
+        cost[tt + 1] = cost[tt] + (p->sw_dB[t64] - p->sw_dA[t64]) + 16;
+    }
+    std::vector<int32_t> tr(ncl + 1, 0);
+    for (int c = 1; c < ncl; c++) {
+        const int64_t target = cost[ntw] * c / ncl;
+        tr[c] = (int32_t)(std::lower_bound(cost.begin(), cost.end(), target) - cost.begin());
+        tr[c] = std::max(tr[c], tr[c - 1]);
+    }
+    tr[ncl] = ntw;
+    pl->wx_C = C;
+    pl->wx_Wc = Wc;
+    pl->wx_ncl = ncl;
+    CK(cudaMalloc(&pl->d_wx_trange, sizeof(int32_t) * (ncl + 1)));
+    CK(cudaMemcpy(pl->d_wx_trange, tr.data(), sizeof(int32_t) * (ncl + 1), cudaMemcpyHostToDevice));
+    return QDT_OK;
+}
+
+// N > GEN_NMAX: only the DMMA forward + fused wide step exist
+static qdt_status build_wide_only_plan(qdt_ctx *ctx, qdt_probes *p, int N, std::unique_ptr<Plan> pl, Plan **out)
+{
+    if (!sweep_enabled() || N % 2) return fail(ctx, QDT_ERR_INVALID_ARG, "N = %d needs the sweep kernels (even pitch)", N);
+    pl->NX = 1;
+    CKS(build_sweep_plan(ctx, p, pl.get()));
+    CKS(build_wide_plan(ctx, p, pl.get()));
+    pl->nR = ctx->nranks == 1 ? (int)((p->D + 7) / 8) : ctx->nblkR;
+    *out = pl.get();
+    p->plans[N] = std::move(pl);
+    return QDT_OK;
+}
+
 static qdt_status build_plan(qdt_ctx *ctx, qdt_probes *p, int N, Plan **out)
 {
     auto it = p->plans.find(N);
@@ -760,9 +833,11 @@ static qdt_status build_plan(qdt_ctx *ctx, qdt_probes *p, int N, Plan **out)
     }
     std::unique_ptr<Plan> pl(new Plan());
     pl->N = N;
+    pl->gen = N <= GEN_NMAX;   // the CUDA-core kernels (hooks, Newton) stop at 1024 outcomes
+    if (!pl->gen) return build_wide_only_plan(ctx, p, N, std::move(pl), out);
     pl->nthr = bwd_threads(N, &pl->CG, &pl->RG, &pl->TC);
     if (pl->CG * pl->RG > 1024)
-        return fail(ctx, QDT_ERR_INVALID_ARG, "N = %d too large for this build (max 8192)", N);
+        return fail(ctx, QDT_ERR_INVALID_ARG, "N = %d too large for the general kernels", N);
     pl->T = pl->RG * TR;
     // row-epilogue segment: smallest power of two with ceil(N/SEG) <= 16 values per lane
     pl->SEG = 1;
@@ -888,8 +963,11 @@ static qdt_status build_plan(qdt_ctx *ctx, qdt_probes *p, int N, Plan **out)
     CK(cudaStreamSynchronize(s));
     pl->NB = sweep_enabled() ? sweep_nb(N) : 0;
     // wide kernels for N > 128 (even): the whole path, or (N <= 160) beside the NB > 16 plain step
-    pl->NW = (sweep_enabled() && (!pl->NB || pl->NB > SW_NBMAX) && N % 2 == 0 && N <= 1024) ? 1 : 0;
-    if (pl->NB || pl->NW) CKS(build_sweep_plan(ctx, p, pl.get()));
+    const bool wide = sweep_enabled() && (!pl->NB || pl->NB > SW_NBMAX) && N % 2 == 0;
+    pl->NX = (wide && !wide_old_forced()) ? 1 : 0;
+    pl->NW = (wide && !pl->NX && N <= 1024) ? 1 : 0;
+    if (pl->NB || pl->NW || pl->NX) CKS(build_sweep_plan(ctx, p, pl.get()));
+    if (pl->NX) CKS(build_wide_plan(ctx, p, pl.get()));
     pl->nR = ctx->nranks == 1 ? (int)((D + 7) / 8) : ctx->nblkR;
     *out = pl.get();
     p->plans[N] = std::move(pl);
@@ -1224,8 +1302,8 @@ static qdt_status fwd_reduce(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, const
     Plan *pl = c.pl;
     qdt_probes *p = c.p;
     const bool multi = ctx->nranks > 1;
-    if (pl->NB || pl->NW) {
-        const int fnb = pl->NW ? wide_nb(c.N) : pl->NB;   // wide N: balanced column chunks
+    if (pl->NB || pl->NW || pl->NX) {
+        const int fnb = (pl->NW || pl->NX) ? wide_nb(c.N) : pl->NB;   // wide N: balanced column chunks
         SweepFwdArgs fa;
         fa.N = c.N;
         fa.Ml = (int)p->Ml;
@@ -1436,6 +1514,39 @@ static WideArgs wide_args(const IterCfg &c, SolveBufs &b, const double *R, const
     return w;
 }
 
+static WStepArgs wstep_args(const IterCfg &c, SolveBufs &b, const double *R, const double *theta, double *out)
+{
+    WStepArgs w;
+    w.N = c.N;
+    w.Nv = nvalid(c);
+    w.Ml = (int)c.p->Ml;
+    w.C = c.pl->wx_C;
+    w.Wc = c.pl->wx_Wc;
+    w.kb = c.p->kb;
+    w.M = c.p->M;
+    w.trange = c.pl->d_wx_trange;
+    w.fb_off = c.p->d_fb_off;
+    w.tile_dA = c.p->d_sw_dA;
+    w.tile_dB = c.p->d_sw_dB;
+    w.Fb = c.p->d_Fb;
+    w.R = R;
+    w.theta = theta;
+    w.theta_prev = nullptr;
+    w.beta = nullptr;
+    w.out = out;
+    w.tstep = b.tstep;
+    w.tscal = nullptr;
+    w.gamma = c.gamma;
+    w.part = b.partT;
+    w.kkt_every = c.kkt_every;
+    w.eval = 0;
+    w.eval_gate = 0;
+    w.state = b.state;
+    return w;
+}
+
+static int wstep_nparts(const IterCfg &c) { return c.pl->wx_ncl * c.pl->wx_C; }
+
 static int wide_nparts(const IterCfg &c)
 {
     return c.p->sw_ntiles * ((c.N + 127) / 128) + wide_proj_blocks((int)c.p->Ml);
@@ -1476,6 +1587,15 @@ static qdt_status iteration(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, int64_
         CK(run_k(ctx, "bwd_step", 1, [&]() { return launch_bwd_mma(a, pl->sw_nbunits, pl->NB, s); }));
         CKS(halo_exchange(ctx, c, b.theta[(j + 1) % 2]));
         CKS(scalars(ctx, c, b, 0, c.p->sw_ntiles));
+        return QDT_OK;
+    }
+    if (!c.fista && pl->NX && (!pl->NB || wide_plain_forced())) {
+        double *cur = b.theta[j % 2], *nxt = b.theta[(j + 1) % 2];
+        CKS(fwd_reduce(ctx, c, b, cur, b.R[0], true));
+        WStepArgs w = wstep_args(c, b, b.R[0], cur, nxt);
+        CK(run_k(ctx, "bwd_step", 1, [&]() { return launch_wide_step(w, pl->wx_ncl, s); }));
+        CKS(halo_exchange(ctx, c, nxt));
+        CKS(scalars(ctx, c, b, 0, wstep_nparts(c)));
         return QDT_OK;
     }
     if (!c.fista && pl->NW && (!pl->NB || wide_plain_forced())) {
@@ -1547,6 +1667,24 @@ static qdt_status iteration(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, int64_
         CK(run_k(ctx, "bwd_step", 1, [&]() { return launch_bwd_any(a, pl->sw_nbunits, pl->NB, s); }));
         CKS(halo_exchange(ctx, c, nxt));
         ntiles = c.p->sw_ntiles;
+    } else if (c.fista && pl->NX) {
+        // FISTA, fused wide step: R_k, R(Y), gated KKT evaluation of Theta_k, then the step from Y
+        double *cur = b.theta[j % 3], *prev = b.theta[(j + 2) % 3], *nxt = b.theta[(j + 1) % 3];
+        double *Rk = b.R[j % 2], *Rkm1 = b.R[(j + 1) % 2];
+        CKS(fwd_reduce(ctx, c, b, cur, Rk, true));
+        CK(run_k(ctx, "fista_rcomb", 1, [&]() {
+            return launch_fista_rcomb(b.RY, Rk, Rkm1, b.beta, c.p->D * (int64_t)c.N, b.state, s);
+        }));
+        WStepArgs ev = wstep_args(c, b, Rk, cur, nullptr);
+        ev.eval = 1;
+        ev.eval_gate = 1;
+        CK(run_k(ctx, "bwd_eval", 1, [&]() { return launch_wide_step(ev, pl->wx_ncl, s); }));
+        WStepArgs w = wstep_args(c, b, b.RY, cur, nxt);
+        w.theta_prev = prev;
+        w.beta = b.beta;
+        CK(run_k(ctx, "bwd_step", 1, [&]() { return launch_wide_step(w, pl->wx_ncl, s); }));
+        CKS(halo_exchange(ctx, c, nxt));
+        ntiles = wstep_nparts(c);
     } else if (c.fista && pl->NW) {
         // FISTA, wide N: R_k, R(Y), gated KKT evaluation of Theta_k, then the step from Y
         double *cur = b.theta[j % 3], *prev = b.theta[(j + 2) % 3], *nxt = b.theta[(j + 1) % 3];
@@ -1626,7 +1764,8 @@ static qdt_status common_bufs(qdt_ctx *ctx, qdt_probes *p, Plan *pl, int64_t N, 
     }
     CKS(ws_get(ctx, "partR", std::max(ctx->nblkR, pl->nR), &b.partR));
     const int ncc = (int)((N + 127) / 128);
-    const int nt = std::max(1, std::max({pl->ntiles, p->sw_ntiles * (pl->NW ? ncc : 1) + (int)((p->Ml + 7) / 8)}));
+    const int nt = std::max(1, std::max({pl->ntiles, p->sw_ntiles * (pl->NW ? ncc : 1) + (int)((p->Ml + 7) / 8),
+                                         pl->wx_ncl * pl->wx_C}));
     if (pl->NW) CKS(ws_get(ctx, "Gw", p->Ml * N + 4, &b.Gw));
     CKS(ws_get(ctx, "partT", (size_t)nt * NSC_TILE, &b.partT));
     CK(cudaMemsetAsync(b.partT, 0, sizeof(double) * nt * NSC_TILE, s));
@@ -1655,7 +1794,12 @@ static qdt_status eval_pass(qdt_ctx *ctx, const IterCfg &c0, SolveBufs &b, doubl
     c.kkt_every = 1;
     Plan *pl = c.pl;
     CKS(fwd_reduce(ctx, c, b, theta, b.R[0], true));
-    if (pl->NW) {
+    if (pl->NX && !(pl->NB && pl->NB <= SW_NBMAX)) {
+        WStepArgs w = wstep_args(c, b, b.R[0], theta, nullptr);
+        w.eval = 1;
+        CK(run_k(ctx, "bwd_eval", 1, [&]() { return launch_wide_step(w, pl->wx_ncl, s); }));
+        CKS(scalars(ctx, c, b, 1, wstep_nparts(c)));
+    } else if (pl->NW) {
         WideArgs w = wide_args(c, b, b.R[0], theta, nullptr);
         w.eval = 1;
         CK(run_k(ctx, "bwd_eval", 1, [&]() { return launch_grad_wide(w, pl->sw_nbunits, s); }));
@@ -1690,12 +1834,12 @@ static qdt_status check_finite_host(qdt_ctx *ctx, const double *x, int64_t n, co
     return QDT_OK;
 }
 
-// Odd N in (128, 1024) (the paper's N = 151): the wide sweep needs an even row pitch, so solve
+// Odd N > 128 (the paper's N = 151): the wide kernels need an even row pitch, so solve
 // and objective run on an internal pitch N + 1 whose pad column is zero in P and Theta (hence in
 // R and G), and is excluded from the projection, the KKT sums and their M*N normalisation.
 static int64_t pad_cols(int64_t N)
 {
-    return (sweep_enabled() && N > 8 * SW_NBMAX && N < 1024 && (N & 1)) ? N + 1 : N;
+    return (sweep_enabled() && N > 8 * SW_NBMAX && (N & 1)) ? N + 1 : N;
 }
 
 // rows x ncols doubles between row pitches (in doubles)
@@ -1717,9 +1861,9 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
                                 qdt_solve_info *info)
 {
     if (!ctx) return fail(nullptr, QDT_ERR_INVALID_ARG, "qdt_solve: ctx is NULL");
-    if (!F || !P || !theta_out) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: NULL pointer");
+    if (!F || !P) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: NULL pointer");
     if (F->ctx != ctx) return fail(ctx, QDT_ERR_STATE, "qdt_solve: probes built on another ctx");
-    if (Nu < 1 || Nu > 8192) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: N = %lld not in [1, 8192]", (long long)Nu);
+    if (Nu < 1 || Nu > QDT_NMAX) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: N = %lld not in [1, %d]", (long long)Nu, QDT_NMAX);
     const int64_t N = pad_cols(Nu);   // internal row pitch
     if (!(gamma >= 0.0) || !isfinite(gamma)) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: gamma must be finite and >= 0");
     if (!(tol >= 0.0)) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: tol must be >= 0");
@@ -1953,7 +2097,7 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     CK(cudaMemcpyAsync(&hst, b.state, sizeof hst, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     stopped = hst.stop != 0;
-    if (stopped && hst.converged && !hst.nonfinite && (pl->NB || pl->NW) && !fista) {
+    if (stopped && hst.converged && !hst.nonfinite && (pl->NB || pl->NW || pl->NX) && !fista) {
         // the sweep loop evaluates the unclamped KKT only; re-evaluate Theta_kd once with the
         // general kernels so that trace/kkt/kkt_paper at kd come from one consistent pass
         DevState sr = hst;
@@ -1974,7 +2118,9 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     const double *res = b.theta[kd % nbuf];
     // ---- outputs
     const bool gather = ctx->nranks > 1 && opt.gather_theta;
-    if (gather) {
+    if (!theta_out) {
+        // result not requested (trace / info only)
+    } else if (gather) {
         // assemble the full M x N on every rank: each rank's slice broadcast into place
         double *full;
         CKS(ws_get(ctx, "gather", M * N, &full));
@@ -2035,7 +2181,7 @@ extern "C" qdt_status qdt_objective(qdt_ctx *ctx, const qdt_probes *F, const dou
     if (!ctx) return fail(nullptr, QDT_ERR_INVALID_ARG, "qdt_objective: ctx is NULL");
     if (!F || !P || !theta || !f_out) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_objective: NULL pointer");
     if (F->ctx != ctx) return fail(ctx, QDT_ERR_STATE, "probes built on another ctx");
-    if (Nu < 1 || Nu > 8192) return fail(ctx, QDT_ERR_INVALID_ARG, "N out of range");
+    if (Nu < 1 || Nu > QDT_NMAX) return fail(ctx, QDT_ERR_INVALID_ARG, "N out of range");
     const int64_t N = pad_cols(Nu);   // internal row pitch (qdt_solve)
     if (!(gamma >= 0.0) || !isfinite(gamma)) return fail(ctx, QDT_ERR_INVALID_ARG, "gamma must be finite >= 0");
     qdt_probes *p = const_cast<qdt_probes *>(F);
@@ -2090,7 +2236,7 @@ static qdt_status hook_common(qdt_ctx *ctx, const qdt_probes *F, int64_t N, Plan
     if (!F) return fail(ctx, QDT_ERR_INVALID_ARG, "probes is NULL");
     if (F->ctx != ctx) return fail(ctx, QDT_ERR_STATE, "probes built on another ctx");
     if (ctx->nranks != 1) return fail(ctx, QDT_ERR_INVALID_ARG, "kernel hooks are single-rank only");
-    if (N < 1 || N > 8192) return fail(ctx, QDT_ERR_INVALID_ARG, "N out of range");
+    if (N < 1 || N > QDT_NMAX) return fail(ctx, QDT_ERR_INVALID_ARG, "N out of range");
     CK(cudaSetDevice(ctx->device));
     return build_plan(ctx, const_cast<qdt_probes *>(F), (int)N, pl);
 }
@@ -2127,6 +2273,7 @@ extern "C" qdt_status qdt_gradient(qdt_ctx *ctx, const qdt_probes *F, const doub
     CKS(hook_common(ctx, F, N, &pl));
     if (!theta || !R || !G_out) return fail(ctx, QDT_ERR_INVALID_ARG, "NULL pointer");
     if (!(gamma >= 0.0) || !isfinite(gamma)) return fail(ctx, QDT_ERR_INVALID_ARG, "gamma must be finite >= 0");
+    if (!pl->gen) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_gradient: N = %lld > %d (general kernels)", (long long)N, GEN_NMAX);
     qdt_probes *p = const_cast<qdt_probes *>(F);
     cudaStream_t s = ctx->stream;
     SolveBufs b;
@@ -2229,7 +2376,7 @@ extern "C" qdt_status qdt_solve_newton(qdt_ctx *ctx, const qdt_probes *F, const 
     if (!F || !P || !theta_out || !o) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve_newton: NULL pointer");
     if (F->ctx != ctx) return fail(ctx, QDT_ERR_STATE, "qdt_solve_newton: probes built on another ctx");
     if (ctx->nranks != 1) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve_newton: single rank only");
-    if (N < 1 || N > 8192) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve_newton: N out of range");
+    if (N < 1 || N > GEN_NMAX) return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve_newton: N out of range (max %d)", GEN_NMAX);
     if (!(gamma >= 0.0) || !isfinite(gamma)) return fail(ctx, QDT_ERR_INVALID_ARG, "gamma must be finite >= 0");
     if (o->max_iter < 0 || o->cg_max < 1 || o->max_ls < 1 || !(eps_kkt >= 0.0))
         return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve_newton: bad options");

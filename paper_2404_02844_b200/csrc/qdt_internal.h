@@ -197,6 +197,8 @@ constexpr int WFP = 36;         // staged F row pitch (32 rows + 4: conflict-fre
 constexpr int W_NBW_MAX = 10;   // n-blocks per warp: <= 640 columns per CTA
 constexpr int W_THREADS = 512;
 constexpr int W_CMAX = 16;      // CTAs per cluster (non-portable above 8)
+constexpr int GEN_NMAX = 1024;  // widest row of the general CUDA-core kernels (hooks, Newton)
+constexpr int QDT_NMAX = W_CMAX * 8 * 8 * W_NBW_MAX;   // widest row of the fused wide step (10 240)
 struct WStepArgs {
     int N, Nv, Ml;
     int C, Wc;                  // CTAs per cluster, columns per CTA (multiple of 8)

@@ -44,7 +44,7 @@ size_t wide_step_smem(int Wc)
     return (size_t)WSTAGES * WKC * ((Wc + 4) + WFP) * sizeof(double);
 }
 
-template <int NBW>
+template <int NBW, bool FIS>
 __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ WStepArgs a)
 {
     extern __shared__ __align__(128) double sm[];
@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
     const int64_t it = st ? st->it : 0;
     if (a.eval_gate && (it % a.kkt_every) != 0) return;
     const bool ev = a.eval != 0;
-    const bool fis = a.beta != nullptr && !ev;     // FISTA step: Y = Theta_k + beta (Theta_k - Theta_{k-1})
+    constexpr bool fis = FIS;                      // FISTA step: Y = Theta_k + beta (Theta_k - Theta_{k-1})
     const double beta = fis ? a.beta[it] : 0.0;
     const bool do_kkt = ev || (!fis && (it % a.kkt_every) == 0);
     const int N = a.N, Nv = a.Nv, C = a.C;
@@ -452,7 +452,8 @@ static cudaError_t launch_nbw(const WStepArgs &a, int grid, size_t smem, cudaStr
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k_wstep<NBW>, a);
+    const bool fis = a.beta != nullptr && !a.eval;
+    return fis ? cudaLaunchKernelEx(&cfg, k_wstep<NBW, true>, a) : cudaLaunchKernelEx(&cfg, k_wstep<NBW, false>, a);
 }
 
 #define QDT_FOR_NBW(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10)
@@ -468,11 +469,13 @@ cudaError_t prepare_wide_kernels()
     if (done_mask & bit) return cudaSuccess;
     cudaError_t e = cudaSuccess;
     const int smax = (int)wide_step_smem(8 * 8 * W_NBW_MAX);
-#define QDT_PREP(n)                                                                                         \
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_wstep<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax); \
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_wstep<n>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+#define QDT_PREP1(n, f)                                                                                        \
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_wstep<n, f>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax); \
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_wstep<n, f>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+#define QDT_PREP(n) QDT_PREP1(n, false) QDT_PREP1(n, true)
     QDT_FOR_NBW(QDT_PREP)
 #undef QDT_PREP
+#undef QDT_PREP1
     if (e == cudaSuccess) done_mask |= bit;
     return e;
 }
@@ -496,7 +499,7 @@ int wide_max_clusters(int C, int Wc)
     cudaError_t e = cudaErrorInvalidValue;
     switch (nbw) {
 #define QDT_CASE(k) \
-    case k: e = cudaOccupancyMaxActiveClusters(&n, k_wstep<k>, &cfg); break;
+    case k: e = cudaOccupancyMaxActiveClusters(&n, k_wstep<k, false>, &cfg); break;
         QDT_FOR_NBW(QDT_CASE)
 #undef QDT_CASE
         default: break;

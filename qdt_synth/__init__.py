@@ -15,6 +15,7 @@ F/P) are not available, these stand in for them with the same shap
 from __future__ import annotations
 
 import dataclasses
+import warnings
 
 import numpy as np
 import scipy.sparse as sp
@@ -148,7 +149,8 @@ def theta_logbins_sparse(M: int, N: int, eta: float = 0.9) -> sp.csr_matrix:
         if sel.size == 0:
             continue
         kk = k[sel]
-        with np.errstate(all="ignore"):
+        with np.errstate(all="ignore"), warnings.catch_warnings():
+            warnings.simplefilter("ignore", DeprecationWarning)   # integral values passed as float
             Fc = np.where(c - 1 >= kk, 1.0, sps.bdtr(np.minimum(c - 1, kk), kk, eta))
             Fa = np.where(a - 1 < 0, 0.0, np.where(a - 1 >= kk, 1.0,
                                                     sps.bdtr(np.maximum(a - 1, 0), kk, eta)))
@@ -160,6 +162,53 @@ def theta_logbins_sparse(M: int, N: int, eta: float = 0.9) -> sp.csr_matrix:
     T = sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
                       shape=(M, N))
     # renormalise rows against the CDF differencing roundoff
+    s = np.asarray(T.sum(axis=1)).ravel()
+    return sp.diags(1.0 / s) @ T
+
+
+def theta_logbins_rows(M: int, N: int, eta: float = 0.9, chunk: int = 1 << 16) -> sp.csr_matrix:
+    """The same Theta_true as theta_logbins_sparse, built row-major and vectorised over
+    (row, bin) pairs (the per-bin loop is too slow at Stress: M = 10^6, N = 10^4)."""
+    npmax = eta * (M - 1)
+    Lg = np.log1p(npmax)
+    nprime = np.arange(int(np.floor(npmax)) + 2)
+    b = np.minimum(N - 1, np.floor(N * np.log1p(nprime) / Lg)).astype(np.int64)
+    first = np.full(N + 1, nprime.shape[0], dtype=np.int64)
+    ub, idx = np.unique(b, return_index=True)
+    first[ub] = idx
+    for n in range(N - 1, -1, -1):
+        first[n] = min(first[n], first[n + 1])
+    first[N] = np.iinfo(np.int64).max // 4
+    edge_f = first.astype(float)
+    rows_all, cols_all, vals_all = [], [], []
+    for k0 in range(0, M, chunk):
+        k = np.arange(k0, min(M, k0 + chunk), dtype=float)
+        mean, sd = eta * k, np.sqrt(eta * (1 - eta) * k)
+        lo_e, hi_e = mean - 12 * sd - 2, mean + 12 * sd + 2
+        # bins n with c_n > lo_e and a_n <= hi_e + 1, c_n = edge_f[n + 1], a_n = edge_f[n]
+        nlo = np.searchsorted(edge_f[1:], lo_e, side="right")          # first n with c_n > lo_e
+        nhi = np.searchsorted(edge_f[:N], hi_e + 1, side="right")      # one past the last a_n <= hi_e + 1
+        cnt = np.maximum(nhi - nlo, 0)
+        # the CDF once per bin edge of each row (cnt + 1 edges), then differences of neighbours
+        ce = np.where(cnt > 0, cnt + 1, 0)
+        r = np.repeat(np.arange(k.shape[0]), ce)
+        n = nlo[r] + (np.arange(ce.sum()) - np.repeat(np.cumsum(ce) - ce, ce))
+        kk = k[r]
+        e = edge_f[n]
+        with np.errstate(all="ignore"), warnings.catch_warnings():
+            warnings.simplefilter("ignore", DeprecationWarning)   # integral values passed as float
+            Fe = np.where(e - 1 < 0, 0.0, np.where(e - 1 >= kk, 1.0, sps.bdtr(np.clip(e - 1, 0, kk), kk, eta)))
+        last = np.zeros(r.shape[0], dtype=bool)
+        if r.shape[0]:
+            last[np.cumsum(ce)[ce > 0] - 1] = True
+        lo_i = np.nonzero(~last)[0]
+        v = np.clip(Fe[lo_i + 1] - Fe[lo_i], 0.0, None)
+        keep = v > 0
+        rows_all.append((r[lo_i] + k0)[keep])
+        cols_all.append(n[lo_i][keep])
+        vals_all.append(v[keep])
+    T = sp.csr_matrix((np.concatenate(vals_all), (np.concatenate(rows_all), np.concatenate(cols_all))),
+                      shape=(M, N))
     s = np.asarray(T.sum(axis=1)).ravel()
     return sp.diags(1.0 / s) @ T
 
@@ -213,6 +262,20 @@ def stress_cut(seed: int = 0) -> Instance:
     T = theta_logbins_sparse(M, N)
     P = np.asarray((coherent_matrix(alpha2, M) @ T).todense())
     return Instance("stress_cut", alpha2, M, P, 1e-5, 3, T)
+
+
+def stress(seed: int = 0, M: int = 10 ** 6, N: int = 10 ** 4, D: int = 2 * 10 ** 4,
+           keep_theta: bool = False) -> Instance:
+    """BASELINE Stress: M = 10^6, N = 10^4 (10^10 elements), D = 2 10^4 probes log-spaced in
+    [1, 9 10^5], Theta_true = efficiency 0.9 thinning into 10^4 log bins, noiseless
+    P = F Theta_true, gamma = 1e-5, 200 iterations.  Smaller M / N / D give the Stress-shaped
+    parity instances (probe means up to 0.9 * 0.9 M, as stress_cut)."""
+    mu_max = 9e5 if M == 10 ** 6 else 0.81 * M
+    alpha2 = np.geomspace(1.0, mu_max, D)
+    T = theta_logbins_rows(M, N)
+    P = np.asarray((coherent_matrix(alpha2, M) @ T).todense())
+    return Instance("stress" if M == 10 ** 6 else f"stress_M{M}_N{N}", alpha2, M, P, 1e-5, 200,
+                    T if keep_theta else None)
 
 
 def random_instance(seed: int, D: int, M: int, N: int, mu_max: float | None = None,
@@ -306,4 +369,4 @@ def fidelities(theta: np.ndarray, theta_true: np.ndarray) -> np.ndarray:
 
 
 CONFIGS = {"tiny": tiny, "medium": medium, "large": large, "megascale": megascale,
-           "stress_cut": stress_cut, "paper_tmd": paper_tmd}
+           "stress": stress, "stress_cut": stress_cut, "paper_tmd": paper_tmd}

@@ -67,3 +67,14 @@ def test_fidelity_definition():
     # column 0: (sqrt(.5))^2 / (1 * 1) = 0.5; column 1: (sqrt(1))^2 / (1 * 1) = 1
     np.testing.assert_allclose(qs.fidelities(a, b), [0.5, 1.0])
     assert qs.fidelities(3 * a, a) == pytest.approx([1.0, 1.0])   # scale invariant
+
+
+def test_logbins_rowwise_builder_matches_binwise():
+    """theta_logbins_rows (vectorised, used at Stress size) builds exactly the Theta_true of the
+    bin-by-bin theta_logbins_sparse."""
+    for M, N in [(3000, 300), (5000, 1200)]:
+        A = qs.theta_logbins_sparse(M, N)
+        B = qs.theta_logbins_rows(M, N, chunk=777)
+        assert A.shape == B.shape and A.nnz == B.nnz
+        assert abs(A - B).max() == 0.0
+        assert np.allclose(np.asarray(B.sum(1)).ravel(), 1.0, atol=1e-14)
