@@ -64,11 +64,23 @@ typedef enum {
 typedef struct qdt_ctx qdt_ctx;       /* device, stream, NCCL comm, workspace, last error  */
 typedef struct qdt_probes qdt_probes; /* banded F of this rank's Fock slice + tile plans     */
 
+typedef enum {
+    QDT_COMM_NCCL = 0,   /* one process per GPU, NCCL over NVLink (the production path)            */
+    QDT_COMM_INPROC = 1  /* virtual ranks: one host thread per rank inside one process, device
+                            buffers shared directly (all ranks on one device, or peer-accessible
+                            devices); the same planner, kernels, halo and reductions as NCCL, with
+                            sums in rank order.  Runs the multi-rank library path on one GPU
+                            (tests); solves run iteration by iteration (no graph). */
+} qdt_comm_kind;
+
 typedef struct {
     int32_t device;             /* CUDA device ordinal                                       */
     int32_t rank, nranks;       /* SPMD rank / world size (1 = single GPU)                   */
     const void *nccl_unique_id; /* 128-byte ncclUniqueId (same on every rank); NULL if nranks==1 */
     void *cuda_stream;          /* cudaStream_t to run on; NULL -> ctx-owned stream           */
+    int32_t comm;               /* qdt_comm_kind (nranks > 1), default QDT_COMM_NCCL            */
+    int64_t group_key;          /* QDT_COMM_INPROC: ranks calling qdt_init with the same key (and
+                                   nranks) form one group; each rank calls from its own thread  */
 } qdt_init_opts;
 
 typedef struct {
@@ -93,6 +105,10 @@ typedef struct {
     double fista_t;        /* tau_k of the Beck-Teboulle sequence at the resume point (>= 1); 0 -> 1 */
     double *theta_prev_out;/* receives Theta_{k-1} of the returned Theta_k (layout of theta_out);
                               may be NULL; FISTA only                                            */
+    int32_t exchange;      /* nranks > 1, residual exchange: 0 (default) allreduce of the D x N
+                              partial residual; 1 band-aware: each rank sums only the probes whose
+                              bands touch its slice, with the peers whose slices they also touch
+                              (the paper's neighbour exchange); not with BB  */
 } qdt_solve_opts;
 
 typedef struct {

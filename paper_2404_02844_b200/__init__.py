@@ -39,9 +39,13 @@ class QdtError(RuntimeError):
         self.status = status
 
 
+QDT_COMM_NCCL, QDT_COMM_INPROC = 0, 1
+
+
 class InitOpts(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int32), ("rank", ctypes.c_int32), ("nranks", ctypes.c_int32),
-                ("nccl_unique_id", ctypes.c_void_p), ("cuda_stream", ctypes.c_void_p)]
+                ("nccl_unique_id", ctypes.c_void_p), ("cuda_stream", ctypes.c_void_p),
+                ("comm", ctypes.c_int32), ("group_key", ctypes.c_int64)]
 
 
 class ProbeOpts(ctypes.Structure):
@@ -54,7 +58,8 @@ class SolveOpts(ctypes.Structure):
                 ("check_every", ctypes.c_int32), ("kkt_every", ctypes.c_int32),
                 ("mem_device", ctypes.c_int32), ("gather_theta", ctypes.c_int32),
                 ("use_graph", ctypes.c_int32), ("theta_prev", ctypes.c_void_p),
-                ("fista_t", ctypes.c_double), ("theta_prev_out", ctypes.c_void_p)]
+                ("fista_t", ctypes.c_double), ("theta_prev_out", ctypes.c_void_p),
+                ("exchange", ctypes.c_int32)]
 
 
 class NewtonOpts(ctypes.Structure):
@@ -186,11 +191,13 @@ def _order_after_torch(ctx: Context):
 
 
 def qdt_init(device: int = 0, rank: int = 0, nranks: int = 1, nccl_unique_id: bytes | None = None,
-             cuda_stream: int | None = None) -> Context:
+             cuda_stream: int | None = None, comm: int = QDT_COMM_NCCL, group_key: int = 0) -> Context:
+    """comm = QDT_COMM_INPROC: virtual ranks of one process (each rank calls every collective
+    function from its own thread; ctypes releases the GIL during the call)."""
     L = load_library()
     uid = ctypes.create_string_buffer(nccl_unique_id, 128) if nccl_unique_id else None
     o = InitOpts(device, rank, nranks, ctypes.cast(uid, ctypes.c_void_p) if uid else None,
-                 cuda_stream)
+                 cuda_stream, int(comm), int(group_key))
     p = ctypes.c_void_p()
     st = L.qdt_init(ctypes.byref(p), ctypes.byref(o))
     if st != 0:
@@ -242,11 +249,12 @@ def qdt_solve(ctx: Context, F: Probes, P, gamma: float, tol: float = 0.0, iters:
               step: int = QDT_STEP_SQS, accel: bool = False, theta0=None, check_every: int = 16,
               kkt_every: int = 1, gather_theta: bool = False, use_graph: bool = True,
               theta_out=None, theta_prev=None, fista_t: float = 0.0, want_prev: bool = False,
-              no_theta: bool = False):
+              no_theta: bool = False, exchange: int = 0, rows=None):
     """Projected-gradient solve.  P: numpy (host) or CUDA tensor (device, then theta0 and
     theta_out are device tensors too).  FISTA resume: theta_prev = Theta_{k-1}, fista_t = tau_k;
     want_prev returns Theta_{k-1} of the result as 'theta_prev'; no_theta copies no result out
-    (theta None).  Returns dict(theta, trace, kkt, info[, theta_prev])."""
+    (theta None); rows: rows of theta_out (nranks > 1 without gather_theta: this rank's slice);
+    exchange 1: band-aware residual exchange between ranks.  Returns dict(theta, trace, kkt, info[, theta_prev])."""
     L = load_library()
     dev = _is_cuda_tensor(P)
     prev_out = None
@@ -254,7 +262,7 @@ def qdt_solve(ctx: Context, F: Probes, P, gamma: float, tol: float = 0.0, iters:
         import torch
         D, N = P.shape
         _dev_arg(ctx, P, "P", (F.D, N))
-        rows = F.M
+        rows = F.M if rows is None else int(rows)
         if theta_out is None and not no_theta:
             theta_out = torch.empty((rows, N), dtype=torch.float64, device=P.device)
         if theta_out is not None:
@@ -272,7 +280,7 @@ def qdt_solve(ctx: Context, F: Probes, P, gamma: float, tol: float = 0.0, iters:
         Pp = _host(P)
         D, N = Pp.shape
         if theta_out is None and not no_theta:
-            theta_out = np.empty((F.M, N))
+            theta_out = np.empty((F.M if rows is None else int(rows), N))
         t0 = _host(theta0) if theta0 is not None else None
         tp = _host(theta_prev) if theta_prev is not None else None
         if want_prev:
@@ -284,7 +292,7 @@ def qdt_solve(ctx: Context, F: Probes, P, gamma: float, tol: float = 0.0, iters:
     trace = np.full(iters + 1, np.nan)
     kkt = np.full(iters + 1, np.nan)
     o = SolveOpts(step, int(accel), t0_ptr, check_every, kkt_every, int(dev), int(gather_theta),
-                  int(use_graph), tp_ptr, float(fista_t), po_ptr)
+                  int(use_graph), tp_ptr, float(fista_t), po_ptr, int(exchange))
     info = SolveInfo()
     _check(ctx, L.qdt_solve(ctx.ptr, F.ptr, p_ptr, N, float(gamma), float(tol), int(iters),
                             ctypes.byref(o), out_ptr, trace.ctypes.data, kkt.ctypes.data,

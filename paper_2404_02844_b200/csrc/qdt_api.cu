@@ -13,7 +13,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <numeric>
 #include <string>
@@ -77,6 +79,24 @@ NcclApi g_nccl;
 }  // namespace
 
 // ------------------------------------------------------------------------------ structures
+// In-process group of virtual ranks (qdt_init_opts.comm = QDT_COMM_INPROC): one host thread per
+// rank, every rank's device memory visible to the others (same device).  A barrier posts, per
+// rank, one pointer / integer and an event recorded on that rank's stream at arrival; posting
+// slots and events alternate by barrier parity, so a rank one barrier ahead never overwrites
+// what a slower rank is still reading.
+struct VGroup {
+    int n = 0;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0, joined = 0;
+    uint64_t gen = 0;
+    const void *ptr[2][VMAX] = {};
+    int64_t ival[2][VMAX] = {};
+    cudaEvent_t ev[2][VMAX] = {};
+};
+static std::mutex g_vg_mu;
+static std::map<int64_t, std::shared_ptr<VGroup>> g_vgroups;
+
 struct DevBuf {
     void *p = nullptr;
     size_t n = 0;
@@ -86,7 +106,7 @@ struct qdt_ctx {
     int device = 0, rank = 0, nranks = 1;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
-    nccl_comm_t comm = nullptr;
+    nccl_comm_t ncomm = nullptr;
     std::string err;
     bool profiling = false;
     std::map<std::string, std::pair<int64_t, double>> prof;
@@ -94,6 +114,10 @@ struct qdt_ctx {
     int64_t launches = 0;
     std::map<std::string, DevBuf> ws;  // grow-only workspace
     int nblkR = 148 * 4;
+    int comm = 0;                      // QDT_COMM_NCCL / QDT_COMM_INPROC
+    std::shared_ptr<VGroup> vg;        // in-process group
+    cudaEvent_t vev[2] = {nullptr, nullptr};
+    uint64_t vpar = 0;                 // barriers passed (parity selects slots / events)
     // the last instantiated solve-loop graph and the key it was captured under (configuration
     // + every device pointer it bakes in): a repeated qdt_solve with the same key replays it
     cudaGraphExec_t gexec = nullptr;
@@ -179,6 +203,7 @@ struct qdt_probes {
     std::vector<int32_t> lo_g, hi_g, lo_l, len_l;
     std::vector<int64_t> off;
     std::vector<int64_t> cuts;   // Fock-axis shard cuts of every rank (nranks + 1)
+    std::vector<int64_t> dlo_r, dhi_r;   // per rank: probes [dlo_r[q], dhi_r[q]) touch rank q's slice
     double min_row_mass = 1.0;
     int64_t uncovered = 0;
     std::map<int, std::unique_ptr<Plan>> plans;
@@ -360,6 +385,28 @@ extern "C" qdt_status qdt_init(qdt_ctx **out, const qdt_init_opts *o)
     CK(prepare_kernels());
     CK(prepare_sweep_kernels());
     CK(prepare_wide_kernels());
+    c->comm = (o && c->nranks > 1) ? o->comm : QDT_COMM_NCCL;
+    if (c->nranks > 1 && c->comm == QDT_COMM_INPROC) {
+        if (c->nranks > VMAX)
+            return fail(nullptr, QDT_ERR_INVALID_ARG, "qdt_init: in-process groups have <= %d ranks", VMAX);
+        CK(cudaEventCreateWithFlags(&c->vev[0], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->vev[1], cudaEventDisableTiming));
+        {
+            std::lock_guard<std::mutex> lk(g_vg_mu);
+            auto &g = g_vgroups[o->group_key];
+            if (!g) {
+                g = std::make_shared<VGroup>();
+                g->n = c->nranks;
+            }
+            if (g->n != c->nranks)
+                return fail(nullptr, QDT_ERR_INVALID_ARG, "qdt_init: group %lld has %d ranks, not %d",
+                            (long long)o->group_key, g->n, c->nranks);
+            c->vg = g;
+            if (++g->joined == g->n) g_vgroups.erase(o->group_key);   // complete: a later group may reuse the key
+        }
+        *out = c.release();
+        return QDT_OK;
+    }
     if (c->nranks > 1) {
         if (!o->nccl_unique_id)
             return fail(nullptr, QDT_ERR_INVALID_ARG, "qdt_init: nranks > 1 needs nccl_unique_id");
@@ -367,7 +414,7 @@ extern "C" qdt_status qdt_init(qdt_ctx **out, const qdt_init_opts *o)
         if (!g_nccl.load(err)) return fail(nullptr, QDT_ERR_NCCL, "qdt_init: %s", err.c_str());
         nccl_uid_t uid;
         memcpy(&uid, o->nccl_unique_id, sizeof uid);
-        nccl_result_t r = g_nccl.commInitRank(&c->comm, c->nranks, uid, c->rank);
+        nccl_result_t r = g_nccl.commInitRank(&c->ncomm, c->nranks, uid, c->rank);
         if (r != 0)
             return fail(nullptr, QDT_ERR_NCCL, "ncclCommInitRank: %s", g_nccl.getErrorString(r));
     }
@@ -382,7 +429,9 @@ extern "C" qdt_status qdt_finalize(qdt_ctx *ctx)
     flush_profile(ctx);
     if (ctx->gexec) cudaGraphExecDestroy(ctx->gexec);
     for (auto &kv : ctx->ws) cudaFree(kv.second.p);
-    if (ctx->comm) g_nccl.commDestroy(ctx->comm);
+    if (ctx->ncomm) g_nccl.commDestroy(ctx->ncomm);
+    if (ctx->vev[0]) cudaEventDestroy(ctx->vev[0]);
+    if (ctx->vev[1]) cudaEventDestroy(ctx->vev[1]);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return QDT_OK;
@@ -422,12 +471,60 @@ extern "C" qdt_status qdt_launch_count(qdt_ctx *ctx, int64_t *count)
 }
 
 // ------------------------------------------------------------------------------ collectives
+// In-process barrier: post (p, iv) and an event of this rank's stream, wait for every rank; out
+// gets every rank's posting, and this rank's stream then waits for every rank's event.
+struct VPost {
+    const void *p[VMAX];
+    int64_t iv[VMAX];
+};
+static qdt_status vg_barrier(qdt_ctx *ctx, const void *p, int64_t iv, VPost *out)
+{
+    VGroup &g = *ctx->vg;
+    const int par = (int)(ctx->vpar & 1);
+    CK(cudaEventRecord(ctx->vev[par], ctx->stream));
+    {
+        std::unique_lock<std::mutex> lk(g.mu);
+        g.ptr[par][ctx->rank] = p;
+        g.ival[par][ctx->rank] = iv;
+        g.ev[par][ctx->rank] = ctx->vev[par];
+        const uint64_t my = g.gen;
+        if (++g.arrived == g.n) {
+            g.arrived = 0;
+            g.gen++;
+            g.cv.notify_all();
+        } else {
+            g.cv.wait(lk, [&] { return g.gen != my; });
+        }
+        for (int q = 0; q < g.n; q++) {
+            if (out) {
+                out->p[q] = g.ptr[par][q];
+                out->iv[q] = g.ival[par][q];
+            }
+            if (q != ctx->rank) CK(cudaStreamWaitEvent(ctx->stream, g.ev[par][q], 0));
+        }
+    }
+    ctx->vpar++;
+    return QDT_OK;
+}
+
 static qdt_status allreduce(qdt_ctx *ctx, double *buf, size_t n, const char *name)
 {
     if (ctx->nranks == 1 || n == 0) return QDT_OK;
+    if (ctx->vg) {   // in-process: every rank sums all buffers in rank order, then copies back
+        VPost post;
+        CKS(vg_barrier(ctx, buf, (int64_t)n, &post));
+        double *tmp;
+        CKS(ws_get(ctx, "vsum_tmp", n, &tmp));
+        VPtrs v;
+        for (int q = 0; q < ctx->nranks; q++) v.p[q] = (const double *)post.p[q];
+        CK(run_k(ctx, name, 1, [&]() { return launch_vsum(v, ctx->nranks, (int64_t)n, tmp, ctx->stream); }));
+        CKS(vg_barrier(ctx, nullptr, 0, nullptr));   // every rank has read every buffer
+        CK(cudaMemcpyAsync(buf, tmp, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+        return QDT_OK;
+    }
     nccl_result_t r = 0;
     cudaError_t e = run_k(ctx, name, 1, [&]() {
-        r = g_nccl.allReduce(buf, buf, n, NCCL_FLOAT64, NCCL_SUM, ctx->comm, ctx->stream);
+        r = g_nccl.allReduce(buf, buf, n, NCCL_FLOAT64, NCCL_SUM, ctx->ncomm, ctx->stream);
         return cudaSuccess;
     });
     (void)e;
@@ -442,14 +539,24 @@ static qdt_status gather_rows(qdt_ctx *ctx, const qdt_probes *p, const double *s
 {
     CK(cudaMemcpyAsync(full + p->kb * N, src, sizeof(double) * p->Ml * N, cudaMemcpyDeviceToDevice, ctx->stream));
     if (ctx->nranks == 1) return QDT_OK;
+    if (ctx->vg) {
+        VPost post;
+        CKS(vg_barrier(ctx, src, 0, &post));
+        for (int q = 0; q < ctx->nranks; q++)
+            if (q != ctx->rank)
+                CK(cudaMemcpyAsync(full + p->cuts[q] * N, post.p[q], sizeof(double) * (p->cuts[q + 1] - p->cuts[q]) * N,
+                                   cudaMemcpyDeviceToDevice, ctx->stream));
+        CKS(vg_barrier(ctx, nullptr, 0, nullptr));
+        return QDT_OK;
+    }
     nccl_result_t e = 0;
     run_k(ctx, "gather", 1, [&]() {
         g_nccl.groupStart();
         for (int q = 0; q < ctx->nranks; q++) {
             if (q == ctx->rank) continue;
             const int64_t qb = p->cuts[q], qe = p->cuts[q + 1];
-            e |= g_nccl.send(src, (size_t)(p->Ml * N), NCCL_FLOAT64, q, ctx->comm, ctx->stream);
-            e |= g_nccl.recv(full + qb * N, (size_t)((qe - qb) * N), NCCL_FLOAT64, q, ctx->comm, ctx->stream);
+            e |= g_nccl.send(src, (size_t)(p->Ml * N), NCCL_FLOAT64, q, ctx->ncomm, ctx->stream);
+            e |= g_nccl.recv(full + qb * N, (size_t)((qe - qb) * N), NCCL_FLOAT64, q, ctx->ncomm, ctx->stream);
         }
         e |= g_nccl.groupEnd();
         return cudaSuccess;
@@ -986,6 +1093,18 @@ static qdt_status finish_probes(qdt_ctx *ctx, qdt_probes *p, const double *vals)
     shard_bounds(p->lo_g, p->hi_g, M, ctx->nranks, cuts);
     p->kb = cuts[ctx->rank];
     p->ke = cuts[ctx->rank + 1];
+    p->dlo_r.assign(ctx->nranks, 0);
+    p->dhi_r.assign(ctx->nranks, 0);
+    for (int q = 0; q < ctx->nranks; q++) {   // band edges are monotone: contiguous probe ranges
+        int64_t a = D, b = 0;
+        for (int64_t d = 0; d < D; d++)
+            if (p->lo_g[d] < cuts[q + 1] && p->hi_g[d] >= cuts[q]) {
+                a = std::min(a, d);
+                b = std::max(b, d + 1);
+            }
+        p->dlo_r[q] = a < b ? a : 0;
+        p->dhi_r[q] = a < b ? b : 0;
+    }
     p->Ml = p->ke - p->kb;
     if (p->Ml < 1) return fail(ctx, QDT_ERR_INVALID_ARG, "rank %d owns no Fock rows (M too small)", ctx->rank);
     p->lo_l.resize(D);
@@ -1194,7 +1313,9 @@ static qdt_status step_setup(qdt_ctx *ctx, qdt_probes *p, Plan *pl, int mode, do
         }));
     }
     if (mode == QDT_STEP_LIPSCHITZ || rho_out) {
-        // v0 = 1/sqrt(M); K_pow iterations of v <- F^T F v / ||F^T F v||; rho = ||F v||^2
+        // v0 = 1/sqrt(M); K_pow iterations of v <- F^T F v / ||F^T F v||; rho = ||F v||^2.  The
+        // products act on single columns: the general tiles of the N = 1 plan serve every N
+        if (!pl->gen) CKS(build_plan(ctx, p, 1, &pl));
         double *v, *u, *q, *part, *nrm;
         const int nb = ctx->nblkR;
         CKS(ws_get(ctx, "pow_v", Ml, &v));
@@ -1291,9 +1412,76 @@ struct IterCfg {
     int bb = 0;                // Barzilai-Borwein step (reading R14)
     double tlip = 0.0;         // its safeguard / first step
     int Nv = 0;                // outcomes when N is a padded pitch (pad_cols), else 0
+    int bx = 0;                // band-aware residual exchange (nranks > 1)
 };
 
 static inline int nvalid(const IterCfg &c) { return c.Nv ? c.Nv : c.N; }
+
+// Band-aware residual exchange: R holds this rank's partial rows
+// (zero for probes that miss the slice).  With every peer q whose slice shares probes with ours,
+// the shared probe rows [max(dlo), min(dhi)) are exchanged (NCCL send/recv, or copies inside an
+// in-process group); k_band_combine sums each touched probe over its ranks in rank order,
+// subtracts P and accumulates ||R||^2 on the probe's lowest rank.
+static qdt_status band_exchange(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, double *R, bool withP)
+{
+    qdt_probes *p = c.p;
+    const int G = ctx->nranks, g = ctx->rank, N = c.N;
+    const int64_t a0 = p->dlo_r[g], a1 = p->dhi_r[g];
+    BandX bx;
+    memset(&bx, 0, sizeof bx);
+    int64_t tot = 0;
+    std::vector<int64_t> ov0(G, 0), ov1(G, 0), off(G, 0);
+    for (int q = 0; q < G; q++) {
+        bx.dlo[q] = p->dlo_r[q];
+        bx.dhi[q] = p->dhi_r[q];
+        if (q == g) continue;
+        ov0[q] = std::max(a0, p->dlo_r[q]);
+        ov1[q] = std::min(a1, p->dhi_r[q]);
+        if (ov1[q] < ov0[q]) ov1[q] = ov0[q];
+        off[q] = tot;
+        tot += (ov1[q] - ov0[q]) * N;
+    }
+    double *recv = nullptr;
+    CKS(ws_get(ctx, "bx_recv", std::max<int64_t>(1, tot), &recv));
+    for (int q = 0; q < G; q++) {
+        bx.src[q] = recv + off[q];
+        bx.start[q] = ov0[q];
+    }
+    if (ctx->vg) {
+        VPost post;
+        CKS(vg_barrier(ctx, R, 0, &post));
+        for (int q = 0; q < G; q++)
+            if (q != g && ov1[q] > ov0[q])
+                CK(cudaMemcpyAsync(recv + off[q], (const double *)post.p[q] + ov0[q] * N,
+                                   sizeof(double) * (ov1[q] - ov0[q]) * N, cudaMemcpyDeviceToDevice, ctx->stream));
+        CKS(vg_barrier(ctx, nullptr, 0, nullptr));
+    } else {
+        nccl_result_t e = 0;
+        run_k(ctx, "band_exchange", 1, [&]() {
+            g_nccl.groupStart();
+            for (int q = 0; q < G; q++) {
+                if (q == g || ov1[q] <= ov0[q]) continue;
+                const size_t n = (size_t)((ov1[q] - ov0[q]) * N);
+                e |= g_nccl.send(R + ov0[q] * N, n, NCCL_FLOAT64, q, ctx->ncomm, ctx->stream);
+                e |= g_nccl.recv(recv + off[q], n, NCCL_FLOAT64, q, ctx->ncomm, ctx->stream);
+            }
+            e |= g_nccl.groupEnd();
+            return cudaSuccess;
+        });
+        if (e != 0) return fail(ctx, QDT_ERR_NCCL, "band-aware exchange failed");
+    }
+    static const double zero = 0.0;
+    (void)zero;
+    double *Pz = b.P;
+    if (!withP) {   // no data term: subtract zeros
+        CKS(ws_get(ctx, "bx_zero", (size_t)p->D * N, &Pz));
+        CK(cudaMemsetAsync(Pz, 0, sizeof(double) * p->D * N, ctx->stream));
+    }
+    CK(run_k(ctx, "reduce_R", 1, [&]() {
+        return launch_band_combine(bx, g, G, Pz, R, N, b.partR, c.pl->nR, b.state, ctx->stream);
+    }));
+    return QDT_OK;
+}
 
 static qdt_status fwd_reduce(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, const double *theta,
                              double *R, bool withP)
@@ -1327,6 +1515,7 @@ static qdt_status fwd_reduce(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, const
             return launch_reduce_R2(b.rpart, pl->d_sw_red_beg, pl->d_sw_red_rows, nullptr, R, (int)p->D,
                                     c.N, nullptr, b.state, s);
         }));
+        if (c.bx) return band_exchange(ctx, c, b, R, withP);
         CKS(allreduce(ctx, R, (size_t)p->D * c.N, "allreduce_R"));
         if (withP)
             CK(run_k(ctx, "reduce_R", 1, [&]() {
@@ -1351,6 +1540,7 @@ static qdt_status fwd_reduce(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, const
                                 R, (int)p->D, c.N, multi ? nullptr : b.partR, b.state, s);
     }));
     if (multi) {
+        if (c.bx) return band_exchange(ctx, c, b, R, withP);
         CKS(allreduce(ctx, R, (size_t)p->D * c.N, "allreduce_R"));
         if (withP)
             CK(run_k(ctx, "reduce_R", 1, [&]() {
@@ -1396,16 +1586,28 @@ static qdt_status halo_exchange(qdt_ctx *ctx, const IterCfg &c, double *theta)
     if (ctx->nranks == 1) return QDT_OK;
     const int N = c.N, r = ctx->rank;
     const int64_t Ml = c.p->Ml;
+    if (ctx->vg) {   // copy the neighbours' edge rows into the halo rows
+        VPost post;
+        CKS(vg_barrier(ctx, theta, Ml, &post));
+        if (r > 0)
+            CK(cudaMemcpyAsync(theta - N, (const double *)post.p[r - 1] + (post.iv[r - 1] - 1) * N, sizeof(double) * N,
+                               cudaMemcpyDeviceToDevice, ctx->stream));
+        if (r + 1 < ctx->nranks)
+            CK(cudaMemcpyAsync(theta + Ml * N, post.p[r + 1], sizeof(double) * N, cudaMemcpyDeviceToDevice, ctx->stream));
+        CKS(vg_barrier(ctx, nullptr, 0, nullptr));
+        ctx->launches += 0;
+        return QDT_OK;
+    }
     nccl_result_t e = 0;
     run_k(ctx, "halo", 1, [&]() {
         g_nccl.groupStart();
         if (r > 0) {
-            e |= g_nccl.send(theta, N, NCCL_FLOAT64, r - 1, ctx->comm, ctx->stream);
-            e |= g_nccl.recv(theta - N, N, NCCL_FLOAT64, r - 1, ctx->comm, ctx->stream);
+            e |= g_nccl.send(theta, N, NCCL_FLOAT64, r - 1, ctx->ncomm, ctx->stream);
+            e |= g_nccl.recv(theta - N, N, NCCL_FLOAT64, r - 1, ctx->ncomm, ctx->stream);
         }
         if (r + 1 < ctx->nranks) {
-            e |= g_nccl.send(theta + (Ml - 1) * N, N, NCCL_FLOAT64, r + 1, ctx->comm, ctx->stream);
-            e |= g_nccl.recv(theta + Ml * N, N, NCCL_FLOAT64, r + 1, ctx->comm, ctx->stream);
+            e |= g_nccl.send(theta + (Ml - 1) * N, N, NCCL_FLOAT64, r + 1, ctx->ncomm, ctx->stream);
+            e |= g_nccl.recv(theta + Ml * N, N, NCCL_FLOAT64, r + 1, ctx->ncomm, ctx->stream);
         }
         e |= g_nccl.groupEnd();
         return cudaSuccess;
@@ -1425,7 +1627,7 @@ static qdt_status scalars(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, int fina
     const bool multi = ctx->nranks > 1;
     const int ke = final_eval ? 1 : c.kkt_every;
     CK(run_k(ctx, "scalars", 1, [&]() {
-        return launch_scalars2(b.partR, c.pl->nR, partT, ntiles, ctx->rank == 0, b.sc2_stage, b.sc2_arrive,
+        return launch_scalars2(b.partR, c.pl->nR, partT, ntiles, (ctx->rank == 0 || c.bx), b.sc2_stage, b.sc2_arrive,
                                b.vec, nvalid(c), c.p->M, c.gamma, c.tol, final_eval, ke, b.trace, b.kkt, b.kktp,
                                c.trace_len, b.state, multi ? 0 : 1, s);
     }));
@@ -1881,6 +2083,10 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
         return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: unknown step mode %d", opt.step);
     if (opt.step == QDT_STEP_BB && opt.accel)
         return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: the BB step is plain projected gradient (accel = 0)");
+    if (opt.exchange != 0 && opt.exchange != 1)
+        return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: exchange must be 0 (allreduce) or 1 (band-aware)");
+    if (opt.exchange == 1 && opt.step == QDT_STEP_BB)
+        return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: the BB step needs the full residual (exchange = 0)");
     if (opt.check_every < 1) opt.check_every = 16;
     if (opt.kkt_every < 1) opt.kkt_every = 1;
     const bool dev = opt.mem_device != 0;
@@ -1989,6 +2195,7 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     }
     IterCfg c{p, pl, (int)N, gamma, tol, fista, opt.kkt_every, tcap};
     c.Nv = (int)Nu;
+    c.bx = (ctx->nranks > 1 && opt.exchange == 1) ? 1 : 0;
     CKS(halo_exchange(ctx, c, b.theta[0]));
     if (pl->fz_on && !fista) CKS(fwd_reduce(ctx, c, b, b.theta[0], b.R[0], true));  // R_0
     if (fista && opt.theta_prev) {
@@ -2014,7 +2221,7 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
 
     // ---- the hot loop: graph of `period` iterations replayed
     const int period = fista ? 12 : 16;   // multiple of the buffer rotation (3 / 2)
-    const bool use_graph = opt.use_graph && !ctx->profiling && iters >= period;
+    const bool use_graph = opt.use_graph && !ctx->profiling && iters >= period && !ctx->vg;
     DevState hst;
     int64_t done = 0;
     bool stopped = false;
@@ -2038,6 +2245,7 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
         put(&c.bb, sizeof c.bb);
         put(&c.tlip, sizeof c.tlip);
         put(&c.Nv, sizeof c.Nv);
+        put(&c.bx, sizeof c.bx);
         put(&b, sizeof b);   // every device pointer the loop reads or writes (pointer-only struct)
         put(&period, sizeof period);
         put(&ctx->stream, sizeof ctx->stream);

@@ -299,6 +299,18 @@ size_t fwd_smem_bytes(int N, int RG, int KR);
 cudaError_t launch_reduce_R(const double *rpart, const int64_t *red_beg, const int64_t *red_rows,
                             const double *P, double *R, int64_t D, int N, double *partR,
                             int nblk, const DevState *st, cudaStream_t s);
+constexpr int VMAX = 16;        // ranks of an in-process (virtual) group
+struct VPtrs {
+    const double *p[VMAX];
+};
+cudaError_t launch_vsum(const VPtrs &v, int n_ranks, int64_t n, double *out, cudaStream_t s);
+struct BandX {                  // band-aware residual exchange tables (per rank of the group)
+    int64_t dlo[VMAX], dhi[VMAX];   // probes touching rank q's slice: [dlo[q], dhi[q])
+    const double *src[VMAX];        // peer q's partial rows (received copy), row start[q]
+    int64_t start[VMAX];
+};
+cudaError_t launch_band_combine(const BandX &bx, int rank, int nranks, const double *P, double *R, int N,
+                                double *partR, int nblk, const DevState *st, cudaStream_t s);
 cudaError_t launch_sub_p_sumsq(double *R, const double *P, int64_t n, double *partR, int nblk,
                                const DevState *st, cudaStream_t s);
 cudaError_t launch_scalars_local(const double *partR, int nblkR, const double *partT,

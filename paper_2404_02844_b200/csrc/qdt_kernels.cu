@@ -19,6 +19,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "qdt_internal.h"
 
 namespace qdt {
@@ -1166,6 +1168,68 @@ cudaError_t launch_reduce_R(const double *rpart, const int64_t *red_beg, const i
     k_reduce_R<<<nblk, 256, 0, s>>>(rpart, red_beg, red_rows, P, R, D, N, partR, st);
     return cudaGetLastError();
 }
+// ---- in-process collective (virtual ranks, SURVEY 4 "virtual shard"): out = sum of the ranks'
+// buffers in rank order (every rank computes the same sum in the same order: replicated results
+// are bitwise identical, as after an allreduce)
+__global__ void k_vsum(VPtrs v, int n_ranks, int64_t n, double *out)
+{
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        double s = v.p[0][e];
+        for (int r = 1; r < n_ranks; r++) s += v.p[r][e];
+        out[e] = s;
+    }
+}
+cudaError_t launch_vsum(const VPtrs &v, int n_ranks, int64_t n, double *out, cudaStream_t s)
+{
+    if (n <= 0) return cudaSuccess;
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, 4 * 148);
+    k_vsum<<<grid, 256, 0, s>>>(v, n_ranks, n, out);
+    return cudaGetLastError();
+}
+
+// ---- band-aware residual exchange: rank g touches the probes
+// [bx.dlo[g], bx.dhi[g]) (contiguous: band edges are monotone); probe d is summed over the ranks
+// S(d) = {q : dlo[q] <= d < dhi[q]} (contiguous) in rank order, its own partial from R and a
+// peer's from src[q] (rows from bx.start[q]); then P is subtracted.  ||R||^2 partials count each
+// probe once, on its owner min S(d).  Warp per probe; block partial to partR[blockIdx.x].
+__global__ void __launch_bounds__(256) k_band_combine(BandX bx, int rank, int nranks, const double *P, double *R,
+                                                      int N, double *partR, const DevState *st)
+{
+    __shared__ double red[8];
+    if (st && st->stop) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double ss = 0.0;
+    for (int64_t d = bx.dlo[rank] + (int64_t)blockIdx.x * 8 + warp; d < bx.dhi[rank]; d += (int64_t)gridDim.x * 8) {
+        int qa = rank, qb = rank;
+        while (qa > 0 && d >= bx.dlo[qa - 1] && d < bx.dhi[qa - 1]) qa--;
+        while (qb + 1 < nranks && d >= bx.dlo[qb + 1] && d < bx.dhi[qb + 1]) qb++;
+        const bool own = qa == rank;
+        for (int n = lane; n < N; n += 32) {
+            double v = 0.0;
+            for (int q = qa; q <= qb; q++)
+                v += (q == rank) ? R[d * N + n] : bx.src[q][(d - bx.start[q]) * N + n];
+            v -= P[d * N + n];
+            R[d * N + n] = v;
+            if (own) ss = fma(v, v, ss);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane == 0) red[warp] = ss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double v = 0.0;
+        for (int w = 0; w < 8; w++) v += red[w];
+        partR[blockIdx.x] = v;
+    }
+}
+cudaError_t launch_band_combine(const BandX &bx, int rank, int nranks, const double *P, double *R, int N,
+                                double *partR, int nblk, const DevState *st, cudaStream_t s)
+{
+    k_band_combine<<<nblk, 256, 0, s>>>(bx, rank, nranks, P, R, N, partR, st);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_sub_p_sumsq(double *R, const double *P, int64_t n, double *partR, int nblk,
                                const DevState *st, cudaStream_t s)
 {
