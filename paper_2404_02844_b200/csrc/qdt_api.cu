@@ -1399,6 +1399,7 @@ struct SolveBufs {
     double *partS = nullptr;   // fused sweep: heavy-tile slots [0, tsplit) + CTA slots
     double *bb_part = nullptr, *bb_vec = nullptr, *tbb = nullptr;  // BB step statistics / scalar
     double *Gw = nullptr;      // wide-N sweep: Ml x N gradient
+    double *tau_prev = nullptr;  // fused wide step: per-row threshold of the last step (warm start)
 };
 
 struct IterCfg {
@@ -1739,6 +1740,7 @@ static WStepArgs wstep_args(const IterCfg &c, SolveBufs &b, const double *R, con
     w.tstep = b.tstep;
     w.tscal = nullptr;
     w.gamma = c.gamma;
+    w.tau_prev = b.tau_prev;
     w.part = b.partT;
     w.kkt_every = c.kkt_every;
     w.eval = 0;
@@ -1969,6 +1971,10 @@ static qdt_status common_bufs(qdt_ctx *ctx, qdt_probes *p, Plan *pl, int64_t N, 
     const int nt = std::max(1, std::max({pl->ntiles, p->sw_ntiles * (pl->NW ? ncc : 1) + (int)((p->Ml + 7) / 8),
                                          pl->wx_ncl * pl->wx_C}));
     if (pl->NW) CKS(ws_get(ctx, "Gw", p->Ml * N + 4, &b.Gw));
+    if (pl->NX) {
+        CKS(ws_get(ctx, "tau_prev", p->Ml, &b.tau_prev));
+        CK(cudaMemsetAsync(b.tau_prev, 0xff, sizeof(double) * p->Ml, s));   // NaN: no warm start yet
+    }
     CKS(ws_get(ctx, "partT", (size_t)nt * NSC_TILE, &b.partT));
     CK(cudaMemsetAsync(b.partT, 0, sizeof(double) * nt * NSC_TILE, s));
     CKS(ws_get(ctx, "vec", NV, &b.vec));

@@ -215,6 +215,7 @@ struct WStepArgs {
     const double *tstep;
     const double *tscal;        // one device scalar step (nullptr: tstep per row)
     double gamma;
+    double *tau_prev;           // per local row: the last step's threshold (warm start), or nullptr
     double *part;               // [grid x NSC_TILE] scalar partials
     int kkt_every;
     int eval, eval_gate;

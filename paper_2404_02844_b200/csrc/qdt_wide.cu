@@ -39,18 +39,53 @@ __device__ __forceinline__ void fence_proxy_async_smem()
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// staged Theta tile row pitch: = 8 mod 16 doubles (conflict-free 16-byte reads of 8 rows)
+__host__ __device__ inline int wide_theta_pitch(int Wc) { return (Wc % 16 == 8) ? Wc : Wc + 8; }
+
 size_t wide_step_smem(int Wc)
 {
-    return (size_t)WSTAGES * WKC * ((Wc + 4) + WFP) * sizeof(double);
+    const size_t ring = (size_t)WSTAGES * WKC * ((Wc + 4) + WFP);
+    const size_t tile = (size_t)(WT + 2) * wide_theta_pitch(Wc);
+    return std::max(ring, tile) * sizeof(double);
+}
+
+// combination of row partials by value kind: 0 min (G), 1 sum, 2 max, 3 min, 4 sum, 5 sum, 6 min
+__device__ __forceinline__ double wcombine(int v, double x, double y)
+{
+    switch (v) {
+        case 0:
+        case 3:
+        case 6: return fmin(x, y);
+        case 2: return fmax(x, y);
+        default: return x + y;
+    }
+}
+// the cluster total of one (row, value) slot: the C CTAs' values combined in CTA order (all
+// loads issued before the combination)
+__device__ __forceinline__ double cluster_total(const double *slot, int v, int C)
+{
+    if (C == 1) return *slot;
+    double x = 0.0;
+    for (int q0 = 0; q0 < C; q0 += 4) {            // four remote loads in flight, combined in CTA order
+        double r[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) r[k] = q0 + k < C ? ld_dsmem(slot, q0 + k) : 0.0;
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+            if (q0 + k < C) x = (q0 + k == 0) ? r[k] : wcombine(v, x, r[k]);
+    }
+    return x;
 }
 
 template <int NBW, bool FIS>
 __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ WStepArgs a)
 {
     extern __shared__ __align__(128) double sm[];
-    __shared__ __align__(8) uint64_t bars[WSTAGES];
-    __shared__ double rowp[WT][8][4];   // per row and n-group warp: quad-reduced partials
-    __shared__ double xb[2][WT][4];     // exchange slots (read by the cluster peers)
+    __shared__ __align__(8) uint64_t bars[WSTAGES + 1];   // chunk ring + the Theta tile
+    __shared__ double rowp[WT][8][8];   // per row and n-group warp: quad-reduced partials
+    __shared__ double xb[2][WT][8];     // exchange slots (read by the cluster peers)
+    __shared__ double comb[8][WT];      // cluster totals per value and row
+    __shared__ double ttry[WT];         // warm-start trial threshold per row (-inf: none)
     __shared__ double trow[WT][3];      // per row: tau, lambda (unclamped), lambda (clamped)
     __shared__ int tcnt[WT];            // per row: |A| of the last Michelot round
     __shared__ int tdone[WT];
@@ -71,38 +106,30 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
     const int cbase = crank * a.Wc;
     const int ncol = min(a.Wc, N - cbase);         // even (N even), > 0 (planner)
     const int Pr = a.Wc + 4;                       // staged R row pitch: = 4 mod 16 doubles
+    const int Pt = wide_theta_pitch(a.Wc);         // staged Theta row pitch: = 8 mod 16 doubles
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
     const int mp = warp & 1, ng = warp >> 1;
     double *Rs = sm;                               // WSTAGES x WKC x Pr
     double *Fs = sm + WSTAGES * WKC * Pr;          // WSTAGES x WKC x WFP
+    double *Ts = sm;                               // the Theta tile (rows k0 - 1 .. k0 + 32) reuses the ring
     const int ta = a.trange[cid], tb = a.trange[cid + 1];
 
     // zero the stages once: a masked tail k-step then multiplies stale but finite values by 0
     for (int i = tid; i < WSTAGES * WKC * (Pr + WFP); i += W_THREADS) sm[i] = 0.0;
     if (tid == 0) {
-        for (int s = 0; s < WSTAGES; s++) mbar_init(&bars[s], 1);
+        for (int s = 0; s <= WSTAGES; s++) mbar_init(&bars[s], 1);
         fence_barrier_init();
     }
     fence_proxy_async_smem();
     __syncthreads();
 
-    // ---- producer (warp 0): the chunk stream of the cluster's tile range, WSTAGES ahead
-    int pt = ta, pc = 0;                           // next chunk to issue: tile, chunk
-    uint32_t issued = 0, used = 0;
-    auto nchunks = [&](int tt) {
-        const int t64 = tt >> 1;
-        return (a.tile_dB[t64] - a.tile_dA[t64] + WKC - 1) / WKC;
-    };
-    auto issue_next = [&]() {                      // warp 0, all lanes
-        while (pt < tb && pc >= nchunks(pt)) {
-            pt++;
-            pc = 0;
-        }
-        if (pt >= tb) return;
-        const int t64 = pt >> 1, half = pt & 1;
+    // ---- producer (warp 0): chunk c of tile tt into the ring slot of the running chunk count
+    uint32_t issued = 0, used = 0, tuse = 0;
+    auto issue_chunk = [&](int tt, int c) {        // warp 0, all lanes
+        const int t64 = tt >> 1, half = tt & 1;
         const int dA = a.tile_dA[t64], W = a.tile_dB[t64] - dA;
-        const int p0 = pc * WKC, kc = min(WKC, W - p0);
+        const int p0 = c * WKC, kc = min(WKC, W - p0);
         const int stg = issued % WSTAGES;
         uint64_t *bar = &bars[stg];
         if (lane == 0) mbar_expect_tx(bar, (uint32_t)kc * (WFP + ncol) * 8u);
@@ -114,10 +141,16 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
                      bar);
         }
         issued++;
-        pc++;
     };
-    if (warp == 0)
-        for (int s = 0; s < WSTAGES; s++) issue_next();
+    auto nchunks = [&](int tt) {
+        const int t64 = tt >> 1;
+        return (a.tile_dB[t64] - a.tile_dA[t64] + WKC - 1) / WKC;
+    };
+    auto start_tile = [&](int tt) {                // warp 0: the first ring's worth of a tile's chunks
+        const int n = min(WSTAGES, nchunks(tt));
+        for (int c = 0; c < n; c++) issue_chunk(tt, c);
+    };
+    if (warp == 0 && ta < tb) start_tile(ta);
 
     double sreg = 0.0, skkt = 0.0, skktp = 0.0;    // per-thread running partials (fixed order)
     int slot = 0;
@@ -143,6 +176,14 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
                 bulk_prefetch_l2(a.theta + (int64_t)(k0 - 1 + r) * N + cbase, (uint32_t)ncol * 8u);
                 if (fis) bulk_prefetch_l2(a.theta_prev + (int64_t)(k0 - 1 + r) * N + cbase, (uint32_t)ncol * 8u);
             }
+        }
+        if (tid < WT) {   // warm start: the row's previous threshold, lowered a little (a trial lower bound)
+            double tr = -INFINITY;
+            if (!ev && a.tau_prev && tid < Tt) {
+                const double tp = a.tau_prev[k0 + tid];
+                if (isfinite(tp)) tr = tp - 0x1p-10 * fmax(fabs(tp), 1e-300);
+            }
+            ttry[tid] = tr;
         }
         double acc[2][NBW][2];
 #pragma unroll
@@ -172,12 +213,31 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
                 }
             }
             __syncthreads();                       // stage consumed
-            if (warp == 0) issue_next();
+            if (warp == 0 && c + WSTAGES < nch) issue_chunk(tt, c + WSTAGES);
+        }
+        // the ring is drained: the Theta tile (rows k0 - 1 .. k0 + Tt) lands in its space (plain
+        // steps and evaluation passes; the FISTA step reads Theta_k / Theta_{k-1} through L2)
+        if (!fis && warp == 0) {
+            uint64_t *bar = &bars[WSTAGES];
+            if (lane == 0) mbar_expect_tx(bar, (uint32_t)(Tt + 2) * ncol * 8u);
+            __syncwarp();
+            for (int r = lane; r < Tt + 2; r += 32)
+                bulk_g2s(Ts + r * Pt, a.theta + (int64_t)(k0 - 1 + r) * N + cbase, (uint32_t)ncol * 8u, bar);
+        }
+        if (warp == 2 && tt + 1 < tb) {            // next tile's first chunks -> L2 during the epilogue
+            const int t1 = (tt + 1) >> 1;
+            const int n1 = min(WSTAGES * WKC, a.tile_dB[t1] - a.tile_dA[t1]);
+            for (int r = lane; r < n1; r += 32)
+                bulk_prefetch_l2(a.R + (int64_t)(a.tile_dA[t1] + r) * N + cbase, (uint32_t)ncol * 8u);
+        }
+        if (!fis) {
+            mbar_wait(&bars[WSTAGES], tuse & 1);
+            tuse++;
         }
 
         // ---- S4 + pass 1: G = acc + gamma L Y; row min of G, sum / max / min of X = Y - t G
         double tk[2];
-        double pmn[2], ps[2], pxm[2], pxn[2];
+        double pmn[2], ps[2], pxm[2], pxn[2], pts[2], ptc[2], ptm[2];
 #pragma unroll
         for (int i = 0; i < 2; i++) {
             const int rl = 16 * mp + 8 * i + g;
@@ -186,17 +246,28 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
             const int64_t kg = a.kb + kl;
             const bool hp = kg > 0, hn = kg + 1 < a.M;
             tk[i] = act ? (a.tscal ? *a.tscal : __ldg(a.tstep + kl)) : 0.0;
+            const double tau_t = ttry[rl];
             double mn = INFINITY, s = 0.0, xm = -INFINITY, xn = INFINITY;
+            double ts = 0.0, tm = INFINITY;
+            int tc = 0;
             if (act) {
-                const double *th = a.theta + (int64_t)kl * N + cbase;
+                const double *thg = a.theta + (int64_t)kl * N + cbase;
+                const double *ths = Ts + (rl + 1) * Pt;
                 const double *tq = fis ? a.theta_prev + (int64_t)kl * N + cbase : nullptr;
 #pragma unroll
                 for (int j = 0; j < NBW; j++) {
                     const int lc = 8 * (ng * NBW + j) + 2 * t;
                     if (lc < ncol) {
-                        const double2 x = __ldg(reinterpret_cast<const double2 *>(th + lc));
-                        const double2 y = hp ? __ldg(reinterpret_cast<const double2 *>(th + lc - N)) : x;
-                        const double2 z = hn ? __ldg(reinterpret_cast<const double2 *>(th + lc + N)) : x;
+                        double2 x, y, z;
+                        if (fis) {
+                            x = __ldg(reinterpret_cast<const double2 *>(thg + lc));
+                            y = hp ? __ldg(reinterpret_cast<const double2 *>(thg + lc - N)) : x;
+                            z = hn ? __ldg(reinterpret_cast<const double2 *>(thg + lc + N)) : x;
+                        } else {
+                            x = *reinterpret_cast<const double2 *>(ths + lc);
+                            y = hp ? *reinterpret_cast<const double2 *>(ths + lc - Pt) : x;
+                            z = hn ? *reinterpret_cast<const double2 *>(ths + lc + Pt) : x;
+                        }
                         double y0[2] = {x.x, x.y}, yp[2] = {y.x, y.y}, yn[2] = {z.x, z.y};
                         const double d20 = x.x - z.x, d21 = x.y - z.y;   // regulariser pair of Theta_k
                         const bool v0 = cbase + lc < Nv, v1 = cbase + lc + 1 < Nv;
@@ -222,6 +293,11 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
                                 s += xv;
                                 xm = fmax(xm, xv);
                                 xn = fmin(xn, xv);
+                                if (xv > tau_t) {   // first Michelot round at the trial threshold
+                                    ts += xv;
+                                    tc++;
+                                    tm = fmin(tm, xv);
+                                }
                             }
                         }
                     }
@@ -231,50 +307,57 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
             ps[i] = quad_sum(s);
             pxm[i] = quad_max(xm);
             pxn[i] = quad_min(xn);
+            pts[i] = quad_sum(ts);
+            ptc[i] = (double)quad_sum_i(tc);
+            ptm[i] = quad_min(tm);
         }
         if (t == 0) {
 #pragma unroll
             for (int i = 0; i < 2; i++) {
                 double *rp = rowp[16 * mp + 8 * i + g][ng];
                 rp[0] = pmn[i], rp[1] = ps[i], rp[2] = pxm[i], rp[3] = pxn[i];
+                rp[4] = pts[i], rp[5] = ptc[i], rp[6] = ptm[i];
             }
         }
         __syncthreads();
-        if (tid < WT) {                            // CTA partial of row tid (n-group order)
-            double mn = INFINITY, s = 0.0, xm = -INFINITY, xn = INFINITY;
-            for (int w = 0; w < 8; w++) {
-                mn = fmin(mn, rowp[tid][w][0]);
-                s += rowp[tid][w][1];
-                xm = fmax(xm, rowp[tid][w][2]);
-                xn = fmin(xn, rowp[tid][w][3]);
-            }
-            xb[slot][tid][0] = mn, xb[slot][tid][1] = s, xb[slot][tid][2] = xm, xb[slot][tid][3] = xn;
+        if (tid < 7 * WT) {                        // CTA partial of (row, value) (n-group order)
+            const int row = tid & (WT - 1), v = tid >> 5;
+            double x = rowp[row][0][v];
+            for (int w = 1; w < 8; w++) x = wcombine(v, x, rowp[row][w][v]);
+            xb[slot][row][v] = x;
         }
         exchange();
-        if (tid < WT) {                            // cluster totals (CTA order) -> lambda, tau_0
-            double mn = INFINITY, s = 0.0, xm = -INFINITY, xn = INFINITY;
-            for (int r = 0; r < C; r++) {
-                const double *x4 = xb[slot][tid];
-                const double v0 = C > 1 ? ld_dsmem(x4 + 0, r) : x4[0];
-                const double v1 = C > 1 ? ld_dsmem(x4 + 1, r) : x4[1];
-                const double v2 = C > 1 ? ld_dsmem(x4 + 2, r) : x4[2];
-                const double v3 = C > 1 ? ld_dsmem(x4 + 3, r) : x4[3];
-                mn = fmin(mn, v0);
-                s += v1;
-                xm = fmax(xm, v2);
-                xn = fmin(xn, v3);
-            }
+        if (tid < 7 * WT) {                        // cluster total of (row, value) in CTA order
+            const int row = tid & (WT - 1), v = tid >> 5;
+            comb[v][row] = cluster_total(&xb[slot][row][v], v, C);
+        }
+        __syncthreads();
+        if (tid < WT) {                            // lambda, tau_0, warm-started first round
+            const double mn = comb[0][tid], s = comb[1][tid], xm = comb[2][tid], xn = comb[3][tid];
             const double lam = -2.0 * mn;
             trow[tid][1] = lam;
             trow[tid][2] = fmax(lam, 0.0);
             // tau_0 = (sum X - 1) / N is exact when every entry stays active; otherwise Michelot
-            // from the lower bound max(tau_0, max X - 1) (reading R4)
+            // from a lower bound (reading R4): the trial threshold when phi(tau_try) =
+            // sum_{x > tau_try} (x - tau_try) >= 1 proves it one (its round is then already
+            // done), else max(tau_0, max X - 1)
             double tau = (s - 1.0) / (double)Nv;
             bool done = tid >= Tt || xn > tau;
-            if (!done) tau = fmax(tau, xm - 1.0);
+            int cnt = Nv + 1;
+            if (!done) {
+                const double tt_ = ttry[tid], st_ = comb[4][tid], mt_ = comb[6][tid];
+                const int ct_ = (int)comb[5][tid];
+                if (ct_ > 0 && st_ - (double)ct_ * tt_ >= 1.0) {
+                    cnt = ct_;
+                    tau = (st_ - 1.0) / (double)ct_;
+                    done = mt_ > tau;
+                } else {
+                    tau = fmax(tau, xm - 1.0);
+                }
+            }
             trow[tid][0] = tau;
             tdone[tid] = done ? 1 : 0;
-            tcnt[tid] = Nv + 1;
+            tcnt[tid] = cnt;
             const unsigned all = __ballot_sync(0xffffffffu, done);
             if (tid == 0) s_alldone = (all == 0xffffffffu);
         }
@@ -288,14 +371,15 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
             const int kl = k0 + rl;
             const bool act = rl < Tt;
             const double lam = trow[rl][1], lamp = trow[rl][2];
-            const double *th = a.theta + (int64_t)kl * N + cbase;
+            const double *thg = a.theta + (int64_t)kl * N + cbase;
+            const double *ths = Ts + (rl + 1) * Pt;
             const double *tq = fis ? a.theta_prev + (int64_t)kl * N + cbase : nullptr;
 #pragma unroll
             for (int j = 0; j < NBW; j++) {
                 const int lc = 8 * (ng * NBW + j) + 2 * t;
                 const bool in = act && lc < ncol;
                 double2 x = make_double2(0.0, 0.0);
-                if (in) x = __ldg(reinterpret_cast<const double2 *>(th + lc));
+                if (in) x = fis ? __ldg(reinterpret_cast<const double2 *>(thg + lc)) : *reinterpret_cast<const double2 *>(ths + lc);
                 double y0[2] = {x.x, x.y};
                 if (fis && in) {
                     const double2 xq = __ldg(reinterpret_cast<const double2 *>(tq + lc));
@@ -318,6 +402,10 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
                 }
             }
         }
+        // the Theta tile is consumed: the next tile's chunks may refill the ring now, under the
+        // Michelot rounds and the stores of this one
+        __syncthreads();
+        if (warp == 0 && tt + 1 < tb) start_tile(tt + 1);
         if (ev) continue;                          // evaluation pass: no step
 
         // ---- S5: Michelot rounds, all rows of the tile in lockstep over the cluster
@@ -354,24 +442,21 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
                 }
             }
             __syncthreads();
-            if (tid < WT) {
-                double s = 0.0, cnt = 0.0, mA = INFINITY;
-                for (int w = 0; w < 8; w++) {
-                    s += rowp[tid][w][0];
-                    cnt += rowp[tid][w][1];
-                    mA = fmin(mA, rowp[tid][w][2]);
-                }
-                xb[slot][tid][0] = s, xb[slot][tid][1] = cnt, xb[slot][tid][2] = mA;
+            if (tid < 3 * WT) {
+                const int row = tid & (WT - 1), v = tid >> 5;   // 0: sum, 1: count (sums), 2: min
+                const int op = v == 2 ? 3 : 1;
+                double x = rowp[row][0][v];
+                for (int w = 1; w < 8; w++) x = wcombine(op, x, rowp[row][w][v]);
+                xb[slot][row][v] = x;
             }
             exchange();
+            if (tid < 3 * WT) {
+                const int row = tid & (WT - 1), v = tid >> 5;
+                comb[v][row] = cluster_total(&xb[slot][row][v], v == 2 ? 3 : 1, C);
+            }
+            __syncthreads();
             if (tid < WT) {
-                double s = 0.0, cntd = 0.0, mA = INFINITY;
-                for (int r = 0; r < C; r++) {
-                    const double *x4 = xb[slot][tid];
-                    s += C > 1 ? ld_dsmem(x4 + 0, r) : x4[0];
-                    cntd += C > 1 ? ld_dsmem(x4 + 1, r) : x4[1];
-                    mA = fmin(mA, C > 1 ? ld_dsmem(x4 + 2, r) : x4[2]);
-                }
+                const double s = comb[0][tid], cntd = comb[1][tid], mA = comb[2][tid];
                 bool done = tdone[tid] != 0;
                 if (!done) {
                     const int cnt = (int)cntd;
@@ -392,6 +477,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
             slot ^= 1;
         }
         // ---- Theta_{k+1} = max(X - tau, 0), stored from registers
+        if (a.tau_prev && tid < Tt && crank == 0) a.tau_prev[k0 + tid] = trow[tid][0];
 #pragma unroll
         for (int i = 0; i < 2; i++) {
             const int rl = 16 * mp + 8 * i + g;
@@ -468,7 +554,7 @@ cudaError_t prepare_wide_kernels()
     const uint64_t bit = dev < 64 ? (1ull << dev) : 0;
     if (done_mask & bit) return cudaSuccess;
     cudaError_t e = cudaSuccess;
-    const int smax = (int)wide_step_smem(8 * 8 * W_NBW_MAX);
+    const int smax = (int)std::max(wide_step_smem(8 * 8 * W_NBW_MAX), wide_step_smem(8 * 8 * W_NBW_MAX - 8));
 #define QDT_PREP1(n, f)                                                                                        \
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_wstep<n, f>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax); \
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_wstep<n, f>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
