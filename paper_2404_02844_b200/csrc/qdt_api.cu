@@ -145,7 +145,7 @@ struct Plan {
     // fused wide step (N > 128, even pitch): clusters of wx_C CTAs x wx_Wc columns per 32-row tile
     int NX = 0;
     int wx_C = 1, wx_Wc = 0, wx_ncl = 0;
-    int32_t *d_wx_trange = nullptr;
+    int32_t *d_wx_tlist = nullptr, *d_wx_toff = nullptr;
     bool gen = true;                  // general (CUDA-core) plan built (N <= 1024)
     int nR = 0;                       // partR entries written by the residual reduction
     int sw_nbunits = 0;
@@ -169,7 +169,8 @@ struct Plan {
     int64_t *d_fz_red_beg = nullptr, *d_fz_red_rows = nullptr;
     ~Plan()
     {
-        cudaFree(d_wx_trange);
+        cudaFree(d_wx_tlist);
+        cudaFree(d_wx_toff);
         cudaFree(d_fz_range);
         cudaFree(d_fz_poff);
         cudaFree(d_fz_bunits);
@@ -214,9 +215,12 @@ struct qdt_probes {
     int32_t *d_sw_dA = nullptr, *d_sw_dB = nullptr;
     int64_t *d_fb_off = nullptr;
     double *d_Fb = nullptr;
+    int32_t *d_row_da = nullptr, *d_row_db = nullptr;   // probes covering each local row (small solve)
     Band band() const { return Band{d_lo, d_len, d_off, d_val}; }
     ~qdt_probes()
     {
+        cudaFree(d_row_da);
+        cudaFree(d_row_db);
         cudaFree(d_sw_dA);
         cudaFree(d_sw_dB);
         cudaFree(d_fb_off);
@@ -661,8 +665,9 @@ static bool sweep_enabled()
 //    consecutive probes over the tiles their bands touch (<= FW_MAXT tiles per unit), so that a
 //    probe gets one partial row per group unit instead of one per tile.
 template <class Emit>
-static void plan_fwd_units(const qdt_probes *p, int t0, int t1, Emit &&emit)
+static void plan_fwd_units(const qdt_probes *p, int t0, int t1, Emit &&emit, int maxt = FW_MAXT)
 {
+    const int FW_MAXT = maxt;   // tiles per unit (fewer on small problems: more units for the SMs)
     const std::vector<int32_t> &dA = p->sw_dA, &dB = p->sw_dB;
     int t = t0;
     while (t < t1) {
@@ -800,11 +805,21 @@ static qdt_status build_sweep_plan(qdt_ctx *ctx, qdt_probes *p, Plan *pl)
     CKS(build_sweep_tiling(ctx, p));
     const int nt = p->sw_ntiles;
     const int64_t D = p->D;
+    const int nsm = device_sm_count();
+    // split cap of the bwd units: SWCAP, halved (down to 32 probes) while the tiles give fewer
+    // than 2 units per SM (small problems such as Medium: 16 tiles of wide windows)
+    int cap = SWCAP;
+    for (;;) {
+        int64_t nu = 0;
+        for (int t = 0; t < nt; t++) nu += std::max(1, (p->sw_dB[t] - p->sw_dA[t] + cap - 1) / cap);
+        if (nu >= 2 * nsm || cap <= 2 * SKC) break;
+        cap /= 2;
+    }
     std::vector<SwUnit> bu;
     int64_t slot = 0;
     for (int t = 0; t < nt; t++) {
         const int dA = p->sw_dA[t], W = p->sw_dB[t] - dA;
-        const int ns = std::max(1, (W + SWCAP - 1) / SWCAP);
+        const int ns = std::max(1, (W + cap - 1) / cap);
         int chunk = ns > 1 ? (W + ns - 1) / ns : W;
         if (ns > 1) chunk = ((chunk + SKC - 1) / SKC) * SKC;
         for (int s = 0; s < ns; s++) {
@@ -840,7 +855,15 @@ static qdt_status build_sweep_plan(qdt_ctx *ctx, qdt_probes *p, Plan *pl)
         for (int d = u0; d < u1; d++) lists[d].push_back(poff + (d - u0));
         poff += u1 - u0;
     };
-    plan_fwd_units(p, 0, nt, emit);
+    // tiles per fwd unit: FW_MAXT, halved while the plan gives fewer than 2 units per SM
+    int maxt = FW_MAXT;
+    for (;;) {
+        int64_t nu = 0;
+        plan_fwd_units(p, 0, nt, [&](int, int, int u0, int u1) { nu += u1 > u0; }, maxt);
+        if (nu >= 2 * nsm || maxt <= 1) break;
+        maxt /= 2;
+    }
+    plan_fwd_units(p, 0, nt, emit, maxt);
     pl->sw_nrpart = poff;
     std::vector<int64_t> red_beg(D + 1, 0), red_rows;
     for (int64_t d = 0; d < D; d++) red_beg[d + 1] = red_beg[d] + (int64_t)lists[d].size();
@@ -865,32 +888,37 @@ static qdt_status build_sweep_plan(qdt_ctx *ctx, qdt_probes *p, Plan *pl)
     return build_fused_plan(ctx, p, pl, bu);
 }
 
-// QDT_WIDE=old: N > 128 on the two-kernel wide sweep (k_grad_wide + k_proj_wide, N <= 1024)
-// instead of the fused cluster step (A/B measurement)
-static bool wide_old_forced()
+// 128 < N <= 1024 runs the two-kernel wide sweep (k_grad_wide + k_proj_wide: measured faster there,
+// profiles/r02_v2); QDT_WIDE=new selects the fused cluster step for them too (A/B, tests).  N > 1024
+// always takes the fused step.
+// QDT_SMALL=0 keeps small problems on the multi-kernel loop (A/B)
+static bool small_enabled()
 {
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("QDT_WIDE");
-        v = (e && !strcmp(e, "old")) ? 1 : 0;
-    }
-    return v == 1;
+    const char *e = getenv("QDT_SMALL");
+    return !(e && e[0] == '0');
+}
+
+static bool wide_new_forced()
+{
+    const char *e = getenv("QDT_WIDE");   // read at every plan build (plans are cached per probe handle and N)
+    return e && !strcmp(e, "new");
 }
 
 // Fused wide step (qdt_wide.cu): C CTAs per cluster, Wc columns each (multiple of 8, <= 640), the
-// 32-row tiles of the slice split over the co-resident clusters in contiguous ranges of equal cost
-// (window probes + a fixed epilogue share per tile).  C: the fewest CTAs with Wc <= 640, raised
-// while the slice has at least ~6 tiles per cluster and the per-CTA chunk stays >= 128 columns,
-// so that small-M / wide-N problems still fill the GPU.
+// 16-row tiles of the slice list-scheduled over the co-resident clusters: tiles in Fock order, each
+// to the cluster whose work so far is least (cost = window probes + a fixed epilogue share), so
+// that every cluster's list is in Fock order and the clusters sweep the axis together (the R rows
+// of the moving window are shared in L2).  C: the fewest CTAs with Wc <= 640, raised while the
+// slice has few tiles per cluster and the per-CTA chunk stays >= 128 columns.
 static qdt_status build_wide_plan(qdt_ctx *ctx, qdt_probes *p, Plan *pl)
 {
     const int N = pl->N;
     const int nbt = (N + 7) / 8;                                   // n-blocks of the row
     const int ntw = (int)((p->Ml + WT - 1) / WT);
     auto wc_of = [&](int C) { return 8 * ((nbt + C - 1) / C); };
-    int C = (nbt + 8 * W_NBW_MAX - 1) / (8 * W_NBW_MAX);
-    if (C > W_CMAX) return fail(ctx, QDT_ERR_INVALID_ARG, "N = %d exceeds the fused wide step (max %d)", N,
-                                W_CMAX * 64 * W_NBW_MAX);
+    const int wmax = 8 * W_NG * W_NBW_MAX;                          // 640 columns per CTA
+    int C = (N + wmax - 1) / wmax;
+    if (C > W_CMAX) return fail(ctx, QDT_ERR_INVALID_ARG, "N = %d exceeds the fused wide step (max %d)", N, W_CMAX * wmax);
     const int nsm = device_sm_count();
     while (C < W_CMAX && wc_of(C + 1) >= 128 && (int64_t)ntw < 6LL * (nsm / C)) C++;
     while (C > 1 && (int64_t)(C - 1) * wc_of(C) >= N) C--;           // every CTA owns >= 1 column pair
@@ -898,23 +926,34 @@ static qdt_status build_wide_plan(qdt_ctx *ctx, qdt_probes *p, Plan *pl)
     int ncl = wide_max_clusters(C, Wc);
     if (ncl <= 0) return fail(ctx, QDT_ERR_CUDA, "fused wide step: no co-resident cluster of %d CTAs", C);
     ncl = std::min(ncl, std::max(1, ntw));
-    std::vector<int64_t> cost(ntw + 1, 0);
+    // list scheduling in Fock order (min-heap of (work, cluster))
+    const int64_t E = 48;   // epilogue share of a tile, in window probes (measured order of magnitude)
+    std::vector<std::vector<int32_t>> lists(ncl);
+    std::vector<std::pair<int64_t, int>> heap;
+    for (int c = 0; c < ncl; c++) heap.push_back({0, c});
+    auto cmp = [](const std::pair<int64_t, int> &x, const std::pair<int64_t, int> &y) { return x > y; };
+    std::make_heap(heap.begin(), heap.end(), cmp);
     for (int tt = 0; tt < ntw; tt++) {
-        const int t64 = tt >> 1;
-        cost[tt + 1] = cost[tt] + (p->sw_dB[t64] - p->sw_dA[t64]) + 16;
+        const int t64 = tt >> 2;
+        std::pop_heap(heap.begin(), heap.end(), cmp);
+        auto &h = heap.back();
+        lists[h.second].push_back(tt);
+        h.first += (p->sw_dB[t64] - p->sw_dA[t64]) + E;
+        std::push_heap(heap.begin(), heap.end(), cmp);
     }
-    std::vector<int32_t> tr(ncl + 1, 0);
-    for (int c = 1; c < ncl; c++) {
-        const int64_t target = cost[ntw] * c / ncl;
-        tr[c] = (int32_t)(std::lower_bound(cost.begin(), cost.end(), target) - cost.begin());
-        tr[c] = std::max(tr[c], tr[c - 1]);
+    std::vector<int32_t> tl, off(ncl + 1, 0);
+    tl.reserve(ntw);
+    for (int c = 0; c < ncl; c++) {
+        tl.insert(tl.end(), lists[c].begin(), lists[c].end());
+        off[c + 1] = (int32_t)tl.size();
     }
-    tr[ncl] = ntw;
     pl->wx_C = C;
     pl->wx_Wc = Wc;
     pl->wx_ncl = ncl;
-    CK(cudaMalloc(&pl->d_wx_trange, sizeof(int32_t) * (ncl + 1)));
-    CK(cudaMemcpy(pl->d_wx_trange, tr.data(), sizeof(int32_t) * (ncl + 1), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&pl->d_wx_tlist, sizeof(int32_t) * std::max<size_t>(1, tl.size())));
+    CK(cudaMalloc(&pl->d_wx_toff, sizeof(int32_t) * (ncl + 1)));
+    if (!tl.empty()) CK(cudaMemcpy(pl->d_wx_tlist, tl.data(), sizeof(int32_t) * tl.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(pl->d_wx_toff, off.data(), sizeof(int32_t) * (ncl + 1), cudaMemcpyHostToDevice));
     return QDT_OK;
 }
 
@@ -1071,7 +1110,7 @@ static qdt_status build_plan(qdt_ctx *ctx, qdt_probes *p, int N, Plan **out)
     pl->NB = sweep_enabled() ? sweep_nb(N) : 0;
     // wide kernels for N > 128 (even): the whole path, or (N <= 160) beside the NB > 16 plain step
     const bool wide = sweep_enabled() && (!pl->NB || pl->NB > SW_NBMAX) && N % 2 == 0;
-    pl->NX = (wide && !wide_old_forced()) ? 1 : 0;
+    pl->NX = (wide && wide_new_forced()) ? 1 : 0;   // N <= 1024: the two-kernel wide sweep by default
     pl->NW = (wide && !pl->NX && N <= 1024) ? 1 : 0;
     if (pl->NB || pl->NW || pl->NX) CKS(build_sweep_plan(ctx, p, pl.get()));
     if (pl->NX) CKS(build_wide_plan(ctx, p, pl.get()));
@@ -1727,7 +1766,8 @@ static WStepArgs wstep_args(const IterCfg &c, SolveBufs &b, const double *R, con
     w.Wc = c.pl->wx_Wc;
     w.kb = c.p->kb;
     w.M = c.p->M;
-    w.trange = c.pl->d_wx_trange;
+    w.tlist = c.pl->d_wx_tlist;
+    w.toff = c.pl->d_wx_toff;
     w.fb_off = c.p->d_fb_off;
     w.tile_dA = c.p->d_sw_dA;
     w.tile_dB = c.p->d_sw_dB;
@@ -2225,9 +2265,28 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     st0.iters_done = -1;
     CK(cudaMemcpyAsync(b.state, &st0, sizeof st0, cudaMemcpyHostToDevice, s));
 
+    // ---- small problems: the whole solve in one persistent CTA (qdt_small.cu)
+    const bool small = ctx->nranks == 1 && !bb && small_enabled() &&
+                       small_solve_smem(D, Ml, (int)N, p->nnz, fista) <= SMALL_SMEM_MAX && D * N < (1LL << 30);
+    if (small && !p->d_row_da) {
+        std::vector<int32_t> da(Ml, 0), db(Ml, 0);
+        int64_t a0 = 0;
+        for (int64_t k = 0; k < Ml; k++) {   // band edges are monotone: contiguous covering probes
+            while (a0 < D && (p->len_l[a0] == 0 || p->lo_l[a0] + p->len_l[a0] - 1 - p->kb < k)) a0++;
+            int64_t b0 = a0;
+            while (b0 < D && p->lo_l[b0] - p->kb <= k && p->len_l[b0] > 0) b0++;
+            da[k] = (int32_t)a0;
+            db[k] = (int32_t)b0;
+        }
+        CK(cudaMalloc(&p->d_row_da, sizeof(int32_t) * Ml));
+        CK(cudaMalloc(&p->d_row_db, sizeof(int32_t) * Ml));
+        CK(cudaMemcpy(p->d_row_da, da.data(), sizeof(int32_t) * Ml, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(p->d_row_db, db.data(), sizeof(int32_t) * Ml, cudaMemcpyHostToDevice));
+    }
+
     // ---- the hot loop: graph of `period` iterations replayed
     const int period = fista ? 12 : 16;   // multiple of the buffer rotation (3 / 2)
-    const bool use_graph = opt.use_graph && !ctx->profiling && iters >= period && !ctx->vg;
+    const bool use_graph = opt.use_graph && !ctx->profiling && iters >= period && !ctx->vg && !small;
     DevState hst;
     int64_t done = 0;
     bool stopped = false;
@@ -2285,6 +2344,38 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     CK(cudaEventRecord(ev0, s));
     const int64_t check = tol > 0.0 ? std::max<int64_t>(period, (opt.check_every / period) * period) : INT64_MAX;
     int64_t since = 0;
+    if (small) {
+        SmallArgs sa;
+        sa.D = (int)D;
+        sa.M = (int)Ml;
+        sa.N = (int)N;
+        sa.nnz = (int)p->nnz;
+        sa.lo = p->d_lo;
+        sa.len = p->d_len;
+        sa.off = p->d_off;
+        sa.val = p->d_val;
+        sa.row_da = p->d_row_da;
+        sa.row_db = p->d_row_db;
+        sa.theta0 = b.theta[0];
+        sa.theta_prev = (fista && opt.theta_prev) ? b.theta[2] : nullptr;
+        sa.P = b.P;
+        sa.tstep = b.tstep;
+        sa.beta = b.beta;
+        sa.gamma = gamma;
+        sa.tol = tol;
+        sa.iters = iters;
+        sa.kkt_every = opt.kkt_every;
+        sa.fista = fista;
+        sa.trace = b.trace;
+        sa.kkt = b.kkt;
+        sa.kktp = b.kktp;
+        sa.trace_len = tcap;
+        sa.theta_out = b.theta[1];
+        sa.prev_out = fista ? b.theta[2] : nullptr;
+        sa.state = b.state;
+        CK(run_k(ctx, "small_solve", 1, [&]() { return launch_small_solve(sa, s); }));
+        done = iters;
+    }
     while (done < iters) {
         if (use_graph && iters - done >= period) {
             CK(cudaGraphLaunch(gexec, s));
@@ -2307,11 +2398,24 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
         }
     }
     CK(cudaEventRecord(ev1, s));
+    if (pl->NX && getenv("QDT_WDEBUG")) {   // diagnostic: fused wide step geometry and exchanges
+        const int ng = pl->wx_ncl * pl->wx_C;
+        std::vector<double> hp((size_t)ng * NSC_TILE);
+        CK(cudaMemcpyAsync(hp.data(), b.partT, sizeof(double) * hp.size(), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        double ex = 0, mx = 0;
+        for (int i = 0; i < ng; i++) {
+            ex += hp[(size_t)i * NSC_TILE + SC_DTH];
+            mx = std::max(mx, hp[(size_t)i * NSC_TILE + SC_DTH]);
+        }
+        fprintf(stderr, "[qdt wide] N=%d C=%d Wc=%d clusters=%d tiles=%lld exchanges/CTA mean %.1f max %.0f (last step)\n",
+                pl->N, pl->wx_C, pl->wx_Wc, pl->wx_ncl, (long long)((p->Ml + WT - 1) / WT), ex / ng, mx);
+    }
     // ---- final evaluation at Theta_iters (if no early stop)
     CK(cudaMemcpyAsync(&hst, b.state, sizeof hst, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     stopped = hst.stop != 0;
-    if (stopped && hst.converged && !hst.nonfinite && (pl->NB || pl->NW || pl->NX) && !fista) {
+    if (!small && stopped && hst.converged && !hst.nonfinite && (pl->NB || pl->NW || pl->NX) && !fista) {
         // the sweep loop evaluates the unclamped KKT only; re-evaluate Theta_kd once with the
         // general kernels so that trace/kkt/kkt_paper at kd come from one consistent pass
         DevState sr = hst;
@@ -2321,7 +2425,7 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
         CKS(eval_pass(ctx, c, b, b.theta[hst.iters_done % nbuf]));
         CK(cudaMemcpyAsync(b.state, &hst, sizeof hst, cudaMemcpyHostToDevice, s));
     }
-    if (!stopped) {
+    if (!small && !stopped) {
         CKS(eval_pass(ctx, c, b, b.theta[iters % nbuf]));
         CK(cudaMemcpyAsync(&hst, b.state, sizeof hst, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -2329,7 +2433,7 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     if (hst.nonfinite)
         return fail(ctx, QDT_ERR_NONFINITE, "non-finite objective at iteration %lld", (long long)hst.iters_done);
     const int64_t kd = hst.iters_done;
-    const double *res = b.theta[kd % nbuf];
+    const double *res = small ? b.theta[1] : b.theta[kd % nbuf];
     // ---- outputs
     const bool gather = ctx->nranks > 1 && opt.gather_theta;
     if (!theta_out) {
@@ -2344,7 +2448,7 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
         CKS(copy_cols(ctx, theta_out, Nu, res, N, Nu, Ml, dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
     }
     if (fista && opt.theta_prev_out) {   // resume state: Theta_{kd-1} (the initial Theta_{-1} when kd = 0)
-        const double *prv = b.theta[(kd + 2) % 3];
+        const double *prv = small ? b.theta[2] : b.theta[(kd + 2) % 3];
         if (gather) {
             double *full;
             CKS(ws_get(ctx, "gather", M * N, &full));

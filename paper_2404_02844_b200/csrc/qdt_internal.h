@@ -189,23 +189,46 @@ struct WideArgs {               // wide-N sweep (N > 128): k_grad_wide + k_proj_
     const double *beta;         // FISTA step: beta_k by state->it (nullptr: plain)
     const DevState *state;
 };
+// ---- single-CTA persistent solve (qdt_small.cu): the whole problem in shared memory
+struct SmallArgs {
+    int D, M, N, nnz;
+    const int32_t *lo, *len;
+    const int64_t *off;
+    const double *val;
+    const int32_t *row_da, *row_db;   // probes covering Fock row k: [row_da[k], row_db[k])
+    const double *theta0, *theta_prev, *P, *tstep, *beta;
+    double gamma, tol;
+    int64_t iters;
+    int kkt_every, fista;
+    double *trace, *kkt, *kktp;
+    int64_t trace_len;
+    double *theta_out, *prev_out;
+    DevState *state;
+};
+size_t small_solve_smem(int64_t D, int64_t M, int N, int64_t nnz, int fista);
+cudaError_t launch_small_solve(const SmallArgs &a, cudaStream_t s);
+constexpr size_t SMALL_SMEM_MAX = 200 * 1024;
+
 // ---- fused wide-row step (qdt_wide.cu): N > 160, one cluster of C CTAs per 32-row tile
-constexpr int WT = 32;          // Fock rows per wide tile (half of a 64-row sweep tile)
+constexpr int WT = 16;          // Fock rows per wide tile (a quarter of a 64-row sweep tile)
 constexpr int WKC = 8;          // probes per staged chunk
 constexpr int WSTAGES = 4;      // chunk ring depth
-constexpr int WFP = 36;         // staged F row pitch (32 rows + 4: conflict-free A fragments)
-constexpr int W_NBW_MAX = 10;   // n-blocks per warp: <= 640 columns per CTA
+constexpr int WFP = 20;         // staged F row pitch (16 rows + 4: conflict-free A fragments)
+constexpr int W_NBW_MAX = 5;    // n-blocks per warp: <= 640 columns per CTA
+constexpr int W_NG = 16;        // n-group warps per CTA
+constexpr unsigned W_LANES = (1u << WT) - 1;   // lanes of warp 0 that own the tile's rows
 constexpr int W_THREADS = 512;
 constexpr int W_CMAX = 16;      // CTAs per cluster (non-portable above 8)
 constexpr int GEN_NMAX = 1024;  // widest row of the general CUDA-core kernels (hooks, Newton)
-constexpr int QDT_NMAX = W_CMAX * 8 * 8 * W_NBW_MAX;   // widest row of the fused wide step (10 240)
+constexpr int QDT_NMAX = W_CMAX * 8 * W_NG * W_NBW_MAX;   // widest row of the fused wide step (10 240)
 struct WStepArgs {
     int N, Nv, Ml;
     int C, Wc;                  // CTAs per cluster, columns per CTA (multiple of 8)
     int64_t kb, M;
-    const int32_t *trange;      // per cluster: tiles [trange[c], trange[c + 1])
+    const int32_t *tlist;       // tile indices, cluster c owns tlist[toff[c] .. toff[c + 1]) (Fock order)
+    const int32_t *toff;
     const int64_t *fb_off;
-    const int32_t *tile_dA, *tile_dB;   // 64-row sweep tiles (tile tt uses sweep tile tt >> 1)
+    const int32_t *tile_dA, *tile_dB;   // 64-row sweep tiles (wide tile tt uses sweep tile tt >> 2)
     const double *Fb;
     const double *R;
     const double *theta;        // local row 0; rows -1 and Ml readable

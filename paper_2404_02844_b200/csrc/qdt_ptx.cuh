@@ -140,4 +140,12 @@ __device__ __forceinline__ double ld_dsmem(const double *p, uint32_t rank)
     asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra) : "memory");
     return v;
 }
+// store a double into the shared memory of CTA `rank` of the cluster at the address that `p` has
+// in this CTA's shared window (ordered before the next barrier.cluster.arrive.release)
+__device__ __forceinline__ void st_dsmem(double *p, uint32_t rank, double v)
+{
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(p)), "r"(rank));
+    asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
+}
 }  // namespace qdt

@@ -15,17 +15,18 @@
 // G and X never reach HBM: per element the kernel reads Theta_k once from DRAM (plus Theta_{k-1}
 // for FISTA) and writes Theta_{k+1} once; the R rows of the window come from L2.
 //
-// Layout of a CTA (512 threads, 16 warps): warp w = (mp, ng), mp = w & 1 owns the m-blocks
-// {2 mp, 2 mp + 1} (rows 16 mp .. 16 mp + 15 of the tile), ng = w >> 1 the n-blocks
-// [ng NBW, (ng + 1) NBW) of the chunk (8 columns each).  In the DMMA accumulator layout a 4-lane
-// quad (lane = 4 g + t) holds columns 8 nb + 2 t, 8 nb + 2 t + 1 of row g of an m-block, so a row's
-// values are spread over one quad in each of the 8 n-group warps and over the C CTAs: row
+// Layout of a CTA (512 threads, 16 warps): every warp holds both m-blocks of the 16-row tile and
+// warp w the n-blocks [w NBW, (w + 1) NBW) of the chunk (8 columns each, NBW <= 5: 20 fp64
+// accumulators per thread, so the epilogue has registers to spare).  In the DMMA accumulator
+// layout a 4-lane quad (lane = 4 g + t) holds columns 8 nb + 2 t, 8 nb + 2 t + 1 of row g of an
+// m-block, so a row's values are spread over one quad in each of the 16 warps and over the C CTAs: row
 // reductions go quad (shuffles) -> CTA (shared memory, fixed n-group order) -> cluster (DSMEM,
 // fixed CTA order).  Every CTA of the cluster combines the same partials in the same order, so
 // all of them take identical tau / stop decisions and the result is bitwise deterministic.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include <algorithm>
 
@@ -42,11 +43,16 @@ __device__ __forceinline__ void fence_proxy_async_smem()
 // staged Theta tile row pitch: = 8 mod 16 doubles (conflict-free 16-byte reads of 8 rows)
 __host__ __device__ inline int wide_theta_pitch(int Wc) { return (Wc % 16 == 8) ? Wc : Wc + 8; }
 
-size_t wide_step_smem(int Wc)
+__host__ __device__ inline size_t wide_ring_doubles(int Wc)
 {
     const size_t ring = (size_t)WSTAGES * WKC * ((Wc + 4) + WFP);
     const size_t tile = (size_t)(WT + 2) * wide_theta_pitch(Wc);
-    return std::max(ring, tile) * sizeof(double);
+    return ((ring > tile ? ring : tile) + 15) & ~(size_t)15;
+}
+
+size_t wide_step_smem(int Wc)
+{
+    return (wide_ring_doubles(Wc) + (size_t)2 * W_CMAX * WT * 8) * sizeof(double);
 }
 
 // combination of row partials by value kind: 0 min (G), 1 sum, 2 max, 3 min, 4 sum, 5 sum, 6 min
@@ -60,30 +66,12 @@ __device__ __forceinline__ double wcombine(int v, double x, double y)
         default: return x + y;
     }
 }
-// the cluster total of one (row, value) slot: the C CTAs' values combined in CTA order (all
-// loads issued before the combination)
-__device__ __forceinline__ double cluster_total(const double *slot, int v, int C)
-{
-    if (C == 1) return *slot;
-    double x = 0.0;
-    for (int q0 = 0; q0 < C; q0 += 4) {            // four remote loads in flight, combined in CTA order
-        double r[4];
-#pragma unroll
-        for (int k = 0; k < 4; k++) r[k] = q0 + k < C ? ld_dsmem(slot, q0 + k) : 0.0;
-#pragma unroll
-        for (int k = 0; k < 4; k++)
-            if (q0 + k < C) x = (q0 + k == 0) ? r[k] : wcombine(v, x, r[k]);
-    }
-    return x;
-}
-
 template <int NBW, bool FIS>
 __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ WStepArgs a)
 {
     extern __shared__ __align__(128) double sm[];
     __shared__ __align__(8) uint64_t bars[WSTAGES + 1];   // chunk ring + the Theta tile
-    __shared__ double rowp[WT][8][8];   // per row and n-group warp: quad-reduced partials
-    __shared__ double xb[2][WT][8];     // exchange slots (read by the cluster peers)
+    __shared__ double rowp[WT][W_NG][8];   // per row and n-group warp: quad-reduced partials
     __shared__ double comb[8][WT];      // cluster totals per value and row
     __shared__ double ttry[WT];         // warm-start trial threshold per row (-inf: none)
     __shared__ double trow[WT][3];      // per row: tau, lambda (unclamped), lambda (clamped)
@@ -109,11 +97,13 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
     const int Pt = wide_theta_pitch(a.Wc);         // staged Theta row pitch: = 8 mod 16 doubles
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
-    const int mp = warp & 1, ng = warp >> 1;
+    const int ng = warp;                           // n-group
     double *Rs = sm;                               // WSTAGES x WKC x Pr
     double *Fs = sm + WSTAGES * WKC * Pr;          // WSTAGES x WKC x WFP
-    double *Ts = sm;                               // the Theta tile (rows k0 - 1 .. k0 + 32) reuses the ring
-    const int ta = a.trange[cid], tb = a.trange[cid + 1];
+    double *Ts = sm;                               // the Theta tile (rows k0 - 1 .. k0 + WT) reuses the ring
+    // exchange slots after the ring: xin[2][W_CMAX][WT][8], slot [r] holds CTA r's partials (pushed by r)
+    auto xin = reinterpret_cast<double(*)[W_CMAX][WT][8]>(sm + wide_ring_doubles(a.Wc));
+    const int ta = a.toff[cid], tb = a.toff[cid + 1];   // this cluster's tiles a.tlist[ta .. tb)
 
     // zero the stages once: a masked tail k-step then multiplies stale but finite values by 0
     for (int i = tid; i < WSTAGES * WKC * (Pr + WFP); i += W_THREADS) sm[i] = 0.0;
@@ -127,7 +117,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
     // ---- producer (warp 0): chunk c of tile tt into the ring slot of the running chunk count
     uint32_t issued = 0, used = 0, tuse = 0;
     auto issue_chunk = [&](int tt, int c) {        // warp 0, all lanes
-        const int t64 = tt >> 1, half = tt & 1;
+        const int t64 = tt >> 2, quarter = tt & 3;
         const int dA = a.tile_dA[t64], W = a.tile_dB[t64] - dA;
         const int p0 = c * WKC, kc = min(WKC, W - p0);
         const int stg = issued % WSTAGES;
@@ -135,7 +125,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
         if (lane == 0) mbar_expect_tx(bar, (uint32_t)kc * (WFP + ncol) * 8u);
         __syncwarp();
         if (lane < kc) {
-            bulk_g2s(Fs + (stg * WKC + lane) * WFP, a.Fb + a.fb_off[t64] + (int64_t)(p0 + lane) * STP + half * WT,
+            bulk_g2s(Fs + (stg * WKC + lane) * WFP, a.Fb + a.fb_off[t64] + (int64_t)(p0 + lane) * STP + quarter * WT,
                      WFP * 8u, bar);
             bulk_g2s(Rs + (stg * WKC + lane) * Pr, a.R + (int64_t)(dA + p0 + lane) * N + cbase, (uint32_t)ncol * 8u,
                      bar);
@@ -143,34 +133,57 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
         issued++;
     };
     auto nchunks = [&](int tt) {
-        const int t64 = tt >> 1;
+        const int t64 = tt >> 2;
         return (a.tile_dB[t64] - a.tile_dA[t64] + WKC - 1) / WKC;
     };
     auto start_tile = [&](int tt) {                // warp 0: the first ring's worth of a tile's chunks
         const int n = min(WSTAGES, nchunks(tt));
         for (int c = 0; c < n; c++) issue_chunk(tt, c);
     };
-    if (warp == 0 && ta < tb) start_tile(ta);
+    if (warp == 0 && ta < tb) start_tile(a.tlist[ta]);
 
     double sreg = 0.0, skkt = 0.0, skktp = 0.0;    // per-thread running partials (fixed order)
     int slot = 0;
-    const double *Fw = Fs + t * WFP + 16 * mp + g;            // A fragment: F[4 ks + t][8 mb + g]
+    int nexch = 0;                                 // cluster exchanges (diagnostic, SC_DTH)
+#ifdef QDT_WPROF
+    unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, tq0 = clock64(), tq1;
+    long long nchk = 0;
+#define QDT_PH(i) (tq1 = clock64(), ph[i] += tq1 - tq0, tq0 = tq1)
+#else
+#define QDT_PH(i) ((void)0)
+#endif
+    const double *Fw = Fs + t * WFP + g;                      // A fragment: F[4 ks + t][8 mb + g]
     const double *Rw = Rs + t * Pr + 8 * ng * NBW + g;        // B fragment: R[4 ks + t][8 nb + g]
 
-    // cluster-wide combination of the 32 rows' partials in xb[slot]: fixed CTA order
+    // this CTA's partial into slot [crank] of every CTA of the cluster (remote shared-memory stores,
+    // made visible by the release / acquire of the cluster barrier)
+    auto push = [&](double *dst, double x) {
+        if (C == 1) {
+            *dst = x;
+            return;
+        }
+        for (int r = 0; r < C; r++) st_dsmem(dst, (uint32_t)r, x);
+    };
+    // cluster-wide barrier after the pushes: every CTA then combines all C partials locally in CTA order
     auto exchange = [&]() {
+        nexch++;
         if (C > 1)
             cluster_sync_all();
         else
             __syncthreads();
     };
 
-    for (int tt = ta; tt < tb; tt++) {
-        const int t64 = tt >> 1;
+    for (int ti = ta; ti < tb; ti++) {
+        const int tt = a.tlist[ti];
+        const int t64 = tt >> 2;
         const int k0 = tt * WT;                    // local first row of the tile
         const int Tt = min(WT, a.Ml - k0);
         const int W = a.tile_dB[t64] - a.tile_dA[t64];
         const int nch = (W + WKC - 1) / WKC;
+#ifdef QDT_WPROF
+        nchk += nch;
+#endif
+        QDT_PH(0);
         if (warp == 1) {                           // Theta rows of the epilogue -> L2 while the GEMM runs
             for (int r = lane; r < Tt + 2; r += 32) {
                 bulk_prefetch_l2(a.theta + (int64_t)(k0 - 1 + r) * N + cbase, (uint32_t)ncol * 8u);
@@ -215,6 +228,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
             __syncthreads();                       // stage consumed
             if (warp == 0 && c + WSTAGES < nch) issue_chunk(tt, c + WSTAGES);
         }
+        QDT_PH(1);
         // the ring is drained: the Theta tile (rows k0 - 1 .. k0 + Tt) lands in its space (plain
         // steps and evaluation passes; the FISTA step reads Theta_k / Theta_{k-1} through L2)
         if (!fis && warp == 0) {
@@ -224,8 +238,8 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
             for (int r = lane; r < Tt + 2; r += 32)
                 bulk_g2s(Ts + r * Pt, a.theta + (int64_t)(k0 - 1 + r) * N + cbase, (uint32_t)ncol * 8u, bar);
         }
-        if (warp == 2 && tt + 1 < tb) {            // next tile's first chunks -> L2 during the epilogue
-            const int t1 = (tt + 1) >> 1;
+        if (warp == 2 && ti + 1 < tb) {            // next tile's first chunks -> L2 during the epilogue
+            const int t1 = a.tlist[ti + 1] >> 2;
             const int n1 = min(WSTAGES * WKC, a.tile_dB[t1] - a.tile_dA[t1]);
             for (int r = lane; r < n1; r += 32)
                 bulk_prefetch_l2(a.R + (int64_t)(a.tile_dA[t1] + r) * N + cbase, (uint32_t)ncol * 8u);
@@ -234,13 +248,14 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
             mbar_wait(&bars[WSTAGES], tuse & 1);
             tuse++;
         }
+        QDT_PH(2);
 
         // ---- S4 + pass 1: G = acc + gamma L Y; row min of G, sum / max / min of X = Y - t G
         double tk[2];
         double pmn[2], ps[2], pxm[2], pxn[2], pts[2], ptc[2], ptm[2];
 #pragma unroll
         for (int i = 0; i < 2; i++) {
-            const int rl = 16 * mp + 8 * i + g;
+            const int rl = 8 * i + g;
             const int kl = k0 + rl;
             const bool act = rl < Tt;
             const int64_t kg = a.kb + kl;
@@ -314,22 +329,25 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
         if (t == 0) {
 #pragma unroll
             for (int i = 0; i < 2; i++) {
-                double *rp = rowp[16 * mp + 8 * i + g][ng];
+                double *rp = rowp[8 * i + g][ng];
                 rp[0] = pmn[i], rp[1] = ps[i], rp[2] = pxm[i], rp[3] = pxn[i];
                 rp[4] = pts[i], rp[5] = ptc[i], rp[6] = ptm[i];
             }
         }
         __syncthreads();
-        if (tid < 7 * WT) {                        // CTA partial of (row, value) (n-group order)
-            const int row = tid & (WT - 1), v = tid >> 5;
+        QDT_PH(7);
+        if (tid < 7 * WT) {                        // CTA partial of (row, value) (n-group order), pushed to every CTA
+            const int row = tid % WT, v = tid / WT;
             double x = rowp[row][0][v];
-            for (int w = 1; w < 8; w++) x = wcombine(v, x, rowp[row][w][v]);
-            xb[slot][row][v] = x;
+            for (int w = 1; w < W_NG; w++) x = wcombine(v, x, rowp[row][w][v]);
+            push(&xin[slot][crank][row][v], x);
         }
         exchange();
         if (tid < 7 * WT) {                        // cluster total of (row, value) in CTA order
-            const int row = tid & (WT - 1), v = tid >> 5;
-            comb[v][row] = cluster_total(&xb[slot][row][v], v, C);
+            const int row = tid % WT, v = tid / WT;
+            double x = xin[slot][0][row][v];
+            for (int r = 1; r < C; r++) x = wcombine(v, x, xin[slot][r][row][v]);
+            comb[v][row] = x;
         }
         __syncthreads();
         if (tid < WT) {                            // lambda, tau_0, warm-started first round
@@ -358,16 +376,17 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
             trow[tid][0] = tau;
             tdone[tid] = done ? 1 : 0;
             tcnt[tid] = cnt;
-            const unsigned all = __ballot_sync(0xffffffffu, done);
-            if (tid == 0) s_alldone = (all == 0xffffffffu);
+            const unsigned all = __ballot_sync(W_LANES, done);
+            if (tid == 0) s_alldone = (all == W_LANES);
         }
         __syncthreads();
         slot ^= 1;
+        QDT_PH(3);
 
         // ---- pass 2: KKT terms with lambda; X = Y - t G in the accumulators
 #pragma unroll
         for (int i = 0; i < 2; i++) {
-            const int rl = 16 * mp + 8 * i + g;
+            const int rl = 8 * i + g;
             const int kl = k0 + rl;
             const bool act = rl < Tt;
             const double lam = trow[rl][1], lamp = trow[rl][2];
@@ -405,7 +424,8 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
         // the Theta tile is consumed: the next tile's chunks may refill the ring now, under the
         // Michelot rounds and the stores of this one
         __syncthreads();
-        if (warp == 0 && tt + 1 < tb) start_tile(tt + 1);
+        if (warp == 0 && ti + 1 < tb) start_tile(a.tlist[ti + 1]);
+        QDT_PH(4);
         if (ev) continue;                          // evaluation pass: no step
 
         // ---- S5: Michelot rounds, all rows of the tile in lockstep over the cluster
@@ -413,7 +433,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
             double rps[2], rpc[2], rmA[2];
 #pragma unroll
             for (int i = 0; i < 2; i++) {
-                const int rl = 16 * mp + 8 * i + g;
+                const int rl = 8 * i + g;
                 const double tau = trow[rl][0];
                 double sA = 0.0, mA = INFINITY;
                 int cA = 0;
@@ -437,22 +457,25 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
             if (t == 0) {
 #pragma unroll
                 for (int i = 0; i < 2; i++) {
-                    double *rp = rowp[16 * mp + 8 * i + g][ng];
+                    double *rp = rowp[8 * i + g][ng];
                     rp[0] = rps[i], rp[1] = rpc[i], rp[2] = rmA[i];
                 }
             }
             __syncthreads();
             if (tid < 3 * WT) {
-                const int row = tid & (WT - 1), v = tid >> 5;   // 0: sum, 1: count (sums), 2: min
+                const int row = tid % WT, v = tid / WT;   // 0: sum, 1: count (sums), 2: min
                 const int op = v == 2 ? 3 : 1;
                 double x = rowp[row][0][v];
-                for (int w = 1; w < 8; w++) x = wcombine(op, x, rowp[row][w][v]);
-                xb[slot][row][v] = x;
+                for (int w = 1; w < W_NG; w++) x = wcombine(op, x, rowp[row][w][v]);
+                push(&xin[slot][crank][row][v], x);
             }
             exchange();
             if (tid < 3 * WT) {
-                const int row = tid & (WT - 1), v = tid >> 5;
-                comb[v][row] = cluster_total(&xb[slot][row][v], v == 2 ? 3 : 1, C);
+                const int row = tid % WT, v = tid / WT;
+                const int op = v == 2 ? 3 : 1;
+                double x = xin[slot][0][row][v];
+                for (int r = 1; r < C; r++) x = wcombine(op, x, xin[slot][r][row][v]);
+                comb[v][row] = x;
             }
             __syncthreads();
             if (tid < WT) {
@@ -470,17 +493,18 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
                     }
                 }
                 tdone[tid] = done ? 1 : 0;
-                const unsigned all = __ballot_sync(0xffffffffu, done);
-                if (tid == 0) s_alldone = (all == 0xffffffffu);
+                const unsigned all = __ballot_sync(W_LANES, done);
+                if (tid == 0) s_alldone = (all == W_LANES);
             }
             __syncthreads();
             slot ^= 1;
         }
+        QDT_PH(5);
         // ---- Theta_{k+1} = max(X - tau, 0), stored from registers
         if (a.tau_prev && tid < Tt && crank == 0) a.tau_prev[k0 + tid] = trow[tid][0];
 #pragma unroll
         for (int i = 0; i < 2; i++) {
-            const int rl = 16 * mp + 8 * i + g;
+            const int rl = 8 * i + g;
             if (rl >= Tt) continue;
             const double tau = trow[rl][0];
             double *o = a.out + (int64_t)(k0 + rl) * N + cbase;
@@ -494,6 +518,13 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
             }
         }
     }
+    QDT_PH(6);
+#ifdef QDT_WPROF
+    if ((blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && tid == 0 && it == 5)
+        printf("[wprof] cta %d tiles %d chunks %lld exch %d | gemm %.0f thwait %.0f pass1 %.0f ex1 %.0f pass2 %.0f rounds %.0f store %.0f (kcycles)\n",
+               blockIdx.x, tb - ta, nchk, nexch, (ph[0] + ph[1]) / 1e3, ph[2] / 1e3, ph[7] / 1e3, ph[3] / 1e3, ph[4] / 1e3,
+               ph[5] / 1e3, ph[6] / 1e3);
+#endif
     // ---- per-CTA scalar partials (fixed order: lanes, then warps)
     sreg = wsum(sreg);
     skkt = wsum(skkt);
@@ -517,7 +548,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
             p[SC_KKTP] = v1;
         }
         p[SC_REG] = v2;
-        p[SC_DTH] = 0.0;
+        p[SC_DTH] = (double)nexch;
     }
     if (C > 1) cluster_sync_all();                 // no CTA leaves while a peer may read its slots
 }
@@ -542,9 +573,9 @@ static cudaError_t launch_nbw(const WStepArgs &a, int grid, size_t smem, cudaStr
     return fis ? cudaLaunchKernelEx(&cfg, k_wstep<NBW, true>, a) : cudaLaunchKernelEx(&cfg, k_wstep<NBW, false>, a);
 }
 
-#define QDT_FOR_NBW(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10)
+#define QDT_FOR_NBW(X) X(1) X(2) X(3) X(4) X(5)
 
-int wide_nbw(int Wc) { return (Wc / 8 + 7) / 8; }
+int wide_nbw(int Wc) { return (Wc / 8 + W_NG - 1) / W_NG; }
 
 cudaError_t prepare_wide_kernels()
 {
@@ -554,7 +585,7 @@ cudaError_t prepare_wide_kernels()
     const uint64_t bit = dev < 64 ? (1ull << dev) : 0;
     if (done_mask & bit) return cudaSuccess;
     cudaError_t e = cudaSuccess;
-    const int smax = (int)std::max(wide_step_smem(8 * 8 * W_NBW_MAX), wide_step_smem(8 * 8 * W_NBW_MAX - 8));
+    const int smax = (int)std::max(wide_step_smem(8 * W_NG * W_NBW_MAX), wide_step_smem(8 * W_NG * W_NBW_MAX - 8));
 #define QDT_PREP1(n, f)                                                                                        \
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_wstep<n, f>, cudaFuncAttributeMaxDynamicSharedMemorySize, smax); \
     if (e == cudaSuccess) e = cudaFuncSetAttribute(k_wstep<n, f>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);

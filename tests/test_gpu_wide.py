@@ -27,6 +27,13 @@ def ctx(q):
     return q.qdt_init(0)
 
 
+@pytest.fixture(autouse=True)
+def fused_wide(monkeypatch):
+    """Every plan built in these tests takes the fused wide step, also at 128 < N <= 1024 (where the
+    two-kernel sweep is the default)."""
+    monkeypatch.setenv("QDT_WIDE", "new")
+
+
 def _trace_ok(tg, to, P):
     tg, to = np.asarray(tg), np.asarray(to)
     floor = 4 * EPS * np.sqrt(np.sum(P ** 2)) * np.sqrt(np.abs(to))
