@@ -57,8 +57,11 @@ typedef enum {
 typedef enum {
     QDT_STEP_SQS = 0,       /* row-constant diagonal majorizer, t_k = 1 / (F^T F 1 + 4 gamma)_k */
     QDT_STEP_LIPSCHITZ = 1, /* scalar t = 1 / (1.01 rho + 4 gamma), rho: 100 power iterations   */
-    QDT_STEP_BB = 2         /* Barzilai-Borwein scalar step <s,s>/<s,Hs> clamped to [t_LIP, 1e6 t_LIP]
-                               (reading R14); plain PG (accel = 0), N <= 128 in this build */
+    QDT_STEP_BB = 2,        /* Barzilai-Borwein scalar step <s,s>/<s,Hs> clamped to [t_LIP, 1e6 t_LIP]
+                               (reading R14); plain PG (accel = 0)                       */
+    QDT_STEP_BB_LS = 3      /* BB + exact line search along d = P(Theta - t G) - Theta:
+                               Theta_{k+1} = Theta + l* d, l* = argmin over [0, 1] of the quadratic
+                               f(Theta + l d) (reading R17); monotone; plain PG, allreduce exchange */
 } qdt_step_mode;
 
 typedef struct qdt_ctx qdt_ctx;       /* device, stream, NCCL comm, workspace, last error  */

@@ -240,7 +240,7 @@ def power_iteration(F: Probes, k_pow: int = 100) -> float:
     return lib().or_power_iteration(*F._args(), F.M, int(k_pow))
 
 
-STEP_SQS, STEP_LIPSCHITZ, STEP_BB = 0, 1, 2
+STEP_SQS, STEP_LIPSCHITZ, STEP_BB, STEP_BB_LS = 0, 1, 2, 3
 
 
 def solve(F: Probes, P, gamma: float, tol: float, iters: int, step: int = STEP_SQS,

@@ -456,6 +456,14 @@ double or_power_iteration(const int64_t *lo, const int64_t *len, const int64_t *
  *            Theta_{k-1}: t_k = <s,s> / <s,Hs>, <s,Hs> = ||R_k - R_{k-1}||^2 + gamma ||D s||^2
  *            (H = F^T F + gamma L, the Hessian of f/2), clamped to [t_LIP, 1e6 t_LIP];
  *            t_LIP when <s,Hs> <= 0.  Plain projected gradient only (accel ignored).
+ *   step 3: BB with the exact line search along the projected direction (SURVEY 8(f) row 3,
+ *            reading R17): t_k as step 2, Z = P_{S^M}(Theta_k - t_k G), d = Z - Theta_k; f is
+ *            quadratic along d, f(Theta + l d) = f + 2 l <G,d> + l^2 (||F d||^2 + gamma ||D d||^2),
+ *            so l* = clip(-<G,d> / (||F d||^2 + gamma ||D d||^2), 0, 1) (1 when the curvature
+ *            is 0) and Theta_{k+1} = Theta_k + l* d (a convex combination: feasible).  The
+ *            projection gives -<G,d> >= ||d||^2 / t_k exactly; near convergence the computed
+ *            <G,d> cancels to roundoff (row-constant multiplier part of G against rows of d that
+ *            sum to 0), so the numerator is max(-<G,d>, ||d||^2 / t_k) (reading R17).
  *   accel 1: FISTA extrapolation Y_k = Theta_k + (tau_k - 1)/tau_{k+1} (Theta_k - Theta_{k-1}),
  *            tau_0 = 1, tau_{k+1} = (1 + sqrt(1 + 4 tau_k^2))/2 (Beck-Teboulle).  Resume state
  *            (SURVEY 8(b)): theta_prev = Theta_{-1} (NULL: Theta_0) and tau0 = tau_0 (< 1: 1);
@@ -487,6 +495,8 @@ int64_t or_solve(const int64_t *lo, const int64_t *len, const int64_t *off, cons
 
     double t_lip = 0.0;
     double *Rprev = NULL;
+    const int bb_ls = step_mode == 3;
+    if (bb_ls) step_mode = 2;
     if (step_mode == 2) {
         accel = 0;
         double rho = or_power_iteration(lo, len, off, val, D, M, 100);
@@ -565,6 +575,27 @@ int64_t or_solve(const int64_t *lo, const int64_t *len, const int64_t *off, cons
             for (int64_t n = 0; n < N; n++) X[r * N + n] = Y[r * N + n] - t[r] * G[r * N + n];
         memcpy(Tprev, Theta, MN * sizeof(double));
         or_project_rows(X, M, N, Theta);
+        if (bb_ls) {
+            /* exact line search along d = Z - Theta_k (Z in Theta, Theta_k in Tprev; X, R scratch) */
+#pragma omp parallel for schedule(static)
+            for (size_t i = 0; i < MN; i++) X[i] = Theta[i] - Tprev[i];
+            double *Fd = (double *)malloc((size_t)(D * N) * sizeof(double));
+            or_forward(lo, len, off, val, D, X, NULL, N, Fd);
+            const double fdd = sumsq(Fd, D * N);
+            const double ddd = or_regul(X, M, N);
+            const double gd = dotl(G, X, (int64_t)MN);   /* G at Theta_k (plain PG: Y = Theta_k) */
+            const double dd = sumsq(X, (int64_t)MN);
+            free(Fd);
+            const double den = fdd + gamma * ddd;
+            const double num = fmax(-gd, dd / t[0]);     /* scalar BB step: t[r] = t_k for every row */
+            double lam = 1.0;
+            if (den > 0.0) {
+                lam = num / den;
+                lam = lam < 0.0 ? 0.0 : (lam > 1.0 ? 1.0 : lam);
+            }
+#pragma omp parallel for schedule(static)
+            for (size_t i = 0; i < MN; i++) Theta[i] = Tprev[i] + lam * X[i];
+        }
         tau = tau_next;
     }
     if (k == iters) {

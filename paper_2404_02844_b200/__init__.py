@@ -20,7 +20,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("QDT_LIB") or os.path.join(_HERE, "libqdt.so")   # QDT_LIB: in-tree A/B build
 
-QDT_STEP_SQS, QDT_STEP_LIPSCHITZ, QDT_STEP_BB = 0, 1, 2
+QDT_STEP_SQS, QDT_STEP_LIPSCHITZ, QDT_STEP_BB, QDT_STEP_BB_LS = 0, 1, 2, 3
 STATUS = {0: "QDT_OK", 1: "QDT_ERR_INVALID_ARG", 2: "QDT_ERR_UNSORTED", 3: "QDT_ERR_NONFINITE",
           4: "QDT_ERR_OOM", 5: "QDT_ERR_CUDA", 6: "QDT_ERR_NCCL", 7: "QDT_ERR_TRUNCATED",
           8: "QDT_ERR_STATE"}

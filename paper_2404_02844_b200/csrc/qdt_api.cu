@@ -806,15 +806,9 @@ static qdt_status build_sweep_plan(qdt_ctx *ctx, qdt_probes *p, Plan *pl)
     const int nt = p->sw_ntiles;
     const int64_t D = p->D;
     const int nsm = device_sm_count();
-    // split cap of the bwd units: SWCAP, halved (down to 32 probes) while the tiles give fewer
-    // than 2 units per SM (small problems such as Medium: 16 tiles of wide windows)
-    int cap = SWCAP;
-    for (;;) {
-        int64_t nu = 0;
-        for (int t = 0; t < nt; t++) nu += std::max(1, (p->sw_dB[t] - p->sw_dA[t] + cap - 1) / cap);
-        if (nu >= 2 * nsm || cap <= 2 * SKC) break;
-        cap /= 2;
-    }
+    // split cap of the bwd units (a smaller cap for small problems measured slower: the split-K
+    // fix-up sums more slots, profiles/r02_v3)
+    const int cap = SWCAP;
     std::vector<SwUnit> bu;
     int64_t slot = 0;
     for (int t = 0; t < nt; t++) {
@@ -1449,7 +1443,7 @@ struct IterCfg {
     int fista;
     int kkt_every;
     int64_t trace_len;
-    int bb = 0;                // Barzilai-Borwein step (reading R14)
+    int bb = 0;                // Barzilai-Borwein step (reading R14): 1 plain, 2 with the line search (R17)
     double tlip = 0.0;         // its safeguard / first step
     int Nv = 0;                // outcomes when N is a padded pitch (pad_cols), else 0
     int bx = 0;                // band-aware residual exchange (nranks > 1)
@@ -1826,11 +1820,40 @@ static qdt_status iteration(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, int64_
         }));
         CKS(allreduce(ctx, b.bb_vec, 3, "allreduce_scalars"));
         CK(run_k(ctx, "bb_step", 1, [&]() { return launch_bb_step(b.bb_vec, c.gamma, c.tlip, b.tbb, b.state, s); }));
-        SweepArgs a = sweep_args(c, b, Rk, cur, b.theta[(j + 1) % 2]);
-        a.tscal = b.tbb;
-        CK(run_k(ctx, "bwd_step", 1, [&]() { return launch_bwd_mma(a, pl->sw_nbunits, pl->NB, s); }));
-        CKS(halo_exchange(ctx, c, b.theta[(j + 1) % 2]));
-        CKS(scalars(ctx, c, b, 0, c.p->sw_ntiles));
+        double *nxt = b.theta[(j + 1) % 2];
+        int nparts = c.p->sw_ntiles;
+        if (pl->NB) {   // N <= 160 (even above 128): k_bwd_mma with the scalar step
+            SweepArgs a = sweep_args(c, b, Rk, cur, nxt);
+            a.tscal = b.tbb;
+            CK(run_k(ctx, "bwd_step", 1, [&]() { return launch_bwd_mma(a, pl->sw_nbunits, pl->NB, s); }));
+        } else if (pl->NX) {
+            WStepArgs w = wstep_args(c, b, Rk, cur, nxt);
+            w.tscal = b.tbb;
+            CK(run_k(ctx, "bwd_step", 1, [&]() { return launch_wide_step(w, pl->wx_ncl, s); }));
+            nparts = wstep_nparts(c);
+        } else {
+            WideArgs w = wide_args(c, b, Rk, cur, nxt);
+            w.tscal = b.tbb;
+            CK(run_k(ctx, "bwd_step", 1, [&]() { return launch_grad_wide(w, pl->sw_nbunits, s); }));
+            CK(run_k(ctx, "proj_step", 1, [&]() { return launch_proj_wide(w, s); }));
+            nparts = wide_nparts(c);
+        }
+        CKS(halo_exchange(ctx, c, nxt));
+        if (c.bb == 2) {
+            // exact line search along d = Z - Theta_k (reading R17): R_Z = F Z - P, the step
+            // statistics, lambda* on the device, Theta_{k+1} = Theta_k + lambda* d over Z
+            CKS(fwd_reduce(ctx, c, b, nxt, b.RY, true));
+            CK(run_k(ctx, "bb_step", 2, [&]() {
+                return launch_bbls_stats(cur, nxt, p->Ml, p->kb, p->M, c.N, ctx->rank == 0 ? Rk : nullptr, b.RY,
+                                         p->D * (int64_t)c.N, b.bb_part, b.bb_vec, b.state, s);
+            }));
+            CKS(allreduce(ctx, b.bb_vec, 5, "allreduce_scalars"));
+            CK(run_k(ctx, "bb_step", 2, [&]() {
+                return launch_bbls_step(b.bb_vec, c.gamma, b.tbb, b.tbb + 1, cur - c.N, nxt - c.N,
+                                        (p->Ml + 2) * (int64_t)c.N, b.state, s);
+            }));
+        }
+        CKS(scalars(ctx, c, b, 0, nparts));
         return QDT_OK;
     }
     if (!c.fista && pl->NX && (!pl->NB || wide_plain_forced())) {
@@ -2125,13 +2148,14 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     if (o) opt = *o;
     if (opt.fista_t != 0.0 && !(opt.fista_t >= 1.0 && isfinite(opt.fista_t)))
         return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: fista_t must be 0 or a finite value >= 1");
-    if (opt.step != QDT_STEP_SQS && opt.step != QDT_STEP_LIPSCHITZ && opt.step != QDT_STEP_BB)
+    if (opt.step < QDT_STEP_SQS || opt.step > QDT_STEP_BB_LS)
         return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: unknown step mode %d", opt.step);
-    if (opt.step == QDT_STEP_BB && opt.accel)
+    const bool bb = opt.step == QDT_STEP_BB || opt.step == QDT_STEP_BB_LS;
+    if (bb && opt.accel)
         return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: the BB step is plain projected gradient (accel = 0)");
     if (opt.exchange != 0 && opt.exchange != 1)
         return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: exchange must be 0 (allreduce) or 1 (band-aware)");
-    if (opt.exchange == 1 && opt.step == QDT_STEP_BB)
+    if (opt.exchange == 1 && bb)
         return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: the BB step needs the full residual (exchange = 0)");
     if (opt.check_every < 1) opt.check_every = 16;
     if (opt.kkt_every < 1) opt.kkt_every = 1;
@@ -2151,9 +2175,7 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     cudaStream_t s = ctx->stream;
     Plan *pl;
     CKS(build_plan(ctx, p, (int)N, &pl));
-    if (opt.step == QDT_STEP_BB && (!pl->NB || pl->NB > SW_NBMAX))
-        return fail(ctx, QDT_ERR_INVALID_ARG, "qdt_solve: the BB step needs N <= %d in this build", 8 * SW_NBMAX);
-    const bool bb = opt.step == QDT_STEP_BB;
+
     // memory plan (fails before allocating the big buffers)
     {
         const int nb = opt.accel ? 3 : 2;
@@ -2184,9 +2206,10 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     if (bb) {
         CKS(ws_get(ctx, "R1", D * N + 4, &b.R[1]));
         CK(cudaMemsetAsync(b.R[1], 0, sizeof(double) * D * N, s));
-        CKS(ws_get(ctx, "bb_part", 3 * BB_NBLK, &b.bb_part));
-        CKS(ws_get(ctx, "bb_vec", 3, &b.bb_vec));
-        CKS(ws_get(ctx, "tbb", 1, &b.tbb));
+        CKS(ws_get(ctx, "bb_part", 5 * BB_NBLK, &b.bb_part));
+        CKS(ws_get(ctx, "bb_vec", 5, &b.bb_vec));
+        CKS(ws_get(ctx, "tbb", 2, &b.tbb));   // [0] t_k, [1] lambda* (line search)
+        if (opt.step == QDT_STEP_BB_LS) CKS(ws_get(ctx, "RY", D * N + 4, &b.RY));
     }
     if (fista) {
         CKS(ws_get(ctx, "R1", D * N + 4, &b.R[1]));
@@ -2258,7 +2281,7 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     double tscalar = 0.0;
     CKS(step_setup(ctx, p, pl, bb ? QDT_STEP_LIPSCHITZ : opt.step, gamma, 100, b.tstep, nullptr, nullptr,
                    &tscalar));
-    c.bb = bb ? 1 : 0;
+    c.bb = bb ? (opt.step == QDT_STEP_BB_LS ? 2 : 1) : 0;
     c.tlip = tscalar;
     DevState st0;
     memset(&st0, 0, sizeof st0);

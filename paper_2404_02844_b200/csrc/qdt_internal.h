@@ -165,6 +165,7 @@ struct SweepFusedArgs {
     const DevState *state;
 };
 struct WideArgs {               // wide-N sweep (N > 128): k_grad_wide + k_proj_wide
+    const double *tscal = nullptr;   // one device scalar step (BB) instead of tstep per row
     int N, Ml, ncc;             // ncc: 128-column chunks (set by launch_grad_wide)
     int Nv;                     // outcomes (< N when the row pitch N carries a zero pad column)
     int64_t kb, M;
@@ -264,6 +265,11 @@ cudaError_t launch_bb_stats(const double *th, const double *tp, int64_t Ml, int6
                             const DevState *st, cudaStream_t s);
 cudaError_t launch_bb_step(const double *vec3, double gamma, double tlip, double *tout,
                            const DevState *st, cudaStream_t s);
+cudaError_t launch_bbls_stats(const double *th, const double *zt, int64_t Ml, int64_t kb, int64_t M, int N,
+                              const double *Rk, const double *Rz, int64_t nR, double *part, double *vec,
+                              const DevState *st, cudaStream_t s);
+cudaError_t launch_bbls_step(const double *vec, double gamma, const double *tbb, double *lam, const double *th,
+                             double *zt, int64_t n, const DevState *st, cudaStream_t s);
 cudaError_t launch_smooth(const double *X, int64_t M, int N, int64_t exclude, int64_t div, double *S,
                           double *T, double *Tx, double *Y, cudaStream_t s);
 cudaError_t launch_sqs_weights_tiled(int ntiles, int Ml, const int32_t *tile_dA,

@@ -89,20 +89,41 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_solve(SmallArgs a)
         for (int i = tid; i < MN; i += nth) T2[i] = a.theta_prev ? a.theta_prev[i] : a.theta0[i];
     __syncthreads();
 
+    // band sums with four independent accumulators (combined in a fixed order): the chains are
+    // latency bound at these sizes
     auto residual = [&](const double *T, double *R, bool withP) {   // R = F T - P
         for (int e = tid; e < DN; e += nth) {
             const int d = e / N, n = e - d * N;
-            double s = 0.0;
             const double *f = Fv + of[d];
-            for (int j = 0; j < ln[d]; j++) s = fma(f[j], T[(lo[d] + j) * N + n], s);
+            const double *tc = T + lo[d] * N + n;
+            const int L = ln[d];
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            int j = 0;
+            for (; j + 4 <= L; j += 4) {
+                s0 = fma(f[j], tc[j * N], s0);
+                s1 = fma(f[j + 1], tc[(j + 1) * N], s1);
+                s2 = fma(f[j + 2], tc[(j + 2) * N], s2);
+                s3 = fma(f[j + 3], tc[(j + 3) * N], s3);
+            }
+            for (; j < L; j++) s0 = fma(f[j], tc[j * N], s0);
+            const double s = (s0 + s1) + (s2 + s3);
             R[e] = withP ? s - Ps[e] : s;
         }
     };
     auto gradient = [&](const double *R, const double *Y, double *G) {   // G = F^T R + gamma L Y
         for (int e = tid; e < MN; e += nth) {
             const int k = e / N, n = e - k * N;
-            double s = 0.0;
-            for (int d = ra[k]; d < rb[k]; d++) s = fma(Fv[of[d] + (k - lo[d])], R[d * N + n], s);
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            int d = ra[k];
+            const int d1 = rb[k];
+            for (; d + 4 <= d1; d += 4) {
+                s0 = fma(Fv[of[d] + (k - lo[d])], R[d * N + n], s0);
+                s1 = fma(Fv[of[d + 1] + (k - lo[d + 1])], R[(d + 1) * N + n], s1);
+                s2 = fma(Fv[of[d + 2] + (k - lo[d + 2])], R[(d + 2) * N + n], s2);
+                s3 = fma(Fv[of[d + 3] + (k - lo[d + 3])], R[(d + 3) * N + n], s3);
+            }
+            for (; d < d1; d++) s0 = fma(Fv[of[d] + (k - lo[d])], R[d * N + n], s0);
+            const double s = (s0 + s1) + (s2 + s3);
             const double y = Y[e];
             const double yp = k > 0 ? Y[e - N] : y, yn = k + 1 < M ? Y[e + N] : y;
             G[e] = fma(a.gamma, (y - yp) + (y - yn), s);

@@ -1440,7 +1440,7 @@ __global__ void __launch_bounds__(256) k_proj_wide(WideArgs a)
     }
     mn = 2.0 * wmin(mn);
     const double lam = -mn, lamp = fmax(lam, 0.0);
-    const double tk = act ? a.tstep[kl] : 0.0;
+    const double tk = act ? (a.tscal ? *a.tscal : a.tstep[kl]) : 0.0;
     double s = 0.0, xm = -INFINITY, xn = INFINITY;
 #pragma unroll
     for (int v = 0; v < VM; v++) {
@@ -1708,6 +1708,101 @@ cudaError_t launch_bb_stats(const double *th, const double *tp, int64_t Ml, int6
     k_bb_sum<<<1, 32, 0, s>>>(part, BB_BLOCKS, vec3, st);
     return cudaGetLastError();
 }
+// BB with the exact line search (reading R17): Z = P(Theta - t G) is in zt (halo rows included),
+// R_k in Rk, R_Z = F Z - P in Rz.  Block partials (fixed order) of
+//   ||F d||^2 = ||R_Z - R_k||^2,  <R_k, F d>,  ||D d||^2,  <D Theta, D d>,  ||d||^2,   d = Z - Theta,
+// then one thread: <G,d> = <R_k, F d> + gamma <D Theta, D d>, lambda* = clip(max(-<G,d>, ||d||^2 / t)
+// / (||F d||^2 + gamma ||D d||^2), 0, 1).
+constexpr int BBLS_VALS = 5;
+__global__ void __launch_bounds__(256) k_bbls_stats(const double *th, const double *zt, int64_t Ml, int64_t kb,
+                                                    int64_t M, int N, const double *Rk, const double *Rz, int64_t nR,
+                                                    double *part, const DevState *st)
+{
+    __shared__ double red[8 * BBLS_VALS];
+    if (st && st->stop) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double v[BBLS_VALS] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    const int64_t tot = Ml * N, chunk = (tot + gridDim.x - 1) / gridDim.x;
+    const int64_t e0 = blockIdx.x * chunk, e1 = min(tot, e0 + chunk);
+    for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+        const double d = zt[e] - th[e];
+        v[4] = fma(d, d, v[4]);
+        const int64_t row = e / N;
+        if (kb + row + 1 < M) {   // pair (row, row + 1), the slice's last row with its halo row
+            const double dn = zt[e + N] - th[e + N];
+            const double dd = d - dn, dt = th[e] - th[e + N];
+            v[2] = fma(dd, dd, v[2]);
+            v[3] = fma(dt, dd, v[3]);
+        }
+    }
+    if (Rk) {
+        const int64_t c2 = (nR + gridDim.x - 1) / gridDim.x, r0 = blockIdx.x * c2, r1 = min(nR, r0 + c2);
+        for (int64_t e = r0 + threadIdx.x; e < r1; e += blockDim.x) {
+            const double fd = Rz[e] - Rk[e];
+            v[0] = fma(fd, fd, v[0]);
+            v[1] = fma(Rk[e], fd, v[1]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < BBLS_VALS; i++) v[i] = wsum(v[i]);
+    if (lane == 0)
+#pragma unroll
+        for (int i = 0; i < BBLS_VALS; i++) red[warp * BBLS_VALS + i] = v[i];
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int i = 0; i < BBLS_VALS; i++) {
+            double x = 0.0;
+            for (int w = 0; w < 8; w++) x += red[w * BBLS_VALS + i];
+            part[blockIdx.x * BBLS_VALS + i] = x;
+        }
+}
+__global__ void k_bbls_sum(const double *part, int nblk, double *vec, const DevState *st)
+{
+    if (threadIdx.x || (st && st->stop)) return;
+    for (int i = 0; i < BBLS_VALS; i++) {
+        double x = 0.0;
+        for (int b = 0; b < nblk; b++) x += part[b * BBLS_VALS + i];
+        vec[i] = x;
+    }
+}
+__global__ void k_bbls_lambda(const double *vec, double gamma, const double *tbb, double *lam, const DevState *st)
+{
+    if (threadIdx.x || (st && st->stop)) return;
+    const double fdd = vec[0], rfd = vec[1], ddd = vec[2], tdd = vec[3], dd = vec[4];
+    const double gd = rfd + gamma * tdd;                 // <G, d>
+    const double den = fdd + gamma * ddd;
+    const double num = fmax(-gd, dd / *tbb);
+    double l = 1.0;
+    if (den > 0.0) {
+        l = num / den;
+        l = l < 0.0 ? 0.0 : (l > 1.0 ? 1.0 : l);
+    }
+    *lam = l;
+}
+// Theta_{k+1} = Theta_k + lambda (Z - Theta_k), in place over Z, halo rows included
+__global__ void k_bbls_update(const double *th, double *zt, int64_t n, const double *lam, const DevState *st)
+{
+    if (st && st->stop) return;
+    const double l = *lam;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+        zt[e] = fma(l, zt[e] - th[e], th[e]);
+}
+cudaError_t launch_bbls_stats(const double *th, const double *zt, int64_t Ml, int64_t kb, int64_t M, int N,
+                              const double *Rk, const double *Rz, int64_t nR, double *part, double *vec,
+                              const DevState *st, cudaStream_t s)
+{
+    k_bbls_stats<<<BB_BLOCKS, 256, 0, s>>>(th, zt, Ml, kb, M, N, Rk, Rz, nR, part, st);
+    k_bbls_sum<<<1, 32, 0, s>>>(part, BB_BLOCKS, vec, st);
+    return cudaGetLastError();
+}
+cudaError_t launch_bbls_step(const double *vec, double gamma, const double *tbb, double *lam, const double *th,
+                             double *zt, int64_t n, const DevState *st, cudaStream_t s)
+{
+    k_bbls_lambda<<<1, 32, 0, s>>>(vec, gamma, tbb, lam, st);
+    k_bbls_update<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, s>>>(th, zt, n, lam, st);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_bb_step(const double *vec3, double gamma, double tlip, double *tout,
                            const DevState *st, cudaStream_t s)
 {

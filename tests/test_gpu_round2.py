@@ -180,3 +180,32 @@ def test_megascale_fista_60_iterations(q, ctx):
     """SQS-FISTA, the mode of the time-to-tol ladder, with the KKT recorded every 5 iterations
     (bench.py's time_to_tol setting)."""
     _full(q, ctx, qs.megascale(), 60, accel=1, kkt_every=5)
+
+
+# ------------------------------------------------------- BB: line search (R17) and N > 128
+@pytest.mark.parametrize("step", ["BB", "BB_LS"])
+@pytest.mark.parametrize("N", [6, 151, 300, 1500])
+def test_bb_modes_first_iterates_and_minimiser(q, ctx, step, N):
+    """BB (R14) and BB with the exact line search (R17) at N <= 128 (k_bwd_mma),
+    odd 151 (padded pitch), 300 (two-kernel wide sweep) and 1500 (fused wide step): the first
+    iterates match the oracle (parity is gated at convergence + first iterates, reading R5) and
+    the long run reaches the oracle's minimiser; BB-LS never increases f."""
+    rng = np.random.default_rng(N)
+    D, M = 70, 40
+    a2 = np.sort(rng.uniform(0.0, 30.0, D))
+    P = rng.dirichlet(np.ones(N), D)
+    g = 1e-2
+    Fo = oracle.Probes(a2, M)
+    Fg = q.qdt_build_probes(ctx, a2, M)
+    so = getattr(oracle, "STEP_" + step)
+    sg = getattr(q, "QDT_STEP_" + step)
+    ro = oracle.solve(Fo, P, g, 0.0, 3, step=so)
+    rg = q.qdt_solve(ctx, Fg, P, g, 0.0, 3, step=sg)
+    assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9
+    ro = oracle.solve(Fo, P, g, 1e-13, 20000, step=so)
+    rg = q.qdt_solve(ctx, Fg, P, g, 1e-13, 20000, step=sg)
+    assert ro["kkt"][-1] <= 1e-12 and rg["kkt"][-1] <= 1e-12
+    assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9
+    if step == "BB_LS":
+        tr = rg["trace"]
+        assert np.all(tr[1:] <= tr[:-1] * (1 + 1e-12))

@@ -573,3 +573,60 @@ def test_fista_resume_continues_the_sequence():
     # a fresh restart from Theta_4 (momentum reset) is a different sequence
     c = oracle.solve(F, P, gamma, 0.0, 5, accel=1, theta0=a["theta"])
     assert np.abs(c["theta"] - full["theta"]).max() > 1e-9
+
+
+# ------------------------------------------------------------- BB + exact line search (R17)
+@pytest.mark.parametrize("gamma", [1e-3, 1e-2])
+def test_bb_line_search_qp_optimum_and_monotone(gamma):
+    """BB with the exact line search along the projected direction (reading
+    R17) converges to the brute-force QP optimum (P11) and, unlike the unsafeguarded BB step,
+    never increases f (an exact minimisation along a feasible direction)."""
+    rng = np.random.default_rng(310)
+    M, N, D = 4, 3, 8
+    F = oracle.Probes(np.sort(rng.uniform(0.3, 3.0, D)), M)
+    P = rng.dirichlet(np.ones(N), size=D)
+    sols = _brute_qp(F.dense(), P, gamma)
+    r = oracle.solve(F, P, gamma, 0.0, 3000, step=oracle.STEP_BB_LS)
+    np.testing.assert_allclose(r["theta"], sols[0][0], atol=1e-12)
+    tr = r["trace"]
+    assert np.all(tr[1:] <= tr[:-1] * (1 + 1e-13) + 1e-300)
+
+
+def test_bb_line_search_step_formula():
+    """Iteration 2 of BB-LS reproduced in dense NumPy: BB t from s = Theta_1 - Theta_0, Z =
+    P_S(Theta_1 - t G), d = Z - Theta_1, l* = clip(-<G,d> / (||F d||^2 + gamma ||D d||^2), 0, 1)
+    from the quadratic f(Theta + l d) (no oracle function on the path except the pinned
+    forward / backward / projection)."""
+    rng = np.random.default_rng(311)
+    F = oracle.Probes(np.sort(rng.uniform(0.2, 6.0, 10)), 7)
+    P = rng.dirichlet(np.ones(4), 10)
+    g = 0.05
+    A = F.dense()
+
+    def f(T):
+        return float(np.sum((A @ T - P) ** 2) + g * np.sum(np.diff(T, axis=0) ** 2))
+
+    th0 = np.full((7, 4), 0.25)
+    rho = oracle.power_iteration(F, 100)
+    tl = 1.0 / (1.01 * rho + 4 * g)
+    th = [th0]
+    for k in range(2):   # two iterations by hand
+        T = th[-1]
+        G = A.T @ (A @ T - P) + g * _np_L(T)
+        if k == 0:
+            t = tl
+        else:
+            s = th[-1] - th[-2]
+            t = np.sum(s * s) / (np.sum((A @ s) ** 2) + g * np.sum(np.diff(s, axis=0) ** 2))
+            t = min(max(t, tl), 1e6 * tl)
+        d = _np_project_rows(T - t * G) - T
+        den = np.sum((A @ d) ** 2) + g * np.sum(np.diff(d, axis=0) ** 2)
+        assert -np.sum(G * d) >= np.sum(d * d) / t * (1 - 1e-12)   # projection property
+        lam = min(max(max(-np.sum(G * d), np.sum(d * d) / t) / den, 0.0), 1.0)
+        nxt = T + lam * d
+        # l* is the exact minimiser of f along d on [0, 1]
+        for l2 in (0.0, 1.0, lam * 0.9, min(1.0, lam * 1.1)):
+            assert f(nxt) <= f(T + l2 * d) + 1e-15
+        th.append(nxt)
+    r = oracle.solve(F, P, g, 0.0, 2, step=oracle.STEP_BB_LS)
+    np.testing.assert_allclose(r["theta"], th[2], atol=1e-13)
