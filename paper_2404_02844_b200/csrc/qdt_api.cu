@@ -1518,8 +1518,13 @@ static qdt_status band_exchange(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, do
 }
 
 static qdt_status fwd_reduce(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, const double *theta,
-                             double *R, bool withP)
+                             double *R, bool withP, double *partR_alt = nullptr)
 {
+    if (partR_alt) {   // a side product (e.g. F d of the line search): keep ||R_k||^2's partials
+        SolveBufs b2 = b;
+        b2.partR = partR_alt;
+        return fwd_reduce(ctx, c, b2, theta, R, withP, nullptr);
+    }
     cudaStream_t s = ctx->stream;
     Plan *pl = c.pl;
     qdt_probes *p = c.p;
@@ -1840,9 +1845,14 @@ static qdt_status iteration(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, int64_
         }
         CKS(halo_exchange(ctx, c, nxt));
         if (c.bb == 2) {
-            // exact line search along d = Z - Theta_k (reading R17): R_Z = F Z - P, the step
-            // statistics, lambda* on the device, Theta_{k+1} = Theta_k + lambda* d over Z
-            CKS(fwd_reduce(ctx, c, b, nxt, b.RY, true));
+            // exact line search along d = Z - Theta_k (reading R17): F d by a forward pass of d, the
+            // step statistics, lambda* on the device, Theta_{k+1} = Theta_k + lambda* d over Z
+            CK(run_k(ctx, "bb_step", 1, [&]() {
+                return launch_bbls_dir(cur - c.N, nxt - c.N, b.theta[2] - c.N, (p->Ml + 2) * (int64_t)c.N, b.state, s);
+            }));
+            double *pr_alt;
+            CKS(ws_get(ctx, "partR_alt", std::max(ctx->nblkR, pl->nR), &pr_alt));
+            CKS(fwd_reduce(ctx, c, b, b.theta[2], b.RY, false, pr_alt));
             CK(run_k(ctx, "bb_step", 2, [&]() {
                 return launch_bbls_stats(cur, nxt, p->Ml, p->kb, p->M, c.N, ctx->rank == 0 ? Rk : nullptr, b.RY,
                                          p->D * (int64_t)c.N, b.bb_part, b.bb_vec, b.state, s);
@@ -2209,7 +2219,13 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
         CKS(ws_get(ctx, "bb_part", 5 * BB_NBLK, &b.bb_part));
         CKS(ws_get(ctx, "bb_vec", 5, &b.bb_vec));
         CKS(ws_get(ctx, "tbb", 2, &b.tbb));   // [0] t_k, [1] lambda* (line search)
-        if (opt.step == QDT_STEP_BB_LS) CKS(ws_get(ctx, "RY", D * N + 4, &b.RY));
+        if (opt.step == QDT_STEP_BB_LS) {
+            CKS(ws_get(ctx, "RY", D * N + 4, &b.RY));
+            double *t2;
+            CKS(ws_get(ctx, "theta2", rowsz + 2, &t2));   // the direction d = Z - Theta_k
+            b.theta[2] = t2 + N;
+            CK(cudaMemsetAsync(t2, 0, sizeof(double) * rowsz, s));
+        }
     }
     if (fista) {
         CKS(ws_get(ctx, "R1", D * N + 4, &b.R[1]));

@@ -268,6 +268,8 @@ cudaError_t launch_bb_step(const double *vec3, double gamma, double tlip, double
 cudaError_t launch_bbls_stats(const double *th, const double *zt, int64_t Ml, int64_t kb, int64_t M, int N,
                               const double *Rk, const double *Rz, int64_t nR, double *part, double *vec,
                               const DevState *st, cudaStream_t s);
+cudaError_t launch_bbls_dir(const double *th, const double *zt, double *dd, int64_t n, const DevState *st,
+                            cudaStream_t s);
 cudaError_t launch_bbls_step(const double *vec, double gamma, const double *tbb, double *lam, const double *th,
                              double *zt, int64_t n, const DevState *st, cudaStream_t s);
 cudaError_t launch_smooth(const double *X, int64_t M, int N, int64_t exclude, int64_t div, double *S,

@@ -1709,8 +1709,8 @@ cudaError_t launch_bb_stats(const double *th, const double *tp, int64_t Ml, int6
     return cudaGetLastError();
 }
 // BB with the exact line search (reading R17): Z = P(Theta - t G) is in zt (halo rows included),
-// R_k in Rk, R_Z = F Z - P in Rz.  Block partials (fixed order) of
-//   ||F d||^2 = ||R_Z - R_k||^2,  <R_k, F d>,  ||D d||^2,  <D Theta, D d>,  ||d||^2,   d = Z - Theta,
+// R_k in Rk, F d in Rz (d = Z - Theta).  Block partials (fixed order) of
+//   ||F d||^2,  <R_k, F d>,  ||D d||^2,  <D Theta, D d>,  ||d||^2,
 // then one thread: <G,d> = <R_k, F d> + gamma <D Theta, D d>, lambda* = clip(max(-<G,d>, ||d||^2 / t)
 // / (||F d||^2 + gamma ||D d||^2), 0, 1).
 constexpr int BBLS_VALS = 5;
@@ -1738,7 +1738,7 @@ __global__ void __launch_bounds__(256) k_bbls_stats(const double *th, const doub
     if (Rk) {
         const int64_t c2 = (nR + gridDim.x - 1) / gridDim.x, r0 = blockIdx.x * c2, r1 = min(nR, r0 + c2);
         for (int64_t e = r0 + threadIdx.x; e < r1; e += blockDim.x) {
-            const double fd = Rz[e] - Rk[e];
+            const double fd = Rz[e];   // F d (a forward pass of d: accurate for small d)
             v[0] = fma(fd, fd, v[0]);
             v[1] = fma(Rk[e], fd, v[1]);
         }
@@ -1778,6 +1778,19 @@ __global__ void k_bbls_lambda(const double *vec, double gamma, const double *tbb
         l = l < 0.0 ? 0.0 : (l > 1.0 ? 1.0 : l);
     }
     *lam = l;
+}
+// d = Z - Theta_k (halo rows included)
+__global__ void k_bbls_dir(const double *th, const double *zt, double *dd, int64_t n, const DevState *st)
+{
+    if (st && st->stop) return;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+        dd[e] = zt[e] - th[e];
+}
+cudaError_t launch_bbls_dir(const double *th, const double *zt, double *dd, int64_t n, const DevState *st,
+                            cudaStream_t s)
+{
+    k_bbls_dir<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, s>>>(th, zt, dd, n, st);
+    return cudaGetLastError();
 }
 // Theta_{k+1} = Theta_k + lambda (Z - Theta_k), in place over Z, halo rows included
 __global__ void k_bbls_update(const double *th, double *zt, int64_t n, const double *lam, const DevState *st)
