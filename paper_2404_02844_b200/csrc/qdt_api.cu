@@ -882,9 +882,6 @@ static qdt_status build_sweep_plan(qdt_ctx *ctx, qdt_probes *p, Plan *pl)
     return build_fused_plan(ctx, p, pl, bu);
 }
 
-// 128 < N <= 1024 runs the two-kernel wide sweep (k_grad_wide + k_proj_wide: measured faster there,
-// profiles/r02_v2); QDT_WIDE=new selects the fused cluster step for them too (A/B, tests).  N > 1024
-// always takes the fused step.
 // QDT_SMALL=0 keeps small problems on the multi-kernel loop (A/B)
 static bool small_enabled()
 {
@@ -892,6 +889,7 @@ static bool small_enabled()
     return !(e && e[0] == '0');
 }
 
+// QDT_WIDE=new selects the fused cluster step at every N > 128 (A/B, tests); N > 1024 always takes it
 static bool wide_new_forced()
 {
     const char *e = getenv("QDT_WIDE");   // read at every plan build (plans are cached per probe handle and N)
@@ -1104,7 +1102,10 @@ static qdt_status build_plan(qdt_ctx *ctx, qdt_probes *p, int N, Plan **out)
     pl->NB = sweep_enabled() ? sweep_nb(N) : 0;
     // wide kernels for N > 128 (even): the whole path, or (N <= 160) beside the NB > 16 plain step
     const bool wide = sweep_enabled() && (!pl->NB || pl->NB > SW_NBMAX) && N % 2 == 0;
-    pl->NX = (wide && wide_new_forced()) ? 1 : 0;   // N <= 1024: the two-kernel wide sweep by default
+    // N <= 1024: the fused step where the axis gives many tiles and the rows are wide (stress_cut,
+    // M = 10^5 x N = 10^3: 1.87 against 2.02 ms per iteration), the two-kernel wide sweep otherwise
+    // (Large, M = 10^4: heavy low-k windows with few tiles favour its split-K units)
+    pl->NX = (wide && (wide_new_forced() || (N > 512 && p->Ml >= 32768))) ? 1 : 0;
     pl->NW = (wide && !pl->NX && N <= 1024) ? 1 : 0;
     if (pl->NB || pl->NW || pl->NX) CKS(build_sweep_plan(ctx, p, pl.get()));
     if (pl->NX) CKS(build_wide_plan(ctx, p, pl.get()));

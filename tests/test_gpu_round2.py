@@ -205,7 +205,11 @@ def test_bb_modes_first_iterates_and_minimiser(q, ctx, step, N):
     ro = oracle.solve(Fo, P, g, 1e-13, 20000, step=so)
     rg = q.qdt_solve(ctx, Fg, P, g, 1e-13, 20000, step=sg)
     assert ro["kkt"][-1] <= 1e-12 and rg["kkt"][-1] <= 1e-12
-    assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9
+    # the same minimiser: f to 1e-12; Theta to the conditioning of the instance (two ORACLE modes,
+    # BB and BB-LS, stopped at r_KKT <= 1e-13 differ by up to 1.3e-8 at N = 1500: a KKT residual of
+    # 1e-13 pins Theta* only that far on these few-probe instances)
+    assert rg["trace"][-1] == pytest.approx(ro["trace"][-1], rel=1e-12)
+    assert np.abs(rg["theta"] - ro["theta"]).max() <= (1e-9 if N <= 128 else 1e-7)
     if step == "BB_LS":
         tr = rg["trace"]
         assert np.all(tr[1:] <= tr[:-1] * (1 + 1e-12))
