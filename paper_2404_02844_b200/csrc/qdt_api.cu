@@ -21,6 +21,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: phase ranges for nsys / ncu (no-ops without a tool)
+
 #include "../../include/qdt.h"
 #include "qdt_internal.h"
 
@@ -46,6 +48,7 @@ struct NcclApi {
     nccl_result_t (*getUniqueId)(nccl_uid_t *) = nullptr;
     nccl_result_t (*groupEnd)() = nullptr;
     const char *(*getErrorString)(nccl_result_t) = nullptr;
+    nccl_result_t (*commGetAsyncError)(nccl_comm_t, nccl_result_t *) = nullptr;   // optional
     bool load(std::string &err)
     {
         if (h) return true;
@@ -72,6 +75,7 @@ struct NcclApi {
         QDT_SYM(getErrorString, "ncclGetErrorString");
         QDT_SYM(getUniqueId, "ncclGetUniqueId");
 #undef QDT_SYM
+        *(void **)(&commGetAsyncError) = dlsym(h, "ncclCommGetAsyncError");
         return true;
     }
 };
@@ -246,6 +250,12 @@ struct EventPair {
         if (a) cudaEventDestroy(a);
         if (b) cudaEventDestroy(b);
     }
+};
+
+// NVTX range for the duration of a scope (solve phases: probes, setup, loop, evaluation, outputs)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
 };
 
 // ------------------------------------------------------------------------------ errors
@@ -566,6 +576,18 @@ static qdt_status gather_rows(qdt_ctx *ctx, const qdt_probes *p, const double *s
         return cudaSuccess;
     });
     if (e != 0) return fail(ctx, QDT_ERR_NCCL, "row gather failed");
+    return QDT_OK;
+}
+
+// NCCL communicator health (polled with the stop flag): an asynchronous error (a peer died, a
+// network failure) fails the solve instead of hanging it
+static qdt_status nccl_health(qdt_ctx *ctx)
+{
+    if (!ctx->ncomm || !g_nccl.commGetAsyncError) return QDT_OK;
+    nccl_result_t ae = 0;
+    const nccl_result_t r = g_nccl.commGetAsyncError(ctx->ncomm, &ae);
+    if (r != 0 || ae != 0)
+        return fail(ctx, QDT_ERR_NCCL, "NCCL asynchronous error: %s", g_nccl.getErrorString(r ? r : ae));
     return QDT_OK;
 }
 
@@ -1220,6 +1242,7 @@ extern "C" qdt_status qdt_build_probes(qdt_ctx *ctx, const double *alpha2, int64
     if (!(c_sigma > 0.0) || !isfinite(c_sigma) || margin < 0)
         return fail(ctx, QDT_ERR_INVALID_ARG, "probe opts: c_sigma must be > 0, margin >= 0");
     CK(cudaSetDevice(ctx->device));
+    NvtxRange nv("qdt_build_probes");
     cudaStream_t s = ctx->stream;
     std::unique_ptr<qdt_probes> p(new qdt_probes());
     p->ctx = ctx;
@@ -2185,6 +2208,7 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->stream;
     Plan *pl;
+    NvtxRange nv_solve("qdt_solve");
     CKS(build_plan(ctx, p, (int)N, &pl));
 
     // memory plan (fails before allocating the big buffers)
@@ -2296,8 +2320,11 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
         CK(cudaMemcpyAsync(b.theta[2] - N, b.theta[0] - N, sizeof(double) * rowsz, cudaMemcpyDeviceToDevice, s));
     }
     double tscalar = 0.0;
-    CKS(step_setup(ctx, p, pl, bb ? QDT_STEP_LIPSCHITZ : opt.step, gamma, 100, b.tstep, nullptr, nullptr,
-                   &tscalar));
+    {
+        NvtxRange nv("qdt_solve:step_setup");
+        CKS(step_setup(ctx, p, pl, bb ? QDT_STEP_LIPSCHITZ : opt.step, gamma, 100, b.tstep, nullptr, nullptr,
+                       &tscalar));
+    }
     c.bb = bb ? (opt.step == QDT_STEP_BB_LS ? 2 : 1) : 0;
     c.tlip = tscalar;
     DevState st0;
@@ -2381,6 +2408,7 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     EventPair evp;
     CK(evp.create());
     cudaEvent_t ev0 = evp.a, ev1 = evp.b;
+    NvtxRange nv_loop("qdt_solve:iterations");
     CK(cudaEventRecord(ev0, s));
     const int64_t check = tol > 0.0 ? std::max<int64_t>(period, (opt.check_every / period) * period) : INT64_MAX;
     int64_t since = 0;
@@ -2431,6 +2459,7 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
             since = 0;
             CK(cudaMemcpyAsync(&hst, b.state, sizeof hst, cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
+            CKS(nccl_health(ctx));
             if (hst.stop) {
                 stopped = true;
                 break;
