@@ -1554,7 +1554,7 @@ static qdt_status fwd_reduce(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, const
     qdt_probes *p = c.p;
     const bool multi = ctx->nranks > 1;
     if (pl->NB || pl->NW || pl->NX) {
-        const int fnb = (pl->NW || pl->NX) ? wide_nb(c.N) : pl->NB;   // wide N: balanced column chunks
+        const int fnb = (pl->NW || pl->NX) ? wide_fwd_nb(c.N) : pl->NB;   // wide N: balanced column chunks
         SweepFwdArgs fa;
         fa.N = c.N;
         fa.Ml = (int)p->Ml;

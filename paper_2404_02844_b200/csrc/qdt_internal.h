@@ -253,6 +253,7 @@ cudaError_t launch_wide_step(const WStepArgs &a, int nclusters, cudaStream_t s);
 cudaError_t launch_grad_wide(const WideArgs &a, int nunits, cudaStream_t s);
 cudaError_t launch_proj_wide(const WideArgs &a, cudaStream_t s);
 int wide_nb(int N);                                  // balanced column-chunk width / 8 (N > 128)
+int wide_fwd_nb(int N);                              // same for the forward (<= 13 n-blocks: 2 CTAs / SM)
 constexpr int PW_BLOCKS = 148 * 8;                   // k_proj_wide grid cap (contiguous row ranges)
 int wide_proj_blocks(int Ml);
 constexpr int SW_FUSED_SMEM_MAX = 220 * 1024;

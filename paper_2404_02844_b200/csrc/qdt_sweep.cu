@@ -1277,6 +1277,15 @@ int wide_nb(int N)
     const int ncc = (N + 127) / 128;
     return ((N + 7) / 8 + ncc - 1) / ncc;
 }
+// forward column chunks at wide N: balanced widths of at most 13 n-blocks, so that the staged
+// half tiles (pitch 8 NB + 4) and F blocks of two CTAs fit one SM (16 warps; 16 n-blocks = 128
+// columns left one CTA per SM, latency bound)
+int wide_fwd_nb(int N)
+{
+    const int nbt = (N + 7) / 8;
+    const int ncc = (nbt + 12) / 13;
+    return (nbt + ncc - 1) / ncc;
+}
 size_t wide_grad_smem() { return (size_t)(2 * SKC * STP + 2 * SKC * (8 * 16 + 4) + 8) * sizeof(double); }
 
 template <int NB>
