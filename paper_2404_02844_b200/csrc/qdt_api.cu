@@ -220,11 +220,17 @@ struct qdt_probes {
     int64_t *d_fb_off = nullptr;
     double *d_Fb = nullptr;
     int32_t *d_row_da = nullptr, *d_row_db = nullptr;   // probes covering each local row (small solve)
+    // step-setup cache (per probe handle): the step t_k per local row of the last (mode, gamma); F
+    // is immutable, so a repeated solve reuses the SQS weights / the 100-step power iteration
+    double *d_tcache = nullptr;
+    int tc_mode = -1;
+    double tc_gamma = NAN, tc_scalar = 0.0;
     Band band() const { return Band{d_lo, d_len, d_off, d_val}; }
     ~qdt_probes()
     {
         cudaFree(d_row_da);
         cudaFree(d_row_db);
+        cudaFree(d_tcache);
         cudaFree(d_sw_dA);
         cudaFree(d_sw_dB);
         cudaFree(d_fb_off);
@@ -2322,8 +2328,18 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     double tscalar = 0.0;
     {
         NvtxRange nv("qdt_solve:step_setup");
-        CKS(step_setup(ctx, p, pl, bb ? QDT_STEP_LIPSCHITZ : opt.step, gamma, 100, b.tstep, nullptr, nullptr,
-                       &tscalar));
+        const int smode = bb ? QDT_STEP_LIPSCHITZ : opt.step;
+        if (p->d_tcache && p->tc_mode == smode && p->tc_gamma == gamma) {   // cached step (same F, mode, gamma)
+            CK(cudaMemcpyAsync(b.tstep, p->d_tcache, sizeof(double) * Ml, cudaMemcpyDeviceToDevice, s));
+            tscalar = p->tc_scalar;
+        } else {
+            CKS(step_setup(ctx, p, pl, smode, gamma, 100, b.tstep, nullptr, nullptr, &tscalar));
+            if (!p->d_tcache) CK(cudaMalloc(&p->d_tcache, sizeof(double) * std::max<int64_t>(1, Ml)));
+            CK(cudaMemcpyAsync(p->d_tcache, b.tstep, sizeof(double) * Ml, cudaMemcpyDeviceToDevice, s));
+            p->tc_mode = smode;
+            p->tc_gamma = gamma;
+            p->tc_scalar = tscalar;
+        }
     }
     c.bb = bb ? (opt.step == QDT_STEP_BB_LS ? 2 : 1) : 0;
     c.tlip = tscalar;

@@ -22,20 +22,30 @@
 
 namespace qdt {
 
-constexpr int SM_THREADS = 1024;
+constexpr int SM_THREADS = 256;   // 8 warps: cheap block barriers; every phase loops over its items
 
-// fixed-order block sum of one value per thread (all threads return the total)
-__device__ __forceinline__ double sm_block_sum(double v, double *red)
+// fixed-order block sums of two values per thread (all threads return the totals)
+__device__ __forceinline__ void sm_block_sum2(double &v0, double &v1, double *red)
 {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    for (int o = 16; o > 0; o >>= 1) {
+        v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+        v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+    }
     __syncthreads();
-    if (lane == 0) red[warp] = v;
+    if (lane == 0) {
+        red[2 * warp] = v0;
+        red[2 * warp + 1] = v1;
+    }
     __syncthreads();
-    double t = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += red[w];
-    return t;
+    double t0 = 0.0, t1 = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+        t0 += red[2 * w];
+        t1 += red[2 * w + 1];
+    }
+    v0 = t0;
+    v1 = t1;
 }
 
 size_t small_solve_smem(int64_t D, int64_t M, int N, int64_t nnz, int fista)
@@ -49,7 +59,7 @@ size_t small_solve_smem(int64_t D, int64_t M, int N, int64_t nnz, int fista)
 __global__ void __launch_bounds__(SM_THREADS, 1) k_small_solve(SmallArgs a)
 {
     extern __shared__ __align__(16) double sm[];
-    __shared__ double red[32];
+    __shared__ double red[64];
     __shared__ int s_stop;
     const int D = a.D, M = a.M, N = a.N;
     const int MN = M * N, DN = D * N;
@@ -144,8 +154,9 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_solve(SmallArgs a)
             }
         }
         const double nm = (double)N * (double)M;
-        *r = sqrt(sm_block_sum(s1, red) / nm);
-        *rp = sqrt(sm_block_sum(s2, red) / nm);
+        sm_block_sum2(s1, s2, red);
+        *r = sqrt(s1 / nm);
+        *rp = sqrt(s2 / nm);
     };
     auto objective = [&](const double *T, const double *R) {
         double s = 0.0, g = 0.0;
@@ -154,9 +165,8 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_solve(SmallArgs a)
             const double dd = T[e] - T[e + N];
             g = fma(dd, dd, g);
         }
-        const double r2 = sm_block_sum(s, red);
-        const double rg = sm_block_sum(g, red);
-        return r2 + a.gamma * rg;
+        sm_block_sum2(s, g, red);
+        return s + a.gamma * g;
     };
 
     double *cur = T0, *nxt = T1, *prv = T2;
