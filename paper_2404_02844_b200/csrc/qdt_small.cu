@@ -51,8 +51,8 @@ __device__ __forceinline__ void sm_block_sum2(double &v0, double &v1, double *re
 size_t small_solve_smem(int64_t D, int64_t M, int N, int64_t nnz, int fista)
 {
     const int64_t MN = M * N, DN = D * N;
-    const int64_t dbl = nnz + (fista ? 4 : 3) * MN + (fista ? 3 : 2) * DN + M;   // F, Theta x3 (+G), P, R (+R_prev), t
-    const int64_t ints = 3 * D + 2 * M + 2;                                      // lo, len, off, row probe ranges
+    const int64_t dbl = 2 * nnz + (fista ? 4 : 3) * MN + (fista ? 3 : 2) * DN + M;   // F, F^T, Theta x3 (+G), P, R (+R_prev), t
+    const int64_t ints = 3 * D + 3 * M + 3;                                          // lo, len, off, row ranges, F^T offsets
     return (size_t)(dbl * 8 + ints * 4 + 64);
 }
 
@@ -65,7 +65,8 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_solve(SmallArgs a)
     const int MN = M * N, DN = D * N;
     const int tid = threadIdx.x, nth = blockDim.x;
     double *Fv = sm;
-    double *T0 = Fv + a.nnz;          // Theta buffers (rotation by the host layout: see below)
+    double *FT = Fv + a.nnz;          // F by Fock row: FT[toff[k] + d - ra[k]] = F[d][k]
+    double *T0 = FT + a.nnz;          // Theta buffers (rotation by the host layout: see below)
     double *T1 = T0 + MN;
     double *T2 = T1 + MN;             // Theta_{k-1} (FISTA) / scratch
     double *Gs = T2 + MN;             // G (FISTA: G at Theta_k for the KKT; plain: G)
@@ -78,6 +79,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_solve(SmallArgs a)
     int *of = ln + D;                 // D + 1
     int *ra = of + D + 1;             // probes covering row k: [ra[k], rb[k])
     int *rb = ra + M;
+    int *toff = rb + M;               // M + 1
     if (!a.fista) Gs = T2;            // plain: the third buffer holds G
 
     // ---- load the problem
@@ -97,6 +99,21 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_solve(SmallArgs a)
     }
     if (a.fista)
         for (int i = tid; i < MN; i += nth) T2[i] = a.theta_prev ? a.theta_prev[i] : a.theta0[i];
+    __syncthreads();
+    if (tid == 0) {   // F^T row offsets (prefix sums of the covering-probe counts)
+        int acc = 0;
+        for (int k = 0; k < M; k++) {
+            toff[k] = acc;
+            acc += rb[k] - ra[k];
+        }
+        toff[M] = acc;
+    }
+    __syncthreads();
+    for (int d = tid; d < D; d += nth)   // scatter F into its row-major transpose
+        for (int j = 0; j < ln[d]; j++) {
+            const int k = lo[d] + j;
+            FT[toff[k] + (d - ra[k])] = Fv[of[d] + j];
+        }
     __syncthreads();
 
     // band sums with four independent accumulators (combined in a fixed order): the chains are
@@ -124,15 +141,17 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_solve(SmallArgs a)
         for (int e = tid; e < MN; e += nth) {
             const int k = e / N, n = e - k * N;
             double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-            int d = ra[k];
-            const int d1 = rb[k];
-            for (; d + 4 <= d1; d += 4) {
-                s0 = fma(Fv[of[d] + (k - lo[d])], R[d * N + n], s0);
-                s1 = fma(Fv[of[d + 1] + (k - lo[d + 1])], R[(d + 1) * N + n], s1);
-                s2 = fma(Fv[of[d + 2] + (k - lo[d + 2])], R[(d + 2) * N + n], s2);
-                s3 = fma(Fv[of[d + 3] + (k - lo[d + 3])], R[(d + 3) * N + n], s3);
+            const double *ft = FT + toff[k];
+            const double *rc = R + ra[k] * N + n;
+            const int L = rb[k] - ra[k];
+            int i = 0;
+            for (; i + 4 <= L; i += 4) {
+                s0 = fma(ft[i], rc[i * N], s0);
+                s1 = fma(ft[i + 1], rc[(i + 1) * N], s1);
+                s2 = fma(ft[i + 2], rc[(i + 2) * N], s2);
+                s3 = fma(ft[i + 3], rc[(i + 3) * N], s3);
             }
-            for (; d < d1; d++) s0 = fma(Fv[of[d] + (k - lo[d])], R[d * N + n], s0);
+            for (; i < L; i++) s0 = fma(ft[i], rc[i * N], s0);
             const double s = (s0 + s1) + (s2 + s3);
             const double y = Y[e];
             const double yp = k > 0 ? Y[e - N] : y, yn = k + 1 < M ? Y[e + N] : y;

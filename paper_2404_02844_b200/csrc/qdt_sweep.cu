@@ -459,7 +459,9 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(con
     if (st && st->stop) return;
     const int64_t it = st ? st->it : 0;
     const int N = a.N;
-    const int Nv = a.Nv > 0 ? a.Nv : N;   // valid outcomes: a padded pitch's zero column is no coordinate
+    // valid outcomes: a padded pitch's zero column is no coordinate (only N > 128 is ever padded, so
+    // the NB <= 16 instantiations keep Nv == N at compile time: no extra register)
+    const int Nv = (NB > SW_NBMAX && a.Nv > 0) ? a.Nv : N;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g4 = lane >> 2, t4 = lane & 3;
     const int G = gridDim.x;
