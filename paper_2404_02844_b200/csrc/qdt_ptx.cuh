@@ -117,12 +117,6 @@ __device__ __forceinline__ double wsum(double v)
     return v;
 }
 
-// ---- programmatic dependent launch: the next kernel of the stream may launch (its prologue overlaps
-// this grid's tail); pdl_wait blocks until the previous grid has completed and its memory is visible.
-// Both are no-ops for a kernel launched without the programmatic-serialization attribute.
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-
 // ---- thread-block clusters (distributed shared memory)
 __device__ __forceinline__ uint32_t cluster_ctarank()
 {

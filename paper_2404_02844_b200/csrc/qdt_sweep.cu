@@ -20,40 +20,11 @@
 #include <stdlib.h>
 
 #include <algorithm>
-#include <utility>
 
 #include "qdt_internal.h"
 #include "qdt_ptx.cuh"
 
 namespace qdt {
-
-// Launch with programmatic stream serialization (PDL) for the kernels of the iteration loop that
-// open with pdl_trigger / pdl_wait: the launch and prologue of each overlap the previous kernel's
-// tail (QDT_PDL=0: ordinary launches)
-static bool pdl_enabled()
-{
-    static int v = -1;
-    if (v < 0) {
-        const char *e = getenv("QDT_PDL");
-        v = (e && e[0] == '0') ? 0 : 1;
-    }
-    return v == 1;
-}
-template <typename... KArgs, typename... Args>
-static cudaError_t launch_pdl(void (*k)(KArgs...), int grid, int block, size_t smem, cudaStream_t s, Args &&...args)
-{
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(block);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
-}
 
 // A 16-byte aligned bulk copy that covers n doubles starting at src: returns the element shift
 // (0 or 1) at which src[0] lands in dst and the byte count to copy.  The caller's buffers carry
@@ -480,8 +451,6 @@ size_t sweep_bwd_smem(int N, int NB, bool fista, bool tp)
 template <int NB, bool FIS, bool TP = false>
 __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(const __grid_constant__ SweepArgs a)
 {
-    pdl_trigger();
-    pdl_wait();
     extern __shared__ __align__(128) double sm[];
     __shared__ __align__(8) uint64_t bars[3];
     __shared__ double red[8 * 3];
@@ -988,8 +957,6 @@ size_t sweep_fwd_smem(int N, int NB)
 template <int NB>
 __global__ void __launch_bounds__(256, 2) k_fwd_mma(SweepFwdArgs a)
 {
-    pdl_trigger();
-    pdl_wait();
     extern __shared__ __align__(128) double sm[];
     __shared__ __align__(8) uint64_t bars[2];
     const DevState *st = a.state;
@@ -1875,8 +1842,6 @@ __global__ void __launch_bounds__(256) k_reduce_R2(const double *rpart, const in
                                                    double *R, int D, int N, double *partR,
                                                    const DevState *st)
 {
-    pdl_trigger();
-    pdl_wait();
     __shared__ double red[8];
     if (st && st->stop) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1926,8 +1891,6 @@ __global__ void __launch_bounds__(1024) k_scalars2(const double *partR, int nR, 
                                                    double *kktp, int64_t trace_len, DevState *st,
                                                    int finalize)
 {
-    pdl_trigger();
-    pdl_wait();
     __shared__ double red[32 * NV];
     (void)stage;
     (void)arrive;
@@ -2115,29 +2078,28 @@ cudaError_t launch_bwd_mma(const SweepArgs &a_in, int nunits, int NB, cudaStream
     const size_t smem = sweep_bwd_smem(a.N, NB, fis, tp);
     const int nsm = device_sm_count();
     const int grid = std::min(nunits, (NB <= 13 && !fis ? 2 : 1) * nsm);
-    cudaError_t e = cudaSuccess;
     switch (NB) {
 #define QDT_CASE(nb)                                                       \
     case nb:                                                               \
         if (fis)                                                           \
-            e = launch_pdl(k_bwd_mma<nb, true>, grid, 256, smem, s, a);    \
+            k_bwd_mma<nb, true><<<grid, 256, smem, s>>>(a);                \
         else if (tp)                                                       \
-            e = launch_pdl(k_bwd_mma<nb, false, true>, grid, 256, smem, s, a); \
+            k_bwd_mma<nb, false, true><<<grid, 256, smem, s>>>(a);         \
         else                                                               \
-            e = launch_pdl(k_bwd_mma<nb, false>, grid, 256, smem, s, a);   \
+            k_bwd_mma<nb, false><<<grid, 256, smem, s>>>(a);               \
         break;
         QDT_FOR_NB(QDT_CASE)
 #undef QDT_CASE
 #define QDT_CASE(nb)                                                       \
     case nb:                                                               \
         if (fis) return cudaErrorInvalidValue;                             \
-        e = launch_pdl(k_bwd_mma<nb, false>, grid, 256, smem, s, a);       \
+        k_bwd_mma<nb, false><<<grid, 256, smem, s>>>(a);                   \
         break;
         QDT_CASE(17) QDT_CASE(18) QDT_CASE(19) QDT_CASE(20)
 #undef QDT_CASE
         default: return cudaErrorInvalidValue;
     }
-    return e != cudaSuccess ? e : cudaGetLastError();
+    return cudaGetLastError();
 }
 
 // N-split bwd (512 threads): used when sweep_split_on(); same arguments as launch_bwd_mma
@@ -2186,15 +2148,14 @@ cudaError_t launch_fwd_mma(const SweepFwdArgs &a_in, int nunits, int NB, cudaStr
     a.ncc = (a.N + 8 * NB - 1) / (8 * NB);
     const size_t smem = sweep_fwd_smem(a.N, NB);
     nunits *= a.ncc;
-    cudaError_t e = cudaSuccess;
     switch (NB) {
 #define QDT_CASE(nb) \
-    case nb: e = launch_pdl(k_fwd_mma<nb>, nunits, 256, smem, s, a); break;
+    case nb: k_fwd_mma<nb><<<nunits, 256, smem, s>>>(a); break;
         QDT_FOR_NB(QDT_CASE)
 #undef QDT_CASE
         default: return cudaErrorInvalidValue;
     }
-    return e != cudaSuccess ? e : cudaGetLastError();
+    return cudaGetLastError();
 }
 
 cudaError_t launch_sweep_fused(const SweepFusedArgs &a, int nctas, int NB, cudaStream_t s)
@@ -2215,8 +2176,7 @@ cudaError_t launch_reduce_R2(const double *rpart, const int64_t *red_beg, const 
                              const double *P, double *R, int D, int N, double *partR,
                              const DevState *st, cudaStream_t s)
 {
-    cudaError_t e = launch_pdl(k_reduce_R2, (D + 7) / 8, 256, 0, s, rpart, red_beg, red_rows, P, R, D, N, partR, st);
-    if (e != cudaSuccess) return e;
+    k_reduce_R2<<<(D + 7) / 8, 256, 0, s>>>(rpart, red_beg, red_rows, P, R, D, N, partR, st);
     return cudaGetLastError();
 }
 
@@ -2226,9 +2186,10 @@ cudaError_t launch_scalars2(const double *partR, int nR, const double *partT, in
                             double *trace, double *kkt, double *kktp, int64_t trace_len,
                             DevState *st, int finalize, cudaStream_t s)
 {
-    cudaError_t e = launch_pdl(k_scalars2, 1, 1024, 0, s, partR, nR, partT, ntiles, include_r2, stage, arrive, vec,
-                               N, M, gamma, tol, final_eval, kkt_every, trace, kkt, kktp, trace_len, st, finalize);
-    return e != cudaSuccess ? e : cudaGetLastError();
+    k_scalars2<<<1, 1024, 0, s>>>(partR, nR, partT, ntiles, include_r2, stage, arrive, vec,
+                                          N, M, gamma, tol, final_eval, kkt_every, trace, kkt, kktp,
+                                          trace_len, st, finalize);
+    return cudaGetLastError();
 }
 
 }  // namespace qdt
