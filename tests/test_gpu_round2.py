@@ -213,3 +213,24 @@ def test_bb_modes_first_iterates_and_minimiser(q, ctx, step, N):
     if step == "BB_LS":
         tr = rg["trace"]
         assert np.all(tr[1:] <= tr[:-1] * (1 + 1e-12))
+
+
+def test_small_solve_resume_and_stop(q, ctx):
+    """The single-CTA solve (Tiny-sized problems): FISTA resume state bit for bit, early stop at the
+    oracle's iteration, BB is routed to the multi-kernel loop."""
+    I = qs.tiny()
+    Fg = q.qdt_build_probes(ctx, I.alpha2, I.M)
+    Fo = oracle.Probes(I.alpha2, I.M)
+    full = q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, 30, accel=True)
+    a = q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, 11, accel=True, want_prev=True)
+    b = q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, 19, accel=True, theta0=a["theta"], theta_prev=a["theta_prev"],
+                    fista_t=a["info"]["fista_t"])
+    assert np.array_equal(b["theta"], full["theta"])
+    ro = oracle.solve(Fo, I.P, I.gamma, 0.0, 30, accel=1)
+    assert np.abs(full["theta"] - ro["theta"]).max() <= 1e-9
+    tol = oracle.solve(Fo, I.P, I.gamma, 0.0, 30)["kkt"][17] * (1 + 1e-7)
+    ro2 = oracle.solve(Fo, I.P, I.gamma, tol, 30)
+    assert ro2["iters_done"] <= 17
+    rg2 = q.qdt_solve(ctx, Fg, I.P, I.gamma, tol, 30)
+    assert rg2["info"]["iters_done"] == ro2["iters_done"]
+    assert np.abs(rg2["theta"] - ro2["theta"]).max() <= 1e-9

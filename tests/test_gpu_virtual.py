@@ -63,6 +63,7 @@ CASES = {
     "sweep100": (400, 6000, 100, 5000.0, 1e-4, 30),
     "tiny10": (120, 3000, 10, 2500.0, 1e-3, 40),
     "wide300": (200, 4000, 300, 3300.0, 1e-4, 12),
+    "fused2048": (150, 3000, 2048, 2500.0, 1e-4, 6),   # N > 1024: the fused cluster step per rank
 }
 
 
