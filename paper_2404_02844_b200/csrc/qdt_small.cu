@@ -48,10 +48,32 @@ __device__ __forceinline__ void sm_block_sum2(double &v0, double &v1, double *re
     v1 = t1;
 }
 
+// segment reductions over S lanes (S a power of two <= 32; a row of N <= S outcomes per segment)
+__device__ __forceinline__ double seg_sum(double v, int S)
+{
+    for (int o = S >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, S);
+    return v;
+}
+__device__ __forceinline__ double seg_min(double v, int S)
+{
+    for (int o = S >> 1; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o, S));
+    return v;
+}
+__device__ __forceinline__ double seg_max(double v, int S)
+{
+    for (int o = S >> 1; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o, S));
+    return v;
+}
+__device__ __forceinline__ int seg_sum_i(int v, int S)
+{
+    for (int o = S >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, S);
+    return v;
+}
+
 size_t small_solve_smem(int64_t D, int64_t M, int N, int64_t nnz, int fista)
 {
     const int64_t MN = M * N, DN = D * N;
-    const int64_t dbl = 2 * nnz + (fista ? 4 : 3) * MN + (fista ? 3 : 2) * DN + M;   // F, F^T, Theta x3 (+G), P, R (+R_prev), t
+    const int64_t dbl = 2 * ((nnz + 1) & ~1LL) + (fista ? 4 : 3) * MN + (fista ? 3 : 2) * DN + M;   // F, F^T, Theta x3 (+G), P, R (+R_prev), t
     const int64_t ints = 3 * D + 3 * M + 3;                                          // lo, len, off, row ranges, F^T offsets
     return (size_t)(dbl * 8 + ints * 4 + 64);
 }
@@ -64,9 +86,10 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_solve(SmallArgs a)
     const int D = a.D, M = a.M, N = a.N;
     const int MN = M * N, DN = D * N;
     const int tid = threadIdx.x, nth = blockDim.x;
+    const int nnz2 = (a.nnz + 1) & ~1;  // keeps the arrays after F 16-byte aligned (double2 access)
     double *Fv = sm;
-    double *FT = Fv + a.nnz;          // F by Fock row: FT[toff[k] + d - ra[k]] = F[d][k]
-    double *T0 = FT + a.nnz;          // Theta buffers (rotation by the host layout: see below)
+    double *FT = Fv + nnz2;           // F by Fock row: FT[toff[k] + d - ra[k]] = F[d][k]
+    double *T0 = FT + nnz2;           // Theta buffers (rotation by the host layout: see below)
     double *T1 = T0 + MN;
     double *T2 = T1 + MN;             // Theta_{k-1} (FISTA) / scratch
     double *Gs = T2 + MN;             // G (FISTA: G at Theta_k for the KKT; plain: G)
@@ -118,7 +141,36 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_solve(SmallArgs a)
 
     // band sums with four independent accumulators (combined in a fixed order): the chains are
     // latency bound at these sizes
+    const bool pairs = (N & 1) == 0;   // even N: two outcomes per thread (double2), F loaded once
     auto residual = [&](const double *T, double *R, bool withP) {   // R = F T - P
+        if (pairs) {
+            const int N2 = N >> 1;
+            for (int e = tid; e < D * N2; e += nth) {
+                const int d = e / N2, n = 2 * (e - d * N2);
+                const double *f = Fv + of[d];
+                const double *tc = T + lo[d] * N + n;
+                const int L = ln[d];
+                double2 s0 = make_double2(0.0, 0.0), s1 = s0;
+                int j = 0;
+                for (; j + 2 <= L; j += 2) {
+                    const double2 t0 = *reinterpret_cast<const double2 *>(tc + j * N);
+                    const double2 t1 = *reinterpret_cast<const double2 *>(tc + (j + 1) * N);
+                    s0.x = fma(f[j], t0.x, s0.x), s0.y = fma(f[j], t0.y, s0.y);
+                    s1.x = fma(f[j + 1], t1.x, s1.x), s1.y = fma(f[j + 1], t1.y, s1.y);
+                }
+                if (j < L) {
+                    const double2 t0 = *reinterpret_cast<const double2 *>(tc + j * N);
+                    s0.x = fma(f[j], t0.x, s0.x), s0.y = fma(f[j], t0.y, s0.y);
+                }
+                double2 o = make_double2(s0.x + s1.x, s0.y + s1.y);
+                if (withP) {
+                    const double2 pp = *reinterpret_cast<const double2 *>(Ps + d * N + n);
+                    o.x -= pp.x, o.y -= pp.y;
+                }
+                *reinterpret_cast<double2 *>(R + d * N + n) = o;
+            }
+            return;
+        }
         for (int e = tid; e < DN; e += nth) {
             const int d = e / N, n = e - d * N;
             const double *f = Fv + of[d];
@@ -138,6 +190,35 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_solve(SmallArgs a)
         }
     };
     auto gradient = [&](const double *R, const double *Y, double *G) {   // G = F^T R + gamma L Y
+        if (pairs) {
+            const int N2 = N >> 1;
+            for (int e = tid; e < M * N2; e += nth) {
+                const int k = e / N2, n = 2 * (e - k * N2);
+                const double *ft = FT + toff[k];
+                const double *rc = R + ra[k] * N + n;
+                const int L = rb[k] - ra[k];
+                double2 s0 = make_double2(0.0, 0.0), s1 = s0;
+                int i = 0;
+                for (; i + 2 <= L; i += 2) {
+                    const double2 r0 = *reinterpret_cast<const double2 *>(rc + i * N);
+                    const double2 r1 = *reinterpret_cast<const double2 *>(rc + (i + 1) * N);
+                    s0.x = fma(ft[i], r0.x, s0.x), s0.y = fma(ft[i], r0.y, s0.y);
+                    s1.x = fma(ft[i + 1], r1.x, s1.x), s1.y = fma(ft[i + 1], r1.y, s1.y);
+                }
+                if (i < L) {
+                    const double2 r0 = *reinterpret_cast<const double2 *>(rc + i * N);
+                    s0.x = fma(ft[i], r0.x, s0.x), s0.y = fma(ft[i], r0.y, s0.y);
+                }
+                const double sx = s0.x + s1.x, sy = s0.y + s1.y;
+                const int e0 = k * N + n;
+                const double2 y = *reinterpret_cast<const double2 *>(Y + e0);
+                const double2 yp = k > 0 ? *reinterpret_cast<const double2 *>(Y + e0 - N) : y;
+                const double2 yn = k + 1 < M ? *reinterpret_cast<const double2 *>(Y + e0 + N) : y;
+                *reinterpret_cast<double2 *>(G + e0) = make_double2(fma(a.gamma, (y.x - yp.x) + (y.x - yn.x), sx),
+                                                                    fma(a.gamma, (y.y - yp.y) + (y.y - yn.y), sy));
+            }
+            return;
+        }
         for (int e = tid; e < MN; e += nth) {
             const int k = e / N, n = e - k * N;
             double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
@@ -159,8 +240,34 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_solve(SmallArgs a)
         }
     };
     // r_KKT of T with gradient G (reading R7; both multipliers), thread per row
+    // rows of N <= 32 outcomes: a segment of S lanes per row, one outcome per lane
+    const int S = N <= 1 ? 1 : (N <= 2 ? 2 : (N <= 4 ? 4 : (N <= 8 ? 8 : (N <= 16 ? 16 : 32))));
+    const bool seg = N <= 32;
+    const int lane = tid & 31, sl = lane & (S - 1);
+    const int spw = 32 / S;                                   // segments per warp
+    const int nseg = (nth / 32) * spw, segid = (tid >> 5) * spw + (lane / S);
+    const int mround = (M + nseg - 1) / nseg;                 // warp-uniform row loop
     auto kkt = [&](const double *T, const double *G, double *r, double *rp) {
         double s1 = 0.0, s2 = 0.0;
+        if (seg) {
+            for (int rr = 0; rr < mround; rr++) {
+                const int k = rr * nseg + segid;
+                const bool ok = k < M && sl < N;
+                const double g2 = ok ? 2.0 * G[k * N + sl] : INFINITY;
+                const double lam = -seg_min(g2, S), lamp = fmax(lam, 0.0);
+                if (ok) {
+                    const double th = T[k * N + sl];
+                    const double x1 = th * (g2 + lam), x2 = th * (g2 + lamp);
+                    s1 = fma(x1, x1, s1);
+                    s2 = fma(x2, x2, s2);
+                }
+            }
+            const double nm = (double)N * (double)M;
+            sm_block_sum2(s1, s2, red);
+            *r = sqrt(s1 / nm);
+            *rp = sqrt(s2 / nm);
+            return;
+        }
         for (int k = tid; k < M; k += nth) {
             double mn = INFINITY;
             for (int n = 0; n < N; n++) mn = fmin(mn, 2.0 * G[k * N + n]);
@@ -240,6 +347,38 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_solve(SmallArgs a)
         // X = Y - t G, row projection (thread per row), Theta_{k+1} -> the buffer of Theta_{k-1}
         const double *Y = a.fista ? nxt : cur;
         double *out = a.fista ? prv : nxt;
+        if (seg) {   // segment per row: X, Michelot rounds by segment reductions, output
+            for (int rr = 0; rr < mround; rr++) {
+                const int row = rr * nseg + segid;
+                const bool ok = row < M && sl < N;
+                const double x = ok ? fma(-ts[row], Gs[row * N + sl], Y[row * N + sl]) : -INFINITY;
+                const double s = seg_sum(ok ? x : 0.0, S), xm = seg_max(x, S), xn = seg_min(ok ? x : INFINITY, S);
+                double tau = (s - 1.0) / (double)N;
+                bool done = row >= M || xn > tau;
+                if (!done) tau = fmax(tau, xm - 1.0);
+                int cnt = N + 1;
+                for (int round = 0; round <= N; round++) {
+                    if (__all_sync(0xffffffffu, done)) break;
+                    const bool in = x > tau;
+                    const double ps = seg_sum(in ? x : 0.0, S);
+                    const int pc = seg_sum_i(in ? 1 : 0, S);
+                    const double mA = seg_min(in ? x : INFINITY, S);
+                    if (!done) {
+                        if (pc >= cnt) {
+                            done = true;
+                        } else {
+                            cnt = pc;
+                            tau = (ps - 1.0) / (double)pc;
+                            done = mA > tau;
+                        }
+                    }
+                }
+                if (ok) {
+                    const double o = x - tau;
+                    out[row * N + sl] = o > 0.0 ? o : 0.0;
+                }
+            }
+        } else
         for (int row = tid; row < M; row += nth) {
             const double t = ts[row];
             double s = 0.0, xm = -INFINITY, xn = INFINITY;
