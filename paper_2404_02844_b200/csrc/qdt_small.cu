@@ -48,28 +48,6 @@ __device__ __forceinline__ void sm_block_sum2(double &v0, double &v1, double *re
     v1 = t1;
 }
 
-// segment reductions over S lanes (S a power of two <= 32; a row of N <= S outcomes per segment)
-__device__ __forceinline__ double seg_sum(double v, int S)
-{
-    for (int o = S >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, S);
-    return v;
-}
-__device__ __forceinline__ double seg_min(double v, int S)
-{
-    for (int o = S >> 1; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o, S));
-    return v;
-}
-__device__ __forceinline__ double seg_max(double v, int S)
-{
-    for (int o = S >> 1; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o, S));
-    return v;
-}
-__device__ __forceinline__ int seg_sum_i(int v, int S)
-{
-    for (int o = S >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, S);
-    return v;
-}
-
 size_t small_solve_smem(int64_t D, int64_t M, int N, int64_t nnz, int fista)
 {
     const int64_t MN = M * N, DN = D * N;
@@ -141,7 +119,10 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_solve(SmallArgs a)
 
     // band sums with four independent accumulators (combined in a fixed order): the chains are
     // latency bound at these sizes
-    const bool pairs = (N & 1) == 0;   // even N: two outcomes per thread (double2), F loaded once
+    // even N: two outcomes per thread (double2 loads, F loaded once per pair).  Rows stay one
+    // thread each in the projection and KKT: a lane segment per row with shuffle reductions measured
+    // slower at Tiny (15.4 against 10.5 us per iteration, tools/small_ab.py)
+    const bool pairs = (N & 1) == 0;
     auto residual = [&](const double *T, double *R, bool withP) {   // R = F T - P
         if (pairs) {
             const int N2 = N >> 1;
@@ -240,34 +221,8 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_solve(SmallArgs a)
         }
     };
     // r_KKT of T with gradient G (reading R7; both multipliers), thread per row
-    // rows of N <= 32 outcomes: a segment of S lanes per row, one outcome per lane
-    const int S = N <= 1 ? 1 : (N <= 2 ? 2 : (N <= 4 ? 4 : (N <= 8 ? 8 : (N <= 16 ? 16 : 32))));
-    const bool seg = N <= 32;
-    const int lane = tid & 31, sl = lane & (S - 1);
-    const int spw = 32 / S;                                   // segments per warp
-    const int nseg = (nth / 32) * spw, segid = (tid >> 5) * spw + (lane / S);
-    const int mround = (M + nseg - 1) / nseg;                 // warp-uniform row loop
     auto kkt = [&](const double *T, const double *G, double *r, double *rp) {
         double s1 = 0.0, s2 = 0.0;
-        if (seg) {
-            for (int rr = 0; rr < mround; rr++) {
-                const int k = rr * nseg + segid;
-                const bool ok = k < M && sl < N;
-                const double g2 = ok ? 2.0 * G[k * N + sl] : INFINITY;
-                const double lam = -seg_min(g2, S), lamp = fmax(lam, 0.0);
-                if (ok) {
-                    const double th = T[k * N + sl];
-                    const double x1 = th * (g2 + lam), x2 = th * (g2 + lamp);
-                    s1 = fma(x1, x1, s1);
-                    s2 = fma(x2, x2, s2);
-                }
-            }
-            const double nm = (double)N * (double)M;
-            sm_block_sum2(s1, s2, red);
-            *r = sqrt(s1 / nm);
-            *rp = sqrt(s2 / nm);
-            return;
-        }
         for (int k = tid; k < M; k += nth) {
             double mn = INFINITY;
             for (int n = 0; n < N; n++) mn = fmin(mn, 2.0 * G[k * N + n]);
@@ -347,38 +302,6 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_solve(SmallArgs a)
         // X = Y - t G, row projection (thread per row), Theta_{k+1} -> the buffer of Theta_{k-1}
         const double *Y = a.fista ? nxt : cur;
         double *out = a.fista ? prv : nxt;
-        if (seg) {   // segment per row: X, Michelot rounds by segment reductions, output
-            for (int rr = 0; rr < mround; rr++) {
-                const int row = rr * nseg + segid;
-                const bool ok = row < M && sl < N;
-                const double x = ok ? fma(-ts[row], Gs[row * N + sl], Y[row * N + sl]) : -INFINITY;
-                const double s = seg_sum(ok ? x : 0.0, S), xm = seg_max(x, S), xn = seg_min(ok ? x : INFINITY, S);
-                double tau = (s - 1.0) / (double)N;
-                bool done = row >= M || xn > tau;
-                if (!done) tau = fmax(tau, xm - 1.0);
-                int cnt = N + 1;
-                for (int round = 0; round <= N; round++) {
-                    if (__all_sync(0xffffffffu, done)) break;
-                    const bool in = x > tau;
-                    const double ps = seg_sum(in ? x : 0.0, S);
-                    const int pc = seg_sum_i(in ? 1 : 0, S);
-                    const double mA = seg_min(in ? x : INFINITY, S);
-                    if (!done) {
-                        if (pc >= cnt) {
-                            done = true;
-                        } else {
-                            cnt = pc;
-                            tau = (ps - 1.0) / (double)pc;
-                            done = mA > tau;
-                        }
-                    }
-                }
-                if (ok) {
-                    const double o = x - tau;
-                    out[row * N + sl] = o > 0.0 ? o : 0.0;
-                }
-            }
-        } else
         for (int row = tid; row < M; row += nth) {
             const double t = ts[row];
             double s = 0.0, xm = -INFINITY, xn = INFINITY;
