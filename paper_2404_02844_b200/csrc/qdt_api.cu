@@ -159,28 +159,10 @@ struct Plan {
     FwUnit *d_fwunits = nullptr;
     int64_t sw_nrpart = 0;
     int64_t *d_sw_red_beg = nullptr, *d_sw_red_rows = nullptr;
-    // fused sweep (single GPU, plain PG): heavy tiles [0, fz_tsplit) by k_bwd_mma + k_fwd_mma,
-    // light tiles by fz_nctas persistent CTAs of k_sweep_fused
-    bool fz_on = false;
-    int fz_cap = 0, fz_tsplit = 0, fz_nctas = 0;
-    int32_t *d_fz_range = nullptr;
-    int64_t *d_fz_poff = nullptr;
-    int fz_nbh = 0;                     // heavy bwd units
-    SwUnit *d_fz_bunits = nullptr;
-    int fz_nfh = 0;                     // heavy fwd units
-    FwUnit *d_fz_funits = nullptr;
-    int64_t fz_nrpart = 0;
-    int64_t *d_fz_red_beg = nullptr, *d_fz_red_rows = nullptr;
     ~Plan()
     {
         cudaFree(d_wx_tlist);
         cudaFree(d_wx_toff);
-        cudaFree(d_fz_range);
-        cudaFree(d_fz_poff);
-        cudaFree(d_fz_bunits);
-        cudaFree(d_fz_funits);
-        cudaFree(d_fz_red_beg);
-        cudaFree(d_fz_red_rows);
         cudaFree(d_swunits);
         cudaFree(d_fwunits);
         cudaFree(d_sw_red_beg);
@@ -730,104 +712,10 @@ static void plan_fwd_units(const qdt_probes *p, int t0, int t1, Emit &&emit, int
     }
 }
 
-// Fused plan (single GPU): light tiles = the longest suffix of tiles whose window fits the ring
-// (cap probes), split into contiguous ranges, one persistent CTA each; the heavy prefix keeps
-// the unfused k_bwd_mma / k_fwd_mma units.  Partial rows: heavy fwd units first, then one row per
-// (CTA, probe of its range); per-probe lists in ascending Fock order.
-static qdt_status build_fused_plan(qdt_ctx *ctx, qdt_probes *p, Plan *pl, const std::vector<SwUnit> &bu_all)
-{
-    pl->fz_on = false;
-    if (ctx->nranks != 1 || pl->NB == 0 || pl->NB > SW_NBMAX) return QDT_OK;
-    // the fused persistent sweep is opt-in (QDT_FUSED=1): at 8 warps per SM it is latency bound and
-    // measured slower than the unfused sweep (profiles/r01_v2)
-    const char *e = getenv("QDT_FUSED");
-    if (!(e && e[0] == '1')) return QDT_OK;
-    const int N = pl->N, NB = pl->NB, nt = p->sw_ntiles;
-    const int64_t D = p->D;
-    int cap = 0;
-    for (int c : {32, 24, 16, 8})
-        if (sweep_fused_smem(N, NB, c) <= (size_t)SW_FUSED_SMEM_MAX) {
-            cap = c;
-            break;
-        }
-    if (!cap) return QDT_OK;
-    int ts = nt;
-    while (ts > 0 && p->sw_dB[ts - 1] - p->sw_dA[ts - 1] <= cap) ts--;
-    const int ntl = nt - ts;
-    if (ntl < 1) return QDT_OK;
-    int nsm = 148;
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device);
-    const int G = std::min(nsm, ntl);
-    std::vector<int32_t> range(2 * G);
-    for (int c = 0; c < G; c++) {
-        range[2 * c] = ts + (int)((int64_t)c * ntl / G);
-        range[2 * c + 1] = ts + (int)((int64_t)(c + 1) * ntl / G);
-    }
-    // heavy fwd units over tiles [0, ts)
-    std::vector<FwUnit> fu;
-    std::vector<std::vector<int64_t>> lists(D);
-    int64_t poff = 0;
-    auto emit = [&](int t0, int t1, int u0, int u1) {
-        if (u1 <= u0) return;
-        FwUnit u;
-        u.t0 = t0;
-        u.t1 = t1;
-        u.u0 = u0;
-        u.u1 = u1;
-        u.poff = poff;
-        fu.push_back(u);
-        for (int d = u0; d < u1; d++) lists[d].push_back(poff + (d - u0));
-        poff += u1 - u0;
-    };
-    plan_fwd_units(p, 0, ts, emit);
-    std::vector<int64_t> cpoff(G);
-    for (int c = 0; c < G; c++) {
-        const int ta = range[2 * c], tb = range[2 * c + 1];
-        const int d0 = p->sw_dA[ta], d1 = p->sw_dB[tb - 1];
-        cpoff[c] = poff;
-        for (int d = d0; d < d1; d++) lists[d].push_back(poff + (d - d0));
-        poff += std::max(0, d1 - d0);
-    }
-    pl->fz_nrpart = poff;
-    std::vector<int64_t> red_beg(D + 1, 0), red_rows;
-    for (int64_t d = 0; d < D; d++) red_beg[d + 1] = red_beg[d] + (int64_t)lists[d].size();
-    red_rows.reserve(red_beg[D]);
-    for (int64_t d = 0; d < D; d++) red_rows.insert(red_rows.end(), lists[d].begin(), lists[d].end());
-    std::stable_sort(fu.begin(), fu.end(), [](const FwUnit &x, const FwUnit &y) {
-        return (int64_t)(x.u1 - x.u0) * (x.t1 - x.t0) > (int64_t)(y.u1 - y.u0) * (y.t1 - y.t0);
-    });
-    std::vector<SwUnit> bh;
-    for (const SwUnit &u : bu_all)
-        if (u.tile < ts) bh.push_back(u);
-    cudaStream_t s = ctx->stream;
-    CK(cudaMalloc(&pl->d_fz_range, sizeof(int32_t) * 2 * G));
-    CK(cudaMalloc(&pl->d_fz_poff, sizeof(int64_t) * G));
-    CK(cudaMalloc(&pl->d_fz_bunits, sizeof(SwUnit) * std::max<size_t>(1, bh.size())));
-    CK(cudaMalloc(&pl->d_fz_funits, sizeof(FwUnit) * std::max<size_t>(1, fu.size())));
-    CK(cudaMalloc(&pl->d_fz_red_beg, sizeof(int64_t) * (D + 1)));
-    CK(cudaMalloc(&pl->d_fz_red_rows, sizeof(int64_t) * std::max<size_t>(1, red_rows.size())));
-    CK(cudaMemcpyAsync(pl->d_fz_range, range.data(), sizeof(int32_t) * 2 * G, cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(pl->d_fz_poff, cpoff.data(), sizeof(int64_t) * G, cudaMemcpyHostToDevice, s));
-    if (!bh.empty()) CK(cudaMemcpyAsync(pl->d_fz_bunits, bh.data(), sizeof(SwUnit) * bh.size(), cudaMemcpyHostToDevice, s));
-    if (!fu.empty()) CK(cudaMemcpyAsync(pl->d_fz_funits, fu.data(), sizeof(FwUnit) * fu.size(), cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpyAsync(pl->d_fz_red_beg, red_beg.data(), sizeof(int64_t) * (D + 1), cudaMemcpyHostToDevice, s));
-    if (!red_rows.empty())
-        CK(cudaMemcpyAsync(pl->d_fz_red_rows, red_rows.data(), sizeof(int64_t) * red_rows.size(),
-                           cudaMemcpyHostToDevice, s));
-    CK(cudaStreamSynchronize(s));
-    pl->fz_cap = cap;
-    pl->fz_tsplit = ts;
-    pl->fz_nctas = G;
-    pl->fz_nbh = (int)bh.size();
-    pl->fz_nfh = (int)fu.size();
-    pl->fz_on = true;
-    return QDT_OK;
-}
 
 // Sweep units for N: bwd units (tile, probe sub-range <= SWCAP, split-K slots), fwd units (runs
 // of <= FW_MAXT tiles whose union window is <= FWCAP probes; wider windows split by FWCAP), and
 // per-probe lists of partial rows in ascending Fock order.
-static qdt_status build_fused_plan(qdt_ctx *ctx, qdt_probes *p, Plan *pl, const std::vector<SwUnit> &bu_all);
 static qdt_status build_sweep_plan(qdt_ctx *ctx, qdt_probes *p, Plan *pl)
 {
     CKS(build_sweep_tiling(ctx, p));
@@ -907,7 +795,7 @@ static qdt_status build_sweep_plan(qdt_ctx *ctx, qdt_probes *p, Plan *pl)
         CK(cudaMemcpyAsync(pl->d_sw_red_rows, red_rows.data(), sizeof(int64_t) * red_rows.size(),
                            cudaMemcpyHostToDevice, s));
     CK(cudaStreamSynchronize(s));
-    return build_fused_plan(ctx, p, pl, bu);
+    return QDT_OK;
 }
 
 // QDT_SMALL=0 keeps small problems on the multi-kernel loop (A/B)
@@ -1459,7 +1347,6 @@ struct SolveBufs {
     DevState *state = nullptr;
     double *sc2_stage = nullptr;
     int *sc2_arrive = nullptr;
-    double *partS = nullptr;   // fused sweep: heavy-tile slots [0, tsplit) + CTA slots
     double *bb_part = nullptr, *bb_vec = nullptr, *tbb = nullptr;  // BB step statistics / scalar
     double *Gw = nullptr;      // wide-N sweep: Ml x N gradient
     double *tau_prev = nullptr;  // fused wide step: per-row threshold of the last step (warm start)
@@ -1915,58 +1802,6 @@ static qdt_status iteration(qdt_ctx *ctx, const IterCfg &c, SolveBufs &b, int64_
         CKS(scalars(ctx, c, b, 0, wide_nparts(c)));
         return QDT_OK;
     }
-    if (!c.fista && pl->fz_on) {
-        // R_j is resident (prologue or the previous iteration's reduce); this iteration writes
-        // Theta_{j+1} and the partial rows of R_{j+1}
-        double *cur = b.theta[j % 2], *nxt = b.theta[(j + 1) % 2];
-        qdt_probes *p = c.p;
-        SweepArgs a = sweep_args(c, b, b.R[0], cur, nxt);
-        a.units = pl->d_fz_bunits;
-        a.part = b.partS;
-        CK(run_k(ctx, "bwd_heavy", 1, [&]() { return launch_bwd_any(a, pl->fz_nbh, pl->NB, s); }));
-        SweepFusedArgs z;
-        z.N = c.N;
-        z.Ml = (int)p->Ml;
-        z.cap = pl->fz_cap;
-        z.kb = p->kb;
-        z.M = p->M;
-        z.range = pl->d_fz_range;
-        z.poff = pl->d_fz_poff;
-        z.fb_off = p->d_fb_off;
-        z.tile_dA = p->d_sw_dA;
-        z.tile_dB = p->d_sw_dB;
-        z.Fb = p->d_Fb;
-        z.R = b.R[0];
-        z.theta = cur;
-        z.out = nxt;
-        z.tstep = b.tstep;
-        z.gamma = c.gamma;
-        z.rpart = b.rpart;
-        z.part = b.partS;
-        z.part_base = pl->fz_tsplit;
-        z.kkt_every = c.kkt_every;
-        z.state = b.state;
-        CK(run_k(ctx, "sweep_fused", 1, [&]() { return launch_sweep_fused(z, pl->fz_nctas, pl->NB, s); }));
-        SweepFwdArgs fa;
-        fa.N = c.N;
-        fa.Ml = (int)p->Ml;
-        fa.units = pl->d_fz_funits;
-        fa.fb_off = p->d_fb_off;
-        fa.tile_dA = p->d_sw_dA;
-        fa.tile_dB = p->d_sw_dB;
-        fa.Fb = p->d_Fb;
-        fa.theta = nxt;
-        fa.rpart = b.rpart;
-        fa.state = b.state;
-        CK(run_k(ctx, "fwd_heavy", 1, [&]() { return launch_fwd_mma(fa, pl->fz_nfh, pl->NB, s); }));
-        // scalars of iteration j (||R_j||^2 from the previous reduce) before R_{j+1} is reduced
-        CKS(scalars(ctx, c, b, 0, pl->fz_tsplit + pl->fz_nctas, b.partS));
-        CK(run_k(ctx, "reduce_R", 1, [&]() {
-            return launch_reduce_R2(b.rpart, pl->d_fz_red_beg, pl->d_fz_red_rows, b.P, b.R[0], (int)p->D, c.N,
-                                    b.partR, b.state, s);
-        }));
-        return QDT_OK;
-    }
     if (!c.fista && pl->NB) {
         double *cur = b.theta[j % 2], *nxt = b.theta[(j + 1) % 2];
         CKS(fwd_reduce(ctx, c, b, cur, b.R[0], true));
@@ -2062,13 +1897,8 @@ static qdt_status common_bufs(qdt_ctx *ctx, qdt_probes *p, Plan *pl, int64_t N, 
     cudaStream_t s = ctx->stream;
     const int64_t D = p->D;
     CKS(ws_get(ctx, "R0", D * N + 4, &b.R[0]));
-    CKS(ws_get(ctx, "rpart", std::max<int64_t>(1, std::max({pl->nrpart, pl->sw_nrpart, pl->fz_nrpart})) * N + 4,
+    CKS(ws_get(ctx, "rpart", std::max<int64_t>(1, std::max(pl->nrpart, pl->sw_nrpart)) * N + 4,
                &b.rpart));
-    if (pl->fz_on) {
-        const int ns = pl->fz_tsplit + pl->fz_nctas;
-        CKS(ws_get(ctx, "partS", (size_t)ns * NSC_TILE, &b.partS));
-        CK(cudaMemsetAsync(b.partS, 0, sizeof(double) * ns * NSC_TILE, s));
-    }
     CKS(ws_get(ctx, "partR", std::max(ctx->nblkR, pl->nR), &b.partR));
     const int ncc = (int)((N + 127) / 128);
     const int nt = std::max(1, std::max({pl->ntiles, p->sw_ntiles * (pl->NW ? ncc : 1) + (int)((p->Ml + 7) / 8),
@@ -2313,7 +2143,6 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     c.Nv = (int)Nu;
     c.bx = (ctx->nranks > 1 && opt.exchange == 1) ? 1 : 0;
     CKS(halo_exchange(ctx, c, b.theta[0]));
-    if (pl->fz_on && !fista) CKS(fwd_reduce(ctx, c, b, b.theta[0], b.R[0], true));  // R_0
     if (fista && opt.theta_prev) {
         // resume: Theta_{k-1} given (same layout as theta0); R_{k-1} = F Theta_{k-1} - P for the
         // first extrapolated residual R(Y) = (1 + beta) R_k - beta R_{k-1}

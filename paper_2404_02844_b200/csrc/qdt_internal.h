@@ -145,25 +145,6 @@ struct SweepFwdArgs {
     int ncc;                    // column chunks of 8 NB outcomes (set by launch_fwd_mma)
     const DevState *state;
 };
-struct SweepFusedArgs {
-    int N, Ml, cap;             // cap: max window of a light tile (ring slots), multiple of 8
-    int64_t kb, M;
-    const int32_t *range;       // per CTA: [ta, tb) light tiles
-    const int64_t *poff;        // per CTA: first partial row (probe tile_dA[ta])
-    const int64_t *fb_off;
-    const int32_t *tile_dA, *tile_dB;
-    const double *Fb;
-    const double *R;
-    const double *theta;
-    double *out;
-    const double *tstep;
-    double gamma;
-    double *rpart;
-    double *part;               // scalar partials: CTA c writes slot part_base + c
-    int part_base;
-    int kkt_every;
-    const DevState *state;
-};
 struct WideArgs {               // wide-N sweep (N > 128): k_grad_wide + k_proj_wide
     const double *tscal = nullptr;   // one device scalar step (BB) instead of tstep per row
     int N, Ml, ncc;             // ncc: 128-column chunks (set by launch_grad_wide)
@@ -256,9 +237,6 @@ int wide_nb(int N);                                  // balanced column-chunk wi
 int wide_fwd_nb(int N);                              // same for the forward (<= 13 n-blocks: 2 CTAs / SM)
 constexpr int PW_BLOCKS = 148 * 8;                   // k_proj_wide grid cap (contiguous row ranges)
 int wide_proj_blocks(int Ml);
-constexpr int SW_FUSED_SMEM_MAX = 220 * 1024;
-size_t sweep_fused_smem(int N, int NB, int cap);
-cudaError_t launch_sweep_fused(const SweepFusedArgs &a, int nctas, int NB, cudaStream_t s);
 cudaError_t prepare_sweep_kernels();
 constexpr int BB_NBLK = 296;
 cudaError_t launch_bb_stats(const double *th, const double *tp, int64_t Ml, int64_t kb, int64_t M, int N,

@@ -229,20 +229,14 @@ __device__ __forceinline__ void row_pass(double (&acc)[NBA][2], const double *th
             if (ok) {
                 s += x;
                 xm = x > xm ? x : xm;
-#ifndef QDT_NO_XN
                 xn = x < xn ? x : xn;
-#endif
             }
             acc[nb][i] = ok ? x : -INFINITY;
         }
     }
     s = quad_sum(s);
     xm = quad_max(xm);
-#ifndef QDT_NO_XN
     xn = quad_min(xn);
-#else
-    xn = -INFINITY;   // A/B: no all-active shortcut (the first Michelot round finds it)
-#endif
     if (PAIR) {
         double v[3] = {s, xm, xn}, o[3];
         pair_xchg<3>(*px, v, o);
@@ -271,11 +265,7 @@ __device__ __forceinline__ void row_project(double (&acc)[NBA][2], double *thr, 
     bool done = !ract || xn > tau;
     if (!done) tau = fmax(tau, xm - 1.0);
     int cnt = N + 1;
-#ifdef QDT_MICH_NOMIN
-    constexpr bool kMin = false;   // A/B: stop only when |A| stops shrinking (one more round, no min)
-#else
-    constexpr bool kMin = true;
-#endif
+    constexpr bool kMin = true;    // stop as soon as min_A X > tau (profiles/r01_v9: faster than waiting for |A|)
     for (int round = 0; round <= N; round++) {
         if (__all_sync(0xffffffffu, done)) break;
         double ps = 0.0, mA = INFINITY;
@@ -317,13 +307,8 @@ __device__ __forceinline__ void row_project(double (&acc)[NBA][2], double *thr, 
             const int gb = CB / 8 + nb;
             const int c = CB + 8 * nb + 2 * t4;
             double o0 = acc[nb][0] - tau, o1 = acc[nb][1] - tau;
-#ifdef QDT_CLAMP_ARITH
-            o0 = (o0 + fabs(o0)) * 0.5;   // A/B: max(o, 0) on the fp64 pipe (exact: 2o * 0.5 = o)
-            o1 = (o1 + fabs(o1)) * 0.5;
-#else
             o0 = o0 > 0.0 ? o0 : 0.0;
             o1 = o1 > 0.0 ? o1 : 0.0;
-#endif
             if (EVEN) {
                 if (gb < NB - 1 || (gb == NB - 1 && v0)) {
                     *reinterpret_cast<double2 *>(orow + c) = make_double2(o0, o1);
@@ -1076,195 +1061,6 @@ __global__ void __launch_bounds__(256, 2) k_fwd_mma(SweepFwdArgs a)
     }
 }
 
-// ------------------------------------------------------------------------------ fused sweep
-// Persistent kernel over the "light" tiles (window <= cap probes): CTA c sweeps a contiguous tile
-// range [ta, tb) in Fock order with a 2-stage bulk-copy pipeline (Theta_k tile + halo, F block,
-// R rows of the window).  Per tile:
-//   1. G = F_blk^T R_win (DMMA), row epilogue (row_step) -> Theta_{k+1} to HBM and in place into
-//      the stage's Theta rows;
-//   2. forward partials of the NEXT iteration: ring[d] += F_blk[d, :] Theta_{k+1,tile} (DMMA) for
-//      the window's probes; the ring keeps one accumulator row per open probe (slot d mod cap);
-//   3. probes whose band ends before the next tile (d < dA_{t+1}) are flushed to their partial row
-//      rpart[poff_c + d - dfirst_c] and their slot zeroed.
-// Scalar partials (regulariser, KKT) accumulate per CTA in registers in a fixed order.
-size_t sweep_fused_smem(int N, int NB, int cap)
-{
-    const int thsz = (((ST + 2) * N + 8 * NB + 4) + 1) & ~1;
-    const int rsz = ((cap * N + 8 * NB + 4) + 1) & ~1;
-    const int stage = thsz + cap * STP + rsz;
-    return (size_t)(2 * stage + cap * 8 * NB) * sizeof(double);
-}
-
-template <int NB>
-__global__ void __launch_bounds__(256, 1) k_sweep_fused(SweepFusedArgs a)
-{
-    extern __shared__ __align__(128) double sm[];
-    __shared__ __align__(8) uint64_t bars[2];
-    __shared__ double red[8 * 3];
-    const DevState *st = a.state;
-    if (st && st->stop) return;
-    const int64_t it = st ? st->it : 0;
-    const int N = a.N, cap = a.cap;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int g4 = lane >> 2, t4 = lane & 3;
-    const int thsz = (((ST + 2) * N + 8 * NB + 4) + 1) & ~1;
-    const int rsz = ((cap * N + 8 * NB + 4) + 1) & ~1;
-    const int stage = thsz + cap * STP + rsz;
-    const int RP = 8 * NB;                       // ring pitch
-    double *ring = sm + 2 * stage;
-    const int ta = a.range[2 * blockIdx.x], tb = a.range[2 * blockIdx.x + 1];
-    const int dfirst = a.tile_dA[ta];
-    const int64_t poff = a.poff[blockIdx.x];
-    const double gamma = a.gamma;
-    const bool do_kkt = (it % a.kkt_every) == 0;
-    const bool even = (N & 1) == 0;
-
-    for (int e = tid; e < cap * RP; e += 256) ring[e] = 0.0;
-    if (tid == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
-        fence_barrier_init();
-    }
-    __syncthreads();
-    auto issue = [&](int j) {
-        const int t = ta + j;
-        const int k0 = t * ST;
-        const int Tt = min(ST, a.Ml - k0);
-        const int dA = a.tile_dA[t], W = a.tile_dB[t] - dA;
-        double *S = sm + (j & 1) * stage;
-        const double *src;
-        int sh;
-        uint32_t by;
-        aligned_span(a.theta + (int64_t)(k0 - 1) * N, (int64_t)(Tt + 2) * N, &src, &sh, &by);
-        const double *rsrc;
-        int rsh;
-        uint32_t rby;
-        aligned_span(a.R + (int64_t)dA * N, (int64_t)W * N, &rsrc, &rsh, &rby);
-        const uint32_t fby = (uint32_t)W * STP * 8;
-        uint64_t *bar = &bars[j & 1];
-        mbar_expect_tx(bar, by + (W ? fby + rby : 0));
-        bulk_g2s(S, src, by, bar);
-        if (W) {
-            bulk_g2s(S + thsz, a.Fb + a.fb_off[t], fby, bar);
-            bulk_g2s(S + thsz + cap * STP, rsrc, rby, bar);
-        }
-    };
-    const int nt = tb - ta;
-    if (tid == 0) {
-        if (nt > 0) issue(0);
-        if (nt > 1) issue(1);
-    }
-    double sreg = 0.0, skkt = 0.0, skktp = 0.0;
-    for (int j = 0; j < nt; j++) {
-        const int t = ta + j;
-        const int k0 = t * ST;
-        const int Tt = min(ST, a.Ml - k0);
-        const int dA = a.tile_dA[t], W = a.tile_dB[t] - dA;
-        double *S = sm + (j & 1) * stage;
-        const int th_sh = (int)(((uintptr_t)(a.theta + (int64_t)(k0 - 1) * N) & 15) >> 3);
-        const int r_sh = (int)(((uintptr_t)(a.R + (int64_t)dA * N) & 15) >> 3);
-        double *Th = S + th_sh;
-        const double *Fs = S + thsz;
-        const double *Rs = S + thsz + cap * STP + r_sh;
-        mbar_wait(&bars[j & 1], (j >> 1) & 1);
-
-        // ---- 1. G = F^T R (warp = m-block of 8 rows, all NB n-blocks), then the row epilogue
-        double acc[NB][2];
-#pragma unroll
-        for (int nb = 0; nb < NB; nb++) acc[nb][0] = acc[nb][1] = 0.0;
-        gemm_bwd<NB>(acc, Fs + 8 * warp + g4, Rs + g4, W, N, t4);
-        {
-            const int r = 8 * warp + g4;
-            const bool act = r < Tt;
-            const int kl = k0 + r;
-            const int64_t kg = a.kb + kl;
-            const bool has_prev = kg > 0, has_next = kg + 1 < a.M;
-            double *thr = Th + (r + 1) * N;
-            const double tk = act ? a.tstep[kl] : 0.0;
-            double *orow = a.out + (int64_t)kl * N;
-            const bool full = Tt == ST && a.kb + k0 > 0 && a.kb + k0 + ST < a.M;
-            if (full && even)
-                row_step<NB, true, true, true>(acc, thr, N, t4, act, has_prev, has_next, gamma, tk, do_kkt,
-                                               false, sreg, skkt, skktp, orow);
-            else if (full)
-                row_step<NB, true, false, true>(acc, thr, N, t4, act, has_prev, has_next, gamma, tk, do_kkt,
-                                                false, sreg, skkt, skktp, orow);
-            else
-                row_step<NB, false, false, true>(acc, thr, N, t4, act, has_prev, has_next, gamma, tk,
-                                                 do_kkt, false, sreg, skkt, skktp, orow);
-        }
-        __syncthreads();  // Theta_{k+1} tile complete in smem
-
-        // ---- 2. ring[d][n] += sum_k F_blk[d][k] Theta_{k+1}[k][n] for the window's probes
-        //      (transposed GEMM: warp w takes outcome m-blocks w and w + 8, all nm <= 4 probe
-        //      n-blocks; every (probe, outcome) pair is owned by one lane: no cross-warp sums)
-        {
-            const int nm = (W + 7) >> 3;
-            int slot[4][2];
-#pragma unroll
-            for (int nb = 0; nb < 4; nb++)
-#pragma unroll
-                for (int i = 0; i < 2; i++) slot[nb][i] = ((dA + 8 * nb + 2 * t4 + i) % cap) * RP;
-            const double *Frow = Fs + g4 * STP + t4;
-            for (int mbo = warp; mbo < NB; mbo += 8) {
-                double cf[4][2];
-#pragma unroll
-                for (int nb = 0; nb < 4; nb++) cf[nb][0] = cf[nb][1] = 0.0;
-                const double *Tcol = Th + N + t4 * N + 8 * mbo + g4;   // Theta_{k+1}, tile row 0
-                if (Tt == ST)
-                    gemm_fwd_t_nm<false>(nm, cf, Tcol, Frow, N, Tt, t4);
-                else
-                    gemm_fwd_t_nm<true>(nm, cf, Tcol, Frow, N, Tt, t4);
-                const int n = 8 * mbo + g4;
-                if (n < N) {
-#pragma unroll
-                    for (int nb = 0; nb < 4; nb++)
-#pragma unroll
-                        for (int i = 0; i < 2; i++)
-                            if (nb < nm && 8 * nb + 2 * t4 + i < W) ring[slot[nb][i] + n] += cf[nb][i];
-                }
-            }
-        }
-        __syncthreads();
-        // ---- 3. flush the probes that leave the window: [dA, next dA) (all at the range end)
-        {
-            const int dnext = (j + 1 < nt) ? a.tile_dA[t + 1] : dA + W;
-            const int nl = dnext - dA;
-            for (int e = tid; e < nl * RP; e += 256) {
-                const int q = e / RP, c = e - q * RP;
-                const int d = dA + q;
-                double *rr = ring + (d % cap) * RP + c;
-                if (c < N) a.rpart[(poff + (d - dfirst)) * (int64_t)N + c] = *rr;
-                *rr = 0.0;
-            }
-        }
-        __syncthreads();
-        if (tid == 0 && j + 2 < nt) issue(j + 2);
-    }
-    // ---- per-CTA scalar partials (fixed order)
-    sreg = wsum(sreg);
-    skkt = wsum(skkt);
-    if (lane == 0) {
-        red[warp * 3 + 0] = skkt;
-        red[warp * 3 + 2] = sreg;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        double v0 = 0.0, v2 = 0.0;
-        for (int w = 0; w < 8; w++) {
-            v0 += red[w * 3 + 0];
-            v2 += red[w * 3 + 2];
-        }
-        double *p = a.part + (int64_t)a.part_base * NSC_TILE + (int64_t)blockIdx.x * NSC_TILE;
-        if (do_kkt) {
-            p[SC_KKT] = v0;
-            p[SC_KKTP] = 0.0;
-        }
-        p[SC_REG] = v2;
-        p[SC_DTH] = 0.0;
-    }
-}
-
 // ------------------------------------------------------------------------------ wide N
 // N > 128 (even, <= 1024): the gradient and the row projection become two kernels.
 //   k_grad_wide  CTA (bwd unit, column chunk of 128 outcomes): G = F_tile^T R_win[:, chunk] by
@@ -1983,9 +1779,6 @@ static cudaError_t prep_nb()
         e = cudaFuncSetAttribute(k_bwd_split<NB, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_fwd_mma<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, big);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_sweep_fused<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 SW_FUSED_SMEM_MAX);
     return e;
 }
 
@@ -2158,19 +1951,6 @@ cudaError_t launch_fwd_mma(const SweepFwdArgs &a_in, int nunits, int NB, cudaStr
     return cudaGetLastError();
 }
 
-cudaError_t launch_sweep_fused(const SweepFusedArgs &a, int nctas, int NB, cudaStream_t s)
-{
-    if (nctas <= 0) return cudaSuccess;
-    const size_t smem = sweep_fused_smem(a.N, NB, a.cap);
-    switch (NB) {
-#define QDT_CASE(nb) \
-    case nb: k_sweep_fused<nb><<<nctas, 256, smem, s>>>(a); break;
-        QDT_FOR_NB(QDT_CASE)
-#undef QDT_CASE
-        default: return cudaErrorInvalidValue;
-    }
-    return cudaGetLastError();
-}
 
 cudaError_t launch_reduce_R2(const double *rpart, const int64_t *red_beg, const int64_t *red_rows,
                              const double *P, double *R, int D, int N, double *partR,

@@ -284,12 +284,9 @@ def test_megascale_solve_parity(q, ctx):
 
 
 @pytest.mark.parametrize("N,gamma", [(20, 1e-3), (37, 0.0), (100, 1e-5), (8, 1e-2)])
-@pytest.mark.parametrize("fused", ["0", "1"])
-def test_fused_sweep_parity(q, ctx, N, gamma, fused, monkeypatch):
-    """Log-spaced probes over a long Fock axis: most tiles have narrow windows, so the solve runs
-    (QDT_FUSED=1) the fused persistent sweep on the light tiles beside the split heavy tiles, or
-    (QDT_FUSED=0) the unfused sweep; 30 iterations against the oracle, P9 invariants, trace."""
-    monkeypatch.setenv("QDT_FUSED", fused)
+def test_long_axis_sweep_parity(q, ctx, N, gamma):
+    """Log-spaced probes over a long Fock axis: most tiles have narrow windows beside a few split
+    heavy tiles; 30 iterations against the oracle, P9 invariants, trace."""
     rng = np.random.default_rng(N)
     D, M = 400, 30000
     a2 = np.geomspace(1.0, 0.9 * M, D)
