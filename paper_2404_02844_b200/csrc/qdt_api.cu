@@ -2179,7 +2179,8 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
 
     // ---- small problems: the whole solve in one persistent CTA (qdt_small.cu)
     const bool small = ctx->nranks == 1 && !bb && small_enabled() &&
-                       small_solve_smem(D, Ml, (int)N, p->nnz, fista) <= SMALL_SMEM_MAX && D * N < (1LL << 30);
+                       (small_solve_smem(D, Ml, (int)N, p->nnz, fista) <= SMALL_SMEM_MAX ||
+                        small_dense_smem(D, Ml, (int)N, fista) <= SMALL_SMEM_MAX) && D * N < (1LL << 30);
     if (small && !p->d_row_da) {
         std::vector<int32_t> da(Ml, 0), db(Ml, 0);
         int64_t a0 = 0;

@@ -188,6 +188,8 @@ struct SmallArgs {
     DevState *state;
 };
 size_t small_solve_smem(int64_t D, int64_t M, int N, int64_t nnz, int fista);
+constexpr int SD_NR = 16;       // dense small solve: widest row held in registers
+size_t small_dense_smem(int64_t D, int64_t M, int N, int fista);   // SIZE_MAX when N > SD_NR
 cudaError_t launch_small_solve(const SmallArgs &a, cudaStream_t s);
 constexpr size_t SMALL_SMEM_MAX = 200 * 1024;
 

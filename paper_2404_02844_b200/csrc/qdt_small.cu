@@ -18,7 +18,10 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <stdlib.h>
+
 #include "qdt_internal.h"
+#include "qdt_ptx.cuh"
 
 namespace qdt {
 
@@ -387,8 +390,396 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_solve(SmallArgs a)
     }
 }
 
+// ------------------------------------------------------------------------------ dense DMMA form
+// The same solve (same iteration, trace, stop and resume semantics) for problems whose F fits in
+// shared memory as a DENSE D x M block (Tiny: 100 x 50, 92 % of it inside the band): both
+// contractions become fp64 tensor-core GEMMs (mma.sync m8n8k4, one 8x8 output tile per warp,
+// two accumulator chains per tile), the row phase takes a quad of lanes per Fock row.
+//   S2  R_k = F Theta_k - P            tiles (8 probes x 8 outcomes), K = Fock rows (zero padded)
+//       FISTA: R(Y_k) = (1 + beta_k) R_k - beta_k R_{k-1} in the same epilogue (F linear)
+//   S3+S4 G = F^T R + gamma L Y         tiles (8 Fock rows x 8 outcomes), K = probes, stencil in
+//       the epilogue (ends: reading R8); FISTA at a KKT iteration also G(Theta_k) from R_k
+//   S5+S6 quad per Fock row (lane t4: outcomes 4 j + t4 in registers): regulariser pair, KKT of
+//       Theta_k (reading R7, both multipliers), X = Y - t G, Michelot threshold (reading R4) by
+//       quad butterflies, Theta_{k+1}; ONE fixed-order block reduction of ||R_k||^2, ||D Theta_k||^2
+//       and the KKT sums per iteration (partials parked in shared memory, summed by one warp).
+// Measured on B200 (tools/dmma_lat.cu): a dependent DMMA takes 26 cycles, and one SM retires one
+// DMMA per 4 cycles, so Tiny's two GEMMs (2 x 364 DMMAs on 8 x 8 tiles) cost >= 2.9 k cycles per
+// iteration on the one SM: 6.8 us per plain iteration against 10.5 us for the band form.
+// Shared-memory pitches are = 4 (mod 16) doubles (M8 + 4, N8 + 4): the fragment loads of a half
+// warp (4 rows x 4 consecutive doubles) hit 16 distinct 8-byte bank pairs.  Every pad row / column
+// of F, Theta, P, R and G is zero, so pad outputs are exactly zero and need no masks.
+constexpr int SD_THREADS = 512;
+constexpr int SD_NJ = SD_NR / 4;   // outcomes per lane of a row quad
+struct DenseLayout {
+    int Dp, M8, N8, PF, PT;
+    int64_t fd, th, r, g, t, total;   // offsets (doubles) and total
+    __host__ __device__ DenseLayout(int D, int M, int N, int fista)
+    {
+        Dp = (D + 7) & ~7;
+        M8 = (M + 7) & ~7;
+        N8 = (N + 7) & ~7;
+        PF = M8 + 4;
+        PT = N8 + 4;
+        fd = 0;
+        th = fd + (int64_t)Dp * PF;                       // Theta x3 (cur, next/prev, spare)
+        r = th + 3LL * M8 * PT;                           // P, R_k, R_{k-1}, R(Y)
+        g = r + 4LL * Dp * PT;                            // G, G(Theta_k) (FISTA)
+        t = g + 2LL * M8 * PT;                            // step weights
+        total = t + M8;
+        (void)fista;
+    }
+};
+
+size_t small_dense_smem(int64_t D, int64_t M, int N, int fista)
+{
+    if (N > SD_NR || D > (1 << 20) || M > (1 << 20)) return SIZE_MAX;
+    const DenseLayout L((int)D, (int)M, N, fista);
+    return (size_t)L.total * 8 + 64;
+}
+
+// one 8x8 output tile: acc += A (8 x K) B (K x 8) over ksteps k-steps of 4, two chains;
+// A element (row g4, k t4) at a[g4 * as_r + t4 * as_k], B element (k t4, col g4) at b[t4 * bs_k + g4]
+__device__ __forceinline__ void sd_tile(double &c0, double &c1, const double *a, int as_r, int as_k,
+                                        const double *b, int bs_k, int ksteps, int g4, int t4)
+{
+    double e0 = 0.0, e1 = 0.0, o0 = 0.0, o1 = 0.0;
+    const double *ap = a + g4 * as_r + t4 * as_k;
+    const double *bp = b + t4 * bs_k + g4;
+    int ks = 0;
+    for (; ks + 2 <= ksteps; ks += 2) {
+        const double a0 = ap[(4 * ks) * as_k], b0 = bp[(4 * ks) * bs_k];
+        const double a1 = ap[(4 * ks + 4) * as_k], b1 = bp[(4 * ks + 4) * bs_k];
+        dmma(e0, e1, a0, b0);
+        dmma(o0, o1, a1, b1);
+    }
+    if (ks < ksteps) dmma(e0, e1, ap[(4 * ks) * as_k], bp[(4 * ks) * bs_k]);
+    c0 = e0 + o0;
+    c1 = e1 + o1;
+}
+
+// fixed-order block sum of 4 values, result in every thread.  Every thread parks its 4 partials
+// in shared memory (no shuffles in most warps); warp 0 sums them (lane l: threads l, l + 32, ...
+// in order, then a butterfly) and publishes the totals.  pbuf: [blockDim.x][4] + 4 totals.
+__device__ __forceinline__ void sd_block_sum4(double (&v)[4], double *pbuf)
+{
+    const int tid = threadIdx.x, lane = tid & 31, nth = blockDim.x;
+    *reinterpret_cast<double4 *>(pbuf + 4 * tid) = make_double4(v[0], v[1], v[2], v[3]);
+    __syncthreads();
+    if (tid < 32) {
+        double w[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int t = lane; t < nth; t += 32) {
+            const double4 q = *reinterpret_cast<const double4 *>(pbuf + 4 * t);
+            w[0] += q.x;
+            w[1] += q.y;
+            w[2] += q.z;
+            w[3] += q.w;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) w[i] += __shfl_xor_sync(0xffffffffu, w[i], o);
+        if (lane == 0) *reinterpret_cast<double4 *>(pbuf + 4 * nth) = make_double4(w[0], w[1], w[2], w[3]);
+    }
+    __syncthreads();
+    const double4 q = *reinterpret_cast<const double4 *>(pbuf + 4 * nth);
+    v[0] = q.x;
+    v[1] = q.y;
+    v[2] = q.z;
+    v[3] = q.w;
+}
+
+__global__ void __launch_bounds__(SD_THREADS, 1) k_small_dense(SmallArgs a)
+{
+    extern __shared__ __align__(16) double sm[];
+    __shared__ __align__(32) double pbuf[4 * SD_THREADS + 4];
+    const int D = a.D, M = a.M, N = a.N;
+    const DenseLayout L(D, M, N, a.fista);
+    const int Dp = L.Dp, M8 = L.M8, N8 = L.N8, PF = L.PF, PT = L.PT;
+    const int tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nth >> 5;
+    const int g4 = lane >> 2, t4 = lane & 3;
+    double *Fd = sm + L.fd;
+    double *Tb[3] = {sm + L.th, sm + L.th + (int64_t)M8 * PT, sm + L.th + 2LL * M8 * PT};
+    double *Ps = sm + L.r;
+    double *Rb[3] = {Ps + (int64_t)Dp * PT, Ps + 2LL * Dp * PT, Ps + 3LL * Dp * PT};   // R_k, R_{k-1}, R(Y)
+    double *Gs = sm + L.g, *G2 = Gs + (int64_t)M8 * PT;
+    double *ts = sm + L.t;
+
+    // ---- load: zero everything (pads), scatter the band of F, copy Theta_0 / P / t
+    for (int64_t i = tid; i < L.total; i += nth) sm[i] = 0.0;
+    __syncthreads();
+    for (int d = warp; d < D; d += nw) {
+        const int lo = a.lo[d], ln = a.len[d];
+        const int64_t of = a.off[d];
+        for (int j = lane; j < ln; j += 32) Fd[(int64_t)d * PF + lo + j] = a.val[of + j];
+    }
+    for (int e = tid; e < M * N; e += nth) {
+        const int k = e / N, n = e - k * N;
+        Tb[0][k * PT + n] = a.theta0[e];
+        if (a.fista) Tb[1][k * PT + n] = a.theta_prev ? a.theta_prev[e] : a.theta0[e];
+    }
+    for (int e = tid; e < D * N; e += nth) {
+        const int d = e / N, n = e - d * N;
+        Ps[d * PT + n] = a.P[e];
+    }
+    for (int k = tid; k < M; k += nth) ts[k] = a.tstep[k];
+    __syncthreads();
+
+    const int nbn = N8 >> 3;
+    // S2: Rdst = F T - P (and, FISTA, RY = R(Y) from Rprev); returns this thread's ||R||^2 part
+    auto residual = [&](const double *T, double *Rdst, const double *Rprev, double *RY, double beta, bool first) {
+        double r2 = 0.0;
+        const int ntile = (Dp >> 3) * nbn;
+        for (int tt = warp; tt < ntile; tt += nw) {
+            const int ib = tt / nbn, jb = tt - ib * nbn;
+            double c0, c1;
+            sd_tile(c0, c1, Fd + (int64_t)(8 * ib) * PF, PF, 1, T + 8 * jb, PT, M8 >> 2, g4, t4);
+            const int d = 8 * ib + g4, n = 8 * jb + 2 * t4;
+            const double2 pp = *reinterpret_cast<const double2 *>(Ps + d * PT + n);
+            const double v0 = c0 - pp.x, v1 = c1 - pp.y;
+            *reinterpret_cast<double2 *>(Rdst + d * PT + n) = make_double2(v0, v1);
+            r2 = fma(v0, v0, r2);
+            r2 = fma(v1, v1, r2);
+            if (RY) {
+                double y0 = v0, y1 = v1;
+                if (!first) {
+                    const double2 q = *reinterpret_cast<const double2 *>(Rprev + d * PT + n);
+                    y0 = fma(beta, v0 - q.x, v0);
+                    y1 = fma(beta, v1 - q.y, v1);
+                }
+                *reinterpret_cast<double2 *>(RY + d * PT + n) = make_double2(y0, y1);
+            }
+        }
+        return r2;
+    };
+    // Y (FISTA: Theta_k + beta (Theta_k - Theta_{k-1}); plain: Theta_k) element
+    auto yv = [&](const double *cur, const double *prv, double beta, int i) {
+        return prv ? fma(beta, cur[i] - prv[i], cur[i]) : cur[i];
+    };
+    // S3+S4: Gdst = F^T Rsrc + gamma L Y   (Y from cur / prv as above)
+    auto gradient = [&](const double *Rsrc, double *Gdst, const double *cur, const double *prv, double beta) {
+        const int ntile = (M8 >> 3) * nbn;
+        for (int tt = warp; tt < ntile; tt += nw) {
+            const int ib = tt / nbn, jb = tt - ib * nbn;
+            double c0, c1;
+            sd_tile(c0, c1, Fd + 8 * ib, 1, PF, Rsrc + 8 * jb, PT, Dp >> 2, g4, t4);
+            const int k = 8 * ib + g4, n = 8 * jb + 2 * t4;
+            double o[2] = {c0, c1};
+            if (k < M) {
+#pragma unroll
+                for (int e = 0; e < 2; e++) {
+                    const int i = k * PT + n + e;
+                    const double y = yv(cur, prv, beta, i);
+                    const double yp = k > 0 ? yv(cur, prv, beta, i - PT) : y;
+                    const double yn = k + 1 < M ? yv(cur, prv, beta, i + PT) : y;
+                    o[e] = fma(a.gamma, (y - yp) + (y - yn), o[e]);
+                }
+            }
+            *reinterpret_cast<double2 *>(Gdst + k * PT + n) = make_double2(o[0], o[1]);
+        }
+    };
+
+    int ic = 0, ip = 1, ix = 2;          // Theta_k, Theta_{k-1} (FISTA) / Theta_{k+1} (plain), spare
+    int rk = 0, rp = 1;                  // R_k, R_{k-1}
+    if (a.fista && a.theta_prev) {       // resume: R_{k-1} = F Theta_{k-1} - P
+        residual(Tb[ip], Rb[rp], nullptr, nullptr, 0.0, true);
+        __syncthreads();
+    }
+    const double nm = (double)N * (double)M;
+    int64_t k = 0;
+    bool converged = false, nonfinite = false, stopped = false;
+    int kmod = 0;                                         // k % kkt_every, kept as a counter
+    double bcur = (a.fista && a.iters > 0) ? a.beta[0] : 0.0;
+    for (k = 0; k <= a.iters; k++, kmod = (kmod + 1 == a.kkt_every) ? 0 : kmod + 1) {
+        const bool fin = k == a.iters;                    // final evaluation at Theta_iters
+        const bool kv = fin || kmod == 0;
+        const double beta = (a.fista && !fin) ? bcur : 0.0;
+        if (a.fista && k + 1 < a.iters) bcur = a.beta[k + 1];   // next iteration's beta, loaded early
+        const bool first = k == 0 && !a.theta_prev;
+        double *cur = Tb[ic];
+        const double *prv = (a.fista && !fin) ? Tb[ip] : nullptr;
+        double *out = a.fista ? Tb[ip] : Tb[ix];          // FISTA: Theta_{k+1} over Theta_{k-1}
+        const bool fis = a.fista && !fin;
+        double part[4] = {0.0, 0.0, 0.0, 0.0};            // ||R_k||^2, ||D Theta_k||^2, kkt, kktp
+        part[0] = residual(cur, Rb[rk], Rb[rp], fis ? Rb[2] : nullptr, beta, first);
+        __syncthreads();
+
+        // G(Y) into Gs; the KKT gradient G(Theta_k) is Gs itself unless FISTA (then G2)
+        gradient(fis ? Rb[2] : Rb[rk], Gs, cur, prv, beta);
+        if (fis && kv) gradient(Rb[rk], G2, cur, nullptr, 0.0);
+        __syncthreads();
+        const double *Gk = fis ? G2 : Gs;
+        // S5/S6: a quad (4 lanes) per Fock row, lane t4 holding outcomes n = 4 j + t4 (j < SD_NR / 4)
+        // in registers; row reductions are quad butterflies (identical in the 4 lanes)
+        for (int rb = 0; rb < M; rb += nth >> 2) {   // warp-uniform trip count (shuffles below)
+            if (rb + 8 * warp >= M) continue;   // the warp's 8 rows are all beyond M
+            const int row = rb + (tid >> 2);
+            const bool act = row < M;
+            const double *cr = cur + row * PT;
+            const bool hn = row + 1 < M;
+            double th[SD_NJ], tn[SD_NJ], gk[SD_NJ], x[SD_NJ];
+#pragma unroll
+            for (int j = 0; j < SD_NJ; j++) {
+                const int n = 4 * j + t4;
+                const bool ok = act && n < N;
+                th[j] = ok ? cr[n] : 0.0;
+                tn[j] = (ok && hn) ? cr[PT + n] : th[j];
+                gk[j] = (ok && kv) ? Gk[row * PT + n] : 0.0;
+                x[j] = (ok && !fin) ? Gs[row * PT + n] : 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < SD_NJ; j++) {   // regulariser pair (k, k+1); 0 for pads / the last row
+                const double dd = th[j] - tn[j];
+                part[1] = fma(dd, dd, part[1]);
+            }
+            if (kv) {
+                double mn = INFINITY;
+#pragma unroll
+                for (int j = 0; j < SD_NJ; j++)
+                    if (4 * j + t4 < N) mn = fmin(mn, 2.0 * gk[j]);
+                mn = quad_min(mn);
+                const double lam = -mn, lamp = fmax(lam, 0.0);
+#pragma unroll
+                for (int j = 0; j < SD_NJ; j++)
+                    if (act && 4 * j + t4 < N) {
+                        const double g2 = 2.0 * gk[j];
+                        const double x1 = th[j] * (g2 + lam), x2 = th[j] * (g2 + lamp);
+                        part[2] = fma(x1, x1, part[2]);
+                        part[3] = fma(x2, x2, part[3]);
+                    }
+            }
+            if (fin) continue;
+            const double t = act ? ts[row] : 0.0;
+            double sx = 0.0, xm = -INFINITY, xn = INFINITY;
+#pragma unroll
+            for (int j = 0; j < SD_NJ; j++) {
+                const int n = 4 * j + t4;
+                if (act && n < N) {
+                    const double tp = prv ? prv[row * PT + n] : 0.0;   // Theta_{k-1} (FISTA)
+                    const double y = prv ? fma(beta, th[j] - tp, th[j]) : th[j];
+                    x[j] = fma(-t, x[j], y);
+                    sx += x[j];
+                    xm = fmax(xm, x[j]);
+                    xn = fmin(xn, x[j]);
+                } else {
+                    x[j] = -INFINITY;
+                }
+            }
+            sx = quad_sum(sx);
+            xm = quad_max(xm);
+            xn = quad_min(xn);
+            double tau = (sx - 1.0) / (double)N;
+            bool done = !act || xn > tau;   // Michelot from max(tau_0, max X - 1) (reading R4)
+            if (!done) tau = fmax(tau, xm - 1.0);
+            int cnt = N + 1;
+            for (int round = 0; round <= N; round++) {
+                if (__all_sync(0xffffffffu, done)) break;
+                double ps = 0.0, mA = INFINITY;
+                int pc = 0;
+#pragma unroll
+                for (int j = 0; j < SD_NJ; j++)
+                    if (x[j] > tau) {
+                        ps += x[j];
+                        pc++;
+                        mA = fmin(mA, x[j]);
+                    }
+                ps = quad_sum(ps);
+                pc = quad_sum_i(pc);
+                mA = quad_min(mA);
+                if (!done) {
+                    if (pc >= cnt) {
+                        done = true;
+                    } else {
+                        cnt = pc;
+                        tau = (ps - 1.0) / (double)pc;
+                        done = mA > tau;
+                    }
+                }
+            }
+            if (act) {
+                double *orow = out + row * PT;
+#pragma unroll
+                for (int j = 0; j < SD_NJ; j++) {
+                    const int n = 4 * j + t4;
+                    if (n < N) {
+                        const double o = x[j] - tau;
+                        orow[n] = o > 0.0 ? o : 0.0;
+                    }
+                }
+            }
+        }
+        sd_block_sum4(part, pbuf);
+
+        const double f = part[0] + a.gamma * part[1];
+        const double r = kv ? sqrt(part[2] / nm) : NAN, rpv = kv ? sqrt(part[3] / nm) : NAN;
+        if (tid == 0 && k < a.trace_len) {
+            a.trace[k] = f;
+            a.kkt[k] = r;
+            a.kktp[k] = rpv;
+        }
+        if (fin) {
+            if (!isfinite(f)) nonfinite = true;
+            break;
+        }
+        if (!isfinite(f)) {
+            nonfinite = stopped = true;
+            break;
+        }
+        if (kv && r <= a.tol) {
+            converged = stopped = true;
+            break;
+        }
+        if (a.fista) {   // Theta_{k+1} (in the old Theta_{k-1} buffer) becomes current
+            const int t2 = ip;
+            ip = ic;
+            ic = t2;
+            const int r2 = rp;   // R_k becomes R_{k-1}
+            rp = rk;
+            rk = r2;
+        } else {
+            const int t2 = ix;
+            ix = ic;
+            ic = t2;
+        }
+        // the next residual overwrites R_{k-1}'s buffer only after every thread passed the
+        // block reduction above (its barrier), so no extra barrier is needed here
+    }
+    const double *cur = Tb[ic];
+    const double *prv = Tb[ip];
+    for (int e = tid; e < M * N; e += nth) {
+        const int kk = e / N, n = e - kk * N;
+        a.theta_out[e] = cur[kk * PT + n];
+        if (a.fista && a.prev_out) a.prev_out[e] = prv[kk * PT + n];
+    }
+    if (tid == 0) {
+        const int64_t kd = stopped ? k : a.iters;
+        a.state->iters_done = kd;
+        a.state->it = kd;
+        a.state->stop = 1;
+        a.state->converged = converged ? 1 : 0;
+        a.state->nonfinite = nonfinite ? 1 : 0;
+    }
+}
+
+bool small_use_dense(const SmallArgs &a)
+{
+    static int v = -1;   // QDT_SMALL_DENSE=0: the band form (A/B)
+    if (v < 0) {
+        const char *e = getenv("QDT_SMALL_DENSE");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1 && small_dense_smem(a.D, a.M, a.N, a.fista) <= SMALL_SMEM_MAX;
+}
+
 cudaError_t launch_small_solve(const SmallArgs &a, cudaStream_t s)
 {
+    if (small_use_dense(a)) {
+        const size_t smem = small_dense_smem(a.D, a.M, a.N, a.fista);
+        cudaError_t e = cudaFuncSetAttribute(k_small_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        k_small_dense<<<1, SD_THREADS, smem, s>>>(a);
+        return cudaGetLastError();
+    }
     const size_t smem = small_solve_smem(a.D, a.M, a.N, a.nnz, a.fista);
     cudaError_t e = cudaFuncSetAttribute(k_small_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

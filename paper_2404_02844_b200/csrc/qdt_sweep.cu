@@ -1647,7 +1647,24 @@ __global__ void __launch_bounds__(256) k_reduce_R2(const double *rpart, const in
         const int64_t j0 = red_beg[d], j1 = red_beg[d + 1];
         for (int n0 = 0; n0 < N; n0 += 128) {          // four independent columns per lane
             double s[4] = {0.0, 0.0, 0.0, 0.0};
-            for (int64_t j = j0; j < j1; j++) {
+            int64_t j = j0;
+            // four partial rows in flight, added in list order (same sums as one row at a time)
+            for (; j + 4 <= j1; j += 4) {
+                const int64_t r0 = red_rows[j], r1 = red_rows[j + 1], r2 = red_rows[j + 2], r3 = red_rows[j + 3];
+                double q[4][4];
+#pragma unroll
+                for (int c = 0; c < 4; c++) {
+                    const bool ok = n0 + lane + 32 * c < N;
+                    const int64_t o = n0 + lane + 32 * c;
+                    q[0][c] = ok ? rpart[r0 * N + o] : 0.0;
+                    q[1][c] = ok ? rpart[r1 * N + o] : 0.0;
+                    q[2][c] = ok ? rpart[r2 * N + o] : 0.0;
+                    q[3][c] = ok ? rpart[r3 * N + o] : 0.0;
+                }
+#pragma unroll
+                for (int c = 0; c < 4; c++) s[c] = (((s[c] + q[0][c]) + q[1][c]) + q[2][c]) + q[3][c];
+            }
+            for (; j < j1; j++) {
                 const double *src = rpart + red_rows[j] * N + n0 + lane;
 #pragma unroll
                 for (int c = 0; c < 4; c++)
@@ -1676,33 +1693,62 @@ __global__ void __launch_bounds__(256) k_reduce_R2(const double *rpart, const in
 }
 
 // ------------------------------------------------------------------------------ scalars
-// One CTA of 1024 threads: thread t sums entries t, t + 1024, ... of the tile partials and of
-// partR (fixed assignment and order), then a fixed-shape tree over warps; thread 0 applies the
-// trace / KKT / stop logic.  Deterministic, no atomics, one launch (latency ~ a few us).
-__global__ void __launch_bounds__(1024) k_scalars2(const double *partR, int nR, const double *partT,
-                                                   int ntiles, int include_r2, double *stage,
-                                                   int *arrive, double *vec, int64_t N, int64_t M,
-                                                   double gamma, double tol, int final_eval,
-                                                   int kkt_every, double *trace, double *kkt,
-                                                   double *kktp, int64_t trace_len, DevState *st,
-                                                   int finalize)
+// G blocks (G <= SC2_BLOCKS): block b sums a contiguous slice of the tile partials and of partR
+// (thread t: entries t, t + blockDim, ... of the slice, in order), then a fixed-shape tree over
+// warps, into stage[b].  The last block to arrive (ticket on *arrive, reset by it) sums the G
+// block partials in block order and applies the trace / KKT / stop logic (thread 0).
+// Deterministic (fixed slices and orders), no floating-point atomics.
+__global__ void __launch_bounds__(256) k_scalars2(const double *partR, int nR, const double *partT,
+                                                  int ntiles, int include_r2, double *stage,
+                                                  int *arrive, double *vec, int64_t N, int64_t M,
+                                                  double gamma, double tol, int final_eval,
+                                                  int kkt_every, double *trace, double *kkt,
+                                                  double *kktp, int64_t trace_len, DevState *st,
+                                                  int finalize)
 {
-    __shared__ double red[32 * NV];
-    (void)stage;
-    (void)arrive;
+    __shared__ double red[8 * NV];
+    __shared__ int s_last;
     if (st->stop) return;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, G = gridDim.x, b = blockIdx.x;
     double v[NV];
 #pragma unroll
     for (int i = 0; i < NV; i++) v[i] = 0.0;
-    if (include_r2)
-        for (int i = threadIdx.x; i < nR; i += blockDim.x) v[V_R2] += partR[i];
-    for (int t = threadIdx.x; t < ntiles; t += blockDim.x) {
-        const double4 q = *reinterpret_cast<const double4 *>(partT + (int64_t)t * NSC_TILE);
-        v[V_KKT] += q.x;
-        v[V_KKTP] += q.y;
-        v[V_REG] += q.z;
-        v[V_DTH] += q.w;
+    constexpr int BQ = 4;   // loads in flight per thread, added in the same order as one at a time
+    if (include_r2) {
+        const int cr = (nR + G - 1) / G, r0 = b * cr, r1 = min(nR, r0 + cr);
+        int i = r0 + threadIdx.x;
+        for (; i + (BQ - 1) * (int)blockDim.x < r1; i += BQ * blockDim.x) {
+            double q[BQ];
+#pragma unroll
+            for (int j = 0; j < BQ; j++) q[j] = partR[i + j * blockDim.x];
+#pragma unroll
+            for (int j = 0; j < BQ; j++) v[V_R2] += q[j];
+        }
+        for (; i < r1; i += blockDim.x) v[V_R2] += partR[i];
+    }
+    {
+        const int ct = (ntiles + G - 1) / G, t0 = b * ct, t1 = min(ntiles, t0 + ct);
+        int t = t0 + threadIdx.x;
+        for (; t + (BQ - 1) * (int)blockDim.x < t1; t += BQ * blockDim.x) {
+            double4 q[BQ];
+#pragma unroll
+            for (int j = 0; j < BQ; j++)
+                q[j] = *reinterpret_cast<const double4 *>(partT + (int64_t)(t + j * blockDim.x) * NSC_TILE);
+#pragma unroll
+            for (int j = 0; j < BQ; j++) {
+                v[V_KKT] += q[j].x;
+                v[V_KKTP] += q[j].y;
+                v[V_REG] += q[j].z;
+                v[V_DTH] += q[j].w;
+            }
+        }
+        for (; t < t1; t += blockDim.x) {
+            const double4 q = *reinterpret_cast<const double4 *>(partT + (int64_t)t * NSC_TILE);
+            v[V_KKT] += q.x;
+            v[V_KKTP] += q.y;
+            v[V_REG] += q.z;
+            v[V_DTH] += q.w;
+        }
     }
 #pragma unroll
     for (int i = 0; i < NV; i++) v[i] = wsum(v[i]);
@@ -1710,12 +1756,36 @@ __global__ void __launch_bounds__(1024) k_scalars2(const double *partR, int nR, 
 #pragma unroll
         for (int i = 0; i < NV; i++) red[warp * NV + i] = v[i];
     __syncthreads();
-    if (warp == 0) {
-        const int nw = blockDim.x >> 5;
+    if (threadIdx.x == 0) {
+        double w[NV];
 #pragma unroll
-        for (int i = 0; i < NV; i++) v[i] = lane < nw ? red[lane * NV + i] : 0.0;
+        for (int i = 0; i < NV; i++) w[i] = 0.0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); k++)
 #pragma unroll
-        for (int i = 0; i < NV; i++) v[i] = wsum(v[i]);
+            for (int i = 0; i < NV; i++) w[i] += red[k * NV + i];
+        if (G == 1) {
+#pragma unroll
+            for (int i = 0; i < NV; i++) v[i] = w[i];
+            s_last = 1;
+        } else {
+#pragma unroll
+            for (int i = 0; i < NV; i++) __stcg(stage + b * NV + i, w[i]);
+            __threadfence();
+            s_last = atomicAdd(arrive, 1) == G - 1;
+        }
+    }
+    __syncthreads();
+    if (!s_last) return;
+    if (G > 1) {   // last block: the block partials in block order (warp 0: lanes b, b + 32)
+        __threadfence();
+        if (warp != 0) return;
+#pragma unroll
+        for (int i = 0; i < NV; i++) {
+            double x = lane < G ? __ldcg(stage + lane * NV + i) : 0.0;
+            if (lane + 32 < G) x += __ldcg(stage + (lane + 32) * NV + i);
+            v[i] = wsum(x);
+        }
+        if (lane == 0) *arrive = 0;
     }
     if (threadIdx.x != 0) return;
     for (int i = 0; i < NV; i++) vec[i] = v[i];
@@ -1966,7 +2036,9 @@ cudaError_t launch_scalars2(const double *partR, int nR, const double *partT, in
                             double *trace, double *kkt, double *kktp, int64_t trace_len,
                             DevState *st, int finalize, cudaStream_t s)
 {
-    k_scalars2<<<1, 1024, 0, s>>>(partR, nR, partT, ntiles, include_r2, stage, arrive, vec,
+    // block count: ~256 tile partials per block (one double4 load per thread), at most SC2_BLOCKS
+    const int G = std::max(1, std::min(SC2_BLOCKS, std::max(ntiles, include_r2 ? nR : 0) / 256));
+    k_scalars2<<<(stage && arrive) ? G : 1, 256, 0, s>>>(partR, nR, partT, ntiles, include_r2, stage, arrive, vec,
                                           N, M, gamma, tol, final_eval, kkt_every, trace, kkt, kktp,
                                           trace_len, st, finalize);
     return cudaGetLastError();

@@ -234,3 +234,42 @@ def test_small_solve_resume_and_stop(q, ctx):
     rg2 = q.qdt_solve(ctx, Fg, I.P, I.gamma, tol, 30)
     assert rg2["info"]["iters_done"] == ro2["iters_done"]
     assert np.abs(rg2["theta"] - ro2["theta"]).max() <= 1e-9
+
+
+@pytest.mark.parametrize("D,M,N", [(100, 50, 10), (37, 21, 1), (64, 33, 7), (90, 60, 16), (50, 30, 17), (120, 24, 24)])
+@pytest.mark.parametrize("accel", [0, 1])
+def test_small_dense_and_band_forms(q, ctx, D, M, N, accel):
+    """Single-CTA solve: the dense DMMA form (N <= 16, F dense in shared memory) and the band form
+    (N > 16) against the oracle: Theta, trace, KKT at every recorded iteration, then an early stop
+    at the oracle's iteration and a FISTA resume bit for bit."""
+    I = qs.random_instance(70 + N + D, D, M, N, gamma=1e-3)
+    Fo = oracle.Probes(I.alpha2, M)
+    Fg = q.qdt_build_probes(ctx, I.alpha2, M)
+    iters, ke = 300, (7 if accel else 1)
+    ro = oracle.solve(Fo, I.P, I.gamma, 0.0, iters, accel=accel, kkt_every=ke)
+    rg = q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, iters, accel=bool(accel), kkt_every=ke)
+    # N = 1: every row is the vertex 1, r_KKT = 0 <= tol = 0 stops both at iteration 0
+    assert rg["info"]["iters_done"] == ro["iters_done"] == (iters if N > 1 else 0)
+    assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9
+    assert _trace_ok(rg["trace"], ro["trace"], I.P)
+    m = ~np.isnan(ro["kkt"])
+    np.testing.assert_array_equal(m, ~np.isnan(rg["kkt"]))
+    np.testing.assert_allclose(rg["kkt"][m], ro["kkt"][m], rtol=1e-8, atol=1e-15)
+    Th = rg["theta"]
+    assert Th.min() >= 0 and np.abs(Th.sum(1) - 1).max() <= 4 * N * EPS
+    if N == 1:
+        return
+    # early stop at the oracle's iteration (tolerance just above a recorded KKT value)
+    j = int(np.flatnonzero(m)[len(np.flatnonzero(m)) // 3])
+    tol = ro["kkt"][j] * (1 + 1e-7)
+    ro2 = oracle.solve(Fo, I.P, I.gamma, tol, iters, accel=accel, kkt_every=ke)
+    rg2 = q.qdt_solve(ctx, Fg, I.P, I.gamma, tol, iters, accel=bool(accel), kkt_every=ke)
+    assert rg2["info"]["iters_done"] == ro2["iters_done"]
+    assert bool(rg2["info"]["converged"]) == (ro2["iters_done"] < iters)
+    assert np.abs(rg2["theta"] - ro2["theta"]).max() <= 1e-9
+    if accel:
+        a = q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, 13, accel=True, want_prev=True, kkt_every=ke)
+        b = q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, 17, accel=True, theta0=a["theta"],
+                        theta_prev=a["theta_prev"], fista_t=a["info"]["fista_t"], kkt_every=ke)
+        full = q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, 30, accel=True, kkt_every=ke)
+        assert np.array_equal(b["theta"], full["theta"])
