@@ -198,6 +198,11 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
             }
             ttry[tid] = tr;
         }
+        // the rows' step weights, loaded before the GEMM to hide their latency
+        double tk[2];
+#pragma unroll
+        for (int i = 0; i < 2; i++)
+            tk[i] = (8 * i + g < Tt) ? (a.tscal ? *a.tscal : __ldg(a.tstep + k0 + 8 * i + g)) : 0.0;
         double acc[2][NBW][2];
 #pragma unroll
         for (int i = 0; i < 2; i++)
@@ -251,7 +256,6 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
         QDT_PH(2);
 
         // ---- S4 + pass 1: G = acc + gamma L Y; row min of G, sum / max / min of X = Y - t G
-        double tk[2];
         double pmn[2], ps[2], pxm[2], pxn[2], pts[2], ptc[2], ptm[2];
 #pragma unroll
         for (int i = 0; i < 2; i++) {
@@ -260,7 +264,6 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
             const bool act = rl < Tt;
             const int64_t kg = a.kb + kl;
             const bool hp = kg > 0, hn = kg + 1 < a.M;
-            tk[i] = act ? (a.tscal ? *a.tscal : __ldg(a.tstep + kl)) : 0.0;
             const double tau_t = ttry[rl];
             double mn = INFINITY, s = 0.0, xm = -INFINITY, xn = INFINITY;
             double ts = 0.0, tm = INFINITY;
