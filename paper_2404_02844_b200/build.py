@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libqdt.so")
 SRCS = [os.path.join(HERE, "csrc", f) for f in ("qdt_api.cu", "qdt_kernels.cu", "qdt_sweep.cu", "qdt_newton.cu",
-                                                            "qdt_wide.cu", "qdt_small.cu")]
+                                                            "qdt_wide.cu", "qdt_small.cu", "qdt_coop.cu")]
 DEPS = SRCS + glob.glob(os.path.join(HERE, "csrc", "*.h")) + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + [os.path.join(ROOT, "include", "qdt.h"),
                                                               os.path.abspath(__file__)]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -201,7 +201,9 @@ struct qdt_probes {
     int32_t *d_sw_dA = nullptr, *d_sw_dB = nullptr;
     int64_t *d_fb_off = nullptr;
     double *d_Fb = nullptr;
-    int32_t *d_row_da = nullptr, *d_row_db = nullptr;   // probes covering each local row (small solve)
+    int32_t *d_row_da = nullptr, *d_row_db = nullptr;   // probes covering each local row (small / coop solve)
+    int64_t *d_toff = nullptr;                         // coop solve: transposed band offsets (Ml + 1)
+    double *d_FT = nullptr;                            // coop solve: transposed band values (nnz)
     // step-setup cache (per probe handle): the step t_k per local row of the last (mode, gamma); F
     // is immutable, so a repeated solve reuses the SQS weights / the 100-step power iteration
     double *d_tcache = nullptr;
@@ -212,6 +214,8 @@ struct qdt_probes {
     {
         cudaFree(d_row_da);
         cudaFree(d_row_db);
+        cudaFree(d_toff);
+        cudaFree(d_FT);
         cudaFree(d_tcache);
         cudaFree(d_sw_dA);
         cudaFree(d_sw_dB);
@@ -804,6 +808,14 @@ static bool small_enabled()
     const char *e = getenv("QDT_SMALL");
     return !(e && e[0] == '0');
 }
+
+// QDT_COOP=0 keeps latency-bound problems on the multi-kernel loop (A/B)
+static bool coop_enabled()
+{
+    const char *e = getenv("QDT_COOP");
+    return !(e && e[0] == '0');
+}
+constexpr int64_t COOP_MAX_ROWS = 16384;   // grid-persistent solve: Fock rows of a latency-bound problem
 
 // QDT_WIDE=new selects the fused cluster step at every N > 128 (A/B, tests); N > 1024 always takes it
 static bool wide_new_forced()
@@ -2181,7 +2193,10 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     const bool small = ctx->nranks == 1 && !bb && small_enabled() &&
                        (small_solve_smem(D, Ml, (int)N, p->nnz, fista) <= SMALL_SMEM_MAX ||
                         small_dense_smem(D, Ml, (int)N, fista) <= SMALL_SMEM_MAX) && D * N < (1LL << 30);
-    if (small && !p->d_row_da) {
+    // ---- latency-bound sizes (Medium): the whole solve in one grid-persistent kernel (qdt_coop.cu)
+    const bool coop = !small && ctx->nranks == 1 && !bb && coop_enabled() && coop_supported((int)N) &&
+                      Ml <= COOP_MAX_ROWS && Ml >= 1 && D * N < (1LL << 30);
+    if ((small || coop) && !p->d_row_da) {
         std::vector<int32_t> da(Ml, 0), db(Ml, 0);
         int64_t a0 = 0;
         for (int64_t k = 0; k < Ml; k++) {   // band edges are monotone: contiguous covering probes
@@ -2196,10 +2211,21 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
         CK(cudaMemcpy(p->d_row_da, da.data(), sizeof(int32_t) * Ml, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(p->d_row_db, db.data(), sizeof(int32_t) * Ml, cudaMemcpyHostToDevice));
     }
+    if (coop && !p->d_FT) {   // transposed band (once per probe handle)
+        std::vector<int32_t> da(Ml), db(Ml);
+        CK(cudaMemcpy(da.data(), p->d_row_da, sizeof(int32_t) * Ml, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(db.data(), p->d_row_db, sizeof(int32_t) * Ml, cudaMemcpyDeviceToHost));
+        std::vector<int64_t> toff(Ml + 1, 0);
+        for (int64_t k = 0; k < Ml; k++) toff[k + 1] = toff[k] + (db[k] - da[k]);
+        CK(cudaMalloc(&p->d_toff, sizeof(int64_t) * (Ml + 1)));
+        CK(cudaMalloc(&p->d_FT, sizeof(double) * std::max<int64_t>(1, toff[Ml])));
+        CK(cudaMemcpy(p->d_toff, toff.data(), sizeof(int64_t) * (Ml + 1), cudaMemcpyHostToDevice));
+        CK(run_k(ctx, "build_FT", 1, [&]() { return launch_build_FT(p->band(), (int)D, p->d_row_da, p->d_toff, p->d_FT, s); }));
+    }
 
     // ---- the hot loop: graph of `period` iterations replayed
     const int period = fista ? 12 : 16;   // multiple of the buffer rotation (3 / 2)
-    const bool use_graph = opt.use_graph && !ctx->profiling && iters >= period && !ctx->vg && !small;
+    const bool use_graph = opt.use_graph && !ctx->profiling && iters >= period && !ctx->vg && !small && !coop;
     DevState hst;
     int64_t done = 0;
     bool stopped = false;
@@ -2289,6 +2315,46 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
         sa.state = b.state;
         CK(run_k(ctx, "small_solve", 1, [&]() { return launch_small_solve(sa, s); }));
         done = iters;
+    } else if (coop) {
+        CoopArgs ca;
+        ca.D = (int)D;
+        ca.M = (int)Ml;
+        ca.N = (int)N;
+        ca.Nv = (int)Nu;
+        ca.lo = p->d_lo;
+        ca.len = p->d_len;
+        ca.off = p->d_off;
+        ca.val = p->d_val;
+        ca.row_da = p->d_row_da;
+        ca.row_db = p->d_row_db;
+        ca.toff = p->d_toff;
+        ca.FT = p->d_FT;
+        for (int i = 0; i < 3; i++) ca.theta[i] = b.theta[i < nbuf ? i : 0];
+        ca.R[0] = b.R[0];
+        ca.R[1] = fista ? b.R[1] : b.R[0];
+        ca.RY = fista ? b.RY : nullptr;
+        ca.P = b.P;
+        ca.tstep = b.tstep;
+        ca.beta = b.beta;
+        ca.gamma = gamma;
+        ca.tol = tol;
+        ca.iters = iters;
+        ca.kkt_every = opt.kkt_every;
+        ca.fista = fista;
+        ca.resume = (fista && opt.theta_prev) ? 1 : 0;
+        ca.trace = b.trace;
+        ca.kkt = b.kkt;
+        ca.kktp = b.kktp;
+        ca.trace_len = tcap;
+        double *cpart, *cbar;
+        CKS(ws_get(ctx, "coop_part", (int64_t)2 * coop_max_grid() * 4, &cpart));
+        CKS(ws_get(ctx, "coop_bar", 1, &cbar));
+        CK(cudaMemsetAsync(cbar, 0, sizeof(double), s));
+        ca.part = cpart;
+        ca.bar = reinterpret_cast<unsigned *>(cbar);
+        ca.state = b.state;
+        CK(run_k(ctx, "coop_solve", 1, [&]() { return launch_coop_solve(ca, s); }));
+        done = iters;
     }
     while (done < iters) {
         if (use_graph && iters - done >= period) {
@@ -2330,7 +2396,7 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     CK(cudaMemcpyAsync(&hst, b.state, sizeof hst, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     stopped = hst.stop != 0;
-    if (!small && stopped && hst.converged && !hst.nonfinite && (pl->NB || pl->NW || pl->NX) && !fista) {
+    if (!small && !coop && stopped && hst.converged && !hst.nonfinite && (pl->NB || pl->NW || pl->NX) && !fista) {
         // the sweep loop evaluates the unclamped KKT only; re-evaluate Theta_kd once with the
         // general kernels so that trace/kkt/kkt_paper at kd come from one consistent pass
         DevState sr = hst;
@@ -2340,7 +2406,7 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
         CKS(eval_pass(ctx, c, b, b.theta[hst.iters_done % nbuf]));
         CK(cudaMemcpyAsync(b.state, &hst, sizeof hst, cudaMemcpyHostToDevice, s));
     }
-    if (!small && !stopped) {
+    if (!small && !coop && !stopped) {
         CKS(eval_pass(ctx, c, b, b.theta[iters % nbuf]));
         CK(cudaMemcpyAsync(&hst, b.state, sizeof hst, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));

@@ -187,6 +187,32 @@ struct SmallArgs {
     double *theta_out, *prev_out;
     DevState *state;
 };
+// ---- grid-persistent cooperative solve (qdt_coop.cu): latency-bound sizes (Medium)
+struct CoopArgs {
+    int D, M, N, Nv;
+    const int32_t *lo, *len;
+    const int64_t *off;
+    const double *val;
+    const int32_t *row_da, *row_db;   // probes covering Fock row k: [row_da[k], row_db[k])
+    const int64_t *toff;              // transposed band: F[d][k] at FT[toff[k] + d - row_da[k]]
+    const double *FT;
+    double *theta[3];                 // Theta_k in theta[k % nbuf] (local row 0)
+    double *R[2];                     // R_k (FISTA: R_k / R_{k-1} alternate by k & 1)
+    double *RY;                       // FISTA: R(Y_k)
+    const double *P, *tstep, *beta;
+    double gamma, tol;
+    int64_t iters;
+    int kkt_every, fista, resume;     // resume: R[1] holds R_{-1} = F Theta_{-1} - P
+    double *trace, *kkt, *kktp;
+    int64_t trace_len;
+    double *part;                     // 2 x grid x 4 per-CTA partials
+    unsigned *bar;                    // grid barrier: arrival counter, generation (zeroed)
+    DevState *state;
+};
+bool coop_supported(int N);
+int coop_max_grid();
+cudaError_t launch_coop_solve(const CoopArgs &a, cudaStream_t s);
+cudaError_t launch_build_FT(Band b, int D, const int32_t *row_da, const int64_t *toff, double *FT, cudaStream_t s);
 size_t small_solve_smem(int64_t D, int64_t M, int N, int64_t nnz, int fista);
 constexpr int SD_NR = 16;       // dense small solve: widest row held in registers
 size_t small_dense_smem(int64_t D, int64_t M, int N, int fista);   // SIZE_MAX when N > SD_NR

@@ -273,3 +273,38 @@ def test_small_dense_and_band_forms(q, ctx, D, M, N, accel):
                         theta_prev=a["theta_prev"], fista_t=a["info"]["fista_t"], kkt_every=ke)
         full = q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, 30, accel=True, kkt_every=ke)
         assert np.array_equal(b["theta"], full["theta"])
+
+
+@pytest.mark.parametrize("N", [2, 31, 64, 100, 127, 128])
+@pytest.mark.parametrize("accel", [0, 1])
+def test_coop_solve_forms(q, ctx, N, accel):
+    """Grid-persistent cooperative solve (latency-bound sizes: Fock rows <= 16384, N <= 128, not
+    small enough for one CTA): Theta, trace and KKT against the oracle, early stop at the oracle's
+    iteration, FISTA resume bit for bit, bitwise run-to-run determinism."""
+    I = qs.random_instance(900 + N + accel, 300, 400, N, mu_max=450.0, gamma=1e-3)
+    Fo = oracle.Probes(I.alpha2, I.M)
+    Fg = q.qdt_build_probes(ctx, I.alpha2, I.M)
+    iters, ke = 150, (5 if accel else 1)
+    ro = oracle.solve(Fo, I.P, I.gamma, 0.0, iters, accel=accel, kkt_every=ke)
+    rg = q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, iters, accel=bool(accel), kkt_every=ke)
+    assert rg["info"]["iters_done"] == ro["iters_done"] == iters
+    assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9
+    assert _trace_ok(rg["trace"], ro["trace"], I.P)
+    m = ~np.isnan(ro["kkt"])
+    np.testing.assert_array_equal(m, ~np.isnan(rg["kkt"]))
+    np.testing.assert_allclose(rg["kkt"][m], ro["kkt"][m], rtol=1e-8, atol=1e-15)
+    rg_again = q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, iters, accel=bool(accel), kkt_every=ke)
+    assert np.array_equal(rg["theta"], rg_again["theta"])
+    assert np.array_equal(rg["trace"], rg_again["trace"])
+    j = int(np.flatnonzero(m)[len(np.flatnonzero(m)) // 3])
+    tol = ro["kkt"][j] * (1 + 1e-7)
+    ro2 = oracle.solve(Fo, I.P, I.gamma, tol, iters, accel=accel, kkt_every=ke)
+    rg2 = q.qdt_solve(ctx, Fg, I.P, I.gamma, tol, iters, accel=bool(accel), kkt_every=ke)
+    assert rg2["info"]["iters_done"] == ro2["iters_done"]
+    assert np.abs(rg2["theta"] - ro2["theta"]).max() <= 1e-9
+    if accel:
+        a = q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, 13, accel=True, want_prev=True, kkt_every=ke)
+        b = q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, 17, accel=True, theta0=a["theta"],
+                        theta_prev=a["theta_prev"], fista_t=a["info"]["fista_t"], kkt_every=ke)
+        full = q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, 30, accel=True, kkt_every=ke)
+        assert np.array_equal(b["theta"], full["theta"])
