@@ -227,7 +227,7 @@ def run_qdt(args):
     solve(prof_iters)
     kern = {}
     for name in ["fwd_partial", "reduce_R", "bwd_step", "proj_step", "bwd_heavy", "sweep_fused", "fwd_heavy",
-                 "scalars", "allreduce_R", "halo"]:
+                 "scalars", "allreduce_R", "halo", "coop_solve", "small_solve"]:
         c, t = q.qdt_profile_get(ctx, name)
         if c:
             kern[name] = {"count": c, "avg_ms": t / c}
@@ -242,7 +242,13 @@ def run_qdt(args):
     f64, f64src = fp64_peak()
     ab = algorithmic_bytes(rows_local, N, D, nnz_local)
     af = algorithmic_flops(rows_local, N, D, nnz_local)
-    dom = max(("bwd_step", "fwd_partial"), key=lambda k: kern.get(k, {}).get("avg_ms", 0))
+    # one-launch solves (the single-CTA small solve, the grid-persistent kernel): the launch covers
+    # the profiled call's prof_iters iterations + the final evaluation, so its algorithmic bytes /
+    # flops are (prof_iters + 1) iterations' worth
+    for k in ("coop_solve", "small_solve"):
+        ab[k] = (prof_iters + 1) * ab["iteration"]
+        af[k] = (prof_iters + 1) * af["iteration"]
+    dom = max(("bwd_step", "fwd_partial", "coop_solve", "small_solve"), key=lambda k: kern.get(k, {}).get("avg_ms", 0))
     dom_ms = kern[dom]["avg_ms"] if dom in kern else float("nan")
     roof = roofline_of(ab[dom], af[dom], dom_ms, hbm, f64)
     traffic = None
