@@ -308,3 +308,20 @@ def test_coop_solve_forms(q, ctx, N, accel):
                         theta_prev=a["theta_prev"], fista_t=a["info"]["fista_t"], kkt_every=ke)
         full = q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, 30, accel=True, kkt_every=ke)
         assert np.array_equal(b["theta"], full["theta"])
+
+
+@pytest.mark.parametrize("D,M,N,mu_max", [(200, 700, 33, 150.0), (57, 2600, 100, 2000.0), (1000, 300, 7, 280.0)])
+def test_coop_solve_shapes(q, ctx, D, M, N, mu_max):
+    """Grid-persistent solve on odd N, Fock rows no probe covers (mu_max << M: empty phase-B tasks),
+    ragged probe / row blocks (D, M not multiples of 8), many probes per row."""
+    I = qs.random_instance(D + M + N, D, M, N, mu_max=mu_max, gamma=1e-3)
+    Fo = oracle.Probes(I.alpha2, I.M)
+    Fg = q.qdt_build_probes(ctx, I.alpha2, I.M)
+    for accel in (0, 1):
+        ro = oracle.solve(Fo, I.P, I.gamma, 0.0, 60, accel=accel, kkt_every=1)
+        rg = q.qdt_solve(ctx, Fg, I.P, I.gamma, 0.0, 60, accel=bool(accel), kkt_every=1)
+        assert rg["info"]["iters_done"] == ro["iters_done"]
+        assert np.abs(rg["theta"] - ro["theta"]).max() <= 1e-9
+        assert _trace_ok(rg["trace"], ro["trace"], I.P)
+        m = ~np.isnan(ro["kkt"])
+        np.testing.assert_allclose(rg["kkt"][m], ro["kkt"][m], rtol=1e-8, atol=1e-15)
