@@ -1681,6 +1681,8 @@ static WideArgs wide_args(const IterCfg &c, SolveBufs &b, const double *R, const
     w.theta_prev = nullptr;
     w.beta = nullptr;
     w.state = b.state;
+    w.row_da = c.p->d_row_da;
+    w.row_db = c.p->d_row_db;
     return w;
 }
 
@@ -2196,7 +2198,7 @@ extern "C" qdt_status qdt_solve(qdt_ctx *ctx, const qdt_probes *F, const double 
     // ---- latency-bound sizes (Medium): the whole solve in one grid-persistent kernel (qdt_coop.cu)
     const bool coop = !small && ctx->nranks == 1 && !bb && coop_enabled() && coop_supported((int)N) &&
                       Ml <= COOP_MAX_ROWS && Ml >= 1 && D * N < (1LL << 30);
-    if ((small || coop) && !p->d_row_da) {
+    if ((small || coop || pl->NW) && !p->d_row_da) {
         std::vector<int32_t> da(Ml, 0), db(Ml, 0);
         int64_t a0 = 0;
         for (int64_t k = 0; k < Ml; k++) {   // band edges are monotone: contiguous covering probes

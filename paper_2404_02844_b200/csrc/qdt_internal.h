@@ -170,6 +170,8 @@ struct WideArgs {               // wide-N sweep (N > 128): k_grad_wide + k_proj_
     const double *theta_prev;   // FISTA step: Theta_{k-1}
     const double *beta;         // FISTA step: beta_k by state->it (nullptr: plain)
     const DevState *state;
+    const int32_t *row_da = nullptr, *row_db = nullptr;   // probes covering local row k: [row_da, row_db)
+                                                          // (k_grad_wide skips k-steps outside a warp's rows)
 };
 // ---- single-CTA persistent solve (qdt_small.cu): the whole problem in shared memory
 struct SmallArgs {

@@ -365,6 +365,24 @@ __device__ __forceinline__ void gemm_bwd(double (&acc)[NB][2], const double *F, 
     }
 }
 
+// gemm_bwd over the k-steps [kslo, kshi) of the chunk only (the others multiply F entries that are
+// zero for this warp's rows: the probes outside the rows' covering range)
+template <int NB>
+__device__ __forceinline__ void gemm_bwd_rng(double (&acc)[NB][2], const double *F, const double *R,
+                                             int kc, int N, int t4, int kslo, int kshi)
+{
+    const int nks = (kc + 3) >> 2;
+    const int k1 = min(nks, kshi);
+    for (int ks = max(0, kslo); ks < k1; ks++) {
+        const int jj = 4 * ks + t4;
+        const bool okj = jj < kc;
+        const double av = okj ? F[jj * STP] : 0.0;
+        const double *rb = R + jj * N;
+#pragma unroll
+        for (int nb = 0; nb < NB; nb++) dmma(acc[nb][0], acc[nb][1], av, okj ? rb[8 * nb] : 0.0);
+    }
+}
+
 // SQS row weights from the tiled F (reading R2): w_k = sum_d F_{d,k} s_d + 4 gamma over the
 // tile's window, t_k = 1/w_k (0 for a frozen row).  Block per tile: 64 rows x 4 probe slices
 // (fixed combination order, deterministic); the window's F rows are read coalesced.
@@ -1130,11 +1148,21 @@ __global__ void __launch_bounds__(256, 2) k_grad_wide(WideArgs a)
     double acc[NB][2];
 #pragma unroll
     for (int nb = 0; nb < NB; nb++) acc[nb][0] = acc[nb][1] = 0.0;
+    // probes covering this warp's 8 rows: [pda, pdb) (contiguous: band edges are monotone); k-steps
+    // of the window outside it multiply zero F entries (narrow low-k bands in a 64-row tile) and
+    // are skipped (warp-uniform)
+    int pda = u.p0, pdb = u.p1;
+    if (a.row_da && 8 * warp < Tt) {
+        pda = max(pda, a.row_da[k0 + 8 * warp]);
+        pdb = min(pdb, a.row_db[min(k0 + 8 * warp + 7, k0 + Tt - 1)]);
+    }
     for (int c = 0; c < nch; c++) {
         if (tid == 0 && c + 1 < nch) issue(c + 1);
         mbar_wait(&bars[c & 1], (c >> 1) & 1);
         const int kc = min(SKC, W - c * SKC);
-        gemm_bwd<NB>(acc, Fs + (c & 1) * SKC * STP + 8 * warp + g4, Rs + (c & 1) * SKC * RPW + g4, kc, RPW, t4);
+        const int pb = u.p0 + c * SKC;
+        gemm_bwd_rng<NB>(acc, Fs + (c & 1) * SKC * STP + 8 * warp + g4, Rs + (c & 1) * SKC * RPW + g4, kc, RPW, t4,
+                         (pda - pb) >> 2, (pdb - pb + 3) >> 2);
         __syncthreads();
     }
     if (u.nsplit > 1) {
