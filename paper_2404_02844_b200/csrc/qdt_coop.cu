@@ -36,7 +36,6 @@
 namespace qdt {
 
 constexpr int CP_THREADS = 256;   // 8 warps, one CTA per SM (255 registers: the pipelined k-loop)
-constexpr int CP_PIPE = 1;        // register double-buffered k-loop (16 warps with a plain loop: same time)
 
 // grid barrier (all CTAs co-resident by the cooperative launch): arrival counter + generation
 __device__ __forceinline__ void cp_grid_sync(unsigned *bar, unsigned nblocks, unsigned &gen)
@@ -89,22 +88,13 @@ __device__ __forceinline__ int wred_sum_i(int v)
 // software pipelined in registers: the operands of the next k-step are loaded (ld.global: F by the
 // read-only path, Theta / R rows by .cg, L2 only: they are written inside the kernel and the SMs'
 // L1 is not coherent) before the current step's DMMAs, so two k-steps of loads are in flight per
-// warp.  (A cp.async shared-memory ring of 6 stages per warp measured 2x slower: the per-lane copy
-// issue and the warp synchronisation cost more than the latency they hide at 8 warps per SM.)
+// warp.  Measured alternatives (grid-persistent path): a plain loop with 16 warps (same
+// time), three k-steps in registers (spills), a 6-stage per-warp cp.async ring and a TMA-staged
+// CTA ring (both slower: per-chunk issue and synchronisation cost more than the latency hidden).
 template <int NB, class LA, class LB>
 __device__ __forceinline__ void cp_kloop(double (&acc)[NB][2], int ks0, int nks, int stride, LA la, LB lb)
 {
     if (ks0 >= nks) return;
-    if (!CP_PIPE) {   // plain loop
-        for (int ks = ks0; ks < nks; ks += stride) {
-            const double av = la(ks);
-            double bv[NB];
-            lb(ks, bv);
-#pragma unroll
-            for (int nb = 0; nb < NB; nb++) dmma(acc[nb][0], acc[nb][1], av, bv[nb]);
-        }
-        return;
-    }
     double a0 = la(ks0), b0[NB];
     lb(ks0, b0);
     for (int ks = ks0; ks < nks; ks += stride) {
