@@ -717,6 +717,23 @@ static void plan_fwd_units(const qdt_probes *p, int t0, int t1, Emit &&emit, int
 }
 
 
+// split cap of the k_grad_wide units (N > 128, plans without k_bwd_mma): every split unit writes
+// and re-reads a 64 x 128 fragment-ordered partial per column chunk (64 KB), which at the SWCAP of
+// k_bwd_mma (128) was ~0.6 GB of scratch traffic per Large gradient (ncu DRAM 1.02 GB against
+// 0.35 GB algorithmic).  Measured at Large (profiles/r02_v7): cap 128 0.551 ms, 256 0.419, 512
+// 0.373, 1024 0.361, 2048 0.361, 4096 0.409, unsplit 1.21 (the 12 746-probe tile 0 serialises).
+// QDT_WIDE_SWCAP overrides (A/B).
+constexpr int WIDE_SWCAP = 2048;
+static int wide_swcap()
+{
+    static const int cap = [] {
+        const char *e = getenv("QDT_WIDE_SWCAP");
+        const int v = e ? atoi(e) : 0;
+        return v >= SKC ? (v / SKC) * SKC : WIDE_SWCAP;
+    }();
+    return cap;
+}
+
 // Sweep units for N: bwd units (tile, probe sub-range <= SWCAP, split-K slots), fwd units (runs
 // of <= FW_MAXT tiles whose union window is <= FWCAP probes; wider windows split by FWCAP), and
 // per-probe lists of partial rows in ascending Fock order.
@@ -728,7 +745,7 @@ static qdt_status build_sweep_plan(qdt_ctx *ctx, qdt_probes *p, Plan *pl)
     const int nsm = device_sm_count();
     // split cap of the bwd units (a smaller cap for small problems measured slower: the split-K
     // fix-up sums more slots, profiles/r02_v3)
-    const int cap = SWCAP;
+    const int cap = (pl->NW && !pl->NB) ? wide_swcap() : SWCAP;   // k_bwd_mma (NB) keeps SWCAP
     std::vector<SwUnit> bu;
     int64_t slot = 0;
     for (int t = 0; t < nt; t++) {

@@ -68,13 +68,13 @@ __device__ __forceinline__ double wred_sum(double v)
 __device__ __forceinline__ double wred_min(double v)
 {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    for (int o = 16; o > 0; o >>= 1) v = dmin(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
 }
 __device__ __forceinline__ double wred_max(double v)
 {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    for (int o = 16; o > 0; o >>= 1) v = dmax(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
 }
 __device__ __forceinline__ int wred_sum_i(int v)
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(CP_THREADS, 1) k_coop_solve(CoopArgs a)
                     double mn = INFINITY;
 #pragma unroll
                     for (int jj = 0; jj < NJ; jj++)
-                        if (lane + 32 * jj < Nv) mn = fmin(mn, 2.0 * gk[jj]);
+                        if (lane + 32 * jj < Nv) mn = dmin(mn, 2.0 * gk[jj]);
                     mn = wred_min(mn);
                     const double lam = -mn, lamp = fmax(lam, 0.0);
 #pragma unroll
@@ -331,8 +331,8 @@ __global__ void __launch_bounds__(CP_THREADS, 1) k_coop_solve(CoopArgs a)
                         if (lane + 32 * jj < Nv) {
                             x[jj] = fma(-t, x[jj], y[jj]);
                             s += x[jj];
-                            xm = fmax(xm, x[jj]);
-                            xn = fmin(xn, x[jj]);
+                            xm = dmax(xm, x[jj]);
+                            xn = dmin(xn, x[jj]);
                         } else {
                             x[jj] = -INFINITY;
                         }
@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(CP_THREADS, 1) k_coop_solve(CoopArgs a)
                                 if (x[jj] > tau) {
                                     ps += x[jj];
                                     pc++;
-                                    mA = fmin(mA, x[jj]);
+                                    mA = dmin(mA, x[jj]);
                                 }
                             ps = wred_sum(ps);
                             pc = wred_sum_i(pc);

@@ -22,6 +22,7 @@
 #include <algorithm>
 
 #include "qdt_internal.h"
+#include "qdt_ptx.cuh"
 
 namespace qdt {
 
@@ -52,7 +53,7 @@ __device__ __forceinline__ int warp_sum_i(int v)
 __device__ __forceinline__ double warp_min(double v)
 {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    for (int o = 16; o > 0; o >>= 1) v = dmin(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
 }
 
@@ -91,12 +92,12 @@ __device__ __forceinline__ int seg_sum_i(int v, int SEG)
 }
 __device__ __forceinline__ double seg_max(double v, int SEG)
 {
-    for (int o = SEG >> 1; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    for (int o = SEG >> 1; o > 0; o >>= 1) v = dmax(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
 }
 __device__ __forceinline__ double seg_min(double v, int SEG)
 {
-    for (int o = SEG >> 1; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    for (int o = SEG >> 1; o > 0; o >>= 1) v = dmin(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
 }
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool pred)
@@ -727,7 +728,7 @@ __global__ void __launch_bounds__(256) k_bwd(BwdArgs a)
                 double mn = INFINITY;
 #pragma unroll
                 for (int v = 0; v < VMAX; v++)
-                    if (colok[v]) mn = fmin(mn, g[v]);
+                    if (colok[v]) mn = dmin(mn, g[v]);
                 mn = 2.0 * seg_min(mn, SEG);
                 const double lam = act ? -mn : 0.0, lamp = fmax(lam, 0.0);
 #pragma unroll
@@ -749,7 +750,7 @@ __global__ void __launch_bounds__(256) k_bwd(BwdArgs a)
                     const double xv = y - t * g[v];
                     g[v] = ok ? xv : -INFINITY;
                     s += ok ? xv : 0.0;
-                    xm = fmax(xm, g[v]);
+                    xm = dmax(xm, g[v]);
                 }
                 s = seg_sum(s, SEG);
                 xm = seg_max(xm, SEG);

@@ -68,6 +68,13 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
+// fp64 min / max as compare + select (DSETP + two FSEL): sm_100a has no fp64 min/max instruction
+// and fmin/fmax lower to a NaN-quieting sequence about twice as long.  For non-NaN operands the
+// value is that of fmin / fmax; a NaN x is skipped (as by fmin / fmax), a NaN m propagates (the
+// solve's non-finite check reports it).
+__device__ __forceinline__ double dmin(double m, double x) { return x < m ? x : m; }
+__device__ __forceinline__ double dmax(double m, double x) { return x > m ? x : m; }
+
 __device__ __forceinline__ double quad_sum(double v)
 {
     v += __shfl_xor_sync(0xffffffffu, v, 1);
@@ -82,26 +89,26 @@ __device__ __forceinline__ int quad_sum_i(int v)
 }
 __device__ __forceinline__ double quad_max(double v)
 {
-    v = fmax(v, __shfl_xor_sync(0xffffffffu, v, 1));
-    v = fmax(v, __shfl_xor_sync(0xffffffffu, v, 2));
+    v = dmax(v, __shfl_xor_sync(0xffffffffu, v, 1));
+    v = dmax(v, __shfl_xor_sync(0xffffffffu, v, 2));
     return v;
 }
 __device__ __forceinline__ double quad_min(double v)
 {
-    v = fmin(v, __shfl_xor_sync(0xffffffffu, v, 1));
-    v = fmin(v, __shfl_xor_sync(0xffffffffu, v, 2));
+    v = dmin(v, __shfl_xor_sync(0xffffffffu, v, 1));
+    v = dmin(v, __shfl_xor_sync(0xffffffffu, v, 2));
     return v;
 }
 __device__ __forceinline__ double wmin(double v)
 {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    for (int o = 16; o > 0; o >>= 1) v = dmin(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
 }
 __device__ __forceinline__ double wmax(double v)
 {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    for (int o = 16; o > 0; o >>= 1) v = dmax(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
 }
 __device__ __forceinline__ int wsum_i(int v)

@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_solve(SmallArgs a)
         double s1 = 0.0, s2 = 0.0;
         for (int k = tid; k < M; k += nth) {
             double mn = INFINITY;
-            for (int n = 0; n < N; n++) mn = fmin(mn, 2.0 * G[k * N + n]);
+            for (int n = 0; n < N; n++) mn = dmin(mn, 2.0 * G[k * N + n]);
             const double lam = -mn, lamp = fmax(lam, 0.0);
             for (int n = 0; n < N; n++) {
                 const double g2 = 2.0 * G[k * N + n], th = T[k * N + n];
@@ -312,8 +312,8 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_solve(SmallArgs a)
                 const double x = fma(-t, Gs[row * N + n], Y[row * N + n]);
                 out[row * N + n] = x;
                 s += x;
-                xm = fmax(xm, x);
-                xn = fmin(xn, x);
+                xm = dmax(xm, x);
+                xn = dmin(xn, x);
             }
             double tau = (s - 1.0) / (double)N;
             if (!(xn > tau)) {   // Michelot from the lower bound max(tau_0, max X - 1)
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(SM_THREADS, 1) k_small_solve(SmallArgs a)
                         if (x > tau) {
                             ps += x;
                             pc++;
-                            mA = fmin(mA, x);
+                            mA = dmin(mA, x);
                         }
                     }
                     if (pc >= cnt) break;
@@ -636,7 +636,7 @@ __global__ void __launch_bounds__(SD_THREADS, 1) k_small_dense(SmallArgs a)
                 double mn = INFINITY;
 #pragma unroll
                 for (int j = 0; j < SD_NJ; j++)
-                    if (4 * j + t4 < N) mn = fmin(mn, 2.0 * gk[j]);
+                    if (4 * j + t4 < N) mn = dmin(mn, 2.0 * gk[j]);
                 mn = quad_min(mn);
                 const double lam = -mn, lamp = fmax(lam, 0.0);
 #pragma unroll
@@ -659,8 +659,8 @@ __global__ void __launch_bounds__(SD_THREADS, 1) k_small_dense(SmallArgs a)
                     const double y = prv ? fma(beta, th[j] - tp, th[j]) : th[j];
                     x[j] = fma(-t, x[j], y);
                     sx += x[j];
-                    xm = fmax(xm, x[j]);
-                    xn = fmin(xn, x[j]);
+                    xm = dmax(xm, x[j]);
+                    xn = dmin(xn, x[j]);
                 } else {
                     x[j] = -INFINITY;
                 }
@@ -681,7 +681,7 @@ __global__ void __launch_bounds__(SD_THREADS, 1) k_small_dense(SmallArgs a)
                     if (x[j] > tau) {
                         ps += x[j];
                         pc++;
-                        mA = fmin(mA, x[j]);
+                        mA = dmin(mA, x[j]);
                     }
                 ps = quad_sum(ps);
                 pc = quad_sum_i(pc);

@@ -183,7 +183,7 @@ __device__ __forceinline__ void row_pass(double (&acc)[NBA][2], const double *th
         if (PAIR) {
             double v[1] = {m1}, o[1];
             pair_xchg<1>(*px, v, o);
-            m1 = fmin(m1, o[0]);
+            m1 = dmin(m1, o[0]);
         }
         lam = -2.0 * m1;
         lamp = lam > 0.0 ? lam : 0.0;
@@ -241,8 +241,8 @@ __device__ __forceinline__ void row_pass(double (&acc)[NBA][2], const double *th
         double v[3] = {s, xm, xn}, o[3];
         pair_xchg<3>(*px, v, o);
         s = px->h ? o[0] + s : s + o[0];   // half 0 + half 1 in both warps
-        xm = fmax(xm, o[1]);
-        xn = fmin(xn, o[2]);
+        xm = dmax(xm, o[1]);
+        xn = dmin(xn, o[2]);
     }
 #undef QDT_VALID
 }
@@ -289,7 +289,7 @@ __device__ __forceinline__ void row_project(double (&acc)[NBA][2], double *thr, 
             pair_xchg<3>(*px, v, o);
             ps = px->h ? o[0] + ps : ps + o[0];
             pc += (int)o[1];
-            mA = fmin(mA, o[2]);
+            mA = dmin(mA, o[2]);
         }
         if (!done) {
             if (pc >= cnt) {
@@ -1098,18 +1098,31 @@ int wide_nb(int N)
 // columns left one CTA per SM, latency bound)
 int wide_fwd_nb(int N)
 {
+    static const int forced = [] {   // QDT_WIDE_FWD_NB: chunk width in n-blocks (A/B)
+        const char *e = getenv("QDT_WIDE_FWD_NB");
+        const int v = e ? atoi(e) : 0;
+        return (v >= 1 && v <= 16) ? v : 0;
+    }();
+    if (forced) return forced;
     const int nbt = (N + 7) / 8;
     const int ncc = (nbt + 12) / 13;
     return (nbt + ncc - 1) / ncc;
 }
-size_t wide_grad_smem() { return (size_t)(2 * SKC * STP + 2 * SKC * (8 * 16 + 4) + 8) * sizeof(double); }
+// k_grad_wide chunk ring depth: GW_STG stages of (F chunk, R chunk), i.e. GW_STG - 1 chunks in
+// flight while one is multiplied.  Measured at Large (profiles/r02_v7/ab_wide_cap_ring.jsonl):
+// 2 stages 0.357 ms, 3 stages 0.359, 4 stages 0.361 -- the double buffer stays.
+#ifndef QDT_GW_STG
+#define QDT_GW_STG 2
+#endif
+constexpr int GW_STG = QDT_GW_STG;
+size_t wide_grad_smem() { return (size_t)(GW_STG * SKC * STP + GW_STG * SKC * (8 * 16 + 4) + 8) * sizeof(double); }
 
 template <int NB>
 __global__ void __launch_bounds__(256, 2) k_grad_wide(WideArgs a)
 {
     constexpr int RPW = 8 * NB + 4;   // staged R row pitch (conflict-free B fragments)
     extern __shared__ __align__(128) double sm[];
-    __shared__ __align__(8) uint64_t bars[2];
+    __shared__ __align__(8) uint64_t bars[GW_STG];
     __shared__ double red[8];
     __shared__ int s_last;
     const DevState *st = a.state;
@@ -1126,25 +1139,26 @@ __global__ void __launch_bounds__(256, 2) k_grad_wide(WideArgs a)
     const int cbase = cc * 8 * NB, ncol = min(8 * NB, N - cbase);
     const int k0 = u.tile * ST, Tt = min(ST, a.Ml - k0);
     double *Fs = sm;
-    double *Rs = sm + 2 * SKC * STP;
+    double *Rs = sm + GW_STG * SKC * STP;
     const int W = u.p1 - u.p0, nch = (W + SKC - 1) / SKC;
     const double *Fg = a.Fb + a.fb_off[u.tile] + (int64_t)(u.p0 - a.tile_dA[u.tile]) * STP;
     if (tid == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+#pragma unroll
+        for (int i = 0; i < GW_STG; i++) mbar_init(&bars[i], 1);
         fence_barrier_init();
     }
     __syncthreads();
     auto issue = [&](int c) {
-        const int pb = c * SKC, kc = min(SKC, W - pb);
-        uint64_t *bar = &bars[c & 1];
+        const int pb = c * SKC, kc = min(SKC, W - pb), sg = c % GW_STG;
+        uint64_t *bar = &bars[sg];
         const uint32_t fby = (uint32_t)kc * STP * 8, rby = (uint32_t)ncol * 8;
         mbar_expect_tx(bar, fby + rby * kc);
-        bulk_g2s(Fs + (c & 1) * SKC * STP, Fg + (int64_t)pb * STP, fby, bar);
+        bulk_g2s(Fs + sg * SKC * STP, Fg + (int64_t)pb * STP, fby, bar);
         for (int j = 0; j < kc; j++)
-            bulk_g2s(Rs + (c & 1) * SKC * RPW + j * RPW, a.R + (int64_t)(u.p0 + pb + j) * N + cbase, rby, bar);
+            bulk_g2s(Rs + sg * SKC * RPW + j * RPW, a.R + (int64_t)(u.p0 + pb + j) * N + cbase, rby, bar);
     };
-    if (tid == 0 && nch > 0) issue(0);
+    if (tid == 0)
+        for (int c = 0; c < GW_STG - 1 && c < nch; c++) issue(c);
     double acc[NB][2];
 #pragma unroll
     for (int nb = 0; nb < NB; nb++) acc[nb][0] = acc[nb][1] = 0.0;
@@ -1157,11 +1171,13 @@ __global__ void __launch_bounds__(256, 2) k_grad_wide(WideArgs a)
         pdb = min(pdb, a.row_db[min(k0 + 8 * warp + 7, k0 + Tt - 1)]);
     }
     for (int c = 0; c < nch; c++) {
-        if (tid == 0 && c + 1 < nch) issue(c + 1);
-        mbar_wait(&bars[c & 1], (c >> 1) & 1);
+        // the stage of chunk c + GW_STG - 1 was last read by chunk c - 1 (released by its barrier)
+        if (tid == 0 && c + GW_STG - 1 < nch) issue(c + GW_STG - 1);
+        const int sg = c % GW_STG;
+        mbar_wait(&bars[sg], (c / GW_STG) & 1);
         const int kc = min(SKC, W - c * SKC);
         const int pb = u.p0 + c * SKC;
-        gemm_bwd_rng<NB>(acc, Fs + (c & 1) * SKC * STP + 8 * warp + g4, Rs + (c & 1) * SKC * RPW + g4, kc, RPW, t4,
+        gemm_bwd_rng<NB>(acc, Fs + sg * SKC * STP + 8 * warp + g4, Rs + sg * SKC * RPW + g4, kc, RPW, t4,
                          (pda - pb) >> 2, (pdb - pb + 3) >> 2);
         __syncthreads();
     }
@@ -1720,6 +1736,86 @@ __global__ void __launch_bounds__(256) k_reduce_R2(const double *rpart, const in
     }
 }
 
+// Even N: the same sums over a balanced item grid.  Item = (probe d, column chunk of 128): lane
+// holds the double2 pairs at columns 128 c + 2 lane + {0, 64}; the partial rows of d are added in
+// list order (the per-column order of k_reduce_R2).  Global warp gw takes items gw, gw + NW, ...
+// (NW = 8 G warps, G = min(nR, 8 x SMs) blocks: one wave, no tail of a third of a wave); its
+// ||R||^2 terms accumulate in item order, the block's warps are combined in warp order into
+// partR[block] (deterministic for a fixed G); block 0 zeroes partR[G, nR).
+__global__ void __launch_bounds__(256) k_reduce_R3(const double *rpart, const int64_t *red_beg,
+                                                   const int64_t *red_rows, const double *P,
+                                                   double *R, int D, int N, double *partR, int nR,
+                                                   const DevState *st)
+{
+    __shared__ double red[8];
+    if (st && st->stop) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nch = (N + 127) >> 7;
+    const int64_t nitems = (int64_t)D * nch;
+    const int64_t NW = 8 * (int64_t)gridDim.x;
+    double ss = 0.0;
+    for (int64_t it = (int64_t)blockIdx.x * 8 + warp; it < nitems; it += NW) {
+        const int d = (int)(it / nch), c = (int)(it - (int64_t)d * nch);
+        const int n0 = 128 * c + 2 * lane, n1 = n0 + 64;
+        const bool ok0 = n0 < N, ok1 = n1 < N;   // N even: a pair is whole or absent
+        const int64_t j0 = red_beg[d], j1 = red_beg[d + 1];
+        double2 s0 = make_double2(0.0, 0.0), s1 = make_double2(0.0, 0.0);
+        int64_t j = j0;
+        for (; j + 4 <= j1; j += 4) {
+            double2 q0[4], q1[4];
+#pragma unroll
+            for (int r = 0; r < 4; r++) {
+                const double *row = rpart + red_rows[j + r] * N;
+                q0[r] = ok0 ? *reinterpret_cast<const double2 *>(row + n0) : make_double2(0.0, 0.0);
+                q1[r] = ok1 ? *reinterpret_cast<const double2 *>(row + n1) : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int r = 0; r < 4; r++) {
+                s0.x += q0[r].x, s0.y += q0[r].y;
+                s1.x += q1[r].x, s1.y += q1[r].y;
+            }
+        }
+        for (; j < j1; j++) {
+            const double *row = rpart + red_rows[j] * N;
+            const double2 q0 = ok0 ? *reinterpret_cast<const double2 *>(row + n0) : make_double2(0.0, 0.0);
+            const double2 q1 = ok1 ? *reinterpret_cast<const double2 *>(row + n1) : make_double2(0.0, 0.0);
+            s0.x += q0.x, s0.y += q0.y;
+            s1.x += q1.x, s1.y += q1.y;
+        }
+        double *Rr = R + (int64_t)d * N;
+        const double *Pr = P ? P + (int64_t)d * N : nullptr;
+        if (ok0) {
+            if (Pr) {
+                const double2 p = *reinterpret_cast<const double2 *>(Pr + n0);
+                s0.x -= p.x, s0.y -= p.y;
+            }
+            *reinterpret_cast<double2 *>(Rr + n0) = s0;
+            ss = fma(s0.x, s0.x, ss);
+            ss = fma(s0.y, s0.y, ss);
+        }
+        if (ok1) {
+            if (Pr) {
+                const double2 p = *reinterpret_cast<const double2 *>(Pr + n1);
+                s1.x -= p.x, s1.y -= p.y;
+            }
+            *reinterpret_cast<double2 *>(Rr + n1) = s1;
+            ss = fma(s1.x, s1.x, ss);
+            ss = fma(s1.y, s1.y, ss);
+        }
+    }
+    ss = wsum(ss);
+    if (lane == 0) red[warp] = ss;
+    __syncthreads();
+    if (!partR) return;
+    if (threadIdx.x == 0) {
+        double v = 0.0;
+        for (int w = 0; w < 8; w++) v += red[w];
+        partR[blockIdx.x] = v;
+    }
+    if (blockIdx.x == 0)
+        for (int i = gridDim.x + threadIdx.x; i < nR; i += blockDim.x) partR[i] = 0.0;
+}
+
 // ------------------------------------------------------------------------------ scalars
 // G blocks (G <= SC2_BLOCKS): block b sums a contiguous slice of the tile partials and of partR
 // (thread t: entries t, t + blockDim, ... of the slice, in order), then a fixed-shape tree over
@@ -2050,11 +2146,27 @@ cudaError_t launch_fwd_mma(const SweepFwdArgs &a_in, int nunits, int NB, cudaStr
 }
 
 
+// QDT_REDUCE_R3=0 selects the block-per-8-probes reduction at even N too (A/B)
+static bool reduce_r3_on()
+{
+    static const bool on = [] {
+        const char *e = getenv("QDT_REDUCE_R3");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 cudaError_t launch_reduce_R2(const double *rpart, const int64_t *red_beg, const int64_t *red_rows,
                              const double *P, double *R, int D, int N, double *partR,
                              const DevState *st, cudaStream_t s)
 {
-    k_reduce_R2<<<(D + 7) / 8, 256, 0, s>>>(rpart, red_beg, red_rows, P, R, D, N, partR, st);
+    const int nR = (D + 7) / 8;   // partR entries (Plan::nR of one rank)
+    if ((N & 1) == 0 && reduce_r3_on()) {
+        const int G = std::max(1, std::min(nR, 8 * device_sm_count()));
+        k_reduce_R3<<<G, 256, 0, s>>>(rpart, red_beg, red_rows, P, R, D, N, partR, nR, st);
+    } else {
+        k_reduce_R2<<<nR, 256, 0, s>>>(rpart, red_beg, red_rows, P, R, D, N, partR, st);
+    }
     return cudaGetLastError();
 }
 

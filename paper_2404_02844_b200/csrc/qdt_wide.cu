@@ -61,8 +61,8 @@ __device__ __forceinline__ double wcombine(int v, double x, double y)
     switch (v) {
         case 0:
         case 3:
-        case 6: return fmin(x, y);
-        case 2: return fmax(x, y);
+        case 6: return dmin(x, y);
+        case 2: return dmax(x, y);
         default: return x + y;
     }
 }
@@ -306,15 +306,15 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
                             const double gv = fma(a.gamma, (y0[e] - yp[e]) + (y0[e] - yn[e]), acc[i][j][e]);
                             acc[i][j][e] = gv;
                             if (e ? v1 : v0) {
-                                mn = fmin(mn, gv);
+                                mn = dmin(mn, gv);
                                 const double xv = fma(-tk[i], gv, y0[e]);
                                 s += xv;
-                                xm = fmax(xm, xv);
-                                xn = fmin(xn, xv);
+                                xm = dmax(xm, xv);
+                                xn = dmin(xn, xv);
                                 if (xv > tau_t) {   // first Michelot round at the trial threshold
                                     ts += xv;
                                     tc++;
-                                    tm = fmin(tm, xv);
+                                    tm = dmin(tm, xv);
                                 }
                             }
                         }
@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
                             if (x > tau) {
                                 sA += x;
                                 cA++;
-                                mA = fmin(mA, x);
+                                mA = dmin(mA, x);
                             }
                         }
                 }
