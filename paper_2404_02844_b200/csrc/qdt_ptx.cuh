@@ -75,6 +75,41 @@ __device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b)
 __device__ __forceinline__ double dmin(double m, double x) { return x < m ? x : m; }
 __device__ __forceinline__ double dmax(double m, double x) { return x > m ? x : m; }
 
+// Order-preserving 32-bit key of a double's high word (sign-magnitude -> two's complement): x <= y
+// implies dkey(x) <= dkey(y).  The key drops the low 32 mantissa bits, so a key minimum / maximum
+// bounds the fp64 one from below through dkey_floor (the least double of the key's bucket).  Used
+// where the row epilogues need a BOUND only (the Michelot start max X - 1, the "every entry stays
+// active" and "min of the active set > tau" early exits): integer-pipe min / max and one 32-bit
+// shuffle per exchange instead of DSETP + two FSEL on the half-rate fp64 pipe and two shuffles.
+__device__ __forceinline__ int dkey(double x)
+{
+    const int h = __double2hiint(x);
+    return h ^ ((h >> 31) & 0x7fffffff);
+}
+__device__ __forceinline__ double dkey_floor(int k)
+{
+    const int h = k ^ ((k >> 31) & 0x7fffffff);
+    return __hiloint2double(h, h >> 31);   // negative: largest magnitude of the bucket
+}
+__device__ __forceinline__ int quad_max_i(int v)
+{
+    v = max(v, __shfl_xor_sync(0xffffffffu, v, 1));
+    v = max(v, __shfl_xor_sync(0xffffffffu, v, 2));
+    return v;
+}
+__device__ __forceinline__ int quad_min_i(int v)
+{
+    v = min(v, __shfl_xor_sync(0xffffffffu, v, 1));
+    v = min(v, __shfl_xor_sync(0xffffffffu, v, 2));
+    return v;
+}
+// max(x, 0) by the sign bit (three integer-pipe operations, no fp64 compare); -0.0 gives +0.0
+__device__ __forceinline__ double dclamp0(double x)
+{
+    const int h = __double2hiint(x), m = ~(h >> 31);
+    return __hiloint2double(h & m, __double2loint(x) & m);
+}
+
 __device__ __forceinline__ double quad_sum(double v)
 {
     v += __shfl_xor_sync(0xffffffffu, v, 1);

@@ -21,8 +21,31 @@
 
 #include <algorithm>
 
+#include <limits.h>
+
 #include "qdt_internal.h"
 #include "qdt_ptx.cuh"
+
+// Row-epilogue forms (A/B on one B200, profiles/r02_v8/ab_ikey.md):
+//  - max(X - tau, 0) by the sign bit (dclamp0): Megascale k_bwd_mma 0.5006 -> 0.4950 ms, the paper's
+//    shape 0.967 -> 0.946 ms; on for every N.
+//  - row max / min bounds and the Michelot active minimum as integer keys (dkey): 9 % fewer warp
+//    instructions, the paper's shape (NB = 19, one CTA per SM) 0.967 -> 0.919 ms, but Megascale
+//    (NB = 13, two CTAs per SM at the 128-register cap) 0.5006 -> 0.513 ms (more spill reloads):
+//    on from QDT_IKEY_MIN_NB column blocks up.
+#ifndef QDT_IKEY_MIN_NB
+#define QDT_IKEY_MIN_NB 17
+#endif
+#ifndef QDT_ICLAMP
+#define QDT_ICLAMP 1
+#endif
+// Scalar partials of k_bwd_mma: 1 = each thread keeps running sums over the CTA's unsplit tiles in
+// shared memory and the CTA reduces them once, at the end (its total goes to the slot of its last
+// unsplit tile, the earlier slots get zeros: the unit -> CTA map is static, so the order is fixed);
+// 0 = a block reduction per tile.
+#ifndef QDT_ACC_SCAL
+#define QDT_ACC_SCAL 0
+#endif
 
 namespace qdt {
 
@@ -190,6 +213,8 @@ __device__ __forceinline__ void row_pass(double (&acc)[NBA][2], const double *th
     }
     // ---- pass 2: KKT terms, X = Theta - t_k G, row sum / max / min of X
     s = 0.0, xm = -INFINITY, xn = INFINITY;
+    constexpr bool IK = NB >= QDT_IKEY_MIN_NB;
+    int kxm = INT_MIN, kxn = INT_MAX;   // IK: bounds only (see dkey), integer-pipe min / max
 #pragma unroll
     for (int nb = 0; nb < NBA; nb++) {
         const int c = CB + 8 * nb + 2 * t4;
@@ -228,15 +253,26 @@ __device__ __forceinline__ void row_pass(double (&acc)[NBA][2], const double *th
             const double x = fma(-tk, g, t0[i]);
             if (ok) {
                 s += x;
-                xm = x > xm ? x : xm;
-                xn = x < xn ? x : xn;
+                if (IK) {
+                    const int kx = dkey(x);
+                    kxm = max(kxm, kx);
+                    kxn = min(kxn, kx);
+                } else {
+                    xm = x > xm ? x : xm;
+                    xn = x < xn ? x : xn;
+                }
             }
             acc[nb][i] = ok ? x : -INFINITY;
         }
     }
     s = quad_sum(s);
-    xm = quad_max(xm);
-    xn = quad_min(xn);
+    if (IK) {
+        xm = dkey_floor(quad_max_i(kxm));   // <= max X: a valid Michelot lower bound after - 1
+        xn = dkey_floor(quad_min_i(kxn));   // <= min X: "every entry stays active" only when certain
+    } else {
+        xm = quad_max(xm);
+        xn = quad_min(xn);
+    }
     if (PAIR) {
         double v[3] = {s, xm, xn}, o[3];
         pair_xchg<3>(*px, v, o);
@@ -254,6 +290,7 @@ __device__ __forceinline__ void row_project(double (&acc)[NBA][2], double *thr, 
                                             bool act, double s, double xm, double xn, double *orow,
                                             PairX *px = nullptr)
 {
+    constexpr bool IK = NB >= QDT_IKEY_MIN_NB;
     const int cl = 8 * (NB - 1) + 2 * t4;
     const bool v0 = cl < N, v1 = cl + 1 < N;
     const bool ract = FULL || act;
@@ -270,6 +307,7 @@ __device__ __forceinline__ void row_project(double (&acc)[NBA][2], double *thr, 
         if (__all_sync(0xffffffffu, done)) break;
         double ps = 0.0, mA = INFINITY;
         int pc = 0;
+        int kmA = INT_MAX;
 #pragma unroll
         for (int nb = 0; nb < NBA; nb++)
 #pragma unroll
@@ -278,12 +316,17 @@ __device__ __forceinline__ void row_project(double (&acc)[NBA][2], double *thr, 
                 if (x > tau) {
                     ps += x;
                     pc++;
-                    if (kMin) mA = x < mA ? x : mA;
+                    if (kMin) {
+                        if (IK)
+                            kmA = min(kmA, dkey(x));
+                        else
+                            mA = x < mA ? x : mA;
+                    }
                 }
             }
         ps = quad_sum(ps);
         pc = quad_sum_i(pc);
-        if (kMin) mA = quad_min(mA);
+        if (kMin) mA = IK ? dkey_floor(quad_min_i(kmA)) : quad_min(mA);   // IK: <= min_A X, stops early only when certain
         if (PAIR) {
             double v[3] = {ps, (double)pc, mA}, o[3];
             pair_xchg<3>(*px, v, o);
@@ -307,8 +350,13 @@ __device__ __forceinline__ void row_project(double (&acc)[NBA][2], double *thr, 
             const int gb = CB / 8 + nb;
             const int c = CB + 8 * nb + 2 * t4;
             double o0 = acc[nb][0] - tau, o1 = acc[nb][1] - tau;
+#if QDT_ICLAMP
+            o0 = dclamp0(o0);
+            o1 = dclamp0(o1);
+#else
             o0 = o0 > 0.0 ? o0 : 0.0;
             o1 = o1 > 0.0 ? o1 : 0.0;
+#endif
             if (EVEN) {
                 if (gb < NB - 1 || (gb == NB - 1 && v0)) {
                     *reinterpret_cast<double2 *>(orow + c) = make_double2(o0, o1);
@@ -458,6 +506,10 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(con
     __shared__ __align__(8) uint64_t bars[3];
     __shared__ double red[8 * 3];
     __shared__ int s_last;
+#if QDT_ACC_SCAL
+    __shared__ double accs[3][256];   // per-thread running sums (KKT, paper KKT, regulariser)
+    __shared__ int s_pend;            // the unsplit tile whose slot takes this CTA's total
+#endif
     const DevState *st = a.state;
     if (st && st->stop) return;
     const int64_t it = st ? st->it : 0;
@@ -487,7 +539,13 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(con
         mbar_init(&bars[1], 1);
         mbar_init(&bars[2], 1);
         fence_barrier_init();
+#if QDT_ACC_SCAL
+        s_pend = -1;
+#endif
     }
+#if QDT_ACC_SCAL
+    accs[0][tid] = accs[1][tid] = accs[2][tid] = 0.0;
+#endif
     __syncthreads();
     // issue helpers (thread 0 only); chunk stage / parity follow a running chunk counter
     uint32_t c_issue = 0, c_use = 0, th_use = 0;
@@ -636,6 +694,27 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(con
                 row_project<NB, true, false, false>(acc, thr, Nv, t4, act, s, xm, xn, orow);
             else
                 row_project<NB, false, false, false>(acc, thr, Nv, t4, act, s, xm, xn, orow);
+#if QDT_ACC_SCAL
+            if (u.nsplit == 1) {
+                // running sums in the thread's own slots; the previous pending tile's slot is zeroed
+                accs[0][tid] += skkt;
+                accs[1][tid] += skktp;
+                accs[2][tid] += sreg;
+                if (tid == 0) {
+                    if (s_pend >= 0) {
+                        double *p = a.part + (int64_t)s_pend * NSC_TILE;
+                        if (do_kkt) p[SC_KKT] = 0.0, p[SC_KKTP] = 0.0;
+                        p[SC_REG] = 0.0;
+                        p[SC_DTH] = 0.0;
+                    }
+                    s_pend = u.tile;
+                }
+#if QDT_ACC_SCAL == 2
+                __syncthreads();
+#endif
+            } else
+#endif
+            {
             // per-tile scalar partials (fixed order: lanes, then warps)
             sreg = wsum(sreg);
             skkt = wsum(skkt);
@@ -661,6 +740,7 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(con
                 p[SC_REG] = v2;
                 p[SC_DTH] = 0.0;
             }
+            }
         } else if (warp == 0 && next < a.nunits && un.nsplit == 1) {
             issue_theta(un);
         }
@@ -668,6 +748,33 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(con
         unit = next;
         u = un;
     }
+#if QDT_ACC_SCAL
+    {   // the CTA's total over its unsplit tiles (fixed order: the thread's tiles, lanes, warps)
+        __syncthreads();   // red may still be read by thread 0 (a split tile's partial)
+        const double skkt = wsum(accs[0][tid]), skktp = wsum(accs[1][tid]), sreg = wsum(accs[2][tid]);
+        if (lane == 0) {
+            red[warp * 3 + 0] = skkt;
+            red[warp * 3 + 1] = skktp;
+            red[warp * 3 + 2] = sreg;
+        }
+        __syncthreads();
+        if (tid == 0 && s_pend >= 0) {
+            double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+            for (int w = 0; w < 8; w++) {
+                v0 += red[w * 3 + 0];
+                v1 += red[w * 3 + 1];
+                v2 += red[w * 3 + 2];
+            }
+            double *p = a.part + (int64_t)s_pend * NSC_TILE;
+            if (do_kkt) {
+                p[SC_KKT] = v0;
+                p[SC_KKTP] = v1;
+            }
+            p[SC_REG] = v2;
+            p[SC_DTH] = 0.0;
+        }
+    }
+#endif
 }
 
 // N-split variant of k_bwd_mma: 512 threads (16 warps) per CTA, warp w owns m-block w & 7 and
