@@ -86,10 +86,14 @@ __device__ __forceinline__ int dkey(double x)
     const int h = __double2hiint(x);
     return h ^ ((h >> 31) & 0x7fffffff);
 }
+// identities of the key max / min: the keys of -inf and +inf (an empty reduction floors to -inf / +inf)
+constexpr int DKEY_NINF = (int)0x800fffffu, DKEY_PINF = 0x7ff00000;
 __device__ __forceinline__ double dkey_floor(int k)
 {
     const int h = k ^ ((k >> 31) & 0x7fffffff);
-    return __hiloint2double(h, h >> 31);   // negative: largest magnitude of the bucket
+    const bool top = (h & 0x7ff00000) == 0x7ff00000;   // the +-inf bucket: the infinity itself
+    // negative: the largest magnitude of the bucket
+    return __hiloint2double(top ? (h & (int)0xfff00000u) : h, (h < 0 && !top) ? -1 : 0);
 }
 __device__ __forceinline__ int quad_max_i(int v)
 {

@@ -39,12 +39,15 @@
 #ifndef QDT_ICLAMP
 #define QDT_ICLAMP 1
 #endif
-// Scalar partials of k_bwd_mma: 1 = each thread keeps running sums over the CTA's unsplit tiles in
-// shared memory and the CTA reduces them once, at the end (its total goes to the slot of its last
-// unsplit tile, the earlier slots get zeros: the unit -> CTA map is static, so the order is fixed);
-// 0 = a block reduction per tile.
-#ifndef QDT_ACC_SCAL
-#define QDT_ACC_SCAL 0
+// Scalar partials of k_bwd_mma from QDT_ACC_MIN_NB column blocks up (one CTA per SM, no register
+// cap): each thread keeps running sums over the CTA's unsplit tiles in shared memory and the CTA
+// reduces them once, at the end (its total goes to the slot of its last unsplit tile, the earlier
+// slots get zeros; the unit -> CTA map is static, so the order is fixed).  Below it: a block
+// reduction per tile.  A/B (profiles/r02_v8/ab_acc_*.jsonl): the paper's shape k_bwd_mma<19>
+// 0.908 -> 0.865 ms; Megascale (NB = 13, two CTAs per SM at 128 registers) 0.493 -> 0.556 ms
+// (spills 144 -> 388 bytes), and neutral with a block barrier kept per tile.
+#ifndef QDT_ACC_MIN_NB
+#define QDT_ACC_MIN_NB 17
 #endif
 
 namespace qdt {
@@ -214,7 +217,7 @@ __device__ __forceinline__ void row_pass(double (&acc)[NBA][2], const double *th
     // ---- pass 2: KKT terms, X = Theta - t_k G, row sum / max / min of X
     s = 0.0, xm = -INFINITY, xn = INFINITY;
     constexpr bool IK = NB >= QDT_IKEY_MIN_NB;
-    int kxm = INT_MIN, kxn = INT_MAX;   // IK: bounds only (see dkey), integer-pipe min / max
+    int kxm = DKEY_NINF, kxn = DKEY_PINF;   // IK: bounds only (see dkey), integer-pipe min / max
 #pragma unroll
     for (int nb = 0; nb < NBA; nb++) {
         const int c = CB + 8 * nb + 2 * t4;
@@ -307,7 +310,7 @@ __device__ __forceinline__ void row_project(double (&acc)[NBA][2], double *thr, 
         if (__all_sync(0xffffffffu, done)) break;
         double ps = 0.0, mA = INFINITY;
         int pc = 0;
-        int kmA = INT_MAX;
+        int kmA = DKEY_PINF;
 #pragma unroll
         for (int nb = 0; nb < NBA; nb++)
 #pragma unroll
@@ -506,10 +509,9 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(con
     __shared__ __align__(8) uint64_t bars[3];
     __shared__ double red[8 * 3];
     __shared__ int s_last;
-#if QDT_ACC_SCAL
-    __shared__ double accs[3][256];   // per-thread running sums (KKT, paper KKT, regulariser)
-    __shared__ int s_pend;            // the unsplit tile whose slot takes this CTA's total
-#endif
+    constexpr bool ACC = NB >= QDT_ACC_MIN_NB;
+    __shared__ double accs[3][ACC ? 256 : 1];   // per-thread running sums (KKT, paper KKT, regulariser)
+    __shared__ int s_pend;                      // the unsplit tile whose slot takes this CTA's total
     const DevState *st = a.state;
     if (st && st->stop) return;
     const int64_t it = st ? st->it : 0;
@@ -539,13 +541,9 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(con
         mbar_init(&bars[1], 1);
         mbar_init(&bars[2], 1);
         fence_barrier_init();
-#if QDT_ACC_SCAL
         s_pend = -1;
-#endif
     }
-#if QDT_ACC_SCAL
-    accs[0][tid] = accs[1][tid] = accs[2][tid] = 0.0;
-#endif
+    if (ACC) accs[0][tid] = accs[1][tid] = accs[2][tid] = 0.0;
     __syncthreads();
     // issue helpers (thread 0 only); chunk stage / parity follow a running chunk counter
     uint32_t c_issue = 0, c_use = 0, th_use = 0;
@@ -694,8 +692,7 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(con
                 row_project<NB, true, false, false>(acc, thr, Nv, t4, act, s, xm, xn, orow);
             else
                 row_project<NB, false, false, false>(acc, thr, Nv, t4, act, s, xm, xn, orow);
-#if QDT_ACC_SCAL
-            if (u.nsplit == 1) {
+            if (ACC && u.nsplit == 1) {
                 // running sums in the thread's own slots; the previous pending tile's slot is zeroed
                 accs[0][tid] += skkt;
                 accs[1][tid] += skktp;
@@ -709,12 +706,7 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(con
                     }
                     s_pend = u.tile;
                 }
-#if QDT_ACC_SCAL == 2
-                __syncthreads();
-#endif
-            } else
-#endif
-            {
+            } else {
             // per-tile scalar partials (fixed order: lanes, then warps)
             sreg = wsum(sreg);
             skkt = wsum(skkt);
@@ -748,8 +740,7 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(con
         unit = next;
         u = un;
     }
-#if QDT_ACC_SCAL
-    {   // the CTA's total over its unsplit tiles (fixed order: the thread's tiles, lanes, warps)
+    if (ACC) {   // the CTA's total over its unsplit tiles (fixed order: the thread's tiles, lanes, warps)
         __syncthreads();   // red may still be read by thread 0 (a split tile's partial)
         const double skkt = wsum(accs[0][tid]), skktp = wsum(accs[1][tid]), sreg = wsum(accs[2][tid]);
         if (lane == 0) {
@@ -774,7 +765,6 @@ __global__ void __launch_bounds__(256, (NB <= 13 && !FIS ? 2 : 1)) k_bwd_mma(con
             p[SC_DTH] = 0.0;
         }
     }
-#endif
 }
 
 // N-split variant of k_bwd_mma: 512 threads (16 warps) per CTA, warp w owns m-block w & 7 and

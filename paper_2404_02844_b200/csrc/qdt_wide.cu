@@ -33,6 +33,12 @@
 #include "qdt_internal.h"
 #include "qdt_ptx.cuh"
 
+// Row bounds of the fused wide step (max X, min X, the minima of the trial / active sets) as
+// integer keys and the final clamp by the sign bit (qdt_ptx.cuh: dkey, dclamp0); A/B switch
+#ifndef QDT_W_IKEY
+#define QDT_W_IKEY 0
+#endif
+
 namespace qdt {
 
 __device__ __forceinline__ void fence_proxy_async_smem()
@@ -268,6 +274,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
             double mn = INFINITY, s = 0.0, xm = -INFINITY, xn = INFINITY;
             double ts = 0.0, tm = INFINITY;
             int tc = 0;
+            int kxm = DKEY_NINF, kxn = DKEY_PINF, ktm = DKEY_PINF;   // QDT_W_IKEY: bounds as integer keys (dkey)
             if (act) {
                 const double *thg = a.theta + (int64_t)kl * N + cbase;
                 const double *ths = Ts + (rl + 1) * Pt;
@@ -309,12 +316,22 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
                                 mn = dmin(mn, gv);
                                 const double xv = fma(-tk[i], gv, y0[e]);
                                 s += xv;
+#if QDT_W_IKEY
+                                const int kx = dkey(xv);
+                                kxm = max(kxm, kx);
+                                kxn = min(kxn, kx);
+#else
                                 xm = dmax(xm, xv);
                                 xn = dmin(xn, xv);
+#endif
                                 if (xv > tau_t) {   // first Michelot round at the trial threshold
                                     ts += xv;
                                     tc++;
+#if QDT_W_IKEY
+                                    ktm = min(ktm, kx);
+#else
                                     tm = dmin(tm, xv);
+#endif
                                 }
                             }
                         }
@@ -323,11 +340,20 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
             }
             pmn[i] = quad_min(mn);
             ps[i] = quad_sum(s);
+#if QDT_W_IKEY
+            pxm[i] = dkey_floor(quad_max_i(kxm));   // <= max X
+            pxn[i] = dkey_floor(quad_min_i(kxn));   // <= min X
+#else
             pxm[i] = quad_max(xm);
             pxn[i] = quad_min(xn);
+#endif
             pts[i] = quad_sum(ts);
             ptc[i] = (double)quad_sum_i(tc);
+#if QDT_W_IKEY
+            ptm[i] = dkey_floor(quad_min_i(ktm));   // <= min of the trial active set
+#else
             ptm[i] = quad_min(tm);
+#endif
         }
         if (t == 0) {
 #pragma unroll
@@ -439,7 +465,7 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
                 const int rl = 8 * i + g;
                 const double tau = trow[rl][0];
                 double sA = 0.0, mA = INFINITY;
-                int cA = 0;
+                int cA = 0, kmA = DKEY_PINF;
                 if (!tdone[rl]) {
 #pragma unroll
                     for (int j = 0; j < NBW; j++)
@@ -449,13 +475,21 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
                             if (x > tau) {
                                 sA += x;
                                 cA++;
+#if QDT_W_IKEY
+                                kmA = min(kmA, dkey(x));
+#else
                                 mA = dmin(mA, x);
+#endif
                             }
                         }
                 }
                 rps[i] = quad_sum(sA);
                 rpc[i] = (double)quad_sum_i(cA);
+#if QDT_W_IKEY
+                rmA[i] = dkey_floor(quad_min_i(kmA));   // <= min_A X: stops early only when certain
+#else
                 rmA[i] = quad_min(mA);
+#endif
             }
             if (t == 0) {
 #pragma unroll
@@ -516,7 +550,11 @@ __global__ void __launch_bounds__(W_THREADS, 1) k_wstep(const __grid_constant__ 
                 const int lc = 8 * (ng * NBW + j) + 2 * t;
                 if (lc < ncol) {
                     const double o0 = acc[i][j][0] - tau, o1 = acc[i][j][1] - tau;
+#if QDT_W_IKEY
+                    *reinterpret_cast<double2 *>(o + lc) = make_double2(dclamp0(o0), dclamp0(o1));
+#else
                     *reinterpret_cast<double2 *>(o + lc) = make_double2(o0 > 0.0 ? o0 : 0.0, o1 > 0.0 ? o1 : 0.0);
+#endif
                 }
             }
         }
