@@ -34,9 +34,11 @@
 #include "qdt_ptx.cuh"
 
 // Row bounds of the fused wide step (max X, min X, the minima of the trial / active sets) as
-// integer keys and the final clamp by the sign bit (qdt_ptx.cuh: dkey, dclamp0); A/B switch
+// integer keys and the final clamp by the sign bit (qdt_ptx.cuh: dkey, dclamp0).  A/B
+// (profiles/r02_v8/ab_wik_stress_cut.jsonl): Stress-cut k_wstep 1.249 -> 1.206 ms (FISTA 1.798 ->
+// 1.745), Stress 257.8 -> 254.4 ms per iteration.
 #ifndef QDT_W_IKEY
-#define QDT_W_IKEY 0
+#define QDT_W_IKEY 1
 #endif
 
 namespace qdt {
