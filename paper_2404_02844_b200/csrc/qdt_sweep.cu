@@ -36,6 +36,10 @@
 #ifndef QDT_IKEY_MIN_NB
 #define QDT_IKEY_MIN_NB 17
 #endif
+// the N-split kernel (k_bwd_split: half a row per thread, 28 accumulator registers) also takes the keys
+#ifndef QDT_IKEY_PAIR
+#define QDT_IKEY_PAIR 0
+#endif
 #ifndef QDT_ICLAMP
 #define QDT_ICLAMP 1
 #endif
@@ -216,7 +220,7 @@ __device__ __forceinline__ void row_pass(double (&acc)[NBA][2], const double *th
     }
     // ---- pass 2: KKT terms, X = Theta - t_k G, row sum / max / min of X
     s = 0.0, xm = -INFINITY, xn = INFINITY;
-    constexpr bool IK = NB >= QDT_IKEY_MIN_NB;
+    constexpr bool IK = NB >= QDT_IKEY_MIN_NB || (QDT_IKEY_PAIR && PAIR);
     int kxm = DKEY_NINF, kxn = DKEY_PINF;   // IK: bounds only (see dkey), integer-pipe min / max
 #pragma unroll
     for (int nb = 0; nb < NBA; nb++) {
@@ -293,7 +297,7 @@ __device__ __forceinline__ void row_project(double (&acc)[NBA][2], double *thr, 
                                             bool act, double s, double xm, double xn, double *orow,
                                             PairX *px = nullptr)
 {
-    constexpr bool IK = NB >= QDT_IKEY_MIN_NB;
+    constexpr bool IK = NB >= QDT_IKEY_MIN_NB || (QDT_IKEY_PAIR && PAIR);
     const int cl = 8 * (NB - 1) + 2 * t4;
     const bool v0 = cl < N, v1 = cl + 1 < N;
     const bool ract = FULL || act;
