@@ -36,9 +36,10 @@
 #ifndef QDT_IKEY_MIN_NB
 #define QDT_IKEY_MIN_NB 17
 #endif
-// the N-split kernel (k_bwd_split: half a row per thread, 28 accumulator registers) also takes the keys
+// the N-split kernel (k_bwd_split: half a row per thread, 28 accumulator registers) also takes the
+// keys: Megascale FISTA step 0.7047 -> 0.6984 ms (profiles/r02_v8/ab_ikp_megascale_fista.jsonl)
 #ifndef QDT_IKEY_PAIR
-#define QDT_IKEY_PAIR 0
+#define QDT_IKEY_PAIR 1
 #endif
 #ifndef QDT_ICLAMP
 #define QDT_ICLAMP 1
