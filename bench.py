@@ -90,13 +90,49 @@ class ClockSampler:
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index):
-        self.index, self.rows, self.proc = index, [], None
+        self.index, self.rows, self.proc, self.sampler = index, [], None, "nvidia-smi"
+
+    def _nvml_loop(self):
+        """In-process NVML sampling (QDT_BENCH_SAMPLER=nvml): the same fields as the nvidia-smi query."""
+        nv, h, idx = self.nv, self.h, self.nv_index
+        bits = [("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+                ("sw_power_cap", 0x4)]
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self.stop_ev.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append([str(idx), str(sm), str(mx), "", hex(r)] +
+                                 ["Active" if r & b else "Not Active" for _, b in bits])
+            except Exception:
+                pass
+            self.stop_ev.wait(self.period)
 
     def __enter__(self):
+        self.period = float(os.environ.get("QDT_BENCH_SAMPLE_MS", "100")) / 1e3
+        # default: in-process NVML (the fields nvidia-smi prints, without a second process polling the
+        # driver: profiles/r02_v8/README.md); QDT_BENCH_SAMPLER=smi or a failing NVML init -> nvidia-smi
+        if os.environ.get("QDT_BENCH_SAMPLER", "nvml") == "nvml":
+            try:
+                import pynvml as nv
+                nv.nvmlInit()
+                vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+                idx = self.index
+                if vis and all(v.strip().isdigit() for v in vis.split(",")):
+                    idx = int(vis.split(",")[self.index])
+                self.nv, self.nv_index, self.h = nv, idx, nv.nvmlDeviceGetHandleByIndex(idx)
+                self.sampler = "nvml"
+                self.stop_ev = threading.Event()
+                self.t = threading.Thread(target=self._nvml_loop, daemon=True)
+                self.t.start()
+                time.sleep(0.3)
+                return self
+            except Exception:
+                pass
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", str(max(10, int(self.period * 1e3)))],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -111,6 +147,8 @@ class ClockSampler:
 
     def __exit__(self, *a):
         time.sleep(0.2)
+        if getattr(self, "stop_ev", None):
+            self.stop_ev.set()
         if self.proc:
             self.proc.terminate()
             try:
@@ -128,7 +166,7 @@ class ClockSampler:
                           if len(r) > 5 + i and r[5 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "samples": len(self.rows), "sampler": self.sampler}
 
 
 def algorithmic_flops(M, N, D, nnz):
